@@ -1,0 +1,486 @@
+#!/usr/bin/env python
+"""bench.py -- the fused pack-attend-unpack hot path (arxiv 2604.15408) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config C3]
+
+One step = one pass of the whole hot path (scan, pack, attention, unpack -- the
+single fused launch ragged_pack_attend_unpack, cu_seqlens included) over one
+batch of synthetic input.  Default workload: BASELINE.json's metric config C3
+(DeiT-B, B = 32, N = 197, H = 12, d = 64, 80 % pruned -> 39 tokens/image,
+Threshold-l2 mask).  Under torchrun each rank processes its own B-image shard
+of a global batch (weak scaling, no data-path collective unless --gather).
+
+Timed region: K steps captured into one CUDA graph and replayed once, bracketed
+by barrier + synchronize, CUDA events on the launching stream, max over ranks.
+L2 protocol: the K steps rotate over 16 input/output buffer sets (~620 MB for
+C3, > 4x the 126 MB L2), so every step reads cold inputs.
+
+The JSON line (rank 0) carries the contract keys plus: roofline of the fused
+kernel, cpu_baseline (the fp64 oracle timed on host cores), e2e through the
+C ABI with host buffers, clocks sampled during the timed region, and the
+paper's Table 1/2 analog measured on this box (ragged_attn alone, padded SDPA,
+FA2 varlen, launch floors, a pruning-ratio sweep).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "ragged attn µs/call (DeiT-B, B=32, 80% pruned); pipeline images/sec"
+N_SETS = 16
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=2000)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C3")
+    ap.add_argument("--dtype", default="bf16", choices=["bf16", "fp16"])
+    ap.add_argument("--prune", type=float, default=None, help="override the config's pruning ratio")
+    ap.add_argument("--method", default=None)
+    ap.add_argument("--engine", type=int, default=0)
+    ap.add_argument("--gather", action="store_true", help="NCCL all-gather of O after every step")
+    ap.add_argument("--no-extras", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--e2e-steps", type=int, default=50)
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------------------
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def workload(args):
+    import synth
+    c = dict(synth.CONFIGS[args.config])
+    if args.prune is not None:
+        c["p"] = args.prune
+    if args.method is not None:
+        c["method"] = args.method
+    H = synth.PRESETS[c["preset"]]["H"]
+    B = c["B"]
+    return c, B, 197, H
+
+
+def algorithmic_bytes(B, N, H, T, with_cu=True):
+    """mask B*N + kept Q/K/V 3*T*H*d*2 + padded O B*N*H*d*2 (+ cu)."""
+    return B * N + 3 * T * H * 64 * 2 + B * N * H * 64 * 2 + (4 * (B + 1) if with_cu else 0)
+
+
+class ClockSampler:
+    """NVML clocks + throttle reasons sampled every ~1 ms while running."""
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+               0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+               0x100: "display_clock_setting"}
+
+    def __init__(self, index, pci_bus_id=None):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            try:
+                self.h = pynvml.nvmlDeviceGetHandleByPciBusId(pci_bus_id)
+            except Exception:
+                self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and bit != 0x1:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.001)
+
+    def __enter__(self):
+        if self.nv:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.nv:
+            self._t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["nvml unavailable"]}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ----------------------------------------------------------------------------
+def run_reference(args):
+    """--impl reference: the fp64 oracle as it stands, on the host cores, over a
+    bounded sample of the same workload (B/8 images per step)."""
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    import numpy as np
+    import oracle
+    import synth
+    from threadpoolctl import threadpool_limits
+    c, B, N, H = workload(args)
+    nb = max(1, B // 8)
+    q, k, v, keep = synth.make_inputs(nb, N, H, c["p"], c["method"], args.dtype, seed=0)
+    keep_np = keep.numpy()
+    with threadpool_limits(1):
+        for _ in range(args.warmup):
+            oracle.pack_attend_unpack(q, k, v, keep_np)
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            oracle.pack_attend_unpack(q, k, v, keep_np)
+        dt = time.perf_counter() - t0
+    value = nb * args.steps / dt
+    sample = f"{nb} of the {B} images of {args.config} per step (fp64 numpy oracle, 1 BLAS thread)"
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "images/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * dt / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{args.config}: {c['name']}", "images_per_step": nb},
+            "cpu_baseline": {"value": value, "unit": "images/s", "cores": 1, "kind": "oracle",
+                             "sample": sample},
+            "e2e": {"value": value, "unit": "images/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def cpu_baseline(args, c, B, N, H):
+    import oracle
+    import synth
+    from threadpoolctl import threadpool_limits
+    q, k, v, keep = synth.make_inputs(B, N, H, c["p"], c["method"], args.dtype, seed=0)
+    keep_np = keep.numpy()
+    calls, t0 = 0, time.perf_counter()
+    with threadpool_limits(1):
+        while True:
+            oracle.pack_attend_unpack(q, k, v, keep_np)
+            calls += 1
+            if time.perf_counter() - t0 >= args.cpu_seconds:
+                break
+    dt = time.perf_counter() - t0
+    return {"value": B * calls / dt, "unit": "images/s", "cores": 1, "kind": "oracle",
+            "sample": f"{calls} full {args.config} batches ({B} images) in {dt:.1f} s, "
+                      f"fp64 numpy oracle, 1 BLAS thread, host {os.cpu_count()} cores"}
+
+
+# ----------------------------------------------------------------------------
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_2604_15408_b200 as rb
+    import synth
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    c, B, N, H = workload(args)
+    dt = synth.DTYPES[args.dtype]
+    q, k, v, keep = synth.make_inputs(B, N, H, c["p"], c["method"], args.dtype, seed=0,
+                                      image_offset=rank * B)
+    T = int(keep.numpy().astype(bool).sum())
+    sets = []
+    for _ in range(N_SETS):
+        sets.append(dict(q=q.to(dev), k=k.to(dev), v=v.to(dev), keep=keep.to(dev),
+                         o=torch.empty(B, N, H, 64, dtype=dt, device=dev),
+                         cu=torch.empty(B + 1, dtype=torch.int32, device=dev)))
+    gathered = torch.empty(ws * B, N, H, 64, dtype=dt, device=dev) if args.gather else None
+
+    def step(i, stream=None):
+        s = sets[i % N_SETS]
+        rb.pack_attend_unpack(s["q"], s["k"], s["v"], s["keep"], o=s["o"], cu=s["cu"],
+                              stream=stream, engine=args.engine)
+        if gathered is not None:
+            dist.all_gather_into_tensor(gathered, s["o"])
+
+    # warm-up: W eager steps
+    for i in range(args.warmup):
+        step(i)
+    torch.cuda.synchronize()
+
+    # capture the K timed steps into one graph (the kernels are ours; the graph is plumbing)
+    g = torch.cuda.CUDAGraph()
+    cap = torch.cuda.Stream()
+    with torch.cuda.graph(g, stream=cap):
+        for i in range(args.steps):
+            step(i)
+    torch.cuda.synchronize()
+    g.replay()                      # untimed replay: clocks up, graph uploaded
+    torch.cuda.synchronize()
+
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    stream = torch.cuda.current_stream()
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    pr = torch.cuda.get_device_properties(dev)
+    bus = f"{pr.pci_domain_id:08X}:{pr.pci_bus_id:02X}:{pr.pci_device_id:02X}.0"
+    with ClockSampler(local, bus) as clk:
+        start.record(stream)
+        g.replay()
+        end.record(stream)
+        torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    ms = start.elapsed_time(end)
+    if ws > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    us_per_call = 1e3 * ms / args.steps
+    value = ws * B * args.steps / (ms * 1e-3)
+
+    # e2e through the C ABI with host buffers (pinned): H2D inputs, fused kernel, D2H output
+    e2e = measure_e2e(args, rb, torch, dev, q, k, v, keep, ws, B, N, H, dt)
+
+    if rank != 0:
+        if ws > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    alg = algorithmic_bytes(B, N, H, T)
+    achieved = alg / (us_per_call * 1e-6) / 1e9
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                "frac": achieved / hbm_peak, "traffic": traffic_from_profile(),
+                "kernel": "attn_kernel<bf16, fused>", "algorithmic_bytes_per_launch": alg,
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650 GB/s"}
+
+    line = {"metric": METRIC, "value": value, "unit": "images/s", "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
+            "config": {"workload": f"{args.config}: {c['name']}", "B_per_gpu": B, "N": N, "H": H,
+                       "d": 64, "prune": c["p"], "method": c["method"], "tok_per_img": T // B,
+                       "T": T, "global_batch": ws * B,
+                       "l2": f"{N_SETS} rotating input/output sets "
+                             f"({N_SETS * (4 * B * N * H * 128) / 1e6:.0f} MB > 126 MB L2)",
+                       "timing": "K steps in one CUDA graph, CUDA events, max over ranks",
+                       "gather": bool(args.gather)},
+            "us_per_call": us_per_call, "images_per_s": value,
+            "gpu_launches": args.steps, "clocks": clk.summary(), "roofline": roofline, "e2e": e2e}
+
+    if ws == 1 and not args.no_extras:
+        line["cpu_baseline"] = cpu_baseline(args, c, B, N, H)
+        try:
+            line["extras"] = extras(args, rb, torch, dev, sets, c, B, N, H, dt, T)
+        except Exception as ex:  # extras are context, never the headline
+            line["extras"] = {"error": repr(ex)}
+    print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def traffic_from_profile():
+    """DRAM bytes per launch of the fused kernel from the committed ncu --set
+    full summary (profiles/), or None."""
+    p = os.path.join(ROOT, "profiles", "ncu_fused_summary.json")
+    try:
+        return json.load(open(p))["dram_bytes_per_launch"]
+    except Exception:
+        return None
+
+
+def measure_e2e(args, rb, torch, dev, q, k, v, keep, ws, B, N, H, dt):
+    qh, kh, vh = (t.pin_memory() for t in (q, k, v))
+    keeph = keep.pin_memory()
+    oh = torch.empty(B, N, H, 64, dtype=dt).pin_memory()
+    qd, kd, vd = (torch.empty_like(t, device=dev) for t in (q, k, v))
+    keepd = torch.empty_like(keep, device=dev)
+    od = torch.empty(B, N, H, 64, dtype=dt, device=dev)
+
+    def one():
+        qd.copy_(qh, non_blocking=True)
+        kd.copy_(kh, non_blocking=True)
+        vd.copy_(vh, non_blocking=True)
+        keepd.copy_(keeph, non_blocking=True)
+        rb.pack_attend_unpack(qd, kd, vd, keepd, o=od)
+        oh.copy_(od, non_blocking=True)
+
+    for _ in range(5):
+        one()
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(args.e2e_steps):
+        one()
+    e.record()
+    torch.cuda.synchronize()
+    ms = s.elapsed_time(e)
+    if ws > 1:
+        import torch.distributed as dist
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    h2d = sum(t.numel() * t.element_size() for t in (q, k, v, keep))
+    return {"value": ws * B * args.e2e_steps / (ms * 1e-3), "unit": "images/s",
+            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": oh.numel() * oh.element_size(),
+            "us_per_step": 1e3 * ms / args.e2e_steps}
+
+
+# ----------------------------------------------------------------------------
+def _graph_time(torch, fns, reps):
+    """Device µs per call: `reps` calls (rotating over fns) in one CUDA graph."""
+    for f in fns:                   # eager first call: one-time attributes outside capture
+        f()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=torch.cuda.Stream()):
+        for i in range(reps):
+            fns[i % len(fns)]()
+    torch.cuda.synchronize()
+    g.replay()
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    g.replay()
+    e.record()
+    torch.cuda.synchronize()
+    return 1e3 * s.elapsed_time(e) / reps
+
+
+def _host_time(torch, fn, warm=10, iters=500):
+    """Paper protocol: 10 warm-up + 500 timed, synchronize per call;
+    host wall clock; returns median µs."""
+    for _ in range(warm):
+        fn()
+        torch.cuda.synchronize()
+    ts = []
+    for _ in range(iters):
+        t0 = time.perf_counter()
+        fn()
+        torch.cuda.synchronize()
+        ts.append(1e6 * (time.perf_counter() - t0))
+    return statistics.median(ts)
+
+
+def extras(args, rb, torch, dev, sets, c, B, N, H, dt, T):
+    import synth
+    out = {}
+    reps = 500
+    # launch floors: empty kernel with the fused grid, graph and host-synced
+    grid = B * H + 1
+    out["launch_floor_us"] = {
+        "empty_kernel_graph_device": _graph_time(torch, [lambda: rb.empty_launch(grid, 128)], reps),
+        "empty_kernel_host_sync": _host_time(torch, lambda: rb.empty_launch(grid, 128)),
+    }
+    s0 = sets[0]
+    out["fused_host_sync_us"] = _host_time(
+        torch, lambda: rb.pack_attend_unpack(s0["q"], s0["k"], s0["v"], s0["keep"], o=s0["o"], cu=s0["cu"]))
+    gr = rb.Graph(s0["q"], s0["k"], s0["v"], s0["keep"], s0["o"], s0["cu"])
+    out["fused_graph_launch_host_sync_us"] = _host_time(torch, gr.launch)
+    gr.close()
+
+    # ragged_attn alone on packed buffers (Table 1 "Ours" analog), cold rotation
+    packed = []
+    for s in sets:
+        packed.append(rb.pack(s["q"], s["k"], s["v"], s["keep"]))
+    torch.cuda.synchronize()
+    ops = [torch.empty_like(p[0]) for p in packed]
+    attn_fns = [(lambda p=p, o=o: rb.attn(p[0], p[1], p[2], p[3], N, op=o)) for p, o in zip(packed, ops)]
+    out["ragged_attn_us"] = _graph_time(torch, attn_fns, reps)
+    out["ragged_attn_host_sync_us"] = _host_time(torch, attn_fns[0])
+    # separate 3-stage path (pack -> attn -> unpack, 4 launches)
+    def sep(i):
+        s, p, o = sets[i], packed[i], ops[i]
+        rb.pack(s["q"], s["k"], s["v"], s["keep"], out=p)
+        rb.attn(p[0], p[1], p[2], p[3], N, op=o)
+        rb.unpack(o, p[4], B, N, o=s["o"])
+    out["separate_path_us"] = _graph_time(torch, [(lambda i=i: sep(i)) for i in range(N_SETS)], reps // 5)
+    out["pack_us"] = _graph_time(torch, [(lambda i=i: rb.pack(sets[i]["q"], sets[i]["k"], sets[i]["v"],
+                                                              sets[i]["keep"], out=packed[i]))
+                                         for i in range(N_SETS)], reps)
+    out["scan_us"] = _graph_time(torch, [(lambda i=i: rb.scan(sets[i]["keep"], packed[i][3], packed[i][4],
+                                                              packed[i][5])) for i in range(N_SETS)], reps)
+    out["unpack_us"] = _graph_time(torch, [(lambda i=i: rb.unpack(ops[i], packed[i][4], B, N, o=sets[i]["o"]))
+                                           for i in range(N_SETS)], reps)
+
+    # padded SDPA baseline on the same box (R15)
+    F = torch.nn.functional
+
+    def sdpa(s):
+        m = s["keep"].bool()[:, None, None, :]
+        return F.scaled_dot_product_attention(s["q"].transpose(1, 2), s["k"].transpose(1, 2),
+                                              s["v"].transpose(1, 2), attn_mask=m)
+    sdpa_fns = [(lambda s=s: sdpa(s)) for s in sets]
+    try:
+        out["padded_sdpa_graph_us"] = _graph_time(torch, sdpa_fns, reps // 5)
+        out["padded_sdpa_host_sync_us"] = _host_time(torch, sdpa_fns[0])
+    except Exception as ex:
+        out["padded_sdpa_error"] = repr(ex)
+
+    # FA2 varlen on the packed buffers, as the paper's comparator (context only)
+    try:
+        from flash_attn import flash_attn_varlen_func
+        p = packed[0]
+        nmax = int((p[3][1:] - p[3][:-1]).max().item())
+        fa = lambda: flash_attn_varlen_func(p[0][:T], p[1][:T], p[2][:T], p[3], p[3], nmax, nmax)  # noqa: E731
+        out["fa2_varlen_host_sync_us"] = _host_time(torch, fa)
+        out["fa2_varlen_graph_us"] = _graph_time(torch, [fa], reps // 5)
+    except Exception as ex:
+        out["fa2_varlen_error"] = repr(ex)[:200]
+
+    # pruning-ratio sweep at this config's shape (BASELINE target: monotone in p,
+    # below padded SDPA for every p >= 0.3)
+    sweep = []
+    q0, k0, v0 = (sets[0][x].cpu() for x in ("q", "k", "v"))
+    for p in (0.0, 0.3, 0.5, 0.7, 0.8, 0.9):
+        kk = synth.kept_tokens(N, p)
+        keep = torch.from_numpy(synth.mask_threshold_l2(B, N, kk, seed=1000, D=H * 64)).to(dev)
+        for s in sets:
+            s["keep"].copy_(keep)
+        f_us = _graph_time(torch, [(lambda s=s: rb.pack_attend_unpack(s["q"], s["k"], s["v"], s["keep"],
+                                                                        o=s["o"], cu=s["cu"])) for s in sets], reps)
+        try:
+            sd_us = _graph_time(torch, sdpa_fns, reps // 5)
+        except Exception:
+            sd_us = None
+        Tp = B * kk
+        ab = algorithmic_bytes(B, N, H, Tp)
+        sweep.append({"p": p, "tok": kk, "fused_us": f_us, "padded_sdpa_us": sd_us,
+                      "fused_hbm_frac": ab / (f_us * 1e-6) / 1e9 / 6560.6, "alg_bytes": ab})
+    out["prune_sweep"] = sweep
+    return out
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,161 @@
+/*
+ * ragged.h -- C ABI of libragged.so: the pack-attend-unpack hot path for
+ * token-pruned ViTs (arxiv 2604.15408), hand-written CUDA for sm_100a (B200).
+ *
+ * Citation keys: P:n = PAPER.md line n (the paper), S:n = SPEC.md line n.
+ *
+ * Conventions shared by every entry point
+ * ---------------------------------------
+ *  - Every tensor pointer is a CUDA DEVICE pointer owned by the caller.  The
+ *    library never allocates, frees or retains them (the paper identifies
+ *    per-call output / workspace allocation as dispatch overhead, P:340-343,
+ *    P:588-592).  The only library-owned objects are ragged_graph handles.
+ *  - Every call is asynchronous on `stream` (a cudaStream_t passed as void*;
+ *    NULL = legacy default stream), never synchronizes the host and never
+ *    reads device data on the host.  In particular the total kept count
+ *    T = cu_seqlens[B] is never read back (the paper's pack does one scalar
+ *    CPU sync for it); buffers are sized by capacity B*N instead.
+ *  - Layouts (token-major, Alg. 1 input "Q,K,V in R^{T x H x d}"):
+ *      keep       uint8 [B, N], nonzero = keep (keep mask m in {0,1}^{B x S})
+ *      q, k, v    padded [B, N, H, d]; consecutive tokens are `ld` elements apart
+ *                 (ld = H*d for separate tensors, 3*H*d for one fused [B,N,3,H,d]
+ *                 buffer with k = q + H*d, v = q + 2*H*d); heads are d apart.
+ *      o          padded [B, N, H, d], contiguous (token stride H*d).
+ *      qp, kp, vp, op  packed [B*N (capacity), H, d], contiguous; rows
+ *                 [0, cu[B]) are valid, image b owns rows [cu[b], cu[b+1]).
+ *      cu_seqlens int32 [B+1]; dst_index, src_index int32 [B*N].
+ *  - Element type: bf16 or fp16 (ragged_problem.dtype); attention accumulates
+ *    in fp32 and rounds its output RNE to the input type (R1).
+ *  - Errors: host-checkable preconditions are validated BEFORE any CUDA call
+ *    and returned synchronously (RAGGED_EINVAL / ENOTSUP / EALIGN); a failed
+ *    launch returns RAGGED_ECUDA with cudaGetErrorString text available from
+ *    ragged_last_error() (thread-local).  Conditions that live in device data
+ *    (an image with no kept token, n_b = 0) are not errors: that image yields
+ *    no packed rows and all-zero padded output rows (R11).
+ *    Malformed caller-supplied cu_seqlens passed to ragged_attn (non-monotone,
+ *    n_b > N, cu[B] > B*N) is undefined behaviour, as for any varlen API.
+ *  - B == 0 is a valid no-op (nothing is launched).
+ */
+#ifndef RAGGED_H
+#define RAGGED_H
+
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define RAGGED_API __attribute__((visibility("default")))
+#else
+#define RAGGED_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum { RAGGED_BF16 = 0, RAGGED_FP16 = 1 } ragged_dtype;
+
+typedef enum {
+  RAGGED_OK = 0,
+  RAGGED_EINVAL = 1,   /* null pointer, B < 0, H < 1, N < 1, ld < H*d          */
+  RAGGED_ENOTSUP = 2,  /* d != 64, N > 256, unknown dtype/engine, B*N > 2^31-1 */
+  RAGGED_EALIGN = 3,   /* a tensor pointer not 16-byte aligned, or ld % 8 != 0 */
+  RAGGED_ECUDA = 4     /* CUDA launch / graph error; see ragged_last_error()  */
+} ragged_status;
+
+/* Attention engine (tensor-core path of step a3).  AUTO picks the fastest
+ * measured engine for the shape. */
+typedef enum {
+  RAGGED_ENGINE_AUTO = 0,
+  RAGGED_ENGINE_MMA_SYNC = 1,   /* mma.sync.m16n8k16, fp32 accumulate in registers */
+  RAGGED_ENGINE_TCGEN05 = 2     /* tcgen05.mma, fp32 accumulate in TMEM            */
+} ragged_engine;
+
+/* The problem statement of the paper: B images, N padded tokens per image
+ * including CLS (DeiT: 197), H heads, head_dim d (DeiT: 64, P:136,
+ * P:330). */
+typedef struct {
+  int32_t B;       /* images, >= 0                                        */
+  int32_t N;       /* padded tokens per image incl. CLS, 1..256           */
+  int32_t H;       /* heads, >= 1 (DeiT-T/S/B: 3/6/12)                    */
+  int32_t d;       /* head dim; must be 64 (B_D = d = 64)      */
+  int32_t dtype;   /* ragged_dtype                                        */
+  int32_t engine;  /* ragged_engine (0 = auto)                            */
+  int64_t ld;      /* token stride of padded q/k/v in elements, >= H*d, % 8 == 0 */
+} ragged_problem;
+
+/* a1 -- scan.  Per-image cumulative sums produce cu_seqlens and per-token
+ * destination indices:
+ *   cu[0] = 0, cu[b+1] = cu[b] + #{n : keep[b,n] != 0}
+ *   dst[b*N+n] = cu[b] + #{n' < n : keep[b,n'] != 0} if keep[b,n] != 0, else -1
+ *   src[dst[i]] = i for every kept i (stable: ascending position within an
+ *   image, image-major -- DESIGN.md R7); src[r] for r >= cu[B] is untouched.
+ * Deterministic, bit-exact.  One launch. */
+RAGGED_API ragged_status ragged_scan(const ragged_problem* prob, const uint8_t* keep,
+                          int32_t* cu_seqlens, int32_t* dst_index, int32_t* src_index,
+                          void* stream);
+
+/* a1 + a2 -- pack.  Runs ragged_scan, then gathers the kept rows:
+ *   qp[r] = q[src[r]], kp[r] = k[src[r]], vp[r] = v[src[r]] for r < cu[B]
+ * (bit copies; whole H*d rows).  Rows >= cu[B] of the
+ * packed buffers are untouched.  Two launches (scan, gather). */
+RAGGED_API ragged_status ragged_pack(const ragged_problem* prob, const uint8_t* keep,
+                          const void* q, const void* k, const void* v,
+                          int32_t* cu_seqlens, int32_t* dst_index, int32_t* src_index,
+                          void* qp, void* kp, void* vp, void* stream);
+
+/* a3 -- ragged attention (Alg. 1).  For every image i and head h,
+ * with s = cu[i], n = cu[i+1] - s (0 <= n <= N):
+ *   op[s:s+n, h, :] = softmax(qp[s:s+n,h,:] kp[s:s+n,h,:]^T / sqrt(d)) vp[s:s+n,h,:]
+ * bidirectional, no dropout, no KV cache.  One CTA per (image,
+ * head) pair, head fastest (pid -> h = pid mod H, i = pid / H).
+ * Packed rows >= cu[B] of op are untouched.  One launch. */
+RAGGED_API ragged_status ragged_attn(const ragged_problem* prob, const void* qp, const void* kp,
+                          const void* vp, const int32_t* cu_seqlens, void* op,
+                          void* stream);
+
+/* a4 -- unpack.  o[i] = op[dst[i]] if dst[i] >= 0, else +0.0 (bit pattern 0)
+ * for every padded row i < B*N (R10).  One launch. */
+RAGGED_API ragged_status ragged_unpack(const ragged_problem* prob, const void* op,
+                            const int32_t* dst_index, void* o, void* stream);
+
+/* a5 -- fused pack-attend-unpack in ONE launch: keep mask -> per-image ranks ->
+ * gather of kept q/k/v rows into shared memory -> attention -> scatter to
+ * padded o, with +0.0 rows for dropped tokens.  Equal, bit for bit, to
+ * ragged_pack; ragged_attn; ragged_unpack.  If cu_seqlens_or_null is non-NULL
+ * it also receives cu_seqlens (one extra CTA computes it concurrently). */
+RAGGED_API ragged_status ragged_pack_attend_unpack(const ragged_problem* prob, const uint8_t* keep,
+                                        const void* q, const void* k, const void* v,
+                                        void* o, int32_t* cu_seqlens_or_null,
+                                        void* stream);
+
+/* a5 -- CUDA-graph capture of one ragged_pack_attend_unpack with fixed
+ * pointers: ragged_graph_launch replays it as a single graph launch with no
+ * argument marshalling.  The handle owns its cudaGraphExec; destroy it with
+ * ragged_graph_destroy (NULL is ignored). */
+typedef struct ragged_graph ragged_graph;
+RAGGED_API ragged_status ragged_graph_create(const ragged_problem* prob, const uint8_t* keep,
+                                  const void* q, const void* k, const void* v, void* o,
+                                  int32_t* cu_seqlens_or_null, ragged_graph** out);
+RAGGED_API ragged_status ragged_graph_launch(ragged_graph* graph, void* stream);
+RAGGED_API void ragged_graph_destroy(ragged_graph* graph);
+
+/* Launch-floor probe: an empty kernel launched with `grid` x
+ * `block` threads; its latency is the dispatch floor of this library. */
+RAGGED_API ragged_status ragged_empty_launch(int32_t grid, int32_t block, void* stream);
+
+/* Host-only helper (no CUDA call): SPEC validate_cu_seqlens.
+ * Returns -1 if cu[0] == 0, cu is non-decreasing and cu[n-1] == total,
+ * otherwise the first violating index (0 for cu[0] != 0, n-1 for the total). */
+RAGGED_API int32_t ragged_validate_cu_seqlens(const int32_t* cu_host, int32_t n, int64_t total);
+
+/* Name of a status code; never NULL. */
+RAGGED_API const char* ragged_status_str(ragged_status s);
+/* Detail of the last error on this thread ("" if none). */
+RAGGED_API const char* ragged_last_error(void);
+/* Build string: version, compile target and engines compiled in. */
+RAGGED_API const char* ragged_build_info(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* RAGGED_H */

@@ -1,0 +1,255 @@
+"""Thin Python binding of libragged.so (include/ragged.h) -- argument
+marshalling only.  Every step of the pack-attend-unpack path runs in the CUDA
+kernels of csrc/; there is no CPU or PyTorch fallback: the first call raises
+ImportError if the shared library is missing (the package itself imports
+without it so that `python -m paper_2604_15408_b200.build` can build it), and
+every call raises RaggedError on a non-OK status.  PyTorch is used only for device memory and streams.
+
+Names follow the C ABI: scan, pack, attn, unpack, pack_attend_unpack, Graph,
+empty_launch (ragged_scan, ragged_pack, ...).  Citations: PAPER.md lines
+P:266-277 (packing), P:286-334 (Alg. 1, grid), BASELINE.json north_star.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import torch
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libragged.so")
+
+BF16, FP16 = 0, 1
+ENGINE_AUTO, ENGINE_MMA_SYNC, ENGINE_TCGEN05 = 0, 1, 2
+OK, EINVAL, ENOTSUP, EALIGN, ECUDA = 0, 1, 2, 3, 4
+_DTYPE = {torch.bfloat16: BF16, torch.float16: FP16}
+
+
+class RaggedError(RuntimeError):
+    def __init__(self, status: int, fn: str):
+        self.status = status
+        super().__init__(f"{fn}: {status_str(status)}: {last_error()}")
+
+
+class Problem(ctypes.Structure):
+    """ragged_problem: B images, N padded tokens (incl. CLS), H heads, d = 64,
+    dtype, engine, ld = token stride of padded q/k/v in elements."""
+    _fields_ = [("B", ctypes.c_int32), ("N", ctypes.c_int32), ("H", ctypes.c_int32),
+                ("d", ctypes.c_int32), ("dtype", ctypes.c_int32), ("engine", ctypes.c_int32),
+                ("ld", ctypes.c_int64)]
+
+
+def _load() -> ctypes.CDLL:
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing: build it with `python -m paper_2604_15408_b200.build` "
+                          "(there is no fallback path)")
+    lib = ctypes.CDLL(LIB_PATH)
+    P, V, I32, I64 = ctypes.POINTER(Problem), ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64
+    sigs = {
+        "ragged_scan": [P, V, V, V, V, V],
+        "ragged_pack": [P, V, V, V, V, V, V, V, V, V, V, V],
+        "ragged_attn": [P, V, V, V, V, V, V],
+        "ragged_unpack": [P, V, V, V, V],
+        "ragged_pack_attend_unpack": [P, V, V, V, V, V, V, V],
+        "ragged_graph_create": [P, V, V, V, V, V, V, ctypes.POINTER(V)],
+        "ragged_graph_launch": [V, V],
+        "ragged_empty_launch": [I32, I32, V],
+        "ragged_validate_cu_seqlens": [ctypes.POINTER(I32), I32, I64],
+    }
+    for name, args in sigs.items():
+        f = getattr(lib, name)
+        f.argtypes = args
+        f.restype = ctypes.c_int32
+    lib.ragged_graph_destroy.argtypes = [V]
+    lib.ragged_graph_destroy.restype = None
+    lib.ragged_status_str.argtypes = [ctypes.c_int32]
+    lib.ragged_status_str.restype = ctypes.c_char_p
+    lib.ragged_last_error.argtypes = []
+    lib.ragged_last_error.restype = ctypes.c_char_p
+    lib.ragged_build_info.argtypes = []
+    lib.ragged_build_info.restype = ctypes.c_char_p
+    return lib
+
+
+_lib = None
+
+EXPORTS = ("ragged_scan", "ragged_pack", "ragged_attn", "ragged_unpack", "ragged_pack_attend_unpack",
+           "ragged_graph_create", "ragged_graph_launch", "ragged_graph_destroy", "ragged_empty_launch",
+           "ragged_validate_cu_seqlens", "ragged_status_str", "ragged_last_error", "ragged_build_info")
+
+
+def lib() -> ctypes.CDLL:
+    """The loaded libragged.so (loaded on first use; raises if it is missing)."""
+    global _lib
+    if _lib is None:
+        _lib = _load()
+    return _lib
+
+
+def status_str(s: int) -> str:
+    return lib().ragged_status_str(s).decode()
+
+
+def last_error() -> str:
+    return lib().ragged_last_error().decode()
+
+
+def build_info() -> str:
+    return lib().ragged_build_info().decode()
+
+
+def _check(status: int, fn: str) -> None:
+    if status != OK:
+        raise RaggedError(status, fn)
+
+
+def _ptr(t) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+def _stream(stream) -> int | None:
+    if stream is None:
+        return torch.cuda.current_stream().cuda_stream
+    return stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+
+
+def problem(B: int, N: int, H: int, d: int = 64, dtype=torch.bfloat16, ld: int | None = None,
+            engine: int = ENGINE_AUTO) -> Problem:
+    dt = _DTYPE[dtype] if isinstance(dtype, torch.dtype) else int(dtype)
+    return Problem(B, N, H, d, dt, engine, H * d if ld is None else ld)
+
+
+def _padded_problem(q, k, v, engine):
+    """Problem for padded q/k/v [B, N, H, d] views sharing one token stride."""
+    if q.dim() != 4:
+        raise ValueError("q/k/v must be [B, N, H, d]")
+    B, N, H, d = q.shape
+    for t in (k, v):
+        if t.shape != q.shape or t.stride() != q.stride() or t.dtype != q.dtype:
+            raise ValueError("q, k, v must share shape, strides and dtype")
+    if q.stride(3) != 1 or q.stride(2) != d or q.stride(0) != N * q.stride(1):
+        raise ValueError("q/k/v must be token-major [B, N, H, d] with unit head-dim stride")
+    if q.dtype not in _DTYPE:
+        raise ValueError("dtype must be bf16 or fp16")
+    return problem(B, N, H, d, q.dtype, q.stride(1), engine)
+
+
+def _keep_u8(keep):
+    if keep.dtype == torch.bool:
+        keep = keep.view(torch.uint8)
+    if keep.dtype != torch.uint8 or not keep.is_contiguous():
+        raise ValueError("keep must be a contiguous uint8/bool [B, N] tensor")
+    return keep
+
+
+def scan(keep, cu=None, dst=None, src=None, stream=None):
+    """a1: keep [B, N] -> (cu [B+1], dst [B*N], src [B*N] capacity)."""
+    keep = _keep_u8(keep)
+    B, N = keep.shape
+    dev = keep.device
+    cu = torch.empty(B + 1, dtype=torch.int32, device=dev) if cu is None else cu
+    dst = torch.empty(B * N, dtype=torch.int32, device=dev) if dst is None else dst
+    src = torch.empty(B * N, dtype=torch.int32, device=dev) if src is None else src
+    p = problem(B, N, 1)
+    _check(lib().ragged_scan(ctypes.byref(p), keep.data_ptr(), cu.data_ptr(), dst.data_ptr(),
+                            src.data_ptr(), _stream(stream)), "ragged_scan")
+    return cu, dst, src
+
+
+def pack(q, k, v, keep, out=None, stream=None, engine=ENGINE_AUTO):
+    """a1 + a2: returns (qp, kp, vp, cu, dst, src); packed buffers
+    have capacity B*N rows, rows [0, cu[B]) valid."""
+    p = _padded_problem(q, k, v, engine)
+    keep = _keep_u8(keep)
+    B, N, H, d = q.shape
+    if out is None:
+        mk = lambda: torch.empty(B * N, H, d, dtype=q.dtype, device=q.device)  # noqa: E731
+        qp, kp, vp = mk(), mk(), mk()
+        cu = torch.empty(B + 1, dtype=torch.int32, device=q.device)
+        dst = torch.empty(B * N, dtype=torch.int32, device=q.device)
+        src = torch.empty(B * N, dtype=torch.int32, device=q.device)
+    else:
+        qp, kp, vp, cu, dst, src = out
+    _check(lib().ragged_pack(ctypes.byref(p), keep.data_ptr(), q.data_ptr(), k.data_ptr(), v.data_ptr(),
+                            cu.data_ptr(), dst.data_ptr(), src.data_ptr(), qp.data_ptr(), kp.data_ptr(),
+                            vp.data_ptr(), _stream(stream)), "ragged_pack")
+    return qp, kp, vp, cu, dst, src
+
+
+def attn(qp, kp, vp, cu, N: int, op=None, stream=None, engine=ENGINE_AUTO):
+    """a3 (Alg. 1): packed [cap, H, d] + cu [B+1] -> packed O."""
+    cap, H, d = qp.shape
+    for t in (qp, kp, vp):
+        if not t.is_contiguous() or t.shape != qp.shape:
+            raise ValueError("packed q/k/v must be contiguous [cap, H, d]")
+    B = cu.numel() - 1
+    op = torch.empty_like(qp) if op is None else op
+    p = problem(B, N, H, d, qp.dtype, H * d, engine)
+    _check(lib().ragged_attn(ctypes.byref(p), qp.data_ptr(), kp.data_ptr(), vp.data_ptr(), cu.data_ptr(),
+                            op.data_ptr(), _stream(stream)), "ragged_attn")
+    return op
+
+
+def unpack(op, dst, B: int, N: int, o=None, stream=None):
+    """a4: packed O -> padded [B, N, H, d]; dropped rows +0.0."""
+    _, H, d = op.shape
+    o = torch.empty(B, N, H, d, dtype=op.dtype, device=op.device) if o is None else o
+    p = problem(B, N, H, d, op.dtype)
+    _check(lib().ragged_unpack(ctypes.byref(p), op.data_ptr(), dst.data_ptr(), o.data_ptr(),
+                              _stream(stream)), "ragged_unpack")
+    return o
+
+
+def pack_attend_unpack(q, k, v, keep, o=None, cu=None, want_cu=False, stream=None,
+                       engine=ENGINE_AUTO):
+    """a5: the fused single-launch path.  Returns o (and cu if requested)."""
+    p = _padded_problem(q, k, v, engine)
+    keep = _keep_u8(keep)
+    B, N, H, d = q.shape
+    o = torch.empty(B, N, H, d, dtype=q.dtype, device=q.device) if o is None else o
+    if want_cu and cu is None:
+        cu = torch.empty(B + 1, dtype=torch.int32, device=q.device)
+    _check(lib().ragged_pack_attend_unpack(ctypes.byref(p), keep.data_ptr(), q.data_ptr(), k.data_ptr(),
+                                          v.data_ptr(), o.data_ptr(), _ptr(cu), _stream(stream)),
+           "ragged_pack_attend_unpack")
+    return (o, cu) if (want_cu or cu is not None) else o
+
+
+class Graph:
+    """ragged_graph: one captured pack_attend_unpack with fixed pointers."""
+
+    def __init__(self, q, k, v, keep, o, cu=None, engine=ENGINE_AUTO):
+        self._p = _padded_problem(q, k, v, engine)
+        keep = _keep_u8(keep)
+        self._refs = (q, k, v, keep, o, cu)     # keep the buffers alive
+        h = ctypes.c_void_p()
+        _check(lib().ragged_graph_create(ctypes.byref(self._p), keep.data_ptr(), q.data_ptr(),
+                                        k.data_ptr(), v.data_ptr(), o.data_ptr(), _ptr(cu),
+                                        ctypes.byref(h)), "ragged_graph_create")
+        self._h = h
+
+    def launch(self, stream=None):
+        _check(lib().ragged_graph_launch(self._h, _stream(stream)), "ragged_graph_launch")
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().ragged_graph_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def empty_launch(grid: int = 1, block: int = 32, stream=None):
+    """Launch-floor probe."""
+    _check(lib().ragged_empty_launch(grid, block, _stream(stream)), "ragged_empty_launch")
+
+
+def validate_cu_seqlens(cu, total: int) -> int:
+    """SPEC validate_cu_seqlens, host only: -1 if valid, else the
+    first violating index."""
+    arr = (ctypes.c_int32 * len(cu))(*[int(x) for x in cu])
+    return int(lib().ragged_validate_cu_seqlens(arr, len(cu), int(total)))

@@ -1,0 +1,253 @@
+// api.cu -- the C ABI declared in include/ragged.h.
+//
+// Host-side work per call is argument validation only (no allocation, no
+// attribute setting after the first call, no device->host traffic): the
+// paper's diagnosis is that this host path is the bottleneck at ViT lengths
+// (P:336-345).
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "../../include/ragged.h"
+#include "launch.h"
+
+namespace {
+
+thread_local std::string g_last_error;
+
+ragged_status fail(ragged_status s, const char* what) {
+  g_last_error = what;
+  return s;
+}
+
+ragged_status cuda_fail(cudaError_t e, const char* where) {
+  g_last_error = std::string(where) + ": " + cudaGetErrorString(e);
+  return RAGGED_ECUDA;
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+// Shape / dtype / stride checks shared by every entry point.
+ragged_status check_problem(const ragged_problem* p) {
+  if (p == nullptr) return fail(RAGGED_EINVAL, "problem is NULL");
+  if (p->B < 0) return fail(RAGGED_EINVAL, "B < 0");
+  if (p->N < 1) return fail(RAGGED_EINVAL, "N < 1");
+  if (p->H < 1) return fail(RAGGED_EINVAL, "H < 1");
+  if (p->N > 256) return fail(RAGGED_ENOTSUP, "N > 256 (one-stage sequence cap, DESIGN.md R12)");
+  if (p->d != 64) return fail(RAGGED_ENOTSUP, "head_dim must be 64 (P:330-331)");
+  if (p->dtype != RAGGED_BF16 && p->dtype != RAGGED_FP16)
+    return fail(RAGGED_ENOTSUP, "dtype must be RAGGED_BF16 or RAGGED_FP16");
+  if (p->engine != RAGGED_ENGINE_AUTO && p->engine != RAGGED_ENGINE_MMA_SYNC)
+    return fail(RAGGED_ENOTSUP, "engine not compiled in this build");
+  if ((long long)p->B * p->N > 0x7fffffffLL) return fail(RAGGED_ENOTSUP, "B*N exceeds int32 indices");
+  if ((long long)p->H * 64 > (1LL << 24)) return fail(RAGGED_ENOTSUP, "H too large");
+  if (p->ld < (int64_t)p->H * p->d) return fail(RAGGED_EINVAL, "ld < H*d");
+  if (p->ld % 8 != 0) return fail(RAGGED_EALIGN, "ld % 8 != 0 (rows must be 16-byte aligned)");
+  return RAGGED_OK;
+}
+
+ragged_status check_ptr(const void* p, const char* name) {
+  static thread_local char buf[96];
+  if (p == nullptr) {
+    snprintf(buf, sizeof buf, "%s is NULL", name);
+    return fail(RAGGED_EINVAL, buf);
+  }
+  if (!aligned16(p)) {
+    snprintf(buf, sizeof buf, "%s is not 16-byte aligned", name);
+    return fail(RAGGED_EALIGN, buf);
+  }
+  return RAGGED_OK;
+}
+
+ragged_status check_ptr_any(const void* p, const char* name) {  // 1-byte / 4-byte arrays
+  static thread_local char buf[96];
+  if (p == nullptr) {
+    snprintf(buf, sizeof buf, "%s is NULL", name);
+    return fail(RAGGED_EINVAL, buf);
+  }
+  return RAGGED_OK;
+}
+
+#define RAGGED_TRY(x)                        \
+  do {                                       \
+    ragged_status _s = (x);                  \
+    if (_s != RAGGED_OK) return _s;          \
+  } while (0)
+
+cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
+
+}  // namespace
+
+struct ragged_graph {
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+};
+
+extern "C" {
+
+ragged_status ragged_scan(const ragged_problem* prob, const uint8_t* keep, int32_t* cu_seqlens,
+                          int32_t* dst_index, int32_t* src_index, void* stream) {
+  RAGGED_TRY(check_problem(prob));
+  if (prob->B == 0) return RAGGED_OK;
+  RAGGED_TRY(check_ptr_any(keep, "keep"));
+  RAGGED_TRY(check_ptr_any(cu_seqlens, "cu_seqlens"));
+  RAGGED_TRY(check_ptr_any(dst_index, "dst_index"));
+  RAGGED_TRY(check_ptr_any(src_index, "src_index"));
+  cudaError_t e = ragged::launch_scan(keep, prob->B, prob->N, cu_seqlens, dst_index, src_index,
+                                      as_stream(stream));
+  return e == cudaSuccess ? RAGGED_OK : cuda_fail(e, "ragged_scan");
+}
+
+ragged_status ragged_pack(const ragged_problem* prob, const uint8_t* keep, const void* q,
+                          const void* k, const void* v, int32_t* cu_seqlens, int32_t* dst_index,
+                          int32_t* src_index, void* qp, void* kp, void* vp, void* stream) {
+  RAGGED_TRY(check_problem(prob));
+  if (prob->B == 0) return RAGGED_OK;
+  RAGGED_TRY(check_ptr_any(keep, "keep"));
+  RAGGED_TRY(check_ptr(q, "q"));
+  RAGGED_TRY(check_ptr(k, "k"));
+  RAGGED_TRY(check_ptr(v, "v"));
+  RAGGED_TRY(check_ptr_any(cu_seqlens, "cu_seqlens"));
+  RAGGED_TRY(check_ptr_any(dst_index, "dst_index"));
+  RAGGED_TRY(check_ptr_any(src_index, "src_index"));
+  RAGGED_TRY(check_ptr(qp, "qp"));
+  RAGGED_TRY(check_ptr(kp, "kp"));
+  RAGGED_TRY(check_ptr(vp, "vp"));
+  cudaStream_t st = as_stream(stream);
+  cudaError_t e = ragged::launch_scan(keep, prob->B, prob->N, cu_seqlens, dst_index, src_index, st);
+  if (e != cudaSuccess) return cuda_fail(e, "ragged_pack/scan");
+  e = ragged::launch_pack(q, k, v, prob->ld, prob->B, prob->N, prob->H, cu_seqlens, src_index, qp,
+                          kp, vp, st);
+  return e == cudaSuccess ? RAGGED_OK : cuda_fail(e, "ragged_pack/gather");
+}
+
+ragged_status ragged_attn(const ragged_problem* prob, const void* qp, const void* kp,
+                          const void* vp, const int32_t* cu_seqlens, void* op, void* stream) {
+  RAGGED_TRY(check_problem(prob));
+  if (prob->B == 0) return RAGGED_OK;
+  RAGGED_TRY(check_ptr(qp, "qp"));
+  RAGGED_TRY(check_ptr(kp, "kp"));
+  RAGGED_TRY(check_ptr(vp, "vp"));
+  RAGGED_TRY(check_ptr_any(cu_seqlens, "cu_seqlens"));
+  RAGGED_TRY(check_ptr(op, "op"));
+  if ((long long)prob->B * prob->H > 0x7fffffffLL) return fail(RAGGED_ENOTSUP, "B*H too large");
+  cudaError_t e = ragged::launch_attn(prob->dtype, qp, kp, vp, cu_seqlens, op, prob->B, prob->N,
+                                      prob->H, as_stream(stream));
+  return e == cudaSuccess ? RAGGED_OK : cuda_fail(e, "ragged_attn");
+}
+
+ragged_status ragged_unpack(const ragged_problem* prob, const void* op, const int32_t* dst_index,
+                            void* o, void* stream) {
+  RAGGED_TRY(check_problem(prob));
+  if (prob->B == 0) return RAGGED_OK;
+  RAGGED_TRY(check_ptr(op, "op"));
+  RAGGED_TRY(check_ptr_any(dst_index, "dst_index"));
+  RAGGED_TRY(check_ptr(o, "o"));
+  cudaError_t e =
+      ragged::launch_unpack(op, dst_index, o, prob->B, prob->N, prob->H, as_stream(stream));
+  return e == cudaSuccess ? RAGGED_OK : cuda_fail(e, "ragged_unpack");
+}
+
+ragged_status ragged_pack_attend_unpack(const ragged_problem* prob, const uint8_t* keep,
+                                        const void* q, const void* k, const void* v, void* o,
+                                        int32_t* cu_seqlens_or_null, void* stream) {
+  RAGGED_TRY(check_problem(prob));
+  if (prob->B == 0) return RAGGED_OK;
+  RAGGED_TRY(check_ptr_any(keep, "keep"));
+  RAGGED_TRY(check_ptr(q, "q"));
+  RAGGED_TRY(check_ptr(k, "k"));
+  RAGGED_TRY(check_ptr(v, "v"));
+  RAGGED_TRY(check_ptr(o, "o"));
+  if ((long long)prob->B * prob->H + 1 > 0x7fffffffLL) return fail(RAGGED_ENOTSUP, "B*H too large");
+  cudaError_t e = ragged::launch_fused(prob->dtype, keep, q, k, v, prob->ld, o, cu_seqlens_or_null,
+                                       prob->B, prob->N, prob->H, as_stream(stream));
+  return e == cudaSuccess ? RAGGED_OK : cuda_fail(e, "ragged_pack_attend_unpack");
+}
+
+ragged_status ragged_graph_create(const ragged_problem* prob, const uint8_t* keep, const void* q,
+                                  const void* k, const void* v, void* o,
+                                  int32_t* cu_seqlens_or_null, ragged_graph** out) {
+  if (out == nullptr) return fail(RAGGED_EINVAL, "out is NULL");
+  *out = nullptr;
+  RAGGED_TRY(check_problem(prob));
+  cudaStream_t st = nullptr;
+  cudaError_t e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+  if (e != cudaSuccess) return cuda_fail(e, "ragged_graph_create/stream");
+  ragged_graph* g = new ragged_graph();
+  e = cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal);
+  if (e != cudaSuccess) {
+    cudaStreamDestroy(st);
+    delete g;
+    return cuda_fail(e, "ragged_graph_create/begin");
+  }
+  ragged_status s = ragged_pack_attend_unpack(prob, keep, q, k, v, o, cu_seqlens_or_null, st);
+  e = cudaStreamEndCapture(st, &g->graph);
+  cudaStreamDestroy(st);
+  if (s != RAGGED_OK) {
+    if (g->graph) cudaGraphDestroy(g->graph);
+    delete g;
+    return s;
+  }
+  if (e != cudaSuccess) {
+    delete g;
+    return cuda_fail(e, "ragged_graph_create/end");
+  }
+  e = cudaGraphInstantiate(&g->exec, g->graph, 0);
+  if (e != cudaSuccess) {
+    cudaGraphDestroy(g->graph);
+    delete g;
+    return cuda_fail(e, "ragged_graph_create/instantiate");
+  }
+  *out = g;
+  return RAGGED_OK;
+}
+
+ragged_status ragged_graph_launch(ragged_graph* graph, void* stream) {
+  if (graph == nullptr || graph->exec == nullptr) return fail(RAGGED_EINVAL, "graph is NULL");
+  cudaError_t e = cudaGraphLaunch(graph->exec, as_stream(stream));
+  return e == cudaSuccess ? RAGGED_OK : cuda_fail(e, "ragged_graph_launch");
+}
+
+void ragged_graph_destroy(ragged_graph* graph) {
+  if (graph == nullptr) return;
+  if (graph->exec) cudaGraphExecDestroy(graph->exec);
+  if (graph->graph) cudaGraphDestroy(graph->graph);
+  delete graph;
+}
+
+ragged_status ragged_empty_launch(int32_t grid, int32_t block, void* stream) {
+  if (grid < 1 || block < 1 || block > 1024) return fail(RAGGED_EINVAL, "bad grid/block");
+  cudaError_t e = ragged::launch_empty(grid, block, as_stream(stream));
+  return e == cudaSuccess ? RAGGED_OK : cuda_fail(e, "ragged_empty_launch");
+}
+
+int32_t ragged_validate_cu_seqlens(const int32_t* cu, int32_t n, int64_t total) {
+  if (cu == nullptr || n < 1) return 0;
+  if (cu[0] != 0) return 0;
+  for (int32_t i = 1; i < n; ++i)
+    if (cu[i] < cu[i - 1]) return i;
+  if ((int64_t)cu[n - 1] != total) return n - 1;
+  return -1;
+}
+
+const char* ragged_status_str(ragged_status s) {
+  switch (s) {
+    case RAGGED_OK: return "RAGGED_OK";
+    case RAGGED_EINVAL: return "RAGGED_EINVAL";
+    case RAGGED_ENOTSUP: return "RAGGED_ENOTSUP";
+    case RAGGED_EALIGN: return "RAGGED_EALIGN";
+    case RAGGED_ECUDA: return "RAGGED_ECUDA";
+  }
+  return "RAGGED_UNKNOWN";
+}
+
+const char* ragged_last_error(void) { return g_last_error.c_str(); }
+
+const char* ragged_build_info(void) {
+  return "libragged 0.1 sm_100a engines=mma_sync";
+}
+
+}  // extern "C"

@@ -1,0 +1,594 @@
+// kernels.cu -- sm_100a kernels of the pack-attend-unpack path (arxiv 2604.15408).
+//
+//   scan_kernel       a1: keep mask -> cu_seqlens, dst_index, src_index
+//   pack_kernel       a2: gather kept Q/K/V rows into packed buffers
+//   attn_kernel<.,0>  a3: ragged attention over packed rows, one CTA per
+//                         (image, head) (Alg. 1)
+//   unpack_kernel     a4: packed O -> padded O, +0.0 for dropped rows
+//   attn_kernel<.,1>  a5: fused pack-attend-unpack, one launch
+//   empty_kernel          launch-floor probe
+//
+// Design notes (DESIGN.md has the full version):
+//  * The attention CTA stages the whole short sequence's K and V head slices
+//    in shared memory (<= 256 rows x 128 B each, XOR-8 swizzled), each warp
+//    takes 16-row query slices, and QK^T / PV run on tensor cores with fp32
+//    accumulation.  Keys are consumed in 64-key chunks with Alg. 1's online
+//    softmax (running max m, sum l, rescale alpha), so registers stay bounded
+//    for any n <= 256.
+//  * P is split into hi + lo 16-bit parts and PV runs for both (R2): the
+//    stated bf16 tolerance (2e-3 vs fp64) is otherwise not met.
+//  * The fused kernel never reads dropped rows: ballot + popc ranks of the
+//    keep mask give the kept positions; the gather reads only those rows,
+//    dropped rows of O are written with zeros while the gather is in flight.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "device.cuh"
+#include "launch.h"
+
+namespace ragged {
+
+// ---------------------------------------------------------------- scan ----
+// One CTA walks the batch in rounds of CH = warps * kIPW images.  Each warp
+// ballots its images' keep bytes (<= 8 words of 32 positions), warp 0 scans
+// the per-image counts, then each warp writes dst/src of its images.
+// Deterministic: no atomics; bit-exact integer output.
+template <int kThreads, int kIPW, bool kWriteIdx>
+__device__ void scan_cta(const uint8_t* __restrict__ keep, int B, int N, int32_t* __restrict__ cu,
+                         int32_t* __restrict__ dst, int32_t* __restrict__ src, uint32_t* s_words,
+                         int32_t* s_cnt, int32_t* s_off) {
+  constexpr int kWarps = kThreads / 32;
+  constexpr int CH = kWarps * kIPW;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nw = (N + 31) >> 5;
+  const uint32_t lt = (1u << lane) - 1u;
+  __shared__ int32_t s_carry;
+  if (threadIdx.x == 0) {
+    cu[0] = 0;
+    s_carry = 0;
+  }
+  for (int base = 0; base < B; base += CH) {
+    // phase A: load keep bytes of kIPW images per warp (all loads in flight), ballot.
+    uint32_t kb[kIPW][8];
+#pragma unroll
+    for (int u = 0; u < kIPW; ++u) {
+      const int i = base + warp + kWarps * u;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int p = lane + 32 * j;
+        kb[u][j] = (i < B && j < nw && p < N) ? keep[(size_t)i * N + p] : 0u;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kIPW; ++u) {
+      const int li = warp + kWarps * u;
+      int cnt = 0;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const uint32_t w = __ballot_sync(0xffffffffu, kb[u][j] != 0u);
+        cnt += __popc(w);
+        if (lane == 0) s_words[li * 8 + j] = w;
+      }
+      if (lane == 0) s_cnt[li] = cnt;
+    }
+    __syncthreads();
+    // phase B: exclusive scan of the CH counts (warp 0), plus the running carry.
+    if (warp == 0) {
+      constexpr int PER = (CH + 31) / 32;
+      int local[PER];
+      int sum = 0;
+#pragma unroll
+      for (int e = 0; e < PER; ++e) {
+        const int li = lane * PER + e;
+        local[e] = (li < CH) ? s_cnt[li] : 0;
+        sum += local[e];
+      }
+      int incl = sum;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+      }
+      int run = s_carry + incl - sum;
+#pragma unroll
+      for (int e = 0; e < PER; ++e) {
+        const int li = lane * PER + e;
+        if (li < CH) s_off[li] = run;
+        run += local[e];
+      }
+      const int total = __shfl_sync(0xffffffffu, incl, 31);
+      __syncwarp();
+      if (lane == 0) s_carry += total;
+    }
+    __syncthreads();
+    // phase C: cu[i+1], and per-token dst / src.
+#pragma unroll
+    for (int u = 0; u < kIPW; ++u) {
+      const int li = warp + kWarps * u;
+      const int i = base + li;
+      if (i >= B) break;
+      const int off = s_off[li];
+      if (lane == 0) cu[i + 1] = off + s_cnt[li];
+      if constexpr (kWriteIdx) {
+        int pre = 0;
+        for (int j = 0; j < nw; ++j) {
+          const uint32_t w = s_words[li * 8 + j];
+          const int p = lane + 32 * j;
+          if (p < N) {
+            const bool kept = (w >> lane) & 1u;
+            const int r = off + pre + __popc(w & lt);
+            dst[(size_t)i * N + p] = kept ? r : -1;
+            if (kept) src[r] = i * N + p;
+          }
+          pre += __popc(w);
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
+constexpr int kScanThreads = 1024;
+constexpr int kScanIPW = 4;
+
+__global__ void __launch_bounds__(kScanThreads, 1)
+    scan_kernel(const uint8_t* __restrict__ keep, int B, int N, int32_t* __restrict__ cu,
+                int32_t* __restrict__ dst, int32_t* __restrict__ src) {
+  constexpr int CH = kScanThreads / 32 * kScanIPW;
+  __shared__ uint32_t s_words[CH * 8];
+  __shared__ int32_t s_cnt[CH];
+  __shared__ int32_t s_off[CH];
+  scan_cta<kScanThreads, kScanIPW, true>(keep, B, N, cu, dst, src, s_words, s_cnt, s_off);
+}
+
+// ---------------------------------------------------------------- pack ----
+// Gather form over packed rows r < T = cu[B] (read on the device): each row
+// is 3 tensors x (H*d*2 / 16) 16-byte chunks; a grid-stride loop over rows in
+// groups of kPackRows, U chunks in flight per thread.
+constexpr int kCopyThreads = 256;
+constexpr int kPackRows = 4;
+constexpr int kCopyUnroll = 4;
+
+__global__ void __launch_bounds__(kCopyThreads)
+    pack_kernel(const uint8_t* __restrict__ q, const uint8_t* __restrict__ k,
+                const uint8_t* __restrict__ v, const int32_t* __restrict__ cu,
+                const int32_t* __restrict__ src, uint8_t* __restrict__ qp, uint8_t* __restrict__ kp,
+                uint8_t* __restrict__ vp, int B, long long ld_bytes, int row_bytes) {
+  const int T = cu[B];
+  const int cpr = row_bytes >> 4;  // chunks per tensor row
+  const int per_row = 3 * cpr;
+  for (long long r0 = (long long)blockIdx.x * kPackRows; r0 < T;
+       r0 += (long long)gridDim.x * kPackRows) {
+    const int rows = (int)(kPackRows < (T - r0) ? (long long)(kPackRows) : (long long)(T - r0));
+    const int total = rows * per_row;
+    for (int f0 = threadIdx.x; f0 < total; f0 += kCopyThreads * kCopyUnroll) {
+      uint4 val[kCopyUnroll];
+      uint8_t* dptr[kCopyUnroll];
+#pragma unroll
+      for (int u = 0; u < kCopyUnroll; ++u) {
+        const int f = f0 + u * kCopyThreads;
+        dptr[u] = nullptr;
+        if (f < total) {
+          const int rl = f / per_row, rem = f - rl * per_row;
+          const int t = rem / cpr, c = rem - t * cpr;
+          const long long r = r0 + rl;
+          const long long s = src[r];
+          const uint8_t* g = t == 0 ? q : (t == 1 ? k : v);
+          uint8_t* p = t == 0 ? qp : (t == 1 ? kp : vp);
+          val[u] = ld_global_nc_16(g + s * ld_bytes + c * 16);
+          dptr[u] = p + r * row_bytes + c * 16;
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kCopyUnroll; ++u)
+        if (dptr[u]) st_global_16(dptr[u], val[u]);
+    }
+  }
+}
+
+// -------------------------------------------------------------- unpack ----
+constexpr int kUnpackRows = 4;
+
+__global__ void __launch_bounds__(kCopyThreads)
+    unpack_kernel(const uint8_t* __restrict__ op, const int32_t* __restrict__ dst,
+                  uint8_t* __restrict__ o, long long BN, int row_bytes) {
+  const int cpr = row_bytes >> 4;
+  for (long long r0 = (long long)blockIdx.x * kUnpackRows; r0 < BN;
+       r0 += (long long)gridDim.x * kUnpackRows) {
+    const int rows = (int)(kUnpackRows < (BN - r0) ? (long long)(kUnpackRows) : (long long)(BN - r0));
+    const int total = rows * cpr;
+    for (int f0 = threadIdx.x; f0 < total; f0 += kCopyThreads * kCopyUnroll) {
+      uint4 val[kCopyUnroll];
+      uint8_t* dptr[kCopyUnroll];
+#pragma unroll
+      for (int u = 0; u < kCopyUnroll; ++u) {
+        const int f = f0 + u * kCopyThreads;
+        dptr[u] = nullptr;
+        if (f < total) {
+          const int rl = f / cpr, c = f - rl * cpr;
+          const long long i = r0 + rl;
+          const int j = dst[i];
+          val[u] = j >= 0 ? ld_global_nc_16(op + (long long)j * row_bytes + c * 16)
+                          : make_uint4(0u, 0u, 0u, 0u);
+          dptr[u] = o + i * row_bytes + c * 16;
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kCopyUnroll; ++u)
+        if (dptr[u]) st_global_16(dptr[u], val[u]);
+    }
+  }
+}
+
+// ----------------------------------------------------------- attention ----
+constexpr int kAttnThreads = 128;  // 4 warps, 16 query rows each per slice
+constexpr int kQBufBytes = 16 * kRowBytes;                  // one 16-row slice
+constexpr int kQAreaBytes = (kAttnThreads / 32) * 2 * kQBufBytes;  // double-buffered per warp
+
+__host__ __device__ inline int attn_rows_cap(int N) { return (N + 15) & ~15; }
+__host__ __device__ inline int attn_smem_bytes(int N) {
+  return 2 * attn_rows_cap(N) * kRowBytes + kQAreaBytes + 2 * kMaxN * 2 + 8 * 4;
+}
+
+struct AttnArgs {
+  const uint8_t* keep;     // fused: keep mask [B, N]
+  const void* q;           // fused: padded [B,N,H,d] (token stride ld); attn: packed [cap,H,d]
+  const void* k;
+  const void* v;
+  void* o;                 // fused: padded O; attn: packed O
+  const int32_t* cu;       // attn: cu_seqlens input
+  int32_t* cu_out;         // fused: optional cu_seqlens output (block 0 computes it)
+  int B, N, H;
+  long long ld;            // input token stride in elements
+};
+
+template <typename T, bool kFused>
+__global__ void __launch_bounds__(kAttnThreads, 3) attn_kernel(const AttnArgs a) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int rows_cap = attn_rows_cap(a.N);
+  uint8_t* sK = smem;
+  uint8_t* sV = sK + rows_cap * kRowBytes;
+  uint8_t* sQ = sV + rows_cap * kRowBytes;
+  int16_t* sPos = reinterpret_cast<int16_t*>(sQ + kQAreaBytes);
+  int16_t* sDrop = sPos + kMaxN;
+  uint32_t* sWords = reinterpret_cast<uint32_t*>(sDrop + kMaxN);
+
+  int bid = blockIdx.x;
+  if constexpr (kFused) {
+    if (a.cu_out != nullptr) {
+      if (bid == 0) {  // the scan CTA: cu_seqlens only, concurrent with the rest
+        constexpr int CH = kAttnThreads / 32 * 8;
+        uint32_t* w = reinterpret_cast<uint32_t*>(sK);
+        int32_t* c = reinterpret_cast<int32_t*>(w + CH * 8);
+        scan_cta<kAttnThreads, 8, false>(a.keep, a.B, a.N, a.cu_out, nullptr, nullptr, w, c, c + CH);
+        return;
+      }
+      bid -= 1;
+    }
+  }
+  const int b = bid / a.H, h = bid - b * a.H;   // head fastest
+  const long long HD = (long long)a.H * kHeadDim;
+  const T* gq = static_cast<const T*>(a.q);
+  const T* gk = static_cast<const T*>(a.k);
+  const T* gv = static_cast<const T*>(a.v);
+  T* go = static_cast<T*>(a.o);
+
+  int n;
+  long long row_base;
+  if constexpr (kFused) {
+    // keep mask row -> ballots -> kept ranks / dropped ranks (no global prefix needed)
+    const uint8_t* km = a.keep + (long long)b * a.N;
+    const int p0 = tid, p1 = tid + kAttnThreads;
+    const bool k0 = p0 < a.N && km[p0] != 0;
+    const bool k1 = p1 < a.N && km[p1] != 0;
+    const uint32_t w0 = __ballot_sync(0xffffffffu, k0);
+    const uint32_t w1 = __ballot_sync(0xffffffffu, k1);
+    if (lane == 0) {
+      sWords[warp] = w0;
+      sWords[4 + warp] = w1;
+    }
+    __syncthreads();
+    int pre0 = 0, pre1 = 0;
+    n = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int c = __popc(sWords[j]);
+      pre0 += j < warp ? c : 0;
+      pre1 += j < 4 + warp ? c : 0;
+      n += c;
+    }
+    const uint32_t lt = (1u << lane) - 1u;
+    const int r0 = pre0 + __popc(w0 & lt);
+    const int r1 = pre1 + __popc(w1 & lt);
+    if (p0 < a.N) {
+      if (k0) sPos[r0] = (int16_t)p0; else sDrop[p0 - r0] = (int16_t)p0;
+    }
+    if (p1 < a.N) {
+      if (k1) sPos[r1] = (int16_t)p1; else sDrop[p1 - r1] = (int16_t)p1;
+    }
+    row_base = (long long)b * a.N;
+    __syncthreads();
+  } else {
+    const int s = a.cu[b];
+    n = min(max(a.cu[b + 1] - s, 0), a.N);
+    row_base = s;
+    for (int r = tid; r < kMaxN; r += kAttnThreads) sPos[r] = (int16_t)r;
+    __syncthreads();
+  }
+  const long long ld_in = kFused ? a.ld : HD;
+
+  // ---- stage K, V (rows [0, n16), zero-filled past n) and each warp's first Q slice
+  const int n16 = (n + 15) & ~15;
+  for (int idx = tid; idx < n16 * 16; idx += kAttnThreads) {
+    const int r = idx >> 4, t = (idx >> 3) & 1, c = idx & 7;
+    const T* g = t ? gv : gk;
+    const bool valid = r < n;
+    const T* srcp = valid ? g + (row_base + sPos[r]) * ld_in + h * kHeadDim + c * 8 : g;
+    cp_async_16(smem_u32((t ? sV : sK) + swz(r, c)), srcp, valid ? 16 : 0);
+  }
+  uint8_t* const qwarp = sQ + warp * 2 * kQBufBytes;  // this warp's two 16-row Q buffers
+  auto load_q = [&](uint8_t* buf, int slice) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int rr = (lane >> 3) + 4 * i, c = lane & 7, r = slice * 16 + rr;
+      const bool valid = r < n;
+      const T* srcp = valid ? gq + (row_base + sPos[r]) * ld_in + h * kHeadDim + c * 8 : gq;
+      cp_async_16(smem_u32(buf + swz(rr, c)), srcp, valid ? 16 : 0);
+    }
+  };
+  if (warp * 16 < n) load_q(qwarp, warp);
+  cp_async_commit();
+
+  if constexpr (kFused) {
+    // dropped rows of this head -> +0.0, overlapped with the gather in flight
+    const int nd = a.N - n;
+    const uint4 z = make_uint4(0u, 0u, 0u, 0u);
+    for (int idx = tid; idx < nd * 8; idx += kAttnThreads) {
+      const int row = sDrop[idx >> 3], c = idx & 7;
+      st_global_16(go + (row_base + row) * HD + h * kHeadDim + c * 8, z);
+    }
+  }
+  cp_async_wait_all();
+  __syncthreads();
+
+  // ---- per-warp query slices: S = Q K^T, online softmax (Alg. 1), O += P V
+  const int g = lane >> 2, t4 = lane & 3;
+  constexpr float kScaleLog2 = 0.18033688011112042f;  // log2(e) / sqrt(64)
+  int buf = 0;
+  for (int slice = warp; slice * 16 < n; slice += 4) {
+    uint8_t* qcur = qwarp + buf * kQBufBytes;
+    uint32_t qf[4][4];
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk)
+      ldmatrix_x4(smem_u32(qcur + swz(lane & 15, 2 * kk + (lane >> 4))), qf[kk][0], qf[kk][1],
+                  qf[kk][2], qf[kk][3]);
+    if ((slice + 4) * 16 < n) load_q(qwarp + (buf ^ 1) * kQBufBytes, slice + 4);
+    cp_async_commit();
+
+    float o[8][4];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) o[j][0] = o[j][1] = o[j][2] = o[j][3] = 0.f;
+    float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
+
+    for (int cb = 0; cb < n; cb += 64) {
+      const int nv = min(64, n - cb);
+      const int nt = (nv + 7) >> 3;
+      float s[8][4];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        s[j][0] = s[j][1] = s[j][2] = s[j][3] = 0.f;
+        if (j < nt) {
+          uint32_t kb[8];
+          const int kr = cb + 8 * j + (lane & 7);
+          ldmatrix_x4(smem_u32(sK + swz(kr, lane >> 3)), kb[0], kb[1], kb[2], kb[3]);
+          ldmatrix_x4(smem_u32(sK + swz(kr, 4 + (lane >> 3))), kb[4], kb[5], kb[6], kb[7]);
+          mma_16816<T>(s[j], qf[0], kb[0], kb[1]);
+          mma_16816<T>(s[j], qf[1], kb[2], kb[3]);
+          mma_16816<T>(s[j], qf[2], kb[4], kb[5]);
+          mma_16816<T>(s[j], qf[3], kb[6], kb[7]);
+        }
+      }
+      // scale to log2 units, mask key columns >= n (R4), row max over the quad
+      float mx0 = -INFINITY, mx1 = -INFINITY;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int col = cb + 8 * j + 2 * t4 + (e & 1);
+          const float val = (j < nt && col < n) ? s[j][e] * kScaleLog2 : -INFINITY;
+          s[j][e] = val;
+        }
+        mx0 = fmaxf(mx0, fmaxf(s[j][0], s[j][1]));
+        mx1 = fmaxf(mx1, fmaxf(s[j][2], s[j][3]));
+      }
+      mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 1));
+      mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 2));
+      mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 1));
+      mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 2));
+      const float mn0 = fmaxf(m0, mx0), mn1 = fmaxf(m1, mx1);
+      const float al0 = ex2(m0 - mn0), al1 = ex2(m1 - mn1);  // alpha = e^{m - m'}
+      m0 = mn0;
+      m1 = mn1;
+      l0 *= al0;
+      l1 *= al1;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        o[j][0] *= al0;
+        o[j][1] *= al0;
+        o[j][2] *= al1;
+        o[j][3] *= al1;
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {  // P = e^{S - m'}
+        s[j][0] = ex2(s[j][0] - mn0);
+        s[j][1] = ex2(s[j][1] - mn0);
+        s[j][2] = ex2(s[j][2] - mn1);
+        s[j][3] = ex2(s[j][3] - mn1);
+        l0 += s[j][0] + s[j][1];
+        l1 += s[j][2] + s[j][3];
+      }
+      // O += P_hi V + P_lo V
+      const int nk = (nv + 15) >> 4;
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) {
+        if (kk < nk) {
+          uint32_t ah[4], al[4];
+          split2<T>(s[2 * kk][0], s[2 * kk][1], ah[0], al[0]);
+          split2<T>(s[2 * kk][2], s[2 * kk][3], ah[1], al[1]);
+          split2<T>(s[2 * kk + 1][0], s[2 * kk + 1][1], ah[2], al[2]);
+          split2<T>(s[2 * kk + 1][2], s[2 * kk + 1][3], ah[3], al[3]);
+#pragma unroll
+          for (int jp = 0; jp < 4; ++jp) {
+            uint32_t vb[4];
+            ldmatrix_x4_trans(smem_u32(sV + swz(cb + 16 * kk + (lane & 15), 2 * jp + (lane >> 4))),
+                              vb[0], vb[1], vb[2], vb[3]);
+            mma_16816<T>(o[2 * jp], ah, vb[0], vb[1]);
+            mma_16816<T>(o[2 * jp], al, vb[0], vb[1]);
+            mma_16816<T>(o[2 * jp + 1], ah, vb[2], vb[3]);
+            mma_16816<T>(o[2 * jp + 1], al, vb[2], vb[3]);
+          }
+        }
+      }
+    }
+    l0 += __shfl_xor_sync(0xffffffffu, l0, 1);
+    l0 += __shfl_xor_sync(0xffffffffu, l0, 2);
+    l1 += __shfl_xor_sync(0xffffffffu, l1, 1);
+    l1 += __shfl_xor_sync(0xffffffffu, l1, 2);
+    const float inv0 = 1.f / l0, inv1 = 1.f / l1;
+
+    // epilogue: o / l -> 16-bit (RNE) -> swizzled smem (this warp's consumed Q
+    // buffer) -> coalesced 16-byte stores of whole 128-byte head rows.
+    __syncwarp();
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      *reinterpret_cast<uint32_t*>(qcur + swz(g, j) + 4 * t4) =
+          pack2<T>(o[j][0] * inv0, o[j][1] * inv0);
+      *reinterpret_cast<uint32_t*>(qcur + swz(g + 8, j) + 4 * t4) =
+          pack2<T>(o[j][2] * inv1, o[j][3] * inv1);
+    }
+    __syncwarp();
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int rr = (lane >> 3) + 4 * i, c = lane & 7, r = slice * 16 + rr;
+      if (r < n) {
+        const uint4 val = *reinterpret_cast<const uint4*>(qcur + swz(rr, c));
+        st_global_16(go + (row_base + sPos[r]) * HD + h * kHeadDim + c * 8, val);
+      }
+    }
+    cp_async_wait_all();
+    __syncwarp();
+    buf ^= 1;
+  }
+}
+
+__global__ void empty_kernel() {}
+
+// --------------------------------------------------------------- launch ----
+static int sm_count(int dev) {
+  static int cache[64] = {0};
+  if (dev < 0 || dev >= 64) return 148;
+  if (cache[dev] == 0) {
+    int v = 148;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    cache[dev] = v;
+  }
+  return cache[dev];
+}
+
+
+cudaError_t launch_scan(const uint8_t* keep, int B, int N, int32_t* cu, int32_t* dst, int32_t* src,
+                        cudaStream_t st) {
+  scan_kernel<<<1, kScanThreads, 0, st>>>(keep, B, N, cu, dst, src);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_pack(const void* q, const void* k, const void* v, long long ld_elems, int B, int N,
+                        int H, const int32_t* cu, const int32_t* src, void* qp, void* kp, void* vp,
+                        cudaStream_t st) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const long long cap_rows = (long long)B * N;
+  const long long want = (cap_rows + kPackRows - 1) / kPackRows;
+  const int grid = (int)(want < ((long long)sm_count(dev) * 8) ? (long long)(want) : (long long)((long long)sm_count(dev) * 8));
+  pack_kernel<<<grid, kCopyThreads, 0, st>>>(
+      static_cast<const uint8_t*>(q), static_cast<const uint8_t*>(k),
+      static_cast<const uint8_t*>(v), cu, src, static_cast<uint8_t*>(qp),
+      static_cast<uint8_t*>(kp), static_cast<uint8_t*>(vp), B, ld_elems * 2, H * kHeadDim * 2);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_unpack(const void* op, const int32_t* dst, void* o, int B, int N, int H,
+                          cudaStream_t st) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const long long BN = (long long)B * N;
+  const long long want = (BN + kUnpackRows - 1) / kUnpackRows;
+  const int grid = (int)(want < ((long long)sm_count(dev) * 8) ? (long long)(want) : (long long)((long long)sm_count(dev) * 8));
+  unpack_kernel<<<grid, kCopyThreads, 0, st>>>(static_cast<const uint8_t*>(op), dst,
+                                               static_cast<uint8_t*>(o), BN, H * kHeadDim * 2);
+  return cudaGetLastError();
+}
+
+template <typename T, bool kFused>
+static cudaError_t launch_attn_t(const AttnArgs& a, int grid, cudaStream_t st) {
+  // The max-dynamic-smem attribute is set once per device (for N = 256, which
+  // covers every N), so the steady-state launch path does no attribute work.
+  static bool done[64] = {false};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64 || !done[dev]) {
+    cudaError_t e = cudaFuncSetAttribute(attn_kernel<T, kFused>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         attn_smem_bytes(kMaxN));
+    if (e != cudaSuccess) return e;
+    if (dev >= 0 && dev < 64) done[dev] = true;
+  }
+  attn_kernel<T, kFused><<<grid, kAttnThreads, attn_smem_bytes(a.N), st>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_attn(int dtype, const void* qp, const void* kp, const void* vp, const int32_t* cu,
+                        void* op, int B, int N, int H, cudaStream_t st) {
+  AttnArgs a{};
+  a.q = qp;
+  a.k = kp;
+  a.v = vp;
+  a.o = op;
+  a.cu = cu;
+  a.B = B;
+  a.N = N;
+  a.H = H;
+  a.ld = (long long)H * kHeadDim;
+  const int grid = B * H;
+  return dtype == 0 ? launch_attn_t<__nv_bfloat16, false>(a, grid, st)
+                    : launch_attn_t<__half, false>(a, grid, st);
+}
+
+cudaError_t launch_fused(int dtype, const uint8_t* keep, const void* q, const void* k,
+                         const void* v, long long ld, void* o, int32_t* cu_out, int B, int N, int H,
+                         cudaStream_t st) {
+  AttnArgs a{};
+  a.keep = keep;
+  a.q = q;
+  a.k = k;
+  a.v = v;
+  a.o = o;
+  a.cu_out = cu_out;
+  a.B = B;
+  a.N = N;
+  a.H = H;
+  a.ld = ld;
+  const int grid = B * H + (cu_out ? 1 : 0);
+  return dtype == 0 ? launch_attn_t<__nv_bfloat16, true>(a, grid, st)
+                    : launch_attn_t<__half, true>(a, grid, st);
+}
+
+cudaError_t launch_empty(int grid, int block, cudaStream_t st) {
+  empty_kernel<<<grid, block, 0, st>>>();
+  return cudaGetLastError();
+}
+
+int fused_smem_bytes(int N) { return attn_smem_bytes(N); }
+
+}  // namespace ragged

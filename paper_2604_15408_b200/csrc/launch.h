@@ -1,0 +1,23 @@
+// launch.h -- internal host launchers (kernels.cu) used by the C ABI (api.cu).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace ragged {
+
+cudaError_t launch_scan(const uint8_t* keep, int B, int N, int32_t* cu, int32_t* dst, int32_t* src,
+                        cudaStream_t st);
+cudaError_t launch_pack(const void* q, const void* k, const void* v, long long ld_elems, int B, int N,
+                        int H, const int32_t* cu, const int32_t* src, void* qp, void* kp, void* vp,
+                        cudaStream_t st);
+cudaError_t launch_attn(int dtype, const void* qp, const void* kp, const void* vp, const int32_t* cu,
+                        void* op, int B, int N, int H, cudaStream_t st);
+cudaError_t launch_unpack(const void* op, const int32_t* dst, void* o, int B, int N, int H,
+                          cudaStream_t st);
+cudaError_t launch_fused(int dtype, const uint8_t* keep, const void* q, const void* k,
+                         const void* v, long long ld, void* o, int32_t* cu_out, int B, int N, int H,
+                         cudaStream_t st);
+cudaError_t launch_empty(int grid, int block, cudaStream_t st);
+int fused_smem_bytes(int N);
+
+}  // namespace ragged

@@ -1,0 +1,123 @@
+"""C-ABI checks that need no GPU: the library loads, exports every entry point
+include/ragged.h declares, and rejects every host-checkable bad argument with
+the documented status BEFORE touching CUDA."""
+import ctypes
+import json
+import os
+import re
+import subprocess
+
+import pytest
+
+from conftest import GOLDEN, ROOT
+
+rb = pytest.importorskip("paper_2604_15408_b200")
+
+
+def _declared():
+    src = open(os.path.join(ROOT, "include", "ragged.h")).read()
+    return sorted(set(re.findall(r"^\s*RAGGED_API\s+(?:ragged_status|void|int32_t|const char\*)\s+(ragged_\w+)\(",
+                                 src, re.M)))
+
+
+def test_header_and_library_exports_agree():
+    names = _declared()
+    assert len(names) >= 12
+    for n in names:
+        assert hasattr(rb.lib(), n), n
+    assert set(names) == set(rb.EXPORTS)
+    out = subprocess.run(["nm", "-D", "--defined-only", rb.LIB_PATH], capture_output=True, text=True).stdout
+    exported = set(re.findall(r"\b(ragged_\w+)\b", out))
+    assert set(names) <= exported
+    assert not [s for s in exported if s not in names], "undeclared ragged_* symbols exported"
+
+
+def test_library_targets_sm100a():
+    out = subprocess.run(["cuobjdump", "--list-elf", rb.LIB_PATH], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+    assert "sm_100a" in rb.build_info()
+
+
+def test_status_strings():
+    for code, name in [(0, "RAGGED_OK"), (1, "RAGGED_EINVAL"), (2, "RAGGED_ENOTSUP"), (3, "RAGGED_EALIGN"),
+                       (4, "RAGGED_ECUDA")]:
+        assert rb.status_str(code) == name
+    assert rb.status_str(99) == "RAGGED_UNKNOWN"
+
+
+FAKE = 0x10000  # 16-byte aligned, never dereferenced (validation fails or B == 0 first)
+
+
+def _call_fused(p, keep=FAKE, q=FAKE, k=FAKE, v=FAKE, o=FAKE):
+    return rb.lib().ragged_pack_attend_unpack(ctypes.byref(p), keep, q, k, v, o, None, None)
+
+
+@pytest.mark.parametrize("field,value,status", [
+    ("B", -1, rb.EINVAL), ("N", 0, rb.EINVAL), ("H", 0, rb.EINVAL), ("N", 257, rb.ENOTSUP),
+    ("d", 128, rb.ENOTSUP), ("dtype", 7, rb.ENOTSUP), ("engine", 9, rb.ENOTSUP),
+    ("ld", 100, rb.EINVAL), ("ld", 772, rb.EALIGN),
+])
+def test_problem_validation(field, value, status):
+    p = rb.problem(4, 197, 12)
+    setattr(p, field, value)
+    assert _call_fused(p) == status
+    assert rb.last_error() != ""
+
+
+def test_pointer_validation():
+    p = rb.problem(4, 197, 12)
+    assert _call_fused(p, q=0) == rb.EINVAL
+    assert _call_fused(p, keep=0) == rb.EINVAL
+    assert _call_fused(p, o=FAKE + 2) == rb.EALIGN
+    assert rb.lib().ragged_attn(ctypes.byref(p), FAKE, FAKE, FAKE + 8, FAKE, FAKE, None) == rb.EALIGN
+    assert rb.lib().ragged_unpack(ctypes.byref(p), FAKE, None, FAKE, None) == rb.EINVAL
+    assert rb.lib().ragged_scan(ctypes.byref(p), FAKE, None, FAKE, FAKE, None) == rb.EINVAL
+    assert rb.lib().ragged_pack(ctypes.byref(p), FAKE, FAKE, FAKE, FAKE, FAKE, FAKE, FAKE,
+                                FAKE, FAKE, FAKE + 4, None) == rb.EALIGN
+    assert rb.lib().ragged_scan(None, FAKE, FAKE, FAKE, FAKE, None) == rb.EINVAL
+    h = ctypes.c_void_p()
+    assert rb.lib().ragged_graph_create(None, FAKE, FAKE, FAKE, FAKE, FAKE, None, ctypes.byref(h)) == rb.EINVAL
+    assert rb.lib().ragged_graph_create(ctypes.byref(p), FAKE, FAKE, FAKE, FAKE, FAKE, None, None) == rb.EINVAL
+    assert rb.lib().ragged_graph_launch(None, None) == rb.EINVAL
+    rb.lib().ragged_graph_destroy(None)
+    assert rb.lib().ragged_empty_launch(0, 32, None) == rb.EINVAL
+
+
+def test_empty_batch_is_noop_without_cuda():
+    """B == 0 returns OK and launches nothing (no CUDA device here)."""
+    p = rb.problem(0, 197, 12)
+    assert _call_fused(p, q=0, k=0, v=0, o=0, keep=0) == rb.OK
+    assert rb.lib().ragged_scan(ctypes.byref(p), None, None, None, None, None) == rb.OK
+    assert rb.lib().ragged_attn(ctypes.byref(p), None, None, None, None, None, None) == rb.OK
+
+
+def test_validate_cu_seqlens_spec_examples():
+    g = json.load(open(os.path.join(GOLDEN, "spec_scan_examples.json")))
+    for c in g["valid_cu"]:
+        assert rb.validate_cu_seqlens(c["cu"], c["T"]) == -1
+    assert rb.validate_cu_seqlens([0, 5, 3], 3) == 2          # non-monotone at index 2
+    assert rb.validate_cu_seqlens([1, 5], 5) == 0
+    assert rb.validate_cu_seqlens([0, 5, 6], 7) == 2
+
+
+def test_python_binding_rejects_bad_layouts():
+    import torch
+    q = torch.zeros(2, 5, 3, 64, dtype=torch.float32)
+    with pytest.raises(ValueError):
+        rb.pack_attend_unpack(q, q, q, torch.ones(2, 5, dtype=torch.uint8))
+    qb = torch.zeros(2, 5, 3, 64, dtype=torch.bfloat16)
+    with pytest.raises(ValueError):
+        rb.pack_attend_unpack(qb, qb.transpose(0, 1).contiguous().transpose(0, 1), qb,
+                              torch.ones(2, 5, dtype=torch.uint8))
+    with pytest.raises(ValueError):
+        rb.pack_attend_unpack(qb, qb, qb, torch.ones(2, 5, dtype=torch.int32))
+
+
+def test_product_package_does_not_import_oracle():
+    """The product path never routes through the oracle (no CPU fallback)."""
+    pkg = os.path.join(ROOT, "paper_2604_15408_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
+                txt = open(os.path.join(dirpath, f)).read()
+                assert "oracle" not in re.sub(r"#.*|//.*", "", txt).replace("oracle/", ""), f

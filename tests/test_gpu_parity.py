@@ -1,0 +1,271 @@
+"""GPU parity: the CUDA path (through the C ABI) against the fp64 oracle.
+
+Integers (cu_seqlens, dst, src) and copies (pack, unpack) must be bit-exact;
+attention within max-abs 2e-3 (bf16) / 5e-4 (fp16) of fp64 (BASELINE.json
+north_star; R2).  Sizes span several tiles and ragged tails (n up to
+256, partial 16/64-row tiles, empty images); the BASELINE configs C1, C3, C4
+are compared in full, C5 (B = 4096) on sampled (image, head) problems plus
+properties that hold at any size."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+from helpers import TOL, bits, check_attention, fused_oracle, to_np
+
+rb = pytest.importorskip("paper_2604_15408_b200")
+pytestmark = pytest.mark.gpu
+DEV = "cuda"
+DT = {"bf16": torch.bfloat16, "fp16": torch.float16}
+
+
+def _dev(*ts):
+    return [t.to(DEV) for t in ts]
+
+
+# ------------------------------------------------------------------ scan ----
+
+def _scan_case(keep_np):
+    keep = torch.from_numpy(keep_np).to(DEV)
+    cu, dst, src = rb.scan(keep)
+    torch.cuda.synchronize()
+    rcu, rdst, rsrc = oracle.scan(keep_np)
+    T = int(rcu[-1])
+    assert cu.cpu().numpy().tolist() == rcu.tolist()
+    assert dst.cpu().numpy().tolist() == rdst.tolist()
+    assert src[:T].cpu().numpy().tolist() == rsrc[:T].tolist()
+
+
+def test_scan_spec_example():
+    _scan_case(np.array([[1, 0, 1], [1, 1, 1]], np.uint8))
+
+
+@pytest.mark.parametrize("B,N", [(1, 1), (3, 7), (5, 31), (4, 32), (7, 33), (32, 197), (33, 256),
+                                 (130, 197), (257, 64), (1000, 197)])
+def test_scan_random_masks(B, N):
+    rng = np.random.default_rng(B * 1000 + N)
+    keep = (rng.random((B, N)) < rng.uniform(0.05, 0.95)).astype(np.uint8)
+    keep[rng.random(B) < 0.1] = 0                      # empty images (R11)
+    keep[keep == 1] = rng.integers(1, 255, size=int(keep.sum()), dtype=np.uint8)  # nonzero = keep
+    _scan_case(keep)
+
+
+def test_scan_c5_scale_exact():
+    keep = synth.mask_threshold_l2(4096, 197, synth.kept_tokens(197, 0.7), seed=1000)
+    _scan_case(keep)
+
+
+# ------------------------------------------------------------------ pack ----
+
+@pytest.mark.parametrize("dtype", ["bf16", "fp16"])
+@pytest.mark.parametrize("B,N,H,p", [(4, 197, 3, 0.5), (3, 33, 2, 0.3), (32, 197, 12, 0.8), (2, 256, 4, 0.0)])
+def test_pack_bitwise(dtype, B, N, H, p):
+    q, k, v, keep = synth.make_inputs(B, N, H, p, "l2", dtype, seed=1)
+    qd, kd, vd, keepd = _dev(q, k, v, keep)
+    qp, kp, vp, cu, dst, src = rb.pack(qd, kd, vd, keepd)
+    torch.cuda.synchronize()
+    rcu, rdst, rsrc = oracle.scan(keep.numpy())
+    T = int(rcu[-1])
+    assert cu.cpu().tolist() == rcu.tolist()
+    for got, x in ((qp, q), (kp, k), (vp, v)):
+        assert np.array_equal(bits(got[:T]), oracle.pack(bits(x), rsrc, T))
+
+
+def test_pack_fused_qkv_layout():
+    """ld = 3*H*d: q/k/v are views of one [B, N, 3, H, d] buffer."""
+    B, N, H = 5, 197, 6
+    qkv = torch.randn(B, N, 3, H, 64, generator=torch.Generator().manual_seed(3)).to(torch.bfloat16)
+    keep = torch.from_numpy(synth.mask_random(B, N, 50, seed=4))
+    d = qkv.to(DEV)
+    q, k, v = d[:, :, 0], d[:, :, 1], d[:, :, 2]
+    assert q.stride(1) == 3 * H * 64
+    qp, kp, vp, cu, dst, src = rb.pack(q, k, v, keep.to(DEV))
+    o = rb.pack_attend_unpack(q, k, v, keep.to(DEV))
+    torch.cuda.synchronize()
+    rcu, _, rsrc = oracle.scan(keep.numpy())
+    T = int(rcu[-1])
+    assert np.array_equal(bits(kp[:T]), oracle.pack(bits(qkv[:, :, 1]), rsrc, T))
+    ref, _ = fused_oracle(qkv[:, :, 0], qkv[:, :, 1], qkv[:, :, 2], keep)
+    check_attention(to_np(o), ref, torch.bfloat16, vmax=float(qkv[:, :, 2].float().abs().max()), dist="heavy")
+
+
+# ------------------------------------------------------------- attention ----
+
+def _attn_case(B, N, H, p, method, dtype, seed, dist="standard"):
+    q, k, v, keep = synth.make_inputs(B, N, H, p, method, dtype, seed=seed, dist=dist)
+    qd, kd, vd, keepd = _dev(q, k, v, keep)
+    qp, kp, vp, cu, dst, src = rb.pack(qd, kd, vd, keepd)
+    op = rb.attn(qp, kp, vp, cu, N)
+    torch.cuda.synchronize()
+    rcu, rdst, rsrc = oracle.scan(keep.numpy())
+    T = int(rcu[-1])
+    f64 = [oracle.as_f64(t) for t in (q, k, v)]
+    ref = oracle.attention(*(oracle.pack(t, rsrc, T) for t in f64), rcu)
+    return check_attention(to_np(op[:T]), ref, DT[dtype], vmax=float(v.float().abs().max()), dist=dist)
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "fp16"])
+@pytest.mark.parametrize("B,N,H,p,method", [
+    (4, 197, 3, 0.5, "l2"),          # C1
+    (6, 197, 2, 0.0, "all"),         # n = 197: 4 kv chunks, 13 query slices, tail 5
+    (5, 256, 2, 0.0, "all"),         # maximum N
+    (8, 130, 2, 0.5, "random"),      # n = 65: tail of one row
+    (8, 129, 3, 0.1, "ats"),         # heterogeneous lengths
+    (9, 40, 4, 0.6, "dynamicvit"),
+    (3, 17, 2, 0.0, "all"),          # n = 17
+])
+def test_attn_matches_oracle(dtype, B, N, H, p, method):
+    _attn_case(B, N, H, p, method, dtype, seed=2)
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "fp16"])
+@pytest.mark.parametrize("dist", ["peaked", "heavy"])
+def test_attn_distributions(dtype, dist):
+    _attn_case(6, 197, 3, 0.3, "l2", dtype, seed=5, dist=dist)
+
+
+def test_attn_single_token_and_empty_images():
+    """n = 1 -> output is the V row exactly; n = 0 -> no rows written."""
+    B, N, H = 6, 31, 2
+    q, k, v = synth.activations(B, N, H, 64, "bf16", seed=6)
+    keep = np.zeros((B, N), np.uint8)
+    keep[0, 0] = 1           # n = 1
+    keep[2, [0, 5]] = 1      # n = 2
+    keep[4, :] = 1           # n = 31; images 1, 3, 5 empty
+    qd, kd, vd = _dev(q, k, v)
+    keepd = torch.from_numpy(keep).to(DEV)
+    sentinel = torch.full((B, N, H, 64), 7.0, dtype=torch.bfloat16, device=DEV)
+    o = rb.pack_attend_unpack(qd, kd, vd, keepd, o=sentinel)
+    torch.cuda.synchronize()
+    assert torch.equal(o[0, 0].cpu(), v[0, 0])
+    for b in (1, 3, 5):
+        assert torch.all(o[b] == 0)
+    ref, _ = fused_oracle(q, k, v, torch.from_numpy(keep))
+    check_attention(to_np(o), ref, torch.bfloat16)
+
+
+# --------------------------------------------------------------- unpack ----
+
+@pytest.mark.parametrize("B,N,H,p", [(4, 197, 3, 0.5), (7, 100, 5, 0.9), (2, 256, 1, 0.0)])
+def test_unpack_bitwise(B, N, H, p):
+    q, k, v, keep = synth.make_inputs(B, N, H, p, "random", "fp16", seed=7)
+    keep_np = keep.numpy().copy()
+    keep_np[B // 2] = 0
+    keepd = torch.from_numpy(keep_np).to(DEV)
+    cu, dst, src = rb.scan(keepd)
+    op = torch.randn(B * N, H, 64, device=DEV).to(torch.float16)
+    o = torch.full((B, N, H, 64), 3.0, dtype=torch.float16, device=DEV)
+    rb.unpack(op, dst, B, N, o=o)
+    torch.cuda.synchronize()
+    _, rdst, _ = oracle.scan(keep_np)
+    assert np.array_equal(bits(o), oracle.unpack(bits(op), rdst, B, N, 0))
+
+
+# ----------------------------------------------------------------- fused ----
+
+@pytest.mark.parametrize("dtype", ["bf16", "fp16"])
+@pytest.mark.parametrize("cfg", ["C1", "C3"])
+def test_fused_baseline_configs_full(dtype, cfg):
+    c = synth.CONFIGS[cfg]
+    H = synth.PRESETS[c["preset"]]["H"]
+    q, k, v, keep = synth.make_inputs(c["B"], 197, H, c["p"], c["method"], dtype, seed=0)
+    qd, kd, vd, keepd = _dev(q, k, v, keep)
+    o, cu = rb.pack_attend_unpack(qd, kd, vd, keepd, want_cu=True)
+    torch.cuda.synchronize()
+    ref, rcu = fused_oracle(q, k, v, keep)
+    assert cu.cpu().tolist() == rcu.tolist()
+    check_attention(to_np(o), ref, DT[dtype])
+    assert np.all(bits(o)[~keep.numpy().astype(bool)] == 0)
+
+
+@pytest.mark.parametrize("method", ["l2", "dynamicvit", "evit", "ats"])
+@pytest.mark.parametrize("p", [0.5, 0.7, 0.9])
+def test_fused_c4_generators_full(method, p):
+    q, k, v, keep = synth.make_inputs(64, 197, 12, p, method, "bf16", seed=0)
+    qd, kd, vd, keepd = _dev(q, k, v, keep)
+    o = rb.pack_attend_unpack(qd, kd, vd, keepd)
+    torch.cuda.synchronize()
+    ref, _ = fused_oracle(q, k, v, keep)
+    check_attention(to_np(o), ref, torch.bfloat16)
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "fp16"])
+@pytest.mark.parametrize("p", [0.0, 0.3, 0.8])
+def test_fused_equals_composed_bitwise(dtype, p):
+    """a5 == a4 . a3 . a2 . a1 bit for bit (same arithmetic, same order)."""
+    q, k, v, keep = synth.make_inputs(16, 197, 6, p, "ats" if p else "all", dtype, seed=8)
+    qd, kd, vd, keepd = _dev(q, k, v, keep)
+    o1, cu1 = rb.pack_attend_unpack(qd, kd, vd, keepd, want_cu=True)
+    qp, kp, vp, cu, dst, src = rb.pack(qd, kd, vd, keepd)
+    op = rb.attn(qp, kp, vp, cu, 197)
+    o2 = rb.unpack(op, dst, 16, 197)
+    torch.cuda.synchronize()
+    assert torch.equal(cu1, cu)
+    assert np.array_equal(bits(o1), bits(o2))
+
+
+def test_graph_replay_and_determinism_bitwise():
+    q, k, v, keep = synth.make_inputs(32, 197, 12, 0.8, "l2", "bf16", seed=9)
+    qd, kd, vd, keepd = _dev(q, k, v, keep)
+    o_eager = rb.pack_attend_unpack(qd, kd, vd, keepd)
+    o_g = torch.empty_like(o_eager)
+    cu_g = torch.empty(33, dtype=torch.int32, device=DEV)
+    g = rb.Graph(qd, kd, vd, keepd, o_g, cu_g)
+    for _ in range(3):
+        o_g.fill_(5.0)
+        g.launch()
+        torch.cuda.synchronize()
+        assert torch.equal(o_g.view(torch.int16), o_eager.view(torch.int16))
+    g.close()
+    again = rb.pack_attend_unpack(qd, kd, vd, keepd)
+    torch.cuda.synchronize()
+    assert torch.equal(again.view(torch.int16), o_eager.view(torch.int16))
+    assert cu_g.cpu().tolist() == oracle.scan(keep.numpy())[0].tolist()
+
+
+def test_cross_image_isolation_bitwise():
+    q, k, v, keep = synth.make_inputs(8, 197, 4, 0.5, "l2", "bf16", seed=10)
+    qd, kd, vd, keepd = _dev(q, k, v, keep)
+    o1 = rb.pack_attend_unpack(qd, kd, vd, keepd)
+    kd2, vd2 = kd.clone(), vd.clone()
+    kd2[3] = -kd2[3]
+    vd2[3] = 0.5 * vd2[3]
+    o2 = rb.pack_attend_unpack(qd, kd2, vd2, keepd)
+    torch.cuda.synchronize()
+    other = [b for b in range(8) if b != 3]
+    assert torch.equal(o1[other].view(torch.int16), o2[other].view(torch.int16))
+    assert not torch.equal(o1[3], o2[3])
+
+
+def test_constant_v_column_is_exact():
+    """A V column equal to c everywhere gives exactly c (checks o / l)."""
+    q, k, v, keep = synth.make_inputs(4, 197, 2, 0.0, "all", "bf16", seed=11)
+    v[..., 5] = 0.375
+    qd, kd, vd, keepd = _dev(q, k, v, keep)
+    o = rb.pack_attend_unpack(qd, kd, vd, keepd)
+    torch.cuda.synchronize()
+    assert torch.all(o[..., 5] == 0.375)
+
+
+def test_c5_scale_sampled():
+    """C5 (DeiT-B, B = 4096, 70 %): cu exact in full; zero rows everywhere;
+    64 sampled (image, head) problems against the oracle one by one."""
+    B, N, H = 4096, 197, 12
+    g = torch.Generator(device=DEV).manual_seed(12)
+    q = torch.randn(B, N, H, 64, generator=g, device=DEV).to(torch.bfloat16)
+    k = torch.randn(B, N, H, 64, generator=g, device=DEV).to(torch.bfloat16)
+    v = (torch.rand(B, N, H, 64, generator=g, device=DEV) * 2 - 1).to(torch.bfloat16)
+    keep_np = synth.mask_threshold_l2(B, N, synth.kept_tokens(N, 0.7), seed=1012)
+    keepd = torch.from_numpy(keep_np).to(DEV)
+    o, cu = rb.pack_attend_unpack(q, k, v, keepd, want_cu=True)
+    torch.cuda.synchronize()
+    assert cu.cpu().numpy().tolist() == oracle.scan(keep_np)[0].tolist()
+    dropped = ~keepd.bool()
+    assert torch.all(o[dropped] == 0)
+    rng = np.random.default_rng(0)
+    for b, h in zip(rng.integers(0, B, 64), rng.integers(0, H, 64)):
+        pos, rows = oracle.attention_image_head(q[b].cpu()[None], k[b].cpu()[None], v[b].cpu()[None],
+                                                keep_np[b][None], 0, int(h))
+        got = o[b, torch.from_numpy(pos).to(DEV), int(h)].double().cpu().numpy()
+        assert np.abs(got - rows).max() <= TOL[torch.bfloat16]
