@@ -17,7 +17,9 @@ import os
 import torch
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libragged.so")
+# RAGGED_LIB selects another build of the same ABI (e.g. the timeline debug
+# build libragged_tl.so used by scripts/timeline.py); default libragged.so.
+LIB_PATH = os.environ.get("RAGGED_LIB") or os.path.join(_PKG, "libragged.so")
 
 BF16, FP16 = 0, 1
 ENGINE_AUTO, ENGINE_MMA_SYNC, ENGINE_TCGEN05 = 0, 1, 2

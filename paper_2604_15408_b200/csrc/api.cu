@@ -12,6 +12,7 @@
 #include <string>
 
 #include "../../include/ragged.h"
+#include "../../include/ragged_debug.h"
 #include "launch.h"
 
 namespace {
@@ -43,7 +44,8 @@ ragged_status check_problem(const ragged_problem* p) {
   if (p->engine != RAGGED_ENGINE_AUTO && p->engine != RAGGED_ENGINE_MMA_SYNC)
     return fail(RAGGED_ENOTSUP, "engine not compiled in this build");
   if ((long long)p->B * p->N > 0x7fffffffLL) return fail(RAGGED_ENOTSUP, "B*N exceeds int32 indices");
-  if ((long long)p->H * 64 > (1LL << 24)) return fail(RAGGED_ENOTSUP, "H too large");
+  if ((long long)p->H * 64 > (1LL << 22)) return fail(RAGGED_ENOTSUP, "H*d > 2^22");
+  if (p->ld > (1LL << 22)) return fail(RAGGED_ENOTSUP, "ld > 2^22 elements");
   if (p->ld < (int64_t)p->H * p->d) return fail(RAGGED_EINVAL, "ld < H*d");
   if (p->ld % 8 != 0) return fail(RAGGED_EALIGN, "ld % 8 != 0 (rows must be 16-byte aligned)");
   return RAGGED_OK;
@@ -245,6 +247,13 @@ const char* ragged_status_str(ragged_status s) {
 }
 
 const char* ragged_last_error(void) { return g_last_error.c_str(); }
+
+#ifdef RAGGED_TIMELINE
+int32_t ragged_debug_timeline(void* host, int32_t max_ctas) {
+  return ragged::timeline_copy(host, max_ctas);
+}
+int32_t ragged_debug_timeline_clear(void) { return ragged::timeline_clear(); }
+#endif
 
 const char* ragged_build_info(void) {
   return "libragged 0.1 sm_100a engines=mma_sync";

@@ -28,6 +28,29 @@
 
 namespace ragged {
 
+// Optional per-CTA timeline (debug build libragged_tl.so only, -DRAGGED_TIMELINE):
+// %globaltimer stamps at the phase boundaries of the attention CTA.
+#ifdef RAGGED_TIMELINE
+constexpr int kTlSlots = 8;
+constexpr int kTlMaxCtas = 1 << 16;
+__device__ unsigned long long g_timeline[kTlMaxCtas * kTlSlots];
+__device__ __forceinline__ void tl_stamp(int slot) {
+  if (threadIdx.x == 0 && blockIdx.x < kTlMaxCtas) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    unsigned int sm;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+    g_timeline[blockIdx.x * kTlSlots + slot] = t;
+    g_timeline[blockIdx.x * kTlSlots + kTlSlots - 1] = sm;
+  }
+}
+#define TL(slot) tl_stamp(slot)
+#else
+#define TL(slot) \
+  do {           \
+  } while (0)
+#endif
+
 // ---------------------------------------------------------------- scan ----
 // One CTA walks the batch in rounds of CH = warps * kIPW images.  Each warp
 // ballots its images' keep bytes (<= 8 words of 32 positions), warp 0 scans
@@ -254,6 +277,7 @@ __global__ void __launch_bounds__(kAttnThreads, 3) attn_kernel(const AttnArgs a)
   int16_t* sDrop = sPos + kMaxN;
   uint32_t* sWords = reinterpret_cast<uint32_t*>(sDrop + kMaxN);
 
+  TL(0);
   int bid = blockIdx.x;
   if constexpr (kFused) {
     if (a.cu_out != nullptr) {
@@ -309,6 +333,7 @@ __global__ void __launch_bounds__(kAttnThreads, 3) attn_kernel(const AttnArgs a)
     }
     row_base = (long long)b * a.N;
     __syncthreads();
+    TL(1);
   } else {
     const int s = a.cu[b];
     n = min(max(a.cu[b + 1] - s, 0), a.N);
@@ -316,41 +341,56 @@ __global__ void __launch_bounds__(kAttnThreads, 3) attn_kernel(const AttnArgs a)
     for (int r = tid; r < kMaxN; r += kAttnThreads) sPos[r] = (int16_t)r;
     __syncthreads();
   }
-  const long long ld_in = kFused ? a.ld : HD;
+  // Byte addressing: one 64-bit image base per tensor, then 32-bit row offsets
+  // (pos < 256, token stride <= 2^23 bytes -- validated in api.cu).
+  const int ldb = (kFused ? (int)a.ld : (int)HD) * 2;  // input token stride, bytes
+  const int HDb = (int)HD * 2;                          // output token stride, bytes
+  const char* img_q = reinterpret_cast<const char*>(gq) + row_base * ldb + h * kRowBytes;
+  const char* img_k = reinterpret_cast<const char*>(gk) + row_base * ldb + h * kRowBytes;
+  const char* img_v = reinterpret_cast<const char*>(gv) + row_base * ldb + h * kRowBytes;
+  char* img_o = reinterpret_cast<char*>(go) + row_base * HDb + h * kRowBytes + (tid & 7) * 16;
 
-  // ---- stage K, V (rows [0, n16), zero-filled past n) and each warp's first Q slice
+  // ---- stage K, V (rows [0, n16), zero-filled past n) and each warp's first Q slice.
+  // Thread -> (chunk c, tensor t, row r0 + 8i): the swizzled chunk c ^ (r & 7) is
+  // constant per thread, so each copy is one LDS + one IMAD + the cp.async.
   const int n16 = (n + 15) & ~15;
-  for (int idx = tid; idx < n16 * 16; idx += kAttnThreads) {
-    const int r = idx >> 4, t = (idx >> 3) & 1, c = idx & 7;
-    const T* g = t ? gv : gk;
-    const bool valid = r < n;
-    const T* srcp = valid ? g + (row_base + sPos[r]) * ld_in + h * kHeadDim + c * 8 : g;
-    cp_async_16(smem_u32((t ? sV : sK) + swz(r, c)), srcp, valid ? 16 : 0);
+  {
+    const int c = tid & 7, t = (tid >> 3) & 1, r0 = tid >> 4;
+    const char* gsrc = (t ? img_v : img_k) + c * 16;
+    uint32_t sdst = smem_u32(t ? sV : sK) + r0 * kRowBytes + ((c ^ r0) << 4);
+    for (int r = r0; r < n16; r += 8, sdst += 8 * kRowBytes) {
+      const bool valid = r < n;
+      cp_async_16(sdst, gsrc + (valid ? sPos[r] * ldb : 0), valid ? 16 : 0);
+    }
   }
   uint8_t* const qwarp = sQ + warp * 2 * kQBufBytes;  // this warp's two 16-row Q buffers
   auto load_q = [&](uint8_t* buf, int slice) {
+    const int c = lane & 7;
+    const char* gsrc = img_q + c * 16;
+    const uint32_t sb = smem_u32(buf);
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-      const int rr = (lane >> 3) + 4 * i, c = lane & 7, r = slice * 16 + rr;
+      const int rr = (lane >> 3) + 4 * i, r = slice * 16 + rr;
       const bool valid = r < n;
-      const T* srcp = valid ? gq + (row_base + sPos[r]) * ld_in + h * kHeadDim + c * 8 : gq;
-      cp_async_16(smem_u32(buf + swz(rr, c)), srcp, valid ? 16 : 0);
+      cp_async_16(sb + rr * kRowBytes + ((c ^ (rr & 7)) << 4), gsrc + (valid ? sPos[r] * ldb : 0),
+                  valid ? 16 : 0);
     }
   };
   if (warp * 16 < n) load_q(qwarp, warp);
   cp_async_commit();
 
   if constexpr (kFused) {
-    // dropped rows of this head -> +0.0, overlapped with the gather in flight
+    // dropped rows of this head -> +0.0, overlapped with the gather in flight;
+    // 8 consecutive threads write one whole 128-byte row.
     const int nd = a.N - n;
     const uint4 z = make_uint4(0u, 0u, 0u, 0u);
-    for (int idx = tid; idx < nd * 8; idx += kAttnThreads) {
-      const int row = sDrop[idx >> 3], c = idx & 7;
-      st_global_16(go + (row_base + row) * HD + h * kHeadDim + c * 8, z);
-    }
+    for (int rr = tid >> 3; rr < nd; rr += kAttnThreads / 8)
+      st_global_16(img_o + sDrop[rr] * HDb, z);
   }
+  TL(2);
   cp_async_wait_all();
   __syncthreads();
+  TL(3);
 
   // ---- per-warp query slices: S = Q K^T, online softmax (Alg. 1), O += P V
   const int g = lane >> 2, t4 = lane & 3;
@@ -406,6 +446,7 @@ __global__ void __launch_bounds__(kAttnThreads, 3) attn_kernel(const AttnArgs a)
       mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 2));
       mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 1));
       mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 2));
+      TL(5);
       const float mn0 = fmaxf(m0, mx0), mn1 = fmaxf(m1, mx1);
       const float al0 = ex2(m0 - mn0), al1 = ex2(m1 - mn1);  // alpha = e^{m - m'}
       m0 = mn0;
@@ -468,18 +509,23 @@ __global__ void __launch_bounds__(kAttnThreads, 3) attn_kernel(const AttnArgs a)
           pack2<T>(o[j][2] * inv1, o[j][3] * inv1);
     }
     __syncwarp();
+    TL(6);
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-      const int rr = (lane >> 3) + 4 * i, c = lane & 7, r = slice * 16 + rr;
+      const int rr = (lane >> 3) + 4 * i, r = slice * 16 + rr;
       if (r < n) {
-        const uint4 val = *reinterpret_cast<const uint4*>(qcur + swz(rr, c));
-        st_global_16(go + (row_base + sPos[r]) * HD + h * kHeadDim + c * 8, val);
+        const uint4 val = *reinterpret_cast<const uint4*>(qcur + swz(rr, lane & 7));
+        st_global_16(img_o + sPos[r] * HDb, val);
       }
     }
     cp_async_wait_all();
     __syncwarp();
     buf ^= 1;
   }
+#ifdef RAGGED_TIMELINE
+  __syncthreads();
+  TL(4);
+#endif
 }
 
 __global__ void empty_kernel() {}
@@ -590,5 +636,17 @@ cudaError_t launch_empty(int grid, int block, cudaStream_t st) {
 }
 
 int fused_smem_bytes(int N) { return attn_smem_bytes(N); }
+
+#ifdef RAGGED_TIMELINE
+int timeline_copy(void* host, int max_ctas) {
+  const int n = max_ctas < kTlMaxCtas ? max_ctas : kTlMaxCtas;
+  return cudaMemcpyFromSymbol(host, g_timeline, (size_t)n * kTlSlots * 8) == cudaSuccess ? n : -1;
+}
+int timeline_clear() {
+  void* p = nullptr;
+  if (cudaGetSymbolAddress(&p, g_timeline) != cudaSuccess) return -1;
+  return cudaMemset(p, 0, sizeof(g_timeline)) == cudaSuccess ? 0 : -1;
+}
+#endif
 
 }  // namespace ragged

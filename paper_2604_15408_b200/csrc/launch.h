@@ -19,5 +19,9 @@ cudaError_t launch_fused(int dtype, const uint8_t* keep, const void* q, const vo
                          cudaStream_t st);
 cudaError_t launch_empty(int grid, int block, cudaStream_t st);
 int fused_smem_bytes(int N);
+#ifdef RAGGED_TIMELINE
+int timeline_copy(void* host, int max_ctas);
+int timeline_clear();
+#endif
 
 }  // namespace ragged
