@@ -207,10 +207,12 @@ def main():
     if ws > 1:
         dist.init_process_group("nccl", device_id=dev)
 
+    from paper_2604_15408_b200.shard import max_over_ranks, shard
     c, B, N, H = workload(args)
     dt = synth.DTYPES[args.dtype]
+    off, B = shard(ws * B, ws, rank)          # weak scaling: B images per GPU
     q, k, v, keep = synth.make_inputs(B, N, H, c["p"], c["method"], args.dtype, seed=0,
-                                      image_offset=rank * B)
+                                      image_offset=off)
     T = int(keep.numpy().astype(bool).sum())
     sets = []
     for _ in range(N_SETS):
@@ -255,11 +257,7 @@ def main():
         torch.cuda.synchronize()
     if ws > 1:
         dist.barrier()
-    ms = start.elapsed_time(end)
-    if ws > 1:
-        t = torch.tensor([ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+    ms = max_over_ranks(start.elapsed_time(end), dev)
     us_per_call = 1e3 * ms / args.steps
     value = ws * B * args.steps / (ms * 1e-3)
 

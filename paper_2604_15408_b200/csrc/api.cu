@@ -41,8 +41,9 @@ ragged_status check_problem(const ragged_problem* p) {
   if (p->d != 64) return fail(RAGGED_ENOTSUP, "head_dim must be 64 (P:330-331)");
   if (p->dtype != RAGGED_BF16 && p->dtype != RAGGED_FP16)
     return fail(RAGGED_ENOTSUP, "dtype must be RAGGED_BF16 or RAGGED_FP16");
-  if (p->engine != RAGGED_ENGINE_AUTO && p->engine != RAGGED_ENGINE_MMA_SYNC)
-    return fail(RAGGED_ENOTSUP, "engine not compiled in this build");
+  if (p->engine != RAGGED_ENGINE_AUTO && p->engine != RAGGED_ENGINE_MMA_SYNC &&
+      p->engine != RAGGED_ENGINE_TCGEN05)
+    return fail(RAGGED_ENOTSUP, "unknown engine");
   if ((long long)p->B * p->N > 0x7fffffffLL) return fail(RAGGED_ENOTSUP, "B*N exceeds int32 indices");
   if ((long long)p->H * 64 > (1LL << 22)) return fail(RAGGED_ENOTSUP, "H*d > 2^22");
   if (p->ld > (1LL << 22)) return fail(RAGGED_ENOTSUP, "ld > 2^22 elements");
@@ -80,6 +81,11 @@ ragged_status check_ptr_any(const void* p, const char* name) {  // 1-byte / 4-by
   } while (0)
 
 cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
+
+// RAGGED_ENGINE_AUTO -> the engine measured fastest.
+int resolve_engine(const ragged_problem* p) {
+  return p->engine == RAGGED_ENGINE_AUTO ? RAGGED_ENGINE_MMA_SYNC : p->engine;
+}
 
 }  // namespace
 
@@ -136,7 +142,7 @@ ragged_status ragged_attn(const ragged_problem* prob, const void* qp, const void
   RAGGED_TRY(check_ptr_any(cu_seqlens, "cu_seqlens"));
   RAGGED_TRY(check_ptr(op, "op"));
   if ((long long)prob->B * prob->H > 0x7fffffffLL) return fail(RAGGED_ENOTSUP, "B*H too large");
-  cudaError_t e = ragged::launch_attn(prob->dtype, qp, kp, vp, cu_seqlens, op, prob->B, prob->N,
+  cudaError_t e = ragged::launch_attn(prob->dtype, resolve_engine(prob), qp, kp, vp, cu_seqlens, op, prob->B, prob->N,
                                       prob->H, as_stream(stream));
   return e == cudaSuccess ? RAGGED_OK : cuda_fail(e, "ragged_attn");
 }
@@ -164,7 +170,7 @@ ragged_status ragged_pack_attend_unpack(const ragged_problem* prob, const uint8_
   RAGGED_TRY(check_ptr(v, "v"));
   RAGGED_TRY(check_ptr(o, "o"));
   if ((long long)prob->B * prob->H + 1 > 0x7fffffffLL) return fail(RAGGED_ENOTSUP, "B*H too large");
-  cudaError_t e = ragged::launch_fused(prob->dtype, keep, q, k, v, prob->ld, o, cu_seqlens_or_null,
+  cudaError_t e = ragged::launch_fused(prob->dtype, resolve_engine(prob), keep, q, k, v, prob->ld, o, cu_seqlens_or_null,
                                        prob->B, prob->N, prob->H, as_stream(stream));
   return e == cudaSuccess ? RAGGED_OK : cuda_fail(e, "ragged_pack_attend_unpack");
 }
@@ -256,7 +262,7 @@ int32_t ragged_debug_timeline_clear(void) { return ragged::timeline_clear(); }
 #endif
 
 const char* ragged_build_info(void) {
-  return "libragged 0.1 sm_100a engines=mma_sync";
+  return "libragged 0.2 sm_100a engines=mma_sync,tcgen05";
 }
 
 }  // extern "C"

@@ -23,8 +23,11 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <type_traits>
+
 #include "device.cuh"
 #include "launch.h"
+#include "tcgen05.cuh"
 
 namespace ragged {
 
@@ -265,43 +268,26 @@ struct AttnArgs {
   long long ld;            // input token stride in elements
 };
 
-template <typename T, bool kFused>
-__global__ void __launch_bounds__(kAttnThreads, 3) attn_kernel(const AttnArgs a) {
-  extern __shared__ __align__(1024) uint8_t smem[];
+// Block 0 of a fused launch that also emits cu_seqlens: one CTA walks the keep
+// mask (scan_cta, counts only) while the other CTAs attend.
+__device__ __forceinline__ void scan_cta_cu(const AttnArgs& a, uint8_t* scratch) {
+  constexpr int CH = kAttnThreads / 32 * 8;
+  uint32_t* w = reinterpret_cast<uint32_t*>(scratch);
+  int32_t* c = reinterpret_cast<int32_t*>(w + CH * 8);
+  scan_cta<kAttnThreads, 8, false>(a.keep, a.B, a.N, a.cu_out, nullptr, nullptr, w, c, c + CH);
+}
+
+// The rows of problem (image b, one head): kept positions sPos[0, n) (ascending,
+// R7) and dropped positions sDrop[0, N - n).
+//   fused:  ballots of the keep row + popc ranks (no cross-image prefix needed);
+//           row_base = b * N (padded rows).
+//   packed: n = cu[b+1] - cu[b], sPos[r] = r; row_base = cu[b] (packed rows).
+// Ends with __syncthreads().  Requires blockDim.x == kAttnThreads, N <= 256.
+template <bool kFused>
+__device__ __forceinline__ void image_rows(const AttnArgs& a, int b, int16_t* sPos, int16_t* sDrop,
+                                           uint32_t* sWords, int& n, long long& row_base) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int rows_cap = attn_rows_cap(a.N);
-  uint8_t* sK = smem;
-  uint8_t* sV = sK + rows_cap * kRowBytes;
-  uint8_t* sQ = sV + rows_cap * kRowBytes;
-  int16_t* sPos = reinterpret_cast<int16_t*>(sQ + kQAreaBytes);
-  int16_t* sDrop = sPos + kMaxN;
-  uint32_t* sWords = reinterpret_cast<uint32_t*>(sDrop + kMaxN);
-
-  TL(0);
-  int bid = blockIdx.x;
   if constexpr (kFused) {
-    if (a.cu_out != nullptr) {
-      if (bid == 0) {  // the scan CTA: cu_seqlens only, concurrent with the rest
-        constexpr int CH = kAttnThreads / 32 * 8;
-        uint32_t* w = reinterpret_cast<uint32_t*>(sK);
-        int32_t* c = reinterpret_cast<int32_t*>(w + CH * 8);
-        scan_cta<kAttnThreads, 8, false>(a.keep, a.B, a.N, a.cu_out, nullptr, nullptr, w, c, c + CH);
-        return;
-      }
-      bid -= 1;
-    }
-  }
-  const int b = bid / a.H, h = bid - b * a.H;   // head fastest (P:293-294)
-  const long long HD = (long long)a.H * kHeadDim;
-  const T* gq = static_cast<const T*>(a.q);
-  const T* gk = static_cast<const T*>(a.k);
-  const T* gv = static_cast<const T*>(a.v);
-  T* go = static_cast<T*>(a.o);
-
-  int n;
-  long long row_base;
-  if constexpr (kFused) {
-    // keep mask row -> ballots -> kept ranks / dropped ranks (no global prefix needed)
     const uint8_t* km = a.keep + (long long)b * a.N;
     const int p0 = tid, p1 = tid + kAttnThreads;
     const bool k0 = p0 < a.N && km[p0] != 0;
@@ -341,6 +327,41 @@ __global__ void __launch_bounds__(kAttnThreads, 3) attn_kernel(const AttnArgs a)
     for (int r = tid; r < kMaxN; r += kAttnThreads) sPos[r] = (int16_t)r;
     __syncthreads();
   }
+}
+
+template <typename T, bool kFused>
+__global__ void __launch_bounds__(kAttnThreads, 3) attn_kernel(const AttnArgs a) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int rows_cap = attn_rows_cap(a.N);
+  uint8_t* sK = smem;
+  uint8_t* sV = sK + rows_cap * kRowBytes;
+  uint8_t* sQ = sV + rows_cap * kRowBytes;
+  int16_t* sPos = reinterpret_cast<int16_t*>(sQ + kQAreaBytes);
+  int16_t* sDrop = sPos + kMaxN;
+  uint32_t* sWords = reinterpret_cast<uint32_t*>(sDrop + kMaxN);
+
+  TL(0);
+  int bid = blockIdx.x;
+  if constexpr (kFused) {
+    if (a.cu_out != nullptr) {
+      if (bid == 0) {  // the scan CTA: cu_seqlens only, concurrent with the rest
+        scan_cta_cu(a, sK);
+        return;
+      }
+      bid -= 1;
+    }
+  }
+  const int b = bid / a.H, h = bid - b * a.H;   // head fastest (P:293-294)
+  const long long HD = (long long)a.H * kHeadDim;
+  const T* gq = static_cast<const T*>(a.q);
+  const T* gk = static_cast<const T*>(a.k);
+  const T* gv = static_cast<const T*>(a.v);
+  T* go = static_cast<T*>(a.o);
+
+  int n;
+  long long row_base;
+  image_rows<kFused>(a, b, sPos, sDrop, sWords, n, row_base);
   // Byte addressing: one 64-bit image base per tensor, then 32-bit row offsets
   // (pos < 256, token stride <= 2^23 bytes -- validated in api.cu).
   const int ldb = (kFused ? (int)a.ld : (int)HD) * 2;  // input token stride, bytes
@@ -528,6 +549,12 @@ __global__ void __launch_bounds__(kAttnThreads, 3) attn_kernel(const AttnArgs a)
 #endif
 }
 
+}  // namespace ragged
+
+#include "attn_tc.cuh"
+
+namespace ragged {
+
 __global__ void empty_kernel() {}
 
 // --------------------------------------------------------------- launch ----
@@ -576,26 +603,37 @@ cudaError_t launch_unpack(const void* op, const int32_t* dst, void* o, int B, in
   return cudaGetLastError();
 }
 
-template <typename T, bool kFused>
+template <typename T, bool kFused, bool kTc>
 static cudaError_t launch_attn_t(const AttnArgs& a, int grid, cudaStream_t st) {
   // The max-dynamic-smem attribute is set once per device (for N = 256, which
   // covers every N), so the steady-state launch path does no attribute work.
   static bool done[64] = {false};
   int dev = 0;
   cudaGetDevice(&dev);
+  auto kern = kTc ? attn_tc_kernel<T, kFused> : attn_kernel<T, kFused>;
+  const int max_bytes = kTc ? tc_smem(kMaxN).bytes : attn_smem_bytes(kMaxN);
+  const int bytes = kTc ? tc_smem(a.N).bytes : attn_smem_bytes(a.N);
   if (dev < 0 || dev >= 64 || !done[dev]) {
-    cudaError_t e = cudaFuncSetAttribute(attn_kernel<T, kFused>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         attn_smem_bytes(kMaxN));
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, max_bytes);
     if (e != cudaSuccess) return e;
     if (dev >= 0 && dev < 64) done[dev] = true;
   }
-  attn_kernel<T, kFused><<<grid, kAttnThreads, attn_smem_bytes(a.N), st>>>(a);
+  kern<<<grid, kAttnThreads, bytes, st>>>(a);
   return cudaGetLastError();
 }
 
-cudaError_t launch_attn(int dtype, const void* qp, const void* kp, const void* vp, const int32_t* cu,
-                        void* op, int B, int N, int H, cudaStream_t st) {
+template <bool kFused>
+static cudaError_t dispatch_attn(int dtype, int engine, const AttnArgs& a, int grid, cudaStream_t st) {
+  const bool tc = engine == 2;
+  if (dtype == 0)
+    return tc ? launch_attn_t<__nv_bfloat16, kFused, true>(a, grid, st)
+              : launch_attn_t<__nv_bfloat16, kFused, false>(a, grid, st);
+  return tc ? launch_attn_t<__half, kFused, true>(a, grid, st)
+            : launch_attn_t<__half, kFused, false>(a, grid, st);
+}
+
+cudaError_t launch_attn(int dtype, int engine, const void* qp, const void* kp, const void* vp,
+                        const int32_t* cu, void* op, int B, int N, int H, cudaStream_t st) {
   AttnArgs a{};
   a.q = qp;
   a.k = kp;
@@ -606,12 +644,10 @@ cudaError_t launch_attn(int dtype, const void* qp, const void* kp, const void* v
   a.N = N;
   a.H = H;
   a.ld = (long long)H * kHeadDim;
-  const int grid = B * H;
-  return dtype == 0 ? launch_attn_t<__nv_bfloat16, false>(a, grid, st)
-                    : launch_attn_t<__half, false>(a, grid, st);
+  return dispatch_attn<false>(dtype, engine, a, B * H, st);
 }
 
-cudaError_t launch_fused(int dtype, const uint8_t* keep, const void* q, const void* k,
+cudaError_t launch_fused(int dtype, int engine, const uint8_t* keep, const void* q, const void* k,
                          const void* v, long long ld, void* o, int32_t* cu_out, int B, int N, int H,
                          cudaStream_t st) {
   AttnArgs a{};
@@ -625,9 +661,7 @@ cudaError_t launch_fused(int dtype, const uint8_t* keep, const void* q, const vo
   a.N = N;
   a.H = H;
   a.ld = ld;
-  const int grid = B * H + (cu_out ? 1 : 0);
-  return dtype == 0 ? launch_attn_t<__nv_bfloat16, true>(a, grid, st)
-                    : launch_attn_t<__half, true>(a, grid, st);
+  return dispatch_attn<true>(dtype, engine, a, B * H + (cu_out ? 1 : 0), st);
 }
 
 cudaError_t launch_empty(int grid, int block, cudaStream_t st) {

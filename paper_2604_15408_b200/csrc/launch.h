@@ -10,11 +10,12 @@ cudaError_t launch_scan(const uint8_t* keep, int B, int N, int32_t* cu, int32_t*
 cudaError_t launch_pack(const void* q, const void* k, const void* v, long long ld_elems, int B, int N,
                         int H, const int32_t* cu, const int32_t* src, void* qp, void* kp, void* vp,
                         cudaStream_t st);
-cudaError_t launch_attn(int dtype, const void* qp, const void* kp, const void* vp, const int32_t* cu,
+// engine: 1 = mma.sync, 2 = tcgen05 (api.cu resolves RAGGED_ENGINE_AUTO)
+cudaError_t launch_attn(int dtype, int engine, const void* qp, const void* kp, const void* vp, const int32_t* cu,
                         void* op, int B, int N, int H, cudaStream_t st);
 cudaError_t launch_unpack(const void* op, const int32_t* dst, void* o, int B, int N, int H,
                           cudaStream_t st);
-cudaError_t launch_fused(int dtype, const uint8_t* keep, const void* q, const void* k,
+cudaError_t launch_fused(int dtype, int engine, const uint8_t* keep, const void* q, const void* k,
                          const void* v, long long ld, void* o, int32_t* cu_out, int B, int N, int H,
                          cudaStream_t st);
 cudaError_t launch_empty(int grid, int block, cudaStream_t st);

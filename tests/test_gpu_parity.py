@@ -18,6 +18,7 @@ rb = pytest.importorskip("paper_2604_15408_b200")
 pytestmark = pytest.mark.gpu
 DEV = "cuda"
 DT = {"bf16": torch.bfloat16, "fp16": torch.float16}
+ENGINES = [rb.ENGINE_MMA_SYNC, rb.ENGINE_TCGEN05]
 
 
 def _dev(*ts):
@@ -81,7 +82,7 @@ def test_pack_fused_qkv_layout():
     q, k, v = d[:, :, 0], d[:, :, 1], d[:, :, 2]
     assert q.stride(1) == 3 * H * 64
     qp, kp, vp, cu, dst, src = rb.pack(q, k, v, keep.to(DEV))
-    o = rb.pack_attend_unpack(q, k, v, keep.to(DEV))
+    o = rb.pack_attend_unpack(q, k, v, keep.to(DEV), engine=rb.ENGINE_TCGEN05)
     torch.cuda.synchronize()
     rcu, _, rsrc = oracle.scan(keep.numpy())
     T = int(rcu[-1])
@@ -92,11 +93,11 @@ def test_pack_fused_qkv_layout():
 
 # ------------------------------------------------------------- attention ----
 
-def _attn_case(B, N, H, p, method, dtype, seed, dist="standard"):
+def _attn_case(B, N, H, p, method, dtype, seed, dist="standard", engine=rb.ENGINE_AUTO):
     q, k, v, keep = synth.make_inputs(B, N, H, p, method, dtype, seed=seed, dist=dist)
     qd, kd, vd, keepd = _dev(q, k, v, keep)
     qp, kp, vp, cu, dst, src = rb.pack(qd, kd, vd, keepd)
-    op = rb.attn(qp, kp, vp, cu, N)
+    op = rb.attn(qp, kp, vp, cu, N, engine=engine)
     torch.cuda.synchronize()
     rcu, rdst, rsrc = oracle.scan(keep.numpy())
     T = int(rcu[-1])
@@ -105,6 +106,7 @@ def _attn_case(B, N, H, p, method, dtype, seed, dist="standard"):
     return check_attention(to_np(op[:T]), ref, DT[dtype], vmax=float(v.float().abs().max()), dist=dist)
 
 
+@pytest.mark.parametrize("engine", ENGINES)
 @pytest.mark.parametrize("dtype", ["bf16", "fp16"])
 @pytest.mark.parametrize("B,N,H,p,method", [
     (4, 197, 3, 0.5, "l2"),          # C1
@@ -115,17 +117,19 @@ def _attn_case(B, N, H, p, method, dtype, seed, dist="standard"):
     (9, 40, 4, 0.6, "dynamicvit"),
     (3, 17, 2, 0.0, "all"),          # n = 17
 ])
-def test_attn_matches_oracle(dtype, B, N, H, p, method):
-    _attn_case(B, N, H, p, method, dtype, seed=2)
+def test_attn_matches_oracle(engine, dtype, B, N, H, p, method):
+    _attn_case(B, N, H, p, method, dtype, seed=2, engine=engine)
 
 
+@pytest.mark.parametrize("engine", ENGINES)
 @pytest.mark.parametrize("dtype", ["bf16", "fp16"])
 @pytest.mark.parametrize("dist", ["peaked", "heavy"])
-def test_attn_distributions(dtype, dist):
-    _attn_case(6, 197, 3, 0.3, "l2", dtype, seed=5, dist=dist)
+def test_attn_distributions(engine, dtype, dist):
+    _attn_case(6, 197, 3, 0.3, "l2", dtype, seed=5, dist=dist, engine=engine)
 
 
-def test_attn_single_token_and_empty_images():
+@pytest.mark.parametrize("engine", ENGINES)
+def test_attn_single_token_and_empty_images(engine):
     """n = 1 -> output is the V row exactly; n = 0 -> no rows written."""
     B, N, H = 6, 31, 2
     q, k, v = synth.activations(B, N, H, 64, "bf16", seed=6)
@@ -136,7 +140,7 @@ def test_attn_single_token_and_empty_images():
     qd, kd, vd = _dev(q, k, v)
     keepd = torch.from_numpy(keep).to(DEV)
     sentinel = torch.full((B, N, H, 64), 7.0, dtype=torch.bfloat16, device=DEV)
-    o = rb.pack_attend_unpack(qd, kd, vd, keepd, o=sentinel)
+    o = rb.pack_attend_unpack(qd, kd, vd, keepd, o=sentinel, engine=engine)
     torch.cuda.synchronize()
     assert torch.equal(o[0, 0].cpu(), v[0, 0])
     for b in (1, 3, 5):
@@ -164,14 +168,15 @@ def test_unpack_bitwise(B, N, H, p):
 
 # ----------------------------------------------------------------- fused ----
 
+@pytest.mark.parametrize("engine", ENGINES)
 @pytest.mark.parametrize("dtype", ["bf16", "fp16"])
 @pytest.mark.parametrize("cfg", ["C1", "C3"])
-def test_fused_baseline_configs_full(dtype, cfg):
+def test_fused_baseline_configs_full(engine, dtype, cfg):
     c = synth.CONFIGS[cfg]
     H = synth.PRESETS[c["preset"]]["H"]
     q, k, v, keep = synth.make_inputs(c["B"], 197, H, c["p"], c["method"], dtype, seed=0)
     qd, kd, vd, keepd = _dev(q, k, v, keep)
-    o, cu = rb.pack_attend_unpack(qd, kd, vd, keepd, want_cu=True)
+    o, cu = rb.pack_attend_unpack(qd, kd, vd, keepd, want_cu=True, engine=engine)
     torch.cuda.synchronize()
     ref, rcu = fused_oracle(q, k, v, keep)
     assert cu.cpu().tolist() == rcu.tolist()
@@ -179,76 +184,82 @@ def test_fused_baseline_configs_full(dtype, cfg):
     assert np.all(bits(o)[~keep.numpy().astype(bool)] == 0)
 
 
+@pytest.mark.parametrize("engine", ENGINES)
 @pytest.mark.parametrize("method", ["l2", "dynamicvit", "evit", "ats"])
 @pytest.mark.parametrize("p", [0.5, 0.7, 0.9])
-def test_fused_c4_generators_full(method, p):
+def test_fused_c4_generators_full(engine, method, p):
     q, k, v, keep = synth.make_inputs(64, 197, 12, p, method, "bf16", seed=0)
     qd, kd, vd, keepd = _dev(q, k, v, keep)
-    o = rb.pack_attend_unpack(qd, kd, vd, keepd)
+    o = rb.pack_attend_unpack(qd, kd, vd, keepd, engine=engine)
     torch.cuda.synchronize()
     ref, _ = fused_oracle(q, k, v, keep)
     check_attention(to_np(o), ref, torch.bfloat16)
 
 
+@pytest.mark.parametrize("engine", ENGINES)
 @pytest.mark.parametrize("dtype", ["bf16", "fp16"])
 @pytest.mark.parametrize("p", [0.0, 0.3, 0.8])
-def test_fused_equals_composed_bitwise(dtype, p):
+def test_fused_equals_composed_bitwise(engine, dtype, p):
     """a5 == a4 . a3 . a2 . a1 bit for bit (same arithmetic, same order)."""
     q, k, v, keep = synth.make_inputs(16, 197, 6, p, "ats" if p else "all", dtype, seed=8)
     qd, kd, vd, keepd = _dev(q, k, v, keep)
-    o1, cu1 = rb.pack_attend_unpack(qd, kd, vd, keepd, want_cu=True)
+    o1, cu1 = rb.pack_attend_unpack(qd, kd, vd, keepd, want_cu=True, engine=engine)
     qp, kp, vp, cu, dst, src = rb.pack(qd, kd, vd, keepd)
-    op = rb.attn(qp, kp, vp, cu, 197)
+    op = rb.attn(qp, kp, vp, cu, 197, engine=engine)
     o2 = rb.unpack(op, dst, 16, 197)
     torch.cuda.synchronize()
     assert torch.equal(cu1, cu)
     assert np.array_equal(bits(o1), bits(o2))
 
 
-def test_graph_replay_and_determinism_bitwise():
+@pytest.mark.parametrize("engine", ENGINES)
+def test_graph_replay_and_determinism_bitwise(engine):
     q, k, v, keep = synth.make_inputs(32, 197, 12, 0.8, "l2", "bf16", seed=9)
     qd, kd, vd, keepd = _dev(q, k, v, keep)
-    o_eager = rb.pack_attend_unpack(qd, kd, vd, keepd)
+    o_eager = rb.pack_attend_unpack(qd, kd, vd, keepd, engine=engine)
     o_g = torch.empty_like(o_eager)
     cu_g = torch.empty(33, dtype=torch.int32, device=DEV)
-    g = rb.Graph(qd, kd, vd, keepd, o_g, cu_g)
+    g = rb.Graph(qd, kd, vd, keepd, o_g, cu_g, engine=engine)
     for _ in range(3):
         o_g.fill_(5.0)
         g.launch()
         torch.cuda.synchronize()
         assert torch.equal(o_g.view(torch.int16), o_eager.view(torch.int16))
     g.close()
-    again = rb.pack_attend_unpack(qd, kd, vd, keepd)
+    again = rb.pack_attend_unpack(qd, kd, vd, keepd, engine=engine)
     torch.cuda.synchronize()
     assert torch.equal(again.view(torch.int16), o_eager.view(torch.int16))
     assert cu_g.cpu().tolist() == oracle.scan(keep.numpy())[0].tolist()
 
 
-def test_cross_image_isolation_bitwise():
+@pytest.mark.parametrize("engine", ENGINES)
+def test_cross_image_isolation_bitwise(engine):
     q, k, v, keep = synth.make_inputs(8, 197, 4, 0.5, "l2", "bf16", seed=10)
     qd, kd, vd, keepd = _dev(q, k, v, keep)
-    o1 = rb.pack_attend_unpack(qd, kd, vd, keepd)
+    o1 = rb.pack_attend_unpack(qd, kd, vd, keepd, engine=engine)
     kd2, vd2 = kd.clone(), vd.clone()
     kd2[3] = -kd2[3]
     vd2[3] = 0.5 * vd2[3]
-    o2 = rb.pack_attend_unpack(qd, kd2, vd2, keepd)
+    o2 = rb.pack_attend_unpack(qd, kd2, vd2, keepd, engine=engine)
     torch.cuda.synchronize()
     other = [b for b in range(8) if b != 3]
     assert torch.equal(o1[other].view(torch.int16), o2[other].view(torch.int16))
     assert not torch.equal(o1[3], o2[3])
 
 
-def test_constant_v_column_is_exact():
+@pytest.mark.parametrize("engine", ENGINES)
+def test_constant_v_column_is_exact(engine):
     """A V column equal to c everywhere gives exactly c (checks o / l)."""
     q, k, v, keep = synth.make_inputs(4, 197, 2, 0.0, "all", "bf16", seed=11)
     v[..., 5] = 0.375
     qd, kd, vd, keepd = _dev(q, k, v, keep)
-    o = rb.pack_attend_unpack(qd, kd, vd, keepd)
+    o = rb.pack_attend_unpack(qd, kd, vd, keepd, engine=engine)
     torch.cuda.synchronize()
     assert torch.all(o[..., 5] == 0.375)
 
 
-def test_c5_scale_sampled():
+@pytest.mark.parametrize("engine", ENGINES)
+def test_c5_scale_sampled(engine):
     """C5 (DeiT-B, B = 4096, 70 %): cu exact in full; zero rows everywhere;
     64 sampled (image, head) problems against the oracle one by one."""
     B, N, H = 4096, 197, 12
@@ -258,7 +269,7 @@ def test_c5_scale_sampled():
     v = (torch.rand(B, N, H, 64, generator=g, device=DEV) * 2 - 1).to(torch.bfloat16)
     keep_np = synth.mask_threshold_l2(B, N, synth.kept_tokens(N, 0.7), seed=1012)
     keepd = torch.from_numpy(keep_np).to(DEV)
-    o, cu = rb.pack_attend_unpack(q, k, v, keepd, want_cu=True)
+    o, cu = rb.pack_attend_unpack(q, k, v, keepd, want_cu=True, engine=engine)
     torch.cuda.synchronize()
     assert cu.cpu().numpy().tolist() == oracle.scan(keep_np)[0].tolist()
     dropped = ~keepd.bool()
