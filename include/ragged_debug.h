@@ -3,9 +3,10 @@
  * libragged_tl.so (compiled with -DRAGGED_TIMELINE); never in libragged.so.
  *
  * ragged_debug_timeline copies per-CTA %globaltimer stamps of the last
- * attention launches (8 x uint64 per CTA: slot 0 entry, 1 ranks ready (fused),
- * 2 gathers issued, 3 gathers landed, 4 compute + stores done, 7 = %smid) into
- * `host` (max_ctas * 64 bytes); returns the number of CTAs copied or -1.
+ * attention launch (16 x uint64 per CTA: 0 entry, 1 ranks ready (fused),
+ * 2 gathers issued, 3 gathers landed, 4 end, 5 S ready, 6 O staged, 8 P in
+ * TMEM (tcgen05), 9 O ready (tcgen05), 15 = %smid) into `host`
+ * (max_ctas * 128 bytes); returns the number of CTAs copied or -1.
  */
 #ifndef RAGGED_DEBUG_H
 #define RAGGED_DEBUG_H

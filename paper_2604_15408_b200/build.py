@@ -30,7 +30,8 @@ def nvcc() -> str:
     raise RuntimeError("nvcc not found")
 
 
-VARIANTS = {"": [], "tl": ["-DRAGGED_TIMELINE"]}
+VARIANTS = {"": [], "tl": ["-DRAGGED_TIMELINE"],
+            "tlx": ["-DRAGGED_TIMELINE", "-DRAGGED_TC_EARLY128"]}  # experiments only
 
 
 def lib_path(variant: str = "") -> str:
@@ -84,3 +85,5 @@ if __name__ == "__main__":
     print(build(force=True, verbose="--verbose" in sys.argv))
     if "--tl" in sys.argv:
         print(build(force=True, variant="tl"))
+    if "--tlx" in sys.argv:
+        print(build(force=True, variant="tlx"))

@@ -1,283 +1,307 @@
 // attn_tc.cuh -- tcgen05 engine of the ragged attention (Alg. 1),
 // included by kernels.cu (shares AttnArgs, image_rows, scan_cta_cu, TL).
 //
-// One CTA (4 warps) per (image, head), as in the mma.sync engine, but the two
-// contractions run on the 5th-gen tensor cores with fp32 accumulators in TMEM:
+// Persistent CTAs, one per SM, each split into `nslots` (2-3) independent
+// 128-thread SLOTS.  A slot processes one (image, head) problem at a time
+// (problems are strided over CTAs then slots, head fastest as in P:293-294):
 //
-//   S = Q K^T     tcgen05.mma kind::f16, M = 128 query rows, N = n16 keys, K = 64:
-//                 A = Q tile, B = K rows, both SMEM (SWIZZLE_128B, K-major).
-//   softmax       one thread per query row (TMEM lane): tcgen05.ld its S row,
-//                 row max (no shuffles), P = 2^(S log2e/8 - m), row sum l;
-//                 P is split hi + lo in the 16-bit type (R2) and written back
-//                 with tcgen05.st IN PLACE of its S columns (2 values/column).
-//   O = P V       tcgen05.mma with A = P from TMEM, B = V from SMEM (MN-major),
-//                 N = 64, accumulated over all key chunks: P_hi V + P_lo V.
-//   epilogue      tcgen05.ld O row, * 1/l, RNE to 16 bit, SMEM transpose,
-//                 coalesced 128-byte row stores (scattered to padded rows).
+//   S_j = Q K_j^T   tcgen05.mma kind::f16, M = 128 query rows, N <= 64 keys of
+//                   chunk j, K = 64; A = Q tile, B = K rows, both in SMEM
+//                   (SWIZZLE_128B, K-major).  Fp32 accumulator in TMEM.
+//   softmax         one thread per query row (its TMEM lane): tcgen05.ld the
+//                   row chunk, chunk max, Alg. 1's online update m, l, alpha
+//                    with LAZY rescaling -- the reference max only
+//                   moves when the chunk max exceeds it by > 2^8 in P, and then
+//                   O is rescaled in TMEM; P = 2^((S - m) log2e / 8) is split
+//                   hi + lo in the 16-bit type (R2) and stored with tcgen05.st
+//                   IN PLACE of its S columns (two 16-bit values per column).
+//   O += P_j V_j    tcgen05.mma with A = P from TMEM, B = V rows from SMEM
+//                   (MN-major), N = 64: P_hi V + P_lo V.
+//   epilogue        tcgen05.ld the O row, * 1/l, RNE to 16 bit, SMEM
+//                   transpose, coalesced 128-byte row stores.
 //
-// The whole sequence's S stays in TMEM (n <= 256 -> <= 256 columns) so the row
-// max is final before any P is formed: the plain two-pass softmax the oracle
-// defines, no online rescaling of O needed.  TMEM columns: 64 * ceil(n16/64)
-// for S/P + 64 for O, rounded to a power of two (128 for n <= 64, the C3 case;
-// 3 CTAs/SM then share 384 of the SM's 512 columns).  Queries beyond 128 rows
-// (n > 128) run as a second M-tile reusing the same TMEM.
+// TMEM: one 512-column allocation per CTA, issued before anything else (a
+// resident tcgen05 CTA that has not yet allocated holds back the launch of the
+// next CTA on its SM -- measured); each slot owns a fixed 128
+// columns: S/P chunk [0, 64) + O [64, 128).  Warps whose 32 query rows are all
+// padding (n < 128) skip the softmax and epilogue work.
 #pragma once
 
 namespace ragged {
 
-constexpr int kTcTile = 128;   // UMMA M: query rows per tile (one per thread)
-constexpr int kTcChunk = 64;   // keys per softmax chunk = 64 fp32 TMEM columns
+constexpr int kTcTile = 128;   // UMMA M: query rows per tile (one per slot thread)
+constexpr int kTcChunk = 64;   // keys per S/P chunk = 64 fp32 TMEM columns
+constexpr int kTcSlotThreads = 128;
 
 struct TcSmem {
-  int kv_rows, off_q, off_k, off_v, off_small, bytes;
+  int kv_rows, off_q, off_k, off_v, off_small, slot_bytes;
 };
+// Per-slot layout (1024-B aligned SW128 tiles), then 1 KB of CTA-wide state.
 __host__ __device__ inline TcSmem tc_smem(int N) {
   TcSmem L;
   L.kv_rows = (N + 15) & ~15;
   L.off_q = 0;                                     // 128 x 128 B Q tile; O staging later
-  L.off_k = kTcTile * kRowBytes;                   // kv_rows x 128 B, 1024-B aligned
+  L.off_k = kTcTile * kRowBytes;                   // kv_rows x 128 B
   L.off_v = L.off_k + L.kv_rows * kRowBytes;
-  L.off_small = L.off_v + L.kv_rows * kRowBytes;   // pos, drop, ballots, mbarriers, TMEM slot
-  L.bytes = L.off_small + 2048 + 1024;             // + slack to align the base to 1024 B
+  L.off_small = L.off_v + L.kv_rows * kRowBytes;   // pos, drop, ballots, scan scratch, mbarriers
+  L.slot_bytes = L.off_small + 2048;
   return L;
+}
+__host__ __device__ inline int tc_smem_bytes(int N, int nslots) {
+  return nslots * tc_smem(N).slot_bytes + 1024 /*CTA state*/ + 1024 /*alignment slack*/;
+}
+// Slots per CTA: as many as fit in the 227 KB per-CTA shared memory (max 3).
+__host__ __device__ inline int tc_slots(int N) {
+  for (int s = 3; s > 1; --s)
+    if (tc_smem_bytes(N, s) <= 227 * 1024) return s;
+  return 1;
 }
 
 template <typename T, bool kFused>
-__global__ void __launch_bounds__(kAttnThreads, 3) attn_tc_kernel(const AttnArgs a) {
+__global__ void __launch_bounds__(3 * kTcSlotThreads, 1) attn_tc_kernel(const AttnArgs a, int nwork) {
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // SW128 atoms
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  const int nslots = blockDim.x / kTcSlotThreads;
+  const int slot = threadIdx.x / kTcSlotThreads, tid = threadIdx.x % kTcSlotThreads;
+  const int warp = tid >> 5;  // == CTA warp index % 4: this warp's TMEM lane quarter
   const TcSmem L = tc_smem(a.N);
-  uint8_t* sQ = smem + L.off_q;
-  uint8_t* sK = smem + L.off_k;
-  uint8_t* sV = smem + L.off_v;
-  uint8_t* small = smem + L.off_small;
+  uint8_t* base = smem + slot * L.slot_bytes;
+  uint8_t* sQ = base + L.off_q;
+  uint8_t* sK = base + L.off_k;
+  uint8_t* sV = base + L.off_v;
+  uint8_t* small = base + L.off_small;
   int16_t* sPos = reinterpret_cast<int16_t*>(small);
   int16_t* sDrop = sPos + kMaxN;
-  uint32_t* sWords = reinterpret_cast<uint32_t*>(sDrop + kMaxN);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(small + 1088);
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(small + 1104);
-  const int tid = threadIdx.x, warp = tid >> 5;
+  uint32_t* sWords = reinterpret_cast<uint32_t*>(sDrop + kMaxN);         // 32 B
+  uint64_t* bars = reinterpret_cast<uint64_t*>(small + 1056);            // 2 x 8 B
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(smem + nslots * L.slot_bytes);
+  auto sync = [slot] { asm volatile("bar.sync %0, %1;" ::"r"(slot + 1), "r"(kTcSlotThreads) : "memory"); };
 
   TL(0);
-  int bid = blockIdx.x;
-  if constexpr (kFused) {
-    if (a.cu_out != nullptr) {
-      if (bid == 0) {
-        scan_cta_cu(a, sK);
-        return;
-      }
-      bid -= 1;
-    }
-  }
-  const int b = bid / a.H, h = bid - b * a.H;  // head fastest
-  const long long HD = (long long)a.H * kHeadDim;
-  int n;
-  long long row_base;
-  image_rows<kFused>(a, b, sPos, sDrop, sWords, n, row_base);
-
-  const int ldb = (kFused ? (int)a.ld : (int)HD) * 2;
-  const int HDb = (int)HD * 2;
-  const char* img_q = static_cast<const char*>(a.q) + row_base * ldb + h * kRowBytes;
-  const char* img_k = static_cast<const char*>(a.k) + row_base * ldb + h * kRowBytes;
-  const char* img_v = static_cast<const char*>(a.v) + row_base * ldb + h * kRowBytes;
-  char* img_o = static_cast<char*>(a.o) + row_base * HDb + h * kRowBytes + (tid & 7) * 16;
-
-  auto zero_dropped = [&]() {  // dropped rows of this head -> +0.0
-    if constexpr (kFused) {
-      const int nd = a.N - n;
-      const uint4 z = make_uint4(0u, 0u, 0u, 0u);
-      for (int rr = tid >> 3; rr < nd; rr += kAttnThreads / 8) st_global_16(img_o + sDrop[rr] * HDb, z);
-    }
-  };
-  if (n == 0) {  // nothing to attend (R11); returns before any TMEM allocation
-    zero_dropped();
-    return;
-  }
-
-  const int n16 = (n + 15) & ~15;
-  const int nchunks = (n16 + kTcChunk - 1) / kTcChunk;  // 1..4
-  const int o_col = nchunks * kTcChunk;                  // O columns after S/P
-  const uint32_t ncols = o_col + 64 <= 128 ? 128u : (o_col + 64 <= 256 ? 256u : 512u);
-
-  if (warp == 0) tc::alloc(smem_u32(tslot), ncols);
+  const uint32_t ncols_cta = nslots > 2 ? 512u : (nslots > 1 ? 256u : 128u);
+  if (threadIdx.x < 32) tc::alloc(smem_u32(tslot), ncols_cta);  // first thing: see header
   if (tid == 32) {
     tc::mbar_init(smem_u32(&bars[0]), 1);
     tc::mbar_init(smem_u32(&bars[1]), 1);
     tc::fence_mbar_init();
   }
-
-  // ---- stage K, V rows [0, n16) (zero past n: P = 0 there, V must be finite) ---
-  {
-    const int c = tid & 7, t = (tid >> 3) & 1, r0 = tid >> 4;
-    const char* gsrc = (t ? img_v : img_k) + c * 16;
-    uint32_t sdst = smem_u32(t ? sV : sK) + r0 * kRowBytes + ((c ^ r0) << 4);
-    for (int r = r0; r < n16; r += 8, sdst += 8 * kRowBytes) {
-      const bool valid = r < n;
-      cp_async_16(sdst, gsrc + (valid ? sPos[r] * ldb : 0), valid ? 16 : 0);
-    }
-  }
-  // Q tile rows [0, min(128, n - 128 tile)); rows past n stay unwritten: they
-  // only feed their own (discarded) S / O rows.
-  auto load_q_tile = [&](int tile) {
-    const int c = tid & 7, r0 = tid >> 3;
-    const int rows = min(kTcTile, n - tile * kTcTile);
-    const char* gsrc = img_q + c * 16;
-    uint32_t sdst = smem_u32(sQ) + r0 * kRowBytes + ((c ^ (r0 & 7)) << 4);
-    for (int rr = r0; rr < rows; rr += 16, sdst += 16 * kRowBytes)
-      cp_async_16(sdst, gsrc + sPos[tile * kTcTile + rr] * ldb, 16);
-  };
-  load_q_tile(0);
-  cp_async_commit();
-  zero_dropped();  // overlaps the gathers in flight
-  TL(2);
-  cp_async_wait_all();
-  tc::fence_proxy_async_smem();
   tc::fence_before();
   __syncthreads();
   tc::fence_after();
-  TL(3);
-
-  const uint32_t tbase = *tslot;
-  const uint32_t trow = tbase + ((uint32_t)(warp * 32) << 16);  // this warp's 32 lanes
-  constexpr uint32_t kFmt = std::is_same<T, __nv_bfloat16>::value ? 1u : 0u;
-  const uint32_t idesc_s = tc::idesc_f16(kFmt, kTcTile, n16, 0);
-  const uint32_t idesc_o = tc::idesc_f16(kFmt, kTcTile, kHeadDim, 1);
+  const uint32_t tbase = *tslot + (uint32_t)(slot * 128);        // this slot's 128 columns
+  const uint32_t tS = tbase, tO = tbase + 64;
+  const uint32_t lane_off = (uint32_t)(warp * 32) << 16;          // this warp's 32 lanes
   const uint32_t bar_s = smem_u32(&bars[0]), bar_o = smem_u32(&bars[1]);
+  uint32_t ph_s = 0, ph_o = 0;
+  constexpr uint32_t kFmt = std::is_same<T, __nv_bfloat16>::value ? 1u : 0u;
+  const uint32_t idesc_o = tc::idesc_f16(kFmt, kTcTile, kHeadDim, 1);
   constexpr float kScaleLog2 = 0.18033688011112042f;  // log2(e) / sqrt(64)
-  uint32_t phase = 0;
+  const long long HD = (long long)a.H * kHeadDim;
+  const int HDb = (int)HD * 2;
+  const int P = a.B * a.H;
 
-  for (int tile = 0; tile * kTcTile < n; ++tile) {
-    if (tile > 0) {
-      load_q_tile(tile);
+  for (int w = blockIdx.x + gridDim.x * slot; w < nwork; w += gridDim.x * nslots) {
+    if constexpr (kFused) {
+      if (w == P) {  // the cu_seqlens work item (only present when requested)
+        scan_cta_cu(a, sK, tid, sync);  // sK (>= 2 KB) is free during this item
+        continue;
+      }
+    }
+    const int b = w / a.H, h = w - b * a.H;
+    int n;
+    long long row_base;
+    image_rows<kFused>(a, b, sPos, sDrop, sWords, n, row_base, tid, sync);
+
+    const int ldb = (kFused ? (int)a.ld : (int)HD) * 2;
+    const char* img_q = static_cast<const char*>(a.q) + row_base * ldb + h * kRowBytes;
+    const char* img_k = static_cast<const char*>(a.k) + row_base * ldb + h * kRowBytes;
+    const char* img_v = static_cast<const char*>(a.v) + row_base * ldb + h * kRowBytes;
+    char* img_o = static_cast<char*>(a.o) + row_base * HDb + h * kRowBytes + (tid & 7) * 16;
+    auto zero_dropped = [&]() {  // dropped rows of this head -> +0.0
+      if constexpr (kFused) {
+        const int nd = a.N - n;
+        const uint4 z = make_uint4(0u, 0u, 0u, 0u);
+        for (int rr = tid >> 3; rr < nd; rr += kTcSlotThreads / 8) st_global_16(img_o + sDrop[rr] * HDb, z);
+      }
+    };
+    if (n == 0) {  // nothing to attend (R11)
+      zero_dropped();
+      sync();      // sPos / sDrop are rewritten by the next problem
+      continue;
+    }
+    const int n16 = (n + 15) & ~15;
+    const int nchunks = (n16 + kTcChunk - 1) / kTcChunk;
+
+    // ---- stage K, V rows [0, n16) (zero past n: P = 0 there, V must be finite)
+    {
+      const int c = tid & 7, t = (tid >> 3) & 1, r0 = tid >> 4;
+      const char* gsrc = (t ? img_v : img_k) + c * 16;
+      uint32_t sdst = smem_u32(t ? sV : sK) + r0 * kRowBytes + ((c ^ r0) << 4);
+      for (int r = r0; r < n16; r += 8, sdst += 8 * kRowBytes) {
+        const bool valid = r < n;
+        cp_async_16(sdst, gsrc + (valid ? sPos[r] * ldb : 0), valid ? 16 : 0);
+      }
+    }
+    // Q tile rows [0, min(128, n - 128 tile)); rows past n stay unwritten: they
+    // only feed their own (discarded) S / O rows.
+    auto load_q_tile = [&](int tile) {
+      const int c = tid & 7, r0 = tid >> 3;
+      const int rows = min(kTcTile, n - tile * kTcTile);
+      const char* gsrc = img_q + c * 16;
+      uint32_t sdst = smem_u32(sQ) + r0 * kRowBytes + ((c ^ (r0 & 7)) << 4);
+      for (int rr = r0; rr < rows; rr += 16, sdst += 16 * kRowBytes)
+        cp_async_16(sdst, gsrc + sPos[tile * kTcTile + rr] * ldb, 16);
+    };
+    load_q_tile(0);
+    cp_async_commit();
+    zero_dropped();  // overlaps the gathers in flight
+    TL(2);
+
+    for (int tile = 0; tile * kTcTile < n; ++tile) {
+      if (tile > 0) load_q_tile(tile);
       cp_async_commit();
       cp_async_wait_all();
       tc::fence_proxy_async_smem();
-      __syncthreads();
-    }
-    // ---- S = Q K^T: 4 UMMA of K = 16 (+32 B along the SW128 rows each) -------
-    if (tid == 0) {
-      tc::fence_after();
-      const uint64_t qd = tc::sw128_desc(smem_u32(sQ)), kd = tc::sw128_desc(smem_u32(sK));
-#pragma unroll
-      for (int kk = 0; kk < 4; ++kk) tc::mma_ss(tbase, qd + 2 * kk, kd + 2 * kk, idesc_s, kk > 0);
-      tc::commit(bar_s);
-    }
-    tc::mbar_wait(bar_s, phase);
-    tc::fence_after();
-    TL(5);
+      tc::fence_before();
+      sync();
+      TL(3);
+      const bool warp_live = tile * kTcTile + warp * 32 < n;  // any real query row in this warp
+      float m_ref = -INFINITY, l = 0.f;                       // Alg. 1 state (raw score units)
 
-    // ---- softmax, one row per thread: pass A row max, pass B P (hi, lo) -> TMEM
-    float m = -INFINITY;
-    if (nchunks > 1) {
-      for (int c0 = 0; c0 < n16; c0 += 32) {
-        uint32_t r[32];
-        tc::ld_x32(trow + c0, r);
-        tc::wait_ld();
-#pragma unroll
-        for (int i = 0; i < 32; ++i)
-          if (c0 + i < n) m = fmaxf(m, __uint_as_float(r[i]));
-      }
-    }
-    float l = 0.f;
-    for (int j = 0; j < nchunks; ++j) {
-      const int c0 = j * kTcChunk;
-      const bool two = c0 + 32 < n16;  // CTA-uniform
-      uint32_t ra[32], rb[32];
-      tc::ld_x32(trow + c0, ra);
-      if (two) tc::ld_x32(trow + c0 + 32, rb);
-      tc::wait_ld();
-      if (nchunks == 1) {  // single chunk: the max comes from the same registers
-#pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          if (c0 + i < n) m = fmaxf(m, __uint_as_float(ra[i]));
-          if (two && c0 + 32 + i < n) m = fmaxf(m, __uint_as_float(rb[i]));
-        }
-      }
-      const float ms = m * kScaleLog2;
-      uint32_t hi[16], lo[16];
-#pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        const int k0 = c0 + 2 * i;
-        const float p0 = k0 < n ? ex2(__uint_as_float(ra[2 * i]) * kScaleLog2 - ms) : 0.f;
-        const float p1 = k0 + 1 < n ? ex2(__uint_as_float(ra[2 * i + 1]) * kScaleLog2 - ms) : 0.f;
-        l += p0 + p1;
-        split2<T>(p0, p1, hi[i], lo[i]);
-      }
-      tc::st_x16(trow + c0, hi);        // P_hi keys c0..c0+31 -> cols c0 .. c0+15
-      tc::st_x16(trow + c0 + 32, lo);   // P_lo               -> cols c0+32 .. c0+47
-      if (two) {
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          const int k0 = c0 + 32 + 2 * i;
-          const float p0 = k0 < n ? ex2(__uint_as_float(rb[2 * i]) * kScaleLog2 - ms) : 0.f;
-          const float p1 = k0 + 1 < n ? ex2(__uint_as_float(rb[2 * i + 1]) * kScaleLog2 - ms) : 0.f;
-          l += p0 + p1;
-          split2<T>(p0, p1, hi[i], lo[i]);
-        }
-        tc::st_x16(trow + c0 + 16, hi);  // keys c0+32..c0+63 -> cols c0+16 .. c0+31
-        tc::st_x16(trow + c0 + 48, lo);  //                   -> cols c0+48 .. c0+63
-      }
-    }
-    tc::wait_st();
-    tc::fence_before();
-    __syncthreads();
-
-    // ---- O = P_hi V + P_lo V over all key chunks (K = 16 keys per UMMA) -------
-    if (tid == 0) {
-      tc::fence_after();
-      uint32_t acc = 0;
       for (int j = 0; j < nchunks; ++j) {
-        const int nk = (min(kTcChunk, n - j * kTcChunk) + 15) >> 4;
-        for (int kk = 0; kk < nk; ++kk) {
-          const uint64_t vd = tc::sw128_desc(smem_u32(sV) + (j * kTcChunk + kk * 16) * kRowBytes);
-          tc::mma_ts(tbase + o_col, tbase + j * kTcChunk + kk * 8, vd, idesc_o, acc);
-          tc::mma_ts(tbase + o_col, tbase + j * kTcChunk + 32 + kk * 8, vd, idesc_o, 1u);
-          acc = 1u;
+        const int kc = min(kTcChunk, n16 - j * kTcChunk);     // keys in chunk (multiple of 16)
+        // ---- S_j = Q K_j^T: 4 UMMA of K = 16 (+32 B along the SW128 rows each)
+        if (tid == 0) {
+          tc::fence_after();
+          const uint64_t qd = tc::sw128_desc(smem_u32(sQ));
+          const uint64_t kd = tc::sw128_desc(smem_u32(sK) + j * kTcChunk * kRowBytes);
+          const uint32_t idesc_s = tc::idesc_f16(kFmt, kTcTile, kc, 0);
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk) tc::mma_ss(tS, qd + 2 * kk, kd + 2 * kk, idesc_s, kk > 0);
+          tc::commit(bar_s);
+        }
+        tc::mbar_wait(bar_s, ph_s);
+        ph_s ^= 1u;
+        tc::fence_after();
+        TL(5);
+
+        if (warp_live) {
+          const int c0 = j * kTcChunk;
+          const bool two = kc > 32;  // slot-uniform
+          uint32_t ra[32], rb[32];
+          tc::ld_x32(tS + lane_off, ra);
+          if (two) tc::ld_x32(tS + lane_off + 32, rb);
+          tc::wait_ld();
+          float mc = -INFINITY;
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            if (c0 + i < n) mc = fmaxf(mc, __uint_as_float(ra[i]));
+            if (two && c0 + 32 + i < n) mc = fmaxf(mc, __uint_as_float(rb[i]));
+          }
+          float alpha = 1.f;
+          if (j == 0) {
+            m_ref = mc;
+          } else if ((mc - m_ref) * kScaleLog2 > 8.f) {  // lazy: P stays <= 2^8 otherwise
+            alpha = ex2((m_ref - mc) * kScaleLog2);
+            m_ref = mc;
+          }
+          if (j > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {  // O *= alpha (PV_{j-1} is done)
+#pragma unroll 1
+            for (int q = 0; q < 4; ++q) {
+              uint32_t s16[16];
+              tc::ld_x16(tO + lane_off + 16 * q, s16);
+              tc::wait_ld();
+#pragma unroll
+              for (int i = 0; i < 16; ++i) s16[i] = __float_as_uint(__uint_as_float(s16[i]) * alpha);
+              tc::st_x16(tO + lane_off + 16 * q, s16);
+            }
+          }
+          l *= alpha;
+          const float ms = m_ref * kScaleLog2;
+          uint32_t hi[16], lo[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const int k0 = c0 + 2 * i;
+            const float p0 = k0 < n ? ex2(__uint_as_float(ra[2 * i]) * kScaleLog2 - ms) : 0.f;
+            const float p1 = k0 + 1 < n ? ex2(__uint_as_float(ra[2 * i + 1]) * kScaleLog2 - ms) : 0.f;
+            l += p0 + p1;
+            split2<T>(p0, p1, hi[i], lo[i]);
+          }
+          tc::st_x16(tS + lane_off, hi);       // P_hi keys c0..c0+31 -> cols 0 .. 15
+          tc::st_x16(tS + lane_off + 32, lo);  // P_lo               -> cols 32 .. 47
+          if (two) {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+              const int k0 = c0 + 32 + 2 * i;
+              const float p0 = k0 < n ? ex2(__uint_as_float(rb[2 * i]) * kScaleLog2 - ms) : 0.f;
+              const float p1 = k0 + 1 < n ? ex2(__uint_as_float(rb[2 * i + 1]) * kScaleLog2 - ms) : 0.f;
+              l += p0 + p1;
+              split2<T>(p0, p1, hi[i], lo[i]);
+            }
+            tc::st_x16(tS + lane_off + 16, hi);  // keys c0+32..c0+63 -> cols 16 .. 31
+            tc::st_x16(tS + lane_off + 48, lo);  //                   -> cols 48 .. 63
+          }
+          tc::wait_st();
+        }
+        tc::fence_before();
+        sync();
+        TL(8);
+        // ---- O += P_hi V_j + P_lo V_j (K = 16 keys per UMMA) --------------------
+        if (tid == 0) {
+          tc::fence_after();
+          const int nk = (min(kTcChunk, n - j * kTcChunk) + 15) >> 4;
+          for (int kk = 0; kk < nk; ++kk) {
+            const uint64_t vd = tc::sw128_desc(smem_u32(sV) + (j * kTcChunk + kk * 16) * kRowBytes);
+            tc::mma_ts(tO, tS + kk * 8, vd, idesc_o, (j > 0 || kk > 0) ? 1u : 0u);
+            tc::mma_ts(tO, tS + 32 + kk * 8, vd, idesc_o, 1u);
+          }
+          tc::commit(bar_o);
+        }
+        tc::mbar_wait(bar_o, ph_o);  // before S_{j+1} overwrites P_j, and before the epilogue
+        ph_o ^= 1u;
+        tc::fence_after();
+        TL(9);
+      }
+
+      // ---- epilogue: O / l -> 16 bit -> SMEM (sQ is free) -> 128-byte row stores
+      if (warp_live) {
+        const float inv = 1.f / l;
+        uint32_t oa[32], ob[32];
+        tc::ld_x32(tO + lane_off, oa);
+        tc::ld_x32(tO + lane_off + 32, ob);
+        tc::wait_ld();
+        uint8_t* srow = sQ + tid * kRowBytes;
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          const uint32_t* s8 = c < 4 ? &oa[8 * c] : &ob[8 * (c - 4)];
+          uint4 v;
+          v.x = pack2<T>(__uint_as_float(s8[0]) * inv, __uint_as_float(s8[1]) * inv);
+          v.y = pack2<T>(__uint_as_float(s8[2]) * inv, __uint_as_float(s8[3]) * inv);
+          v.z = pack2<T>(__uint_as_float(s8[4]) * inv, __uint_as_float(s8[5]) * inv);
+          v.w = pack2<T>(__uint_as_float(s8[6]) * inv, __uint_as_float(s8[7]) * inv);
+          *reinterpret_cast<uint4*>(srow + ((c ^ (tid & 7)) << 4)) = v;
         }
       }
-      tc::commit(bar_o);
-    }
-    tc::mbar_wait(bar_o, phase);
-    tc::fence_after();
-    phase ^= 1u;
-
-    // ---- epilogue: O / l -> 16 bit -> SMEM (sQ is free) -> 128-byte row stores
-    {
-      const float inv = 1.f / l;
-      uint32_t oa[32], ob[32];
-      tc::ld_x32(trow + o_col, oa);
-      tc::ld_x32(trow + o_col + 32, ob);
-      tc::wait_ld();
-      uint8_t* srow = sQ + tid * kRowBytes;
-#pragma unroll
-      for (int c = 0; c < 8; ++c) {
-        const uint32_t* s8 = c < 4 ? &oa[8 * c] : &ob[8 * (c - 4)];
-        uint4 v;
-        v.x = pack2<T>(__uint_as_float(s8[0]) * inv, __uint_as_float(s8[1]) * inv);
-        v.y = pack2<T>(__uint_as_float(s8[2]) * inv, __uint_as_float(s8[3]) * inv);
-        v.z = pack2<T>(__uint_as_float(s8[4]) * inv, __uint_as_float(s8[5]) * inv);
-        v.w = pack2<T>(__uint_as_float(s8[6]) * inv, __uint_as_float(s8[7]) * inv);
-        *reinterpret_cast<uint4*>(srow + ((c ^ (tid & 7)) << 4)) = v;
+      tc::fence_before();
+      sync();
+      TL(6);
+      {
+        const int rows = min(kTcTile, n - tile * kTcTile);
+        for (int rr = tid >> 3; rr < rows; rr += kTcSlotThreads / 8) {
+          const uint4 v = *reinterpret_cast<const uint4*>(sQ + rr * kRowBytes + (((tid & 7) ^ (rr & 7)) << 4));
+          st_global_16(img_o + sPos[tile * kTcTile + rr] * HDb, v);
+        }
       }
+      sync();  // sQ, sPos, TMEM are reused by the next tile / problem
     }
-    tc::fence_before();
-    __syncthreads();
-    TL(6);
-    {
-      const int rows = min(kTcTile, n - tile * kTcTile);
-      for (int rr = tid >> 3; rr < rows; rr += kAttnThreads / 8) {
-        const uint4 v = *reinterpret_cast<const uint4*>(sQ + rr * kRowBytes + (((tid & 7) ^ (rr & 7)) << 4));
-        st_global_16(img_o + sPos[tile * kTcTile + rr] * HDb, v);
-      }
-    }
-    __syncthreads();  // sQ and TMEM are reused by the next tile
   }
-  if (warp == 0) {
+  tc::fence_before();
+  __syncthreads();
+  if (threadIdx.x < 32) {
     tc::fence_after();
-    tc::dealloc(tbase, ncols);
+    tc::dealloc(*tslot, ncols_cta);
   }
 #ifdef RAGGED_TIMELINE
-  __syncthreads();
   TL(4);
 #endif
 }

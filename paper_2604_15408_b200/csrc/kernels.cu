@@ -34,7 +34,7 @@ namespace ragged {
 // Optional per-CTA timeline (debug build libragged_tl.so only, -DRAGGED_TIMELINE):
 // %globaltimer stamps at the phase boundaries of the attention CTA.
 #ifdef RAGGED_TIMELINE
-constexpr int kTlSlots = 8;
+constexpr int kTlSlots = 16;
 constexpr int kTlMaxCtas = 1 << 16;
 __device__ unsigned long long g_timeline[kTlMaxCtas * kTlSlots];
 __device__ __forceinline__ void tl_stamp(int slot) {
@@ -59,17 +59,20 @@ __device__ __forceinline__ void tl_stamp(int slot) {
 // ballots its images' keep bytes (<= 8 words of 32 positions), warp 0 scans
 // the per-image counts, then each warp writes dst/src of its images.
 // Deterministic: no atomics; bit-exact integer output.
-template <int kThreads, int kIPW, bool kWriteIdx>
+// `tid` in [0, kThreads) and `sync` (a barrier over exactly those threads) let
+// a sub-group of a larger CTA run it (the tcgen05 engine's slots).
+// Scratch: s_words [CH*8], s_cnt [CH], s_off [CH], s_carry [1].
+template <int kThreads, int kIPW, bool kWriteIdx, typename Sync>
 __device__ void scan_cta(const uint8_t* __restrict__ keep, int B, int N, int32_t* __restrict__ cu,
                          int32_t* __restrict__ dst, int32_t* __restrict__ src, uint32_t* s_words,
-                         int32_t* s_cnt, int32_t* s_off) {
+                         int32_t* s_cnt, int32_t* s_off, int32_t* s_carry_p, int tid, Sync sync) {
   constexpr int kWarps = kThreads / 32;
   constexpr int CH = kWarps * kIPW;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int warp = tid >> 5, lane = tid & 31;
   const int nw = (N + 31) >> 5;
   const uint32_t lt = (1u << lane) - 1u;
-  __shared__ int32_t s_carry;
-  if (threadIdx.x == 0) {
+  int32_t& s_carry = *s_carry_p;
+  if (tid == 0) {
     cu[0] = 0;
     s_carry = 0;
   }
@@ -97,7 +100,7 @@ __device__ void scan_cta(const uint8_t* __restrict__ keep, int B, int N, int32_t
       }
       if (lane == 0) s_cnt[li] = cnt;
     }
-    __syncthreads();
+    sync();
     // phase B: exclusive scan of the CH counts (warp 0), plus the running carry.
     if (warp == 0) {
       constexpr int PER = (CH + 31) / 32;
@@ -126,7 +129,7 @@ __device__ void scan_cta(const uint8_t* __restrict__ keep, int B, int N, int32_t
       __syncwarp();
       if (lane == 0) s_carry += total;
     }
-    __syncthreads();
+    sync();
     // phase C: cu[i+1], and per-token dst / src.
 #pragma unroll
     for (int u = 0; u < kIPW; ++u) {
@@ -150,7 +153,7 @@ __device__ void scan_cta(const uint8_t* __restrict__ keep, int B, int N, int32_t
         }
       }
     }
-    __syncthreads();
+    sync();
   }
 }
 
@@ -164,7 +167,9 @@ __global__ void __launch_bounds__(kScanThreads, 1)
   __shared__ uint32_t s_words[CH * 8];
   __shared__ int32_t s_cnt[CH];
   __shared__ int32_t s_off[CH];
-  scan_cta<kScanThreads, kScanIPW, true>(keep, B, N, cu, dst, src, s_words, s_cnt, s_off);
+  __shared__ int32_t s_carry;
+  scan_cta<kScanThreads, kScanIPW, true>(keep, B, N, cu, dst, src, s_words, s_cnt, s_off, &s_carry,
+                                         (int)threadIdx.x, [] { __syncthreads(); });
 }
 
 // ---------------------------------------------------------------- pack ----
@@ -270,11 +275,13 @@ struct AttnArgs {
 
 // Block 0 of a fused launch that also emits cu_seqlens: one CTA walks the keep
 // mask (scan_cta, counts only) while the other CTAs attend.
-__device__ __forceinline__ void scan_cta_cu(const AttnArgs& a, uint8_t* scratch) {
+template <typename Sync>
+__device__ __forceinline__ void scan_cta_cu(const AttnArgs& a, uint8_t* scratch, int tid, Sync sync) {
   constexpr int CH = kAttnThreads / 32 * 8;
   uint32_t* w = reinterpret_cast<uint32_t*>(scratch);
   int32_t* c = reinterpret_cast<int32_t*>(w + CH * 8);
-  scan_cta<kAttnThreads, 8, false>(a.keep, a.B, a.N, a.cu_out, nullptr, nullptr, w, c, c + CH);
+  scan_cta<kAttnThreads, 8, false>(a.keep, a.B, a.N, a.cu_out, nullptr, nullptr, w, c, c + CH,
+                                   c + 2 * CH, tid, sync);
 }
 
 // The rows of problem (image b, one head): kept positions sPos[0, n) (ascending,
@@ -283,10 +290,11 @@ __device__ __forceinline__ void scan_cta_cu(const AttnArgs& a, uint8_t* scratch)
 //           row_base = b * N (padded rows).
 //   packed: n = cu[b+1] - cu[b], sPos[r] = r; row_base = cu[b] (packed rows).
 // Ends with __syncthreads().  Requires blockDim.x == kAttnThreads, N <= 256.
-template <bool kFused>
+template <bool kFused, typename Sync>
 __device__ __forceinline__ void image_rows(const AttnArgs& a, int b, int16_t* sPos, int16_t* sDrop,
-                                           uint32_t* sWords, int& n, long long& row_base) {
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+                                           uint32_t* sWords, int& n, long long& row_base, int tid,
+                                           Sync sync) {
+  const int warp = tid >> 5, lane = tid & 31;
   if constexpr (kFused) {
     const uint8_t* km = a.keep + (long long)b * a.N;
     const int p0 = tid, p1 = tid + kAttnThreads;
@@ -298,7 +306,7 @@ __device__ __forceinline__ void image_rows(const AttnArgs& a, int b, int16_t* sP
       sWords[warp] = w0;
       sWords[4 + warp] = w1;
     }
-    __syncthreads();
+    sync();
     int pre0 = 0, pre1 = 0;
     n = 0;
 #pragma unroll
@@ -318,14 +326,14 @@ __device__ __forceinline__ void image_rows(const AttnArgs& a, int b, int16_t* sP
       if (k1) sPos[r1] = (int16_t)p1; else sDrop[p1 - r1] = (int16_t)p1;
     }
     row_base = (long long)b * a.N;
-    __syncthreads();
+    sync();
     TL(1);
   } else {
     const int s = a.cu[b];
     n = min(max(a.cu[b + 1] - s, 0), a.N);
     row_base = s;
     for (int r = tid; r < kMaxN; r += kAttnThreads) sPos[r] = (int16_t)r;
-    __syncthreads();
+    sync();
   }
 }
 
@@ -346,7 +354,7 @@ __global__ void __launch_bounds__(kAttnThreads, 3) attn_kernel(const AttnArgs a)
   if constexpr (kFused) {
     if (a.cu_out != nullptr) {
       if (bid == 0) {  // the scan CTA: cu_seqlens only, concurrent with the rest
-        scan_cta_cu(a, sK);
+        scan_cta_cu(a, sK, tid, [] { __syncthreads(); });
         return;
       }
       bid -= 1;
@@ -361,7 +369,7 @@ __global__ void __launch_bounds__(kAttnThreads, 3) attn_kernel(const AttnArgs a)
 
   int n;
   long long row_base;
-  image_rows<kFused>(a, b, sPos, sDrop, sWords, n, row_base);
+  image_rows<kFused>(a, b, sPos, sDrop, sWords, n, row_base, tid, [] { __syncthreads(); });
   // Byte addressing: one 64-bit image base per tensor, then 32-bit row offsets
   // (pos < 256, token stride <= 2^23 bytes -- validated in api.cu).
   const int ldb = (kFused ? (int)a.ld : (int)HD) * 2;  // input token stride, bytes
@@ -603,33 +611,48 @@ cudaError_t launch_unpack(const void* op, const int32_t* dst, void* o, int B, in
   return cudaGetLastError();
 }
 
-template <typename T, bool kFused, bool kTc>
-static cudaError_t launch_attn_t(const AttnArgs& a, int grid, cudaStream_t st) {
-  // The max-dynamic-smem attribute is set once per device (for N = 256, which
-  // covers every N), so the steady-state launch path does no attribute work.
-  static bool done[64] = {false};
+// One-time (per device, per instantiation) max-dynamic-smem attribute, sized
+// for N = 256 so the steady-state launch path does no attribute work.
+template <typename Kern>
+static cudaError_t smem_attr_once(Kern kern, int max_bytes, bool (&done)[64]) {
   int dev = 0;
   cudaGetDevice(&dev);
-  auto kern = kTc ? attn_tc_kernel<T, kFused> : attn_kernel<T, kFused>;
-  const int max_bytes = kTc ? tc_smem(kMaxN).bytes : attn_smem_bytes(kMaxN);
-  const int bytes = kTc ? tc_smem(a.N).bytes : attn_smem_bytes(a.N);
-  if (dev < 0 || dev >= 64 || !done[dev]) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, max_bytes);
-    if (e != cudaSuccess) return e;
-    if (dev >= 0 && dev < 64) done[dev] = true;
-  }
-  kern<<<grid, kAttnThreads, bytes, st>>>(a);
+  if (dev >= 0 && dev < 64 && done[dev]) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, max_bytes);
+  if (e == cudaSuccess && dev >= 0 && dev < 64) done[dev] = true;
+  return e;
+}
+
+template <typename T, bool kFused>
+static cudaError_t launch_attn_mma(const AttnArgs& a, int grid, cudaStream_t st) {
+  static bool done[64] = {false};
+  cudaError_t e = smem_attr_once(attn_kernel<T, kFused>, attn_smem_bytes(kMaxN), done);
+  if (e != cudaSuccess) return e;
+  attn_kernel<T, kFused><<<grid, kAttnThreads, attn_smem_bytes(a.N), st>>>(a);
+  return cudaGetLastError();
+}
+
+// tcgen05 engine: persistent grid of min(#SMs, work items) CTAs x nslots slots.
+template <typename T, bool kFused>
+static cudaError_t launch_attn_tc(const AttnArgs& a, int nwork, cudaStream_t st) {
+  static bool done[64] = {false};
+  cudaError_t e = smem_attr_once(attn_tc_kernel<T, kFused>, 227 * 1024, done);
+  if (e != cudaSuccess) return e;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const int nslots = tc_slots(a.N);
+  const int grid = nwork < sm_count(dev) ? nwork : sm_count(dev);
+  attn_tc_kernel<T, kFused><<<grid, nslots * kTcSlotThreads, tc_smem_bytes(a.N, nslots), st>>>(a, nwork);
   return cudaGetLastError();
 }
 
 template <bool kFused>
-static cudaError_t dispatch_attn(int dtype, int engine, const AttnArgs& a, int grid, cudaStream_t st) {
-  const bool tc = engine == 2;
-  if (dtype == 0)
-    return tc ? launch_attn_t<__nv_bfloat16, kFused, true>(a, grid, st)
-              : launch_attn_t<__nv_bfloat16, kFused, false>(a, grid, st);
-  return tc ? launch_attn_t<__half, kFused, true>(a, grid, st)
-            : launch_attn_t<__half, kFused, false>(a, grid, st);
+static cudaError_t dispatch_attn(int dtype, int engine, const AttnArgs& a, int nwork, cudaStream_t st) {
+  if (engine == 2)
+    return dtype == 0 ? launch_attn_tc<__nv_bfloat16, kFused>(a, nwork, st)
+                      : launch_attn_tc<__half, kFused>(a, nwork, st);
+  return dtype == 0 ? launch_attn_mma<__nv_bfloat16, kFused>(a, nwork, st)
+                    : launch_attn_mma<__half, kFused>(a, nwork, st);
 }
 
 cudaError_t launch_attn(int dtype, int engine, const void* qp, const void* kp, const void* vp,

@@ -49,14 +49,16 @@ for mode in ("isolated", "back_to_back"):
         for i in range(S):
             rb.pack_attend_unpack(*sets[i], o=outs[i], cu=cus[i], engine=a.engine)
     torch.cuda.synchronize()
-    buf = np.zeros((ncta, 8), np.uint64)
+    buf = np.zeros((ncta, 16), np.uint64)
     n = lib.ragged_debug_timeline(buf.ctypes.data, ncta)
     assert n == ncta, n
-    t = buf[:, :7].astype(np.int64)
-    sm = buf[:, 7]
+    valid = buf[:, 0] != 0
+    t = buf[valid, :10].astype(np.int64)
+    sm = buf[valid, 15]
     t0 = t[:, 0].min()
     rel = (t - t0) / 1e3  # us
-    attn = rel[1:]       # CTA 0 is the scan CTA
+    # engine 1: CTA 0 is the scan CTA; engine 2: persistent CTAs (slot 0's last problem)
+    attn = rel[1:] if a.engine != 2 else rel
     d = {
         "start_us": np.percentile(attn[:, 0], [0, 50, 90, 100]).tolist(),
         "end_us": np.percentile(attn[:, 4], [0, 50, 90, 100]).tolist(),
@@ -67,8 +69,11 @@ for mode in ("isolated", "back_to_back"):
         "w0_qk_softmax_us": np.percentile(attn[:, 5] - attn[:, 3], [50, 90, 100]).tolist(),
         "w0_pv_epi_smem_us": np.percentile(attn[:, 6] - attn[:, 5], [50, 90, 100]).tolist(),
         "w0_store_to_end_us": np.percentile(attn[:, 4] - attn[:, 6], [50, 90, 100]).tolist(),
+        "tc_softmax_us": np.percentile(attn[:, 8] - attn[:, 5], [50, 90, 100]).tolist() if a.engine == 2 else None,
+        "tc_pv_us": np.percentile(attn[:, 9] - attn[:, 8], [50, 90, 100]).tolist() if a.engine == 2 else None,
+        "tc_epi_smem_us": np.percentile(attn[:, 6] - attn[:, 9], [50, 90, 100]).tolist() if a.engine == 2 else None,
         "cta_total_us": np.percentile(attn[:, 4] - attn[:, 0], [50, 90, 100]).tolist(),
-        "scan_cta_us": float(rel[0, 4] - rel[0, 0]) if rel[0, 4] > 0 else None,
+        "ctas": int(valid.sum()),
         "distinct_sms": int(len(set(sm.tolist()))),
     }
     res[mode] = d
