@@ -78,6 +78,7 @@ __global__ void __launch_bounds__(3 * kTcSlotThreads, 1) attn_tc_kernel(const At
   auto sync = [slot] { asm volatile("bar.sync %0, %1;" ::"r"(slot + 1), "r"(kTcSlotThreads) : "memory"); };
 
   TL(0);
+  pdl_launch_dependents();
   const uint32_t ncols_cta = nslots > 2 ? 512u : (nslots > 1 ? 256u : 128u);
   if (threadIdx.x < 32) tc::alloc(smem_u32(tslot), ncols_cta);  // first thing: see header
   if (tid == 32) {
@@ -88,6 +89,7 @@ __global__ void __launch_bounds__(3 * kTcSlotThreads, 1) attn_tc_kernel(const At
   tc::fence_before();
   __syncthreads();
   tc::fence_after();
+  pdl_wait_prerequisites();  // TMEM/barrier setup above overlaps the previous grid's tail
   const uint32_t tbase = *tslot + (uint32_t)(slot * 128);        // this slot's 128 columns
   const uint32_t tS = tbase, tO = tbase + 64;
   const uint32_t lane_off = (uint32_t)(warp * 32) << 16;          // this warp's 32 lanes
@@ -117,15 +119,16 @@ __global__ void __launch_bounds__(3 * kTcSlotThreads, 1) attn_tc_kernel(const At
     const char* img_k = static_cast<const char*>(a.k) + row_base * ldb + h * kRowBytes;
     const char* img_v = static_cast<const char*>(a.v) + row_base * ldb + h * kRowBytes;
     char* img_o = static_cast<char*>(a.o) + row_base * HDb + h * kRowBytes + (tid & 7) * 16;
-    auto zero_dropped = [&]() {  // dropped rows of this head -> +0.0
+    // Dropped rows of this head -> +0.0, by threads [t0, t0 + nthr) of the slot.
+    auto zero_dropped = [&](int t, int nthr) {
       if constexpr (kFused) {
         const int nd = a.N - n;
         const uint4 z = make_uint4(0u, 0u, 0u, 0u);
-        for (int rr = tid >> 3; rr < nd; rr += kTcSlotThreads / 8) st_global_16(img_o + sDrop[rr] * HDb, z);
+        for (int rr = t >> 3; rr < nd; rr += nthr >> 3) st_global_16(img_o + sDrop[rr] * HDb, z);
       }
     };
     if (n == 0) {  // nothing to attend (R11)
-      zero_dropped();
+      zero_dropped(tid, kTcSlotThreads);
       sync();      // sPos / sDrop are rewritten by the next problem
       continue;
     }
@@ -154,8 +157,10 @@ __global__ void __launch_bounds__(3 * kTcSlotThreads, 1) attn_tc_kernel(const At
     };
     load_q_tile(0);
     cp_async_commit();
-    zero_dropped();  // overlaps the gathers in flight
     TL(2);
+    // warps [live, 4) own no query row of tile 0: they write the zero rows while
+    // the others run the softmax; with no idle warp, every thread does it last.
+    const int live = n >= kTcTile ? 4 : (n + 31) >> 5;
 
     for (int tile = 0; tile * kTcTile < n; ++tile) {
       if (tile > 0) load_q_tile(tile);
@@ -167,6 +172,7 @@ __global__ void __launch_bounds__(3 * kTcSlotThreads, 1) attn_tc_kernel(const At
       TL(3);
       const bool warp_live = tile * kTcTile + warp * 32 < n;  // any real query row in this warp
       float m_ref = -INFINITY, l = 0.f;                       // Alg. 1 state (raw score units)
+      if (tile == 0 && live < 4 && warp >= live) zero_dropped(tid - live * 32, (4 - live) * 32);
 
       for (int j = 0; j < nchunks; ++j) {
         const int kc = min(kTcChunk, n16 - j * kTcChunk);     // keys in chunk (multiple of 16)
@@ -293,6 +299,10 @@ __global__ void __launch_bounds__(3 * kTcSlotThreads, 1) attn_tc_kernel(const At
         }
       }
       sync();  // sQ, sPos, TMEM are reused by the next tile / problem
+    }
+    if (live == 4) {
+      zero_dropped(tid, kTcSlotThreads);
+      sync();  // sDrop is rewritten by the next problem
     }
   }
   tc::fence_before();

@@ -11,6 +11,17 @@ constexpr int kHeadDim = 64;          // d = B_D = 64
 constexpr int kRowBytes = kHeadDim * 2;  // one head slice of one token: 128 B
 constexpr int kMaxN = 256;            // sequence-length cap (R12)
 
+// Programmatic dependent launch (PDL): every kernel of the library lets the
+// next kernel in the stream launch early (its CTAs become resident during our
+// tail) and waits for its own prerequisite grid before reading global inputs.
+// Both are no-ops when the launch carries no programmatic dependency.
+__device__ __forceinline__ void pdl_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void pdl_wait_prerequisites() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }

@@ -24,6 +24,7 @@
 #include <stdint.h>
 
 #include <type_traits>
+#include <utility>
 
 #include "device.cuh"
 #include "launch.h"
@@ -168,6 +169,8 @@ __global__ void __launch_bounds__(kScanThreads, 1)
   __shared__ int32_t s_cnt[CH];
   __shared__ int32_t s_off[CH];
   __shared__ int32_t s_carry;
+  pdl_launch_dependents();
+  pdl_wait_prerequisites();
   scan_cta<kScanThreads, kScanIPW, true>(keep, B, N, cu, dst, src, s_words, s_cnt, s_off, &s_carry,
                                          (int)threadIdx.x, [] { __syncthreads(); });
 }
@@ -185,6 +188,8 @@ __global__ void __launch_bounds__(kCopyThreads)
                 const uint8_t* __restrict__ v, const int32_t* __restrict__ cu,
                 const int32_t* __restrict__ src, uint8_t* __restrict__ qp, uint8_t* __restrict__ kp,
                 uint8_t* __restrict__ vp, int B, long long ld_bytes, int row_bytes) {
+  pdl_launch_dependents();
+  pdl_wait_prerequisites();
   const int T = cu[B];
   const int cpr = row_bytes >> 4;  // chunks per tensor row
   const int per_row = 3 * cpr;
@@ -223,6 +228,8 @@ constexpr int kUnpackRows = 4;
 __global__ void __launch_bounds__(kCopyThreads)
     unpack_kernel(const uint8_t* __restrict__ op, const int32_t* __restrict__ dst,
                   uint8_t* __restrict__ o, long long BN, int row_bytes) {
+  pdl_launch_dependents();
+  pdl_wait_prerequisites();
   const int cpr = row_bytes >> 4;
   for (long long r0 = (long long)blockIdx.x * kUnpackRows; r0 < BN;
        r0 += (long long)gridDim.x * kUnpackRows) {
@@ -350,6 +357,8 @@ __global__ void __launch_bounds__(kAttnThreads, 3) attn_kernel(const AttnArgs a)
   uint32_t* sWords = reinterpret_cast<uint32_t*>(sDrop + kMaxN);
 
   TL(0);
+  pdl_launch_dependents();
+  pdl_wait_prerequisites();
   int bid = blockIdx.x;
   if constexpr (kFused) {
     if (a.cu_out != nullptr) {
@@ -408,18 +417,25 @@ __global__ void __launch_bounds__(kAttnThreads, 3) attn_kernel(const AttnArgs a)
   if (warp * 16 < n) load_q(qwarp, warp);
   cp_async_commit();
 
-  if constexpr (kFused) {
-    // dropped rows of this head -> +0.0, overlapped with the gather in flight;
-    // 8 consecutive threads write one whole 128-byte row.
-    const int nd = a.N - n;
-    const uint4 z = make_uint4(0u, 0u, 0u, 0u);
-    for (int rr = tid >> 3; rr < nd; rr += kAttnThreads / 8)
-      st_global_16(img_o + sDrop[rr] * HDb, z);
-  }
   TL(2);
   cp_async_wait_all();
   __syncthreads();
   TL(3);
+
+  // Dropped rows of this head -> +0.0 (8 consecutive threads write one 128-byte
+  // row).  Issued by the warps that own no query slice, concurrently with the
+  // others' compute; if every warp has a slice, after the compute.  Keeping
+  // these stores out of the gather phase leaves the SM->L2 path to the gathers.
+  const int nsl = (n + 15) >> 4;
+  const int busy = nsl < 4 ? nsl : 4;  // warps [0, busy) own slices
+  auto zero_dropped = [&](int t, int nthr) {
+    if constexpr (kFused) {
+      const int nd = a.N - n;
+      const uint4 z = make_uint4(0u, 0u, 0u, 0u);
+      for (int rr = t >> 3; rr < nd; rr += nthr >> 3) st_global_16(img_o + sDrop[rr] * HDb, z);
+    }
+  };
+  if (busy < 4 && warp >= busy) zero_dropped(tid - busy * 32, (4 - busy) * 32);
 
   // ---- per-warp query slices: S = Q K^T, online softmax (Alg. 1), O += P V
   const int g = lane >> 2, t4 = lane & 3;
@@ -551,6 +567,7 @@ __global__ void __launch_bounds__(kAttnThreads, 3) attn_kernel(const AttnArgs a)
     __syncwarp();
     buf ^= 1;
   }
+  if (busy == 4) zero_dropped(tid, kAttnThreads);
 #ifdef RAGGED_TIMELINE
   __syncthreads();
   TL(4);
@@ -578,10 +595,26 @@ static int sm_count(int dev) {
 }
 
 
+// All launches carry the programmatic-stream-serialization attribute (PDL).
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                              cudaStream_t st, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
 cudaError_t launch_scan(const uint8_t* keep, int B, int N, int32_t* cu, int32_t* dst, int32_t* src,
                         cudaStream_t st) {
-  scan_kernel<<<1, kScanThreads, 0, st>>>(keep, B, N, cu, dst, src);
-  return cudaGetLastError();
+  return launch_pdl(scan_kernel, dim3(1), dim3(kScanThreads), 0, st, keep, B, N, cu, dst, src);
 }
 
 cudaError_t launch_pack(const void* q, const void* k, const void* v, long long ld_elems, int B, int N,
@@ -592,11 +625,11 @@ cudaError_t launch_pack(const void* q, const void* k, const void* v, long long l
   const long long cap_rows = (long long)B * N;
   const long long want = (cap_rows + kPackRows - 1) / kPackRows;
   const int grid = (int)(want < ((long long)sm_count(dev) * 8) ? (long long)(want) : (long long)((long long)sm_count(dev) * 8));
-  pack_kernel<<<grid, kCopyThreads, 0, st>>>(
-      static_cast<const uint8_t*>(q), static_cast<const uint8_t*>(k),
-      static_cast<const uint8_t*>(v), cu, src, static_cast<uint8_t*>(qp),
-      static_cast<uint8_t*>(kp), static_cast<uint8_t*>(vp), B, ld_elems * 2, H * kHeadDim * 2);
-  return cudaGetLastError();
+  return launch_pdl(pack_kernel, dim3(grid), dim3(kCopyThreads), 0, st,
+                    static_cast<const uint8_t*>(q), static_cast<const uint8_t*>(k),
+                    static_cast<const uint8_t*>(v), cu, (const int32_t*)src, static_cast<uint8_t*>(qp),
+                    static_cast<uint8_t*>(kp), static_cast<uint8_t*>(vp), B, ld_elems * 2,
+                    H * kHeadDim * 2);
 }
 
 cudaError_t launch_unpack(const void* op, const int32_t* dst, void* o, int B, int N, int H,
@@ -606,9 +639,9 @@ cudaError_t launch_unpack(const void* op, const int32_t* dst, void* o, int B, in
   const long long BN = (long long)B * N;
   const long long want = (BN + kUnpackRows - 1) / kUnpackRows;
   const int grid = (int)(want < ((long long)sm_count(dev) * 8) ? (long long)(want) : (long long)((long long)sm_count(dev) * 8));
-  unpack_kernel<<<grid, kCopyThreads, 0, st>>>(static_cast<const uint8_t*>(op), dst,
-                                               static_cast<uint8_t*>(o), BN, H * kHeadDim * 2);
-  return cudaGetLastError();
+  return launch_pdl(unpack_kernel, dim3(grid), dim3(kCopyThreads), 0, st,
+                    static_cast<const uint8_t*>(op), dst, static_cast<uint8_t*>(o), BN,
+                    H * kHeadDim * 2);
 }
 
 // One-time (per device, per instantiation) max-dynamic-smem attribute, sized
@@ -628,8 +661,7 @@ static cudaError_t launch_attn_mma(const AttnArgs& a, int grid, cudaStream_t st)
   static bool done[64] = {false};
   cudaError_t e = smem_attr_once(attn_kernel<T, kFused>, attn_smem_bytes(kMaxN), done);
   if (e != cudaSuccess) return e;
-  attn_kernel<T, kFused><<<grid, kAttnThreads, attn_smem_bytes(a.N), st>>>(a);
-  return cudaGetLastError();
+  return launch_pdl(attn_kernel<T, kFused>, dim3(grid), dim3(kAttnThreads), attn_smem_bytes(a.N), st, a);
 }
 
 // tcgen05 engine: persistent grid of min(#SMs, work items) CTAs x nslots slots.
@@ -642,8 +674,8 @@ static cudaError_t launch_attn_tc(const AttnArgs& a, int nwork, cudaStream_t st)
   cudaGetDevice(&dev);
   const int nslots = tc_slots(a.N);
   const int grid = nwork < sm_count(dev) ? nwork : sm_count(dev);
-  attn_tc_kernel<T, kFused><<<grid, nslots * kTcSlotThreads, tc_smem_bytes(a.N, nslots), st>>>(a, nwork);
-  return cudaGetLastError();
+  return launch_pdl(attn_tc_kernel<T, kFused>, dim3(grid), dim3(nslots * kTcSlotThreads),
+                    tc_smem_bytes(a.N, nslots), st, a, nwork);
 }
 
 template <bool kFused>

@@ -1,5 +1,13 @@
 mkdir -p gpurun_out
-python scripts/timeline.py --config C3 --out gpurun_out/tl_c3.json 2>&1 | tail -60
-timeout 300 python -m pytest tests -m gpu -q -x --timeout 200 -p no:cacheprovider 2>&1 | tail -3
-timeout 300 python bench.py --steps 2000 --warmup 20 --no-extras --e2e-steps 5 > gpurun_out/bench_quick.json 2>gpurun_out/bench_quick.err; python -c "
-import json; d=json.load(open('gpurun_out/bench_quick.json')); print('us_per_call', d['us_per_call'], 'frac', d['roofline']['frac'], d['clocks'])"
+timeout 900 python -m pytest tests -m gpu -q --timeout 200 -p no:cacheprovider -x 2>&1 | tail -3
+for e in 1 2; do
+  timeout 300 python bench.py --steps 2000 --warmup 20 --engine $e --no-extras --e2e-steps 5 > gpurun_out/bench_e$e.json 2>gpurun_out/bench_e$e.err
+  python scripts/timeline.py --config C3 --engine $e --out gpurun_out/tl_c3_e$e.json > /dev/null 2>&1
+done
+python - <<'PY'
+import json
+for e in (1,2):
+    d=json.load(open(f'gpurun_out/bench_e{e}.json')); print(e, 'us', round(d['us_per_call'],3), 'frac', round(d['roofline']['frac'],3))
+    t=json.load(open(f'gpurun_out/tl_c3_e{e}.json'))['back_to_back']
+    print({k: [round(x,2) for x in v] if isinstance(v,list) else v for k,v in t.items()})
+PY
