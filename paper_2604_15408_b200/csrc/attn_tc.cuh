@@ -121,11 +121,7 @@ __global__ void __launch_bounds__(3 * kTcSlotThreads, 1) attn_tc_kernel(const At
     char* img_o = static_cast<char*>(a.o) + row_base * HDb + h * kRowBytes + (tid & 7) * 16;
     // Dropped rows of this head -> +0.0, by threads [t0, t0 + nthr) of the slot.
     auto zero_dropped = [&](int t, int nthr) {
-      if constexpr (kFused) {
-        const int nd = a.N - n;
-        const uint4 z = make_uint4(0u, 0u, 0u, 0u);
-        for (int rr = t >> 3; rr < nd; rr += nthr >> 3) st_global_16(img_o + sDrop[rr] * HDb, z);
-      }
+      if constexpr (kFused) zero_rows(img_o, sDrop, t >> 3, a.N - n, nthr >> 3, HDb);
     };
     if (n == 0) {  // nothing to attend (R11)
       zero_dropped(tid, kTcSlotThreads);
@@ -170,11 +166,19 @@ __global__ void __launch_bounds__(3 * kTcSlotThreads, 1) attn_tc_kernel(const At
       tc::fence_before();
       sync();
       TL(3);
-      const bool warp_live = tile * kTcTile + warp * 32 < n;  // any real query row in this warp
-      float m_ref = -INFINITY, l = 0.f;                       // Alg. 1 state (raw score units)
-      if (tile == 0 && live < 4 && warp >= live) zero_dropped(tid - live * 32, (4 - live) * 32);
+      // Warps [0, live_t) own real query rows of this tile and run the chunk loop;
+      // the others skip straight to the store phase (on tile 0 they write the
+      // zero rows meanwhile).  Inside the loop only the live warps synchronize.
+      const int rows_t = n - tile * kTcTile;
+      const int live_t = rows_t >= kTcTile ? 4 : (rows_t + 31) >> 5;
+      const bool warp_live = warp < live_t;
+      auto sync_live = [&] {
+        asm volatile("bar.sync %0, %1;" ::"r"(4 + slot), "r"(live_t * 32) : "memory");
+      };
+      float m_ref = -INFINITY, l = 0.f;                       // Alg. 1 state (log2 units)
+      if (!warp_live && tile == 0) zero_dropped(tid - live * 32, (4 - live) * 32);
 
-      for (int j = 0; j < nchunks; ++j) {
+      for (int j = 0; warp_live && j < nchunks; ++j) {
         const int kc = min(kTcChunk, n16 - j * kTcChunk);     // keys in chunk (multiple of 16)
         // ---- S_j = Q K_j^T: 4 UMMA of K = 16 (+32 B along the SW128 rows each)
         if (tid == 0) {
@@ -191,24 +195,44 @@ __global__ void __launch_bounds__(3 * kTcSlotThreads, 1) attn_tc_kernel(const At
         tc::fence_after();
         TL(5);
 
-        if (warp_live) {
+        {
           const int c0 = j * kTcChunk;
           const bool two = kc > 32;  // slot-uniform
-          uint32_t ra[32], rb[32];
-          tc::ld_x32(tS + lane_off, ra);
-          if (two) tc::ld_x32(tS + lane_off + 32, rb);
-          tc::wait_ld();
-          float mc = -INFINITY;
+          // x = S * log2(e)/8 in log2 units, key columns >= n masked to -inf (R4).
+          // Groups of 8 columns wholly past n are skipped (warp-uniform): the
+          // exp2 unit (16 lanes/clk/SM) is this phase's bottleneck.
+          const int nv = min(kTcChunk, n - c0);  // valid keys in this chunk, >= 1
+          float x[64];
+          {
+            uint32_t r[32];
+            tc::ld_x32(tS + lane_off, r);
+            tc::wait_ld();
 #pragma unroll
-          for (int i = 0; i < 32; ++i) {
-            if (c0 + i < n) mc = fmaxf(mc, __uint_as_float(ra[i]));
-            if (two && c0 + 32 + i < n) mc = fmaxf(mc, __uint_as_float(rb[i]));
+            for (int i = 0; i < 32; ++i) x[i] = i < nv ? __uint_as_float(r[i]) * kScaleLog2 : -INFINITY;
+            if (two) {
+              tc::ld_x32(tS + lane_off + 32, r);
+              tc::wait_ld();
+#pragma unroll
+              for (int i = 0; i < 32; ++i) x[32 + i] = 32 + i < nv ? __uint_as_float(r[i]) * kScaleLog2 : -INFINITY;
+            } else {
+#pragma unroll
+              for (int i = 0; i < 32; ++i) x[32 + i] = -INFINITY;
+            }
           }
+          TL(10);
+          float t[16];  // chunk max: a tree, not a 64-long dependency chain
+#pragma unroll
+          for (int i = 0; i < 16; ++i) t[i] = fmaxf(fmaxf(x[i], x[i + 16]), fmaxf(x[i + 32], x[i + 48]));
+#pragma unroll
+          for (int w2 = 8; w2 > 0; w2 >>= 1)
+#pragma unroll
+            for (int i = 0; i < w2; ++i) t[i] = fmaxf(t[i], t[i + w2]);
+          const float mc = t[0];
           float alpha = 1.f;
           if (j == 0) {
             m_ref = mc;
-          } else if ((mc - m_ref) * kScaleLog2 > 8.f) {  // lazy: P stays <= 2^8 otherwise
-            alpha = ex2((m_ref - mc) * kScaleLog2);
+          } else if (mc - m_ref > 8.f) {  // lazy: P stays <= 2^8 otherwise
+            alpha = ex2(m_ref - mc);
             m_ref = mc;
           }
           if (j > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {  // O *= alpha (PV_{j-1} is done)
@@ -222,35 +246,40 @@ __global__ void __launch_bounds__(3 * kTcSlotThreads, 1) attn_tc_kernel(const At
               tc::st_x16(tO + lane_off + 16 * q, s16);
             }
           }
-          l *= alpha;
-          const float ms = m_ref * kScaleLog2;
+#pragma unroll
+          for (int g = 0; g < 8; ++g) {  // P = e^{S - m}; 0 where masked
+            if (8 * g < nv) {
+#pragma unroll
+              for (int i = 0; i < 8; ++i) x[8 * g + i] = ex2(x[8 * g + i] - m_ref);
+            } else {
+#pragma unroll
+              for (int i = 0; i < 8; ++i) x[8 * g + i] = 0.f;
+            }
+          }
+#pragma unroll
+          for (int i = 0; i < 16; ++i) t[i] = (x[i] + x[i + 16]) + (x[i + 32] + x[i + 48]);
+#pragma unroll
+          for (int w2 = 8; w2 > 0; w2 >>= 1)
+#pragma unroll
+            for (int i = 0; i < w2; ++i) t[i] += t[i + w2];
+          l = l * alpha + t[0];
+          TL(11);
           uint32_t hi[16], lo[16];
 #pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            const int k0 = c0 + 2 * i;
-            const float p0 = k0 < n ? ex2(__uint_as_float(ra[2 * i]) * kScaleLog2 - ms) : 0.f;
-            const float p1 = k0 + 1 < n ? ex2(__uint_as_float(ra[2 * i + 1]) * kScaleLog2 - ms) : 0.f;
-            l += p0 + p1;
-            split2<T>(p0, p1, hi[i], lo[i]);
-          }
+          for (int i = 0; i < 16; ++i) split2<T>(x[2 * i], x[2 * i + 1], hi[i], lo[i]);
           tc::st_x16(tS + lane_off, hi);       // P_hi keys c0..c0+31 -> cols 0 .. 15
           tc::st_x16(tS + lane_off + 32, lo);  // P_lo               -> cols 32 .. 47
           if (two) {
 #pragma unroll
-            for (int i = 0; i < 16; ++i) {
-              const int k0 = c0 + 32 + 2 * i;
-              const float p0 = k0 < n ? ex2(__uint_as_float(rb[2 * i]) * kScaleLog2 - ms) : 0.f;
-              const float p1 = k0 + 1 < n ? ex2(__uint_as_float(rb[2 * i + 1]) * kScaleLog2 - ms) : 0.f;
-              l += p0 + p1;
-              split2<T>(p0, p1, hi[i], lo[i]);
-            }
+            for (int i = 0; i < 16; ++i) split2<T>(x[32 + 2 * i], x[33 + 2 * i], hi[i], lo[i]);
             tc::st_x16(tS + lane_off + 16, hi);  // keys c0+32..c0+63 -> cols 16 .. 31
             tc::st_x16(tS + lane_off + 48, lo);  //                   -> cols 48 .. 63
           }
           tc::wait_st();
+          TL(12);
         }
         tc::fence_before();
-        sync();
+        sync_live();
         TL(8);
         // ---- O += P_hi V_j + P_lo V_j (K = 16 keys per UMMA) --------------------
         if (tid == 0) {
@@ -269,6 +298,10 @@ __global__ void __launch_bounds__(3 * kTcSlotThreads, 1) attn_tc_kernel(const At
         TL(9);
       }
 
+      if (!warp_live) {  // keep the mbarrier parities in step with the live warps
+        ph_s ^= (uint32_t)(nchunks & 1);
+        ph_o ^= (uint32_t)(nchunks & 1);
+      }
       // ---- epilogue: O / l -> 16 bit -> SMEM (sQ is free) -> 128-byte row stores
       if (warp_live) {
         const float inv = 1.f / l;

@@ -280,6 +280,23 @@ struct AttnArgs {
   long long ld;            // input token stride in elements
 };
 
+// Zero (+0.0) the 128-byte head slices of dropped rows sDrop[first], [first +
+// step], ... < nd; img_o already includes this thread's 16-byte chunk (8
+// threads per row).  Unrolled by 4 so the shared loads batch ahead of the stores.
+__device__ __forceinline__ void zero_rows(char* img_o, const int16_t* sDrop, int first, int nd,
+                                          int step, int HDb) {
+  const uint4 z = make_uint4(0u, 0u, 0u, 0u);
+  int rr = first;
+  for (; rr + 3 * step < nd; rr += 4 * step) {
+    const int d0 = sDrop[rr], d1 = sDrop[rr + step], d2 = sDrop[rr + 2 * step], d3 = sDrop[rr + 3 * step];
+    st_global_16(img_o + d0 * HDb, z);
+    st_global_16(img_o + d1 * HDb, z);
+    st_global_16(img_o + d2 * HDb, z);
+    st_global_16(img_o + d3 * HDb, z);
+  }
+  for (; rr < nd; rr += step) st_global_16(img_o + sDrop[rr] * HDb, z);
+}
+
 // Block 0 of a fused launch that also emits cu_seqlens: one CTA walks the keep
 // mask (scan_cta, counts only) while the other CTAs attend.
 template <typename Sync>
@@ -429,11 +446,7 @@ __global__ void __launch_bounds__(kAttnThreads, 3) attn_kernel(const AttnArgs a)
   const int nsl = (n + 15) >> 4;
   const int busy = nsl < 4 ? nsl : 4;  // warps [0, busy) own slices
   auto zero_dropped = [&](int t, int nthr) {
-    if constexpr (kFused) {
-      const int nd = a.N - n;
-      const uint4 z = make_uint4(0u, 0u, 0u, 0u);
-      for (int rr = t >> 3; rr < nd; rr += nthr >> 3) st_global_16(img_o + sDrop[rr] * HDb, z);
-    }
+    if constexpr (kFused) zero_rows(img_o, sDrop, t >> 3, a.N - n, nthr >> 3, HDb);
   };
   if (busy < 4 && warp >= busy) zero_dropped(tid - busy * 32, (4 - busy) * 32);
 
@@ -506,13 +519,17 @@ __global__ void __launch_bounds__(kAttnThreads, 3) attn_kernel(const AttnArgs a)
         o[j][3] *= al1;
       }
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {  // P = e^{S - m'}
-        s[j][0] = ex2(s[j][0] - mn0);
-        s[j][1] = ex2(s[j][1] - mn0);
-        s[j][2] = ex2(s[j][2] - mn1);
-        s[j][3] = ex2(s[j][3] - mn1);
-        l0 += s[j][0] + s[j][1];
-        l1 += s[j][2] + s[j][3];
+      for (int j = 0; j < 8; ++j) {  // P = e^{S - m'}; key tiles past n skipped (exp2 unit)
+        if (j < nt) {
+          s[j][0] = ex2(s[j][0] - mn0);
+          s[j][1] = ex2(s[j][1] - mn0);
+          s[j][2] = ex2(s[j][2] - mn1);
+          s[j][3] = ex2(s[j][3] - mn1);
+          l0 += s[j][0] + s[j][1];
+          l1 += s[j][2] + s[j][3];
+        } else {
+          s[j][0] = s[j][1] = s[j][2] = s[j][3] = 0.f;
+        }
       }
       // O += P_hi V + P_lo V
       const int nk = (nv + 15) >> 4;

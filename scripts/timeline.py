@@ -53,7 +53,7 @@ for mode in ("isolated", "back_to_back"):
     n = lib.ragged_debug_timeline(buf.ctypes.data, ncta)
     assert n == ncta, n
     valid = buf[:, 0] != 0
-    t = buf[valid, :10].astype(np.int64)
+    t = buf[valid, :13].astype(np.int64)
     sm = buf[valid, 15]
     t0 = t[:, 0].min()
     rel = (t - t0) / 1e3  # us
@@ -70,6 +70,10 @@ for mode in ("isolated", "back_to_back"):
         "w0_pv_epi_smem_us": np.percentile(attn[:, 6] - attn[:, 5], [50, 90, 100]).tolist(),
         "w0_store_to_end_us": np.percentile(attn[:, 4] - attn[:, 6], [50, 90, 100]).tolist(),
         "tc_softmax_us": np.percentile(attn[:, 8] - attn[:, 5], [50, 90, 100]).tolist() if a.engine == 2 else None,
+        "tc_sm_ld_us": np.percentile(attn[:, 10] - attn[:, 5], [50, 90, 100]).tolist() if a.engine == 2 else None,
+        "tc_sm_exp_us": np.percentile(attn[:, 11] - attn[:, 10], [50, 90, 100]).tolist() if a.engine == 2 else None,
+        "tc_sm_st_us": np.percentile(attn[:, 12] - attn[:, 11], [50, 90, 100]).tolist() if a.engine == 2 else None,
+        "tc_sm_bar_us": np.percentile(attn[:, 8] - attn[:, 12], [50, 90, 100]).tolist() if a.engine == 2 else None,
         "tc_pv_us": np.percentile(attn[:, 9] - attn[:, 8], [50, 90, 100]).tolist() if a.engine == 2 else None,
         "tc_epi_smem_us": np.percentile(attn[:, 6] - attn[:, 9], [50, 90, 100]).tolist() if a.engine == 2 else None,
         "cta_total_us": np.percentile(attn[:, 4] - attn[:, 0], [50, 90, 100]).tolist(),
