@@ -477,7 +477,85 @@ def extras(args, rb, torch, dev, sets, c, B, N, H, dt, T):
         sweep.append({"p": p, "tok": kk, "fused_us": f_us, "padded_sdpa_us": sd_us,
                       "fused_hbm_frac": ab / (f_us * 1e-6) / 1e9 / 6560.6, "alg_bytes": ab})
     out["prune_sweep"] = sweep
+    out["configs"] = config_extras(rb, torch, dev, dt)
     return out
+
+
+def config_extras(rb, torch, dev, dt):
+    """The other BASELINE.json configs, device-timed (graph replay, cold-L2
+    rotation where the working set would fit in L2)."""
+    import synth
+    F = torch.nn.functional
+    res = {}
+
+    def fused_fn(s):
+        return lambda: rb.pack_attend_unpack(s["q"], s["k"], s["v"], s["keep"], o=s["o"])
+
+    def sdpa_fn(s):
+        m = s["keep"].bool()[:, None, None, :]
+        return lambda: F.scaled_dot_product_attention(s["q"].transpose(1, 2), s["k"].transpose(1, 2),
+                                                      s["v"].transpose(1, 2), attn_mask=m)
+
+    def make_sets(B, H, p, method, nsets, seed=0):
+        q, k, v, keep = synth.make_inputs(B, 197, H, p, method, "bf16" if dt == torch.bfloat16 else "fp16",
+                                          seed=seed)
+        sets = [dict(q=q.to(dev), k=k.to(dev), v=v.to(dev), keep=keep.to(dev),
+                     o=torch.empty(B, 197, H, 64, dtype=dt, device=dev)) for _ in range(nsets)]
+        return sets, int(keep.numpy().astype(bool).sum())
+
+    # C1: DeiT-Ti single layer, B = 4, l2 keep 50 %
+    sets, T = make_sets(4, 3, 0.5, "l2", 64)
+    us = _graph_time(torch, [fused_fn(s) for s in sets], 500)
+    res["C1"] = {"fused_us": us, "images_per_s": 4 / (us * 1e-6), "tok_per_img": T // 4,
+                 "padded_sdpa_us": _graph_time(torch, [sdpa_fn(s) for s in sets[:8]], 200)}
+    # C2: DeiT-S 12 layers, B = 32: layers 1-4 all kept (P:361), 5-12 l2 mask at p
+    # (pack-once semantics, P:364); 12 distinct per-layer Q/K/V sets (> L2).
+    c2 = []
+    base = [make_sets(32, 6, 0.0, "all", 1, seed=100 + L)[0][0] for L in range(12)]
+    for p in (0.0, 0.1, 0.2, 0.3, 0.4, 0.5, 0.6, 0.7, 0.8, 0.9):
+        keep_p = torch.from_numpy(synth.mask_threshold_l2(32, 197, synth.kept_tokens(197, p), 1000, D=384)).to(dev)
+        keep_all = torch.ones(32, 197, dtype=torch.uint8, device=dev)
+        layers = [dict(base[L], keep=(keep_all if L < 4 else keep_p)) for L in range(12)]
+
+        def step(layers=layers):
+            for s in layers:
+                rb.pack_attend_unpack(s["q"], s["k"], s["v"], s["keep"], o=s["o"])
+        us = _graph_time(torch, [step], 50)
+
+        def step_sdpa(layers=layers):
+            for s in layers:
+                sdpa_fn(s)()
+        us_sd = _graph_time(torch, [step_sdpa], 10)
+        c2.append({"p": p, "tok": synth.kept_tokens(197, p), "us_12_layers": us,
+                   "images_per_s": 32 / (us * 1e-6), "padded_sdpa_us_12_layers": us_sd,
+                   "padded_sdpa_images_per_s": 32 / (us_sd * 1e-6)})
+    res["C2"] = c2
+    # C4: DeiT-B, B = 64, four generators x {50, 70, 90} %
+    c4 = []
+    for method in ("l2", "dynamicvit", "evit", "ats"):
+        for p in (0.5, 0.7, 0.9):
+            sets, T = make_sets(64, 12, p, method, 8)
+            us = _graph_time(torch, [fused_fn(s) for s in sets], 200)
+            c4.append({"method": method, "p": p, "mean_tok": T / 64, "fused_us": us,
+                       "padded_sdpa_us": _graph_time(torch, [sdpa_fn(s) for s in sets], 40)})
+    res["C4"] = c4
+    # C5: DeiT-B, B = 4096, 70 % (3.7 GB of Q/K/V: cold by size); device-drawn inputs
+    g = torch.Generator(device=dev).manual_seed(5)
+    B5 = 4096
+    q = torch.randn(B5, 197, 12, 64, generator=g, device=dev).to(dt)
+    k = torch.randn(B5, 197, 12, 64, generator=g, device=dev).to(dt)
+    v = (torch.rand(B5, 197, 12, 64, generator=g, device=dev) * 2 - 1).to(dt)
+    keep = torch.from_numpy(synth.mask_threshold_l2(B5, 197, synth.kept_tokens(197, 0.7), 1005)).to(dev)
+    o = torch.empty_like(q)
+    s5 = dict(q=q, k=k, v=v, keep=keep, o=o)
+    us = _graph_time(torch, [fused_fn(s5)], 10)
+    T5 = int(keep.sum().item())
+    ab = algorithmic_bytes(B5, 197, 12, T5)
+    res["C5"] = {"fused_us": us, "images_per_s": B5 / (us * 1e-6), "alg_bytes": ab,
+                 "hbm_frac": ab / (us * 1e-6) / 1e9 / 6560.6}
+    del q, k, v, o, s5
+    torch.cuda.empty_cache()
+    return res
 
 
 if __name__ == "__main__":

@@ -31,7 +31,8 @@ def nvcc() -> str:
 
 
 VARIANTS = {"": [], "tl": ["-DRAGGED_TIMELINE"],
-            "tlx": ["-DRAGGED_TIMELINE", "-DRAGGED_TC_EARLY128"]}  # experiments only
+            "tlx": ["-DRAGGED_TIMELINE", "-DRAGGED_TC_ZERO_LATE"],  # experiments only
+            "x": ["-DRAGGED_TC_ZERO_LATE"]}
 
 
 def lib_path(variant: str = "") -> str:
@@ -87,3 +88,4 @@ if __name__ == "__main__":
         print(build(force=True, variant="tl"))
     if "--tlx" in sys.argv:
         print(build(force=True, variant="tlx"))
+        print(build(force=True, variant="x"))

@@ -176,7 +176,9 @@ __global__ void __launch_bounds__(3 * kTcSlotThreads, 1) attn_tc_kernel(const At
         asm volatile("bar.sync %0, %1;" ::"r"(4 + slot), "r"(live_t * 32) : "memory");
       };
       float m_ref = -INFINITY, l = 0.f;                       // Alg. 1 state (log2 units)
+#ifndef RAGGED_TC_ZERO_LATE
       if (!warp_live && tile == 0) zero_dropped(tid - live * 32, (4 - live) * 32);
+#endif
 
       for (int j = 0; warp_live && j < nchunks; ++j) {
         const int kc = min(kTcChunk, n16 - j * kTcChunk);     // keys in chunk (multiple of 16)
@@ -333,7 +335,11 @@ __global__ void __launch_bounds__(3 * kTcSlotThreads, 1) attn_tc_kernel(const At
       }
       sync();  // sQ, sPos, TMEM are reused by the next tile / problem
     }
+#ifdef RAGGED_TC_ZERO_LATE
+    if (true) {
+#else
     if (live == 4) {
+#endif
       zero_dropped(tid, kTcSlotThreads);
       sync();  // sDrop is rewritten by the next problem
     }
