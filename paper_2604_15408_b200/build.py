@@ -32,7 +32,7 @@ def nvcc() -> str:
 
 VARIANTS = {"": [], "tl": ["-DRAGGED_TIMELINE"],
             "tlx": ["-DRAGGED_TIMELINE", "-DRAGGED_TC_ZERO_LATE"],  # experiments only
-            "x": ["-DRAGGED_TC_ZERO_LATE"]}
+            "x": ["-DRAGGED_TC_ABLATE_SOFTMAX"]}
 
 
 def lib_path(variant: str = "") -> str:

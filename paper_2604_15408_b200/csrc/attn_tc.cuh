@@ -29,7 +29,7 @@
 
 namespace ragged {
 
-constexpr int kTcTile = 128;   // UMMA M: query rows per tile (one per slot thread)
+constexpr int kTcTile = 64;    // UMMA M: query rows per tile (16 per warp, 4 threads per row)
 constexpr int kTcChunk = 64;   // keys per S/P chunk = 64 fp32 TMEM columns
 constexpr int kTcSlotThreads = 128;
 
@@ -40,7 +40,7 @@ struct TcSmem {
 __host__ __device__ inline TcSmem tc_smem(int N) {
   TcSmem L;
   L.kv_rows = (N + 15) & ~15;
-  L.off_q = 0;                                     // 128 x 128 B Q tile; O staging later
+  L.off_q = 0;                                     // 64 x 128 B Q tile; O staging later
   L.off_k = kTcTile * kRowBytes;                   // kv_rows x 128 B
   L.off_v = L.off_k + L.kv_rows * kRowBytes;
   L.off_small = L.off_v + L.kv_rows * kRowBytes;   // pos, drop, ballots, scan scratch, mbarriers
@@ -92,7 +92,9 @@ __global__ void __launch_bounds__(3 * kTcSlotThreads, 1) attn_tc_kernel(const At
   pdl_wait_prerequisites();  // TMEM/barrier setup above overlaps the previous grid's tail
   const uint32_t tbase = *tslot + (uint32_t)(slot * 128);        // this slot's 128 columns
   const uint32_t tS = tbase, tO = tbase + 64;
-  const uint32_t lane_off = (uint32_t)(warp * 32) << 16;          // this warp's 32 lanes
+  // M = 64 accumulators: tile row 16w + i lives in TMEM lane 32w + i (i < 16)
+  const uint32_t lane_off = (uint32_t)(warp * 32) << 16;          // this warp's lane quarter
+  const int g = (tid & 31) >> 2, t4 = tid & 3;                     // fragment row / column pair
   const uint32_t bar_s = smem_u32(&bars[0]), bar_o = smem_u32(&bars[1]);
   uint32_t ph_s = 0, ph_o = 0;
   constexpr uint32_t kFmt = std::is_same<T, __nv_bfloat16>::value ? 1u : 0u;
@@ -156,7 +158,7 @@ __global__ void __launch_bounds__(3 * kTcSlotThreads, 1) attn_tc_kernel(const At
     TL(2);
     // warps [live, 4) own no query row of tile 0: they write the zero rows while
     // the others run the softmax; with no idle warp, every thread does it last.
-    const int live = n >= kTcTile ? 4 : (n + 31) >> 5;
+    const int live = n >= kTcTile ? 4 : (n + 15) >> 4;
 
     for (int tile = 0; tile * kTcTile < n; ++tile) {
       if (tile > 0) load_q_tile(tile);
@@ -170,12 +172,14 @@ __global__ void __launch_bounds__(3 * kTcSlotThreads, 1) attn_tc_kernel(const At
       // the others skip straight to the store phase (on tile 0 they write the
       // zero rows meanwhile).  Inside the loop only the live warps synchronize.
       const int rows_t = n - tile * kTcTile;
-      const int live_t = rows_t >= kTcTile ? 4 : (rows_t + 31) >> 5;
+      const int live_t = rows_t >= kTcTile ? 4 : (rows_t + 15) >> 4;
       const bool warp_live = warp < live_t;
       auto sync_live = [&] {
         asm volatile("bar.sync %0, %1;" ::"r"(4 + slot), "r"(live_t * 32) : "memory");
       };
-      float m_ref = -INFINITY, l = 0.f;                       // Alg. 1 state (log2 units)
+      // Alg. 1 state for this thread's two rows g and g + 8 (log2 units); l is the
+      // thread's partial row sum over its columns (quad-reduced at the end).
+      float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
 #ifndef RAGGED_TC_ZERO_LATE
       if (!warp_live && tile == 0) zero_dropped(tid - live * 32, (4 - live) * 32);
 #endif
@@ -198,87 +202,76 @@ __global__ void __launch_bounds__(3 * kTcSlotThreads, 1) attn_tc_kernel(const At
         TL(5);
 
         {
+          // S chunk in the accumulator fragment layout (16x256b): per 8-key group
+          // jg, x[jg][0..1] = row g keys 8jg + 2t4 + {0,1}, x[jg][2..3] = row g + 8.
           const int c0 = j * kTcChunk;
-          const bool two = kc > 32;  // slot-uniform
-          // x = S * log2(e)/8 in log2 units, key columns >= n masked to -inf (R4).
-          // Groups of 8 columns wholly past n are skipped (warp-uniform): the
-          // exp2 unit (16 lanes/clk/SM) is this phase's bottleneck.
           const int nv = min(kTcChunk, n - c0);  // valid keys in this chunk, >= 1
-          float x[64];
+          const int ngv = (nv + 7) >> 3;         // 8-key groups holding valid keys
+          float x[8][4];
           {
             uint32_t r[32];
-            tc::ld_x32(tS + lane_off, r);
+            tc::ld_16x256b_x8(tS + lane_off, r);
             tc::wait_ld();
 #pragma unroll
-            for (int i = 0; i < 32; ++i) x[i] = i < nv ? __uint_as_float(r[i]) * kScaleLog2 : -INFINITY;
-            if (two) {
-              tc::ld_x32(tS + lane_off + 32, r);
-              tc::wait_ld();
+            for (int jg = 0; jg < 8; ++jg)
 #pragma unroll
-              for (int i = 0; i < 32; ++i) x[32 + i] = 32 + i < nv ? __uint_as_float(r[i]) * kScaleLog2 : -INFINITY;
-            } else {
-#pragma unroll
-              for (int i = 0; i < 32; ++i) x[32 + i] = -INFINITY;
-            }
+              for (int e = 0; e < 4; ++e) {
+                const int key = 8 * jg + 2 * t4 + (e & 1);
+                x[jg][e] = key < nv ? __uint_as_float(r[4 * jg + e]) * kScaleLog2 : -INFINITY;
+              }
           }
-          TL(10);
-          float t[16];  // chunk max: a tree, not a 64-long dependency chain
+          float mx0 = -INFINITY, mx1 = -INFINITY;
 #pragma unroll
-          for (int i = 0; i < 16; ++i) t[i] = fmaxf(fmaxf(x[i], x[i + 16]), fmaxf(x[i + 32], x[i + 48]));
-#pragma unroll
-          for (int w2 = 8; w2 > 0; w2 >>= 1)
-#pragma unroll
-            for (int i = 0; i < w2; ++i) t[i] = fmaxf(t[i], t[i + w2]);
-          const float mc = t[0];
-          float alpha = 1.f;
+          for (int jg = 0; jg < 8; ++jg) {
+            mx0 = fmaxf(mx0, fmaxf(x[jg][0], x[jg][1]));
+            mx1 = fmaxf(mx1, fmaxf(x[jg][2], x[jg][3]));
+          }
+          mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 1));
+          mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 2));
+          mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 1));
+          mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 2));
+          float al0 = 1.f, al1 = 1.f;
           if (j == 0) {
-            m_ref = mc;
-          } else if (mc - m_ref > 8.f) {  // lazy: P stays <= 2^8 otherwise
-            alpha = ex2(m_ref - mc);
-            m_ref = mc;
+            m0 = mx0;
+            m1 = mx1;
+          } else {  // lazy: the reference max moves only if P would exceed 2^8
+            if (mx0 - m0 > 8.f) { al0 = ex2(m0 - mx0); m0 = mx0; }
+            if (mx1 - m1 > 8.f) { al1 = ex2(m1 - mx1); m1 = mx1; }
           }
-          if (j > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {  // O *= alpha (PV_{j-1} is done)
-#pragma unroll 1
-            for (int q = 0; q < 4; ++q) {
-              uint32_t s16[16];
-              tc::ld_x16(tO + lane_off + 16 * q, s16);
-              tc::wait_ld();
+          if (j > 0 && __any_sync(0xffffffffu, al0 != 1.f || al1 != 1.f)) {  // O *= alpha
+            uint32_t o[32];
+            tc::ld_16x256b_x8(tO + lane_off, o);
+            tc::wait_ld();
 #pragma unroll
-              for (int i = 0; i < 16; ++i) s16[i] = __float_as_uint(__uint_as_float(s16[i]) * alpha);
-              tc::st_x16(tO + lane_off + 16 * q, s16);
+            for (int jg = 0; jg < 8; ++jg) {
+              o[4 * jg + 0] = __float_as_uint(__uint_as_float(o[4 * jg + 0]) * al0);
+              o[4 * jg + 1] = __float_as_uint(__uint_as_float(o[4 * jg + 1]) * al0);
+              o[4 * jg + 2] = __float_as_uint(__uint_as_float(o[4 * jg + 2]) * al1);
+              o[4 * jg + 3] = __float_as_uint(__uint_as_float(o[4 * jg + 3]) * al1);
             }
+            tc::st_16x256b_x8(tO + lane_off, o);
           }
-#pragma unroll
-          for (int g = 0; g < 8; ++g) {  // P = e^{S - m}; 0 where masked
-            if (8 * g < nv) {
-#pragma unroll
-              for (int i = 0; i < 8; ++i) x[8 * g + i] = ex2(x[8 * g + i] - m_ref);
-            } else {
-#pragma unroll
-              for (int i = 0; i < 8; ++i) x[8 * g + i] = 0.f;
-            }
-          }
-#pragma unroll
-          for (int i = 0; i < 16; ++i) t[i] = (x[i] + x[i + 16]) + (x[i + 32] + x[i + 48]);
-#pragma unroll
-          for (int w2 = 8; w2 > 0; w2 >>= 1)
-#pragma unroll
-            for (int i = 0; i < w2; ++i) t[i] += t[i + w2];
-          l = l * alpha + t[0];
-          TL(11);
+          l0 *= al0;
+          l1 *= al1;
           uint32_t hi[16], lo[16];
 #pragma unroll
-          for (int i = 0; i < 16; ++i) split2<T>(x[2 * i], x[2 * i + 1], hi[i], lo[i]);
-          tc::st_x16(tS + lane_off, hi);       // P_hi keys c0..c0+31 -> cols 0 .. 15
-          tc::st_x16(tS + lane_off + 32, lo);  // P_lo               -> cols 32 .. 47
-          if (two) {
-#pragma unroll
-            for (int i = 0; i < 16; ++i) split2<T>(x[32 + 2 * i], x[33 + 2 * i], hi[i], lo[i]);
-            tc::st_x16(tS + lane_off + 16, hi);  // keys c0+32..c0+63 -> cols 16 .. 31
-            tc::st_x16(tS + lane_off + 48, lo);  //                   -> cols 48 .. 63
+          for (int jg = 0; jg < 8; ++jg) {  // P = e^{S - m}; groups past n skipped (exp2 unit)
+            float p0 = 0.f, p1 = 0.f, p2 = 0.f, p3 = 0.f;
+            if (jg < ngv) {
+              p0 = ex2(x[jg][0] - m0);
+              p1 = ex2(x[jg][1] - m0);
+              p2 = ex2(x[jg][2] - m1);
+              p3 = ex2(x[jg][3] - m1);
+            }
+            l0 += p0 + p1;
+            l1 += p2 + p3;
+            // packed pair (keys 8jg + 2t4, +1) = P column 4jg + t4: the 16x128b store slot
+            split2<T>(p0, p1, hi[2 * jg], lo[2 * jg]);
+            split2<T>(p2, p3, hi[2 * jg + 1], lo[2 * jg + 1]);
           }
+          tc::st_16x128b_x8(tS + lane_off, hi);       // P_hi: cols [0, 32) of the chunk
+          tc::st_16x128b_x8(tS + lane_off + 32, lo);  // P_lo: cols [32, 64)
           tc::wait_st();
-          TL(12);
         }
         tc::fence_before();
         sync_live();
@@ -306,21 +299,21 @@ __global__ void __launch_bounds__(3 * kTcSlotThreads, 1) attn_tc_kernel(const At
       }
       // ---- epilogue: O / l -> 16 bit -> SMEM (sQ is free) -> 128-byte row stores
       if (warp_live) {
-        const float inv = 1.f / l;
-        uint32_t oa[32], ob[32];
-        tc::ld_x32(tO + lane_off, oa);
-        tc::ld_x32(tO + lane_off + 32, ob);
+        l0 += __shfl_xor_sync(0xffffffffu, l0, 1);
+        l0 += __shfl_xor_sync(0xffffffffu, l0, 2);
+        l1 += __shfl_xor_sync(0xffffffffu, l1, 1);
+        l1 += __shfl_xor_sync(0xffffffffu, l1, 2);
+        const float inv0 = 1.f / l0, inv1 = 1.f / l1;
+        uint32_t o[32];
+        tc::ld_16x256b_x8(tO + lane_off, o);
         tc::wait_ld();
-        uint8_t* srow = sQ + tid * kRowBytes;
+        const int r0 = warp * 16 + g, r1 = r0 + 8;  // tile rows of this thread
 #pragma unroll
-        for (int c = 0; c < 8; ++c) {
-          const uint32_t* s8 = c < 4 ? &oa[8 * c] : &ob[8 * (c - 4)];
-          uint4 v;
-          v.x = pack2<T>(__uint_as_float(s8[0]) * inv, __uint_as_float(s8[1]) * inv);
-          v.y = pack2<T>(__uint_as_float(s8[2]) * inv, __uint_as_float(s8[3]) * inv);
-          v.z = pack2<T>(__uint_as_float(s8[4]) * inv, __uint_as_float(s8[5]) * inv);
-          v.w = pack2<T>(__uint_as_float(s8[6]) * inv, __uint_as_float(s8[7]) * inv);
-          *reinterpret_cast<uint4*>(srow + ((c ^ (tid & 7)) << 4)) = v;
+        for (int jg = 0; jg < 8; ++jg) {  // dims 8jg + 2t4, +1 -> 4 bytes at chunk jg
+          *reinterpret_cast<uint32_t*>(sQ + swz(r0, jg) + 4 * t4) =
+              pack2<T>(__uint_as_float(o[4 * jg + 0]) * inv0, __uint_as_float(o[4 * jg + 1]) * inv0);
+          *reinterpret_cast<uint32_t*>(sQ + swz(r1, jg) + 4 * t4) =
+              pack2<T>(__uint_as_float(o[4 * jg + 2]) * inv1, __uint_as_float(o[4 * jg + 3]) * inv1);
         }
       }
       tc::fence_before();
