@@ -3,28 +3,32 @@
 //
 // Persistent CTAs, one per SM, each split into `nslots` (2-3) independent
 // 128-thread SLOTS.  A slot processes one (image, head) problem at a time
-// (problems are strided over CTAs then slots, head fastest as in P:293-294):
+// (problems are strided over CTAs then slots, head fastest as in P:293-294),
+// in query tiles of 64 rows (16 per warp) and key chunks of 64:
 //
-//   S_j = Q K_j^T   tcgen05.mma kind::f16, M = 128 query rows, N <= 64 keys of
-//                   chunk j, K = 64; A = Q tile, B = K rows, both in SMEM
-//                   (SWIZZLE_128B, K-major).  Fp32 accumulator in TMEM.
-//   softmax         one thread per query row (its TMEM lane): tcgen05.ld the
-//                   row chunk, chunk max, Alg. 1's online update m, l, alpha
-//                    with LAZY rescaling -- the reference max only
-//                   moves when the chunk max exceeds it by > 2^8 in P, and then
-//                   O is rescaled in TMEM; P = 2^((S - m) log2e / 8) is split
-//                   hi + lo in the 16-bit type (R2) and stored with tcgen05.st
-//                   IN PLACE of its S columns (two 16-bit values per column).
+//   S_j = Q K_j^T   tcgen05.mma kind::f16, M = 64, N <= 64 keys, K = 64; A = Q
+//                   tile, B = K rows, both SMEM (SWIZZLE_128B, K-major); fp32
+//                   accumulator in TMEM (tile row 16w + i -> lane 32w + i).
+//   softmax         tcgen05.ld.16x256b: each thread holds rows g, g+8 of its
+//                   warp's 16 and 2 of every 8 keys (the mma.sync fragment
+//                   shape), 4 threads per row (quad shuffles for max / sum).
+//                   Alg. 1's online update m, l, alpha with LAZY
+//                   rescaling: the reference max only moves when a chunk max
+//                   exceeds it by > 8 (log2), and then O is rescaled in TMEM.
+//                   P = 2^(S log2e / 8 - m), split hi + lo in the 16-bit type
+//                   (R2); the packed pair (keys 8j+2t, +1) is exactly what
+//                   tcgen05.st.16x128b puts at P column 4j + t, so P lands IN
+//                   PLACE of its S columns in the TS-UMMA A layout, no shuffles.
 //   O += P_j V_j    tcgen05.mma with A = P from TMEM, B = V rows from SMEM
 //                   (MN-major), N = 64: P_hi V + P_lo V.
-//   epilogue        tcgen05.ld the O row, * 1/l, RNE to 16 bit, SMEM
+//   epilogue        tcgen05.ld.16x256b the O rows, * 1/l, RNE to 16 bit, SMEM
 //                   transpose, coalesced 128-byte row stores.
 //
 // TMEM: one 512-column allocation per CTA, issued before anything else (a
 // resident tcgen05 CTA that has not yet allocated holds back the launch of the
 // next CTA on its SM -- measured); each slot owns a fixed 128
-// columns: S/P chunk [0, 64) + O [64, 128).  Warps whose 32 query rows are all
-// padding (n < 128) skip the softmax and epilogue work.
+// columns: S/P chunk [0, 64) + O [64, 128).  Warps whose 16 query rows are all
+// padding skip the softmax and epilogue (and write the zero rows instead).
 #pragma once
 
 namespace ragged {
