@@ -431,6 +431,15 @@ def extras(args, rb, torch, dev, sets, c, B, N, H, dt, T):
                                                               packed[i][5])) for i in range(N_SETS)], reps)
     out["unpack_us"] = _graph_time(torch, [(lambda i=i: rb.unpack(ops[i], packed[i][4], B, N, o=sets[i]["o"]))
                                            for i in range(N_SETS)], reps)
+    # per-kernel algorithmic bytes -> fraction of the measured HBM peak
+    HDe = H * 64 * 2
+    kb = {"scan_us": B * N + 4 * (B + 1) + 8 * B * N,
+          "pack_us": B * N + 4 * (B + 1) + 8 * B * N + 6 * T * HDe,   # ragged_pack = scan + gather
+          "ragged_attn_us": 4 * T * HDe,
+          "unpack_us": 4 * B * N + T * HDe + B * N * HDe}
+    out["separate_kernels_roofline"] = {
+        k: {"alg_bytes": v, "achieved_GBps": v / (out[k] * 1e-6) / 1e9,
+            "frac_of_measured_hbm": v / (out[k] * 1e-6) / 1e9 / 6560.6} for k, v in kb.items()}
 
     # padded SDPA baseline on the same box (R15)
     F = torch.nn.functional

@@ -158,21 +158,107 @@ __device__ void scan_cta(const uint8_t* __restrict__ keep, int B, int N, int32_t
   }
 }
 
+// a1 as ONE flat prefix sum.  In image-major order the definition
+// restates as: dst[i] = #kept positions in [0, i) for a kept i, and
+// cu[b] = #kept positions in [0, b*N).  One CTA; each round 1024 threads take 16
+// contiguous mask bytes each (16-byte vector load when aligned), a block-wide
+// exclusive scan of the per-thread counts gives every position's rank, and a
+// carry links the rounds.  Deterministic, no atomics.
 constexpr int kScanThreads = 1024;
-constexpr int kScanIPW = 4;
+constexpr int kScanRun = 16;  // mask bytes per thread per round
 
 __global__ void __launch_bounds__(kScanThreads, 1)
     scan_kernel(const uint8_t* __restrict__ keep, int B, int N, int32_t* __restrict__ cu,
                 int32_t* __restrict__ dst, int32_t* __restrict__ src) {
-  constexpr int CH = kScanThreads / 32 * kScanIPW;
-  __shared__ uint32_t s_words[CH * 8];
-  __shared__ int32_t s_cnt[CH];
-  __shared__ int32_t s_off[CH];
+  __shared__ int32_t s_warp[32];
   __shared__ int32_t s_carry;
   pdl_launch_dependents();
   pdl_wait_prerequisites();
-  scan_cta<kScanThreads, kScanIPW, true>(keep, B, N, cu, dst, src, s_words, s_cnt, s_off, &s_carry,
-                                         (int)threadIdx.x, [] { __syncthreads(); });
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const long long total = (long long)B * N;
+  const bool vec_in = (reinterpret_cast<uintptr_t>(keep) & 15) == 0;
+  const bool vec_out = (reinterpret_cast<uintptr_t>(dst) & 15) == 0;
+  if (tid == 0) s_carry = 0;
+  __syncthreads();
+  for (long long base = 0; base < total; base += (long long)kScanThreads * kScanRun) {
+    const long long p0 = base + (long long)tid * kScanRun;
+    uint32_t flags = 0;  // bit e: position p0 + e is kept
+    if (vec_in && p0 + kScanRun <= total) {
+      const uint4 v = *reinterpret_cast<const uint4*>(keep + p0);
+      const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int e = 0; e < kScanRun; ++e) flags |= ((w[e >> 2] >> (8 * (e & 3))) & 0xffu) ? (1u << e) : 0u;
+    } else {
+#pragma unroll
+      for (int e = 0; e < kScanRun; ++e)
+        if (p0 + e < total && keep[p0 + e] != 0) flags |= 1u << e;
+    }
+    const int cnt = __popc(flags);
+    int incl = cnt;  // warp inclusive scan, then across warps
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += t;
+    }
+    if (lane == 31) s_warp[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+      int w = s_warp[lane];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, w, o);
+        if (lane >= o) w += t;
+      }
+      s_warp[lane] = w;
+    }
+    __syncthreads();
+    const int carry = s_carry;
+    const int excl = carry + (warp ? s_warp[warp - 1] : 0) + incl - cnt;
+    // dst for the 16 positions (4 x int4 stores when aligned)
+    if (vec_out && p0 + kScanRun <= total) {
+      int d[kScanRun];
+      int r = excl;
+#pragma unroll
+      for (int e = 0; e < kScanRun; ++e) {
+        const bool kept = (flags >> e) & 1u;
+        d[e] = kept ? r : -1;
+        r += kept ? 1 : 0;
+      }
+#pragma unroll
+      for (int q = 0; q < kScanRun / 4; ++q)
+        *reinterpret_cast<int4*>(dst + p0 + 4 * q) = make_int4(d[4 * q], d[4 * q + 1], d[4 * q + 2], d[4 * q + 3]);
+    } else {
+      int r = excl;
+#pragma unroll
+      for (int e = 0; e < kScanRun; ++e) {
+        if (p0 + e < total) {
+          const bool kept = (flags >> e) & 1u;
+          dst[p0 + e] = kept ? r : -1;
+          r += kept ? 1 : 0;
+        }
+      }
+    }
+    // src for kept positions
+    {
+      uint32_t f = flags;
+      int r = excl;
+      while (f) {
+        const int e = __ffs(f) - 1;
+        src[r++] = (int32_t)(p0 + e);
+        f &= f - 1u;
+      }
+    }
+    // cu[b] at every image boundary b*N inside [p0, p0 + 16)
+    if (p0 < total) {
+      long long b = (p0 + N - 1) / N;
+      for (long long pos = b * N; pos < p0 + kScanRun && pos < total; pos += N, ++b)
+        cu[b] = excl + __popc(flags & ((1u << (int)(pos - p0)) - 1u));
+    }
+    __syncthreads();
+    if (tid == 0) s_carry = carry + s_warp[31];
+    __syncthreads();
+  }
+  if (tid == 0) cu[B] = s_carry;
 }
 
 // ---------------------------------------------------------------- pack ----
