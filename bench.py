@@ -50,6 +50,7 @@ def parse():
     ap.add_argument("--method", default=None)
     ap.add_argument("--engine", type=int, default=0)
     ap.add_argument("--gather", action="store_true", help="NCCL all-gather of O after every step")
+    ap.add_argument("--no-cu", action="store_true", help="experiment: do not request cu_seqlens")
     ap.add_argument("--no-extras", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--e2e-steps", type=int, default=50)
@@ -223,8 +224,8 @@ def main():
 
     def step(i, stream=None):
         s = sets[i % N_SETS]
-        rb.pack_attend_unpack(s["q"], s["k"], s["v"], s["keep"], o=s["o"], cu=s["cu"],
-                              stream=stream, engine=args.engine)
+        rb.pack_attend_unpack(s["q"], s["k"], s["v"], s["keep"], o=s["o"],
+                              cu=None if args.no_cu else s["cu"], stream=stream, engine=args.engine)
         if gathered is not None:
             dist.all_gather_into_tensor(gathered, s["o"])
 

@@ -31,8 +31,9 @@ def nvcc() -> str:
 
 
 VARIANTS = {"": [], "tl": ["-DRAGGED_TIMELINE"],
-            "tlx": ["-DRAGGED_TIMELINE", "-DRAGGED_TC_ZERO_LATE"],  # experiments only
-            "x": ["-DRAGGED_TC_ABLATE_SOFTMAX"]}
+            # timing experiments only: ablations of the mma.sync engine
+            "tlz": ["-DRAGGED_TIMELINE", "-DRAGGED_ABLATE_QK", "-DRAGGED_ABLATE_PV", "-DRAGGED_ABLATE_EXP",
+                    "-DRAGGED_ABLATE_ZERO"]}
 
 
 def lib_path(variant: str = "") -> str:
@@ -86,6 +87,5 @@ if __name__ == "__main__":
     print(build(force=True, verbose="--verbose" in sys.argv))
     if "--tl" in sys.argv:
         print(build(force=True, variant="tl"))
-    if "--tlx" in sys.argv:
-        print(build(force=True, variant="tlx"))
-        print(build(force=True, variant="x"))
+    if "--tlz" in sys.argv:
+        print(build(force=True, variant="tlz"))

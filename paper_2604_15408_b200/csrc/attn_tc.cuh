@@ -110,7 +110,7 @@ __global__ void __launch_bounds__(3 * kTcSlotThreads, 1) attn_tc_kernel(const At
 
   for (int w = blockIdx.x + gridDim.x * slot; w < nwork; w += gridDim.x * nslots) {
     if constexpr (kFused) {
-      if (w == P) {  // the cu_seqlens work item (only present when requested)
+      if (w == P) {  // the cu_seqlens work item (cu_mode 1 only)
         scan_cta_cu(a, sK, tid, sync);  // sK (>= 2 KB) is free during this item
         continue;
       }
@@ -129,9 +129,26 @@ __global__ void __launch_bounds__(3 * kTcSlotThreads, 1) attn_tc_kernel(const At
     auto zero_dropped = [&](int t, int nthr) {
       if constexpr (kFused) zero_rows(img_o, sDrop, t >> 3, a.N - n, nthr >> 3, HDb);
     };
+    // cu_mode 2: the head-0 problem of image b counts the keeps of images [0, b)
+    // (while its gathers are in flight); reduced at the next slot barrier.
+    const bool cu_here = kFused && a.cu_mode == 2 && h == 0;
+    auto count_prefix = [&]() {
+      int c = count_kept(a.keep, (long long)b * a.N, tid, kTcSlotThreads);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+      if ((tid & 31) == 0) sWords[warp] = (uint32_t)c;  // ballot words are dead now
+    };
+    auto write_cu = [&]() {  // after a slot barrier
+      const int pre = (int)(sWords[0] + sWords[1] + sWords[2] + sWords[3]);
+      a.cu_out[b] = pre;
+      if (b == a.B - 1) a.cu_out[a.B] = pre + n;
+    };
     if (n == 0) {  // nothing to attend (R11)
+      if (cu_here) count_prefix();
       zero_dropped(tid, kTcSlotThreads);
       sync();      // sPos / sDrop are rewritten by the next problem
+      if (cu_here && tid == 0) write_cu();
+      sync();
       continue;
     }
     const int n16 = (n + 15) & ~15;
@@ -159,6 +176,7 @@ __global__ void __launch_bounds__(3 * kTcSlotThreads, 1) attn_tc_kernel(const At
     };
     load_q_tile(0);
     cp_async_commit();
+    if (cu_here) count_prefix();
     TL(2);
     // warps [live, 4) own no query row of tile 0: they write the zero rows while
     // the others run the softmax; with no idle warp, every thread does it last.
@@ -172,6 +190,7 @@ __global__ void __launch_bounds__(3 * kTcSlotThreads, 1) attn_tc_kernel(const At
       tc::fence_before();
       sync();
       TL(3);
+      if (tile == 0 && cu_here && tid == 0) write_cu();
       // Warps [0, live_t) own real query rows of this tile and run the chunk loop;
       // the others skip straight to the store phase (on tile 0 they write the
       // zero rows meanwhile).  Inside the loop only the live warps synchronize.

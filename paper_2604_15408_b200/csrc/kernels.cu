@@ -361,7 +361,9 @@ struct AttnArgs {
   const void* v;
   void* o;                 // fused: padded O; attn: packed O
   const int32_t* cu;       // attn: cu_seqlens input
-  int32_t* cu_out;         // fused: optional cu_seqlens output (block 0 computes it)
+  int32_t* cu_out;         // fused: optional cu_seqlens output
+  int cu_mode;             // 0: none; 1: one extra CTA / work item scans the mask;
+                           // 2: every head-0 CTA counts the keeps before its image
   int B, N, H;
   long long ld;            // input token stride in elements
 };
@@ -381,6 +383,25 @@ __device__ __forceinline__ void zero_rows(char* img_o, const int16_t* sDrop, int
     st_global_16(img_o + d3 * HDb, z);
   }
   for (; rr < nd; rr += step) st_global_16(img_o + sDrop[rr] * HDb, z);
+}
+
+// Kept positions in keep[0, len) -- this thread's share (stride nthr): 16-byte
+// loads when the mask is 16-byte aligned, nonzero bytes counted with __vcmpne4.
+__device__ __forceinline__ int count_kept(const uint8_t* __restrict__ keep, long long len, int t,
+                                          int nthr) {
+  int cnt = 0;
+  long long p = t;
+  if ((reinterpret_cast<uintptr_t>(keep) & 15) == 0) {
+    const long long nfull = len >> 4;
+    for (long long c = t; c < nfull; c += nthr) {
+      const uint4 v = *reinterpret_cast<const uint4*>(keep + (c << 4));
+      cnt += (__popc(__vcmpne4(v.x, 0u)) + __popc(__vcmpne4(v.y, 0u)) + __popc(__vcmpne4(v.z, 0u)) +
+              __popc(__vcmpne4(v.w, 0u))) >> 3;
+    }
+    p = (nfull << 4) + t;
+  }
+  for (; p < len; p += nthr) cnt += keep[p] != 0 ? 1 : 0;
+  return cnt;
 }
 
 // Block 0 of a fused launch that also emits cu_seqlens: one CTA walks the keep
@@ -464,7 +485,7 @@ __global__ void __launch_bounds__(kAttnThreads, 3) attn_kernel(const AttnArgs a)
   pdl_wait_prerequisites();
   int bid = blockIdx.x;
   if constexpr (kFused) {
-    if (a.cu_out != nullptr) {
+    if (a.cu_mode == 1) {
       if (bid == 0) {  // the scan CTA: cu_seqlens only, concurrent with the rest
         scan_cta_cu(a, sK, tid, [] { __syncthreads(); });
         return;
@@ -519,11 +540,25 @@ __global__ void __launch_bounds__(kAttnThreads, 3) attn_kernel(const AttnArgs a)
   };
   if (warp * 16 < n) load_q(qwarp, warp);
   cp_async_commit();
+  // cu_mode 2: the head-0 CTA of image b counts the keeps of images [0, b) while
+  // its gathers are in flight (L2-hot mask bytes); reduced at the barrier below.
+  const bool cu_here = kFused && a.cu_mode == 2 && h == 0;
+  if (cu_here) {
+    int c = count_kept(a.keep, (long long)b * a.N, tid, kAttnThreads);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    if (lane == 0) sWords[warp] = (uint32_t)c;  // ballot words are dead after image_rows
+  }
 
   TL(2);
   cp_async_wait_all();
   __syncthreads();
   TL(3);
+  if (cu_here && tid == 0) {
+    const int pre = (int)(sWords[0] + sWords[1] + sWords[2] + sWords[3]);
+    a.cu_out[b] = pre;
+    if (b == a.B - 1) a.cu_out[a.B] = pre + n;
+  }
 
   // Dropped rows of this head -> +0.0 (8 consecutive threads write one 128-byte
   // row).  Issued by the warps that own no query slice, concurrently with the
@@ -532,7 +567,9 @@ __global__ void __launch_bounds__(kAttnThreads, 3) attn_kernel(const AttnArgs a)
   const int nsl = (n + 15) >> 4;
   const int busy = nsl < 4 ? nsl : 4;  // warps [0, busy) own slices
   auto zero_dropped = [&](int t, int nthr) {
+#ifndef RAGGED_ABLATE_ZERO
     if constexpr (kFused) zero_rows(img_o, sDrop, t >> 3, a.N - n, nthr >> 3, HDb);
+#endif
   };
   if (busy < 4 && warp >= busy) zero_dropped(tid - busy * 32, (4 - busy) * 32);
 
@@ -562,7 +599,11 @@ __global__ void __launch_bounds__(kAttnThreads, 3) attn_kernel(const AttnArgs a)
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
         s[j][0] = s[j][1] = s[j][2] = s[j][3] = 0.f;
+#ifdef RAGGED_ABLATE_QK
+        if (false) {
+#else
         if (j < nt) {
+#endif
           uint32_t kb[8];
           const int kr = cb + 8 * j + (lane & 7);
           ldmatrix_x4(smem_u32(sK + swz(kr, lane >> 3)), kb[0], kb[1], kb[2], kb[3]);
@@ -606,7 +647,11 @@ __global__ void __launch_bounds__(kAttnThreads, 3) attn_kernel(const AttnArgs a)
       }
 #pragma unroll
       for (int j = 0; j < 8; ++j) {  // P = e^{S - m'}; key tiles past n skipped (exp2 unit)
+#ifdef RAGGED_ABLATE_EXP
+        if (false) {
+#else
         if (j < nt) {
+#endif
           s[j][0] = ex2(s[j][0] - mn0);
           s[j][1] = ex2(s[j][1] - mn0);
           s[j][2] = ex2(s[j][2] - mn1);
@@ -618,7 +663,11 @@ __global__ void __launch_bounds__(kAttnThreads, 3) attn_kernel(const AttnArgs a)
         }
       }
       // O += P_hi V + P_lo V
+#ifdef RAGGED_ABLATE_PV
+      const int nk = 0;
+#else
       const int nk = (nv + 15) >> 4;
+#endif
 #pragma unroll
       for (int kk = 0; kk < 4; ++kk) {
         if (kk < nk) {
@@ -815,11 +864,15 @@ cudaError_t launch_fused(int dtype, int engine, const uint8_t* keep, const void*
   a.v = v;
   a.o = o;
   a.cu_out = cu_out;
+  // Small batches: each head-0 CTA derives its own cu[b] (no extra CTA on the
+  // critical path); large: one extra scan CTA / work item, hidden by the rest.
+  a.cu_mode = cu_out == nullptr ? 0 : ((long long)B * N <= 65536 ? 2 : 1);
+
   a.B = B;
   a.N = N;
   a.H = H;
   a.ld = ld;
-  return dispatch_attn<true>(dtype, engine, a, B * H + (cu_out ? 1 : 0), st);
+  return dispatch_attn<true>(dtype, engine, a, B * H + (a.cu_mode == 1 ? 1 : 0), st);
 }
 
 cudaError_t launch_empty(int grid, int block, cudaStream_t st) {

@@ -280,3 +280,21 @@ def test_c5_scale_sampled(engine):
                                                 keep_np[b][None], 0, int(h))
         got = o[b, torch.from_numpy(pos).to(DEV), int(h)].double().cpu().numpy()
         assert np.abs(got - rows).max() <= TOL[torch.bfloat16]
+
+
+@pytest.mark.parametrize("engine", ENGINES)
+@pytest.mark.parametrize("B,N", [(9, 197), (5, 33), (400, 197)])  # B*N <= / > 65536: both cu modes
+def test_fused_cu_with_empty_images(engine, B, N):
+    """cu_seqlens from the fused launch (head-0 prefix mode and scan-CTA mode),
+    including empty first / last images, equals the oracle's."""
+    rng = np.random.default_rng(B + N)
+    keep = (rng.random((B, N)) < 0.3).astype(np.uint8)
+    keep[0] = 0
+    keep[-1] = 0
+    keep[B // 2] = 0
+    q, k, v = synth.activations(B, N, 2, 64, "bf16", seed=3)
+    qd, kd, vd = _dev(q, k, v)
+    o, cu = rb.pack_attend_unpack(qd, kd, vd, torch.from_numpy(keep).to(DEV), want_cu=True, engine=engine)
+    torch.cuda.synchronize()
+    assert cu.cpu().numpy().tolist() == oracle.scan(keep)[0].tolist()
+    assert torch.all(o[0] == 0) and torch.all(o[-1] == 0)
