@@ -1,5 +1,5 @@
 """fp64 CPU oracle (TEST INFRASTRUCTURE ONLY; see ragged_oracle.py header)."""
 from .ragged_oracle import (  # noqa: F401
     as_f64, scan, pack, attention_one, softmax_weights, attention, unpack,
-    pack_attend_unpack, attention_image_head,
+    pack_attend_unpack, attention_image_head, l2_scores, keep_topk_l2,
 )

@@ -28,6 +28,9 @@ Passages followed (PAPER.md line numbers):
              dropped positions hold +0.0 (reading R10; not in the paper).
   fused      pack_attend_unpack = unpack o attention o pack (BASELINE.json).
 
+  prune      (NEXT row N2) Threshold-l2 keep mask: l2 norm of each token's
+             hidden state, CLS + top-(k-1) (R20).
+
 Pins (tests/test_oracle.py, run with -m "not gpu"): SPEC worked examples,
 Table 1 token counts and the T = 6,304 / 12,608 totals (P:167-179, P:202,
 P:238), brute-force global ranks, torch.nonzero / flash_attn.bert_padding
@@ -138,6 +141,29 @@ def pack_attend_unpack(q, k, v, keep):
     T = int(cu[B])
     op = attention(pack(q, src, T), pack(k, src, T), pack(v, src, T), cu)
     return unpack(op, dst, B, N, 0.0), cu
+
+
+def l2_scores(x) -> np.ndarray:
+    """Threshold-l2 token scores (the paper names the scorer but never
+    defines it, S:312 -- DESIGN.md R20): score[b, n] = ||x[b, n, :]||_2 in fp64,
+    with CLS (n = 0) set to +inf so it always survives (R6)."""
+    x = as_f64(x)
+    s = np.sqrt((x * x).sum(axis=2))
+    s[:, 0] = np.inf
+    return s
+
+
+def keep_topk_l2(x, k: int) -> np.ndarray:
+    """keep [B, N] uint8: CLS + the k - 1 highest-scoring other tokens of each
+    image (P:362-363 "any supported method produces a binary keep mask"); ties
+    go to the lower position (stable order, R20)."""
+    s = l2_scores(x)
+    B, N = s.shape
+    keep = np.zeros((B, N), np.uint8)
+    for b in range(B):
+        order = np.argsort(-s[b], kind="stable")
+        keep[b, order[:max(0, min(k, N))]] = 1
+    return keep
 
 
 def attention_image_head(q, k, v, keep, b: int, h: int):

@@ -88,6 +88,21 @@ def activations(B: int, N: int, H: int, d: int = HEAD_DIM, dtype=torch.bfloat16,
     return q, k, v
 
 
+def hidden_states(B: int, N: int, D: int, dtype=torch.bfloat16, seed: int = 0,
+                  image_offset: int = 0) -> torch.Tensor:
+    """Synthetic hidden states x [B, N, D] at the prune point (after layer 4,
+    P:361-362): per-token LogNormal(0, 0.5) scale times N(0, I_D), rounded once
+    to `dtype` -- the heavy-tailed token norms Threshold-l2 ranks."""
+    if isinstance(dtype, str):
+        dtype = DTYPES[dtype]
+    x = torch.empty(B, N, D, dtype=dtype)
+    for b in range(B):
+        g = _img_gen(seed, image_offset + b, 2)
+        scale = torch.exp(0.5 * torch.randn(N, 1, generator=g))
+        x[b] = (scale * torch.randn(N, D, generator=g)).to(dtype)
+    return x
+
+
 # --------------------------------------------------------------------------
 # keep-mask generators: uint8 [B, N], nonzero = keep, CLS (position 0) kept.
 # --------------------------------------------------------------------------

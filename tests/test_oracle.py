@@ -301,3 +301,39 @@ def test_oracle_rejects_nonfinite():
     x[1, 0, 0] = np.nan
     with pytest.raises(ValueError):
         oracle.attention(x, x, x, np.array([0, 3]))
+
+
+# ------------------------------------------------- N2: Threshold-l2 mask ----
+
+def test_keep_topk_l2_brute_force():
+    """Brute force on tiny inputs: the kept set is CLS plus the k-1 positions
+    with the largest ||x||, ties to the lower index (checked by enumerating
+    every subset of size k-1 and picking the lexicographic best)."""
+    rng = np.random.default_rng(21)
+    for trial in range(30):
+        N, D = int(rng.integers(2, 8)), int(rng.integers(1, 5))
+        x = np.round(rng.standard_normal((1, N, D)) * 2) / 2        # exact ties happen
+        k = int(rng.integers(1, N + 1))
+        got = oracle.keep_topk_l2(x, k)[0]
+        norms = [math.sqrt(sum(v * v for v in x[0, n])) for n in range(N)]
+        best = None
+        for subset in itertools.combinations(range(1, N), k - 1):
+            key = (sorted((-norms[n], n) for n in subset))
+            if best is None or key < best[0]:
+                best = (key, subset)
+        want = np.zeros(N, np.uint8)
+        want[0] = 1
+        want[list(best[1])] = 1
+        assert np.array_equal(got, want), (x, k)
+
+
+def test_keep_topk_l2_invariants_and_table1_counts():
+    x = synth.hidden_states(8, 197, 64, "bf16", seed=3)
+    for p, tok in ((0.0, 197), (0.5, 99), (0.8, 39)):                 # Table 1, P:167-179
+        keep = oracle.keep_topk_l2(x, synth.kept_tokens(197, p))
+        assert np.all(keep.sum(1) == tok) and np.all(keep[:, 0] == 1)
+        s = oracle.l2_scores(x)
+        for b in range(8):
+            kept, dropped = s[b][keep[b] == 1], s[b][keep[b] == 0]
+            if dropped.size:
+                assert kept.min() >= dropped.max()                      # threshold property
