@@ -488,6 +488,21 @@ def extras(args, rb, torch, dev, sets, c, B, N, H, dt, T):
                       "fused_hbm_frac": ab / (f_us * 1e-6) / 1e9 / 6560.6, "alg_bytes": ab})
     out["prune_sweep"] = sweep
     out["configs"] = config_extras(rb, torch, dev, dt)
+    # NEXT row N2: on-device Threshold-l2 keep mask from hidden states (x is
+    # B x N x H*64, the tensor the paper prunes at layer 4), alone and
+    # ahead of the fused path (two launches, PDL-overlapped)
+    xs = [synth.hidden_states(B, N, H * 64, args.dtype, seed=40 + i).to(dev) for i in range(4)]
+    kk = synth.kept_tokens(N, c["p"])
+    keeps = [torch.empty(B, N, dtype=torch.uint8, device=dev) for _ in range(N_SETS)]
+    out["prune_l2_mask_us"] = _graph_time(torch, [(lambda i=i: rb.keep_topk_l2(xs[i % 4], kk, keep=keeps[i]))
+                                                  for i in range(N_SETS)], reps)
+    out["prune_l2_mask_alg_bytes"] = B * N * H * 64 * 2 + B * N
+
+    def prune_fused(i):
+        s = sets[i]
+        rb.keep_topk_l2(xs[i % 4], kk, keep=keeps[i])
+        rb.pack_attend_unpack(s["q"], s["k"], s["v"], keeps[i], o=s["o"], cu=s["cu"])
+    out["prune_then_fused_us"] = _graph_time(torch, [(lambda i=i: prune_fused(i)) for i in range(N_SETS)], reps)
     return out
 
 

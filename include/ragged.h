@@ -138,6 +138,15 @@ RAGGED_API ragged_status ragged_graph_create(const ragged_problem* prob, const u
 RAGGED_API ragged_status ragged_graph_launch(ragged_graph* graph, void* stream);
 RAGGED_API void ragged_graph_destroy(ragged_graph* graph);
 
+/* NEXT row N2 -- on-device Threshold-l2 keep mask: for
+ * hidden states x [B, N, D] (D = H*d, token stride ld elements, bf16/fp16 by
+ * prob->dtype) write keep[b, n] = 1 for CLS (n = 0) and the k - 1 other tokens
+ * with the largest ||x[b, n, :]||_2 (ties to the lower position; scores in
+ * fp32), 0 otherwise (R20).  k < 0 -> RAGGED_EINVAL; k >= N keeps all.
+ * One launch, one CTA per image.  Feeds ragged_pack / ragged_pack_attend_unpack. */
+RAGGED_API ragged_status ragged_keep_topk_l2(const ragged_problem* prob, const void* x, int32_t k,
+                                             uint8_t* keep, void* stream);
+
 /* Launch-floor probe: an empty kernel launched with `grid` x
  * `block` threads; its latency is the dispatch floor of this library. */
 RAGGED_API ragged_status ragged_empty_launch(int32_t grid, int32_t block, void* stream);

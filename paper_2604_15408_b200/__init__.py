@@ -56,6 +56,7 @@ def _load() -> ctypes.CDLL:
         "ragged_graph_create": [P, V, V, V, V, V, V, ctypes.POINTER(V)],
         "ragged_graph_launch": [V, V],
         "ragged_empty_launch": [I32, I32, V],
+        "ragged_keep_topk_l2": [P, V, I32, V, V],
         "ragged_validate_cu_seqlens": [ctypes.POINTER(I32), I32, I64],
     }
     for name, args in sigs.items():
@@ -77,7 +78,8 @@ _lib = None
 
 EXPORTS = ("ragged_scan", "ragged_pack", "ragged_attn", "ragged_unpack", "ragged_pack_attend_unpack",
            "ragged_graph_create", "ragged_graph_launch", "ragged_graph_destroy", "ragged_empty_launch",
-           "ragged_validate_cu_seqlens", "ragged_status_str", "ragged_last_error", "ragged_build_info")
+           "ragged_validate_cu_seqlens", "ragged_status_str", "ragged_last_error", "ragged_build_info",
+           "ragged_keep_topk_l2")
 
 
 def lib() -> ctypes.CDLL:
@@ -243,6 +245,21 @@ class Graph:
             self.close()
         except Exception:
             pass
+
+
+def keep_topk_l2(x, k: int, keep=None, stream=None):
+    """N2: Threshold-l2 keep mask from hidden states
+    x [B, N, D] (token stride x.stride(1)) -> uint8 keep [B, N]."""
+    if x.dim() != 3 or x.stride(2) != 1 or x.dtype not in _DTYPE:
+        raise ValueError("x must be [B, N, D] bf16/fp16 with unit feature stride")
+    B, N, D = x.shape
+    if D % 64 != 0 or x.stride(0) != N * x.stride(1):
+        raise ValueError("D must be a multiple of 64 and tokens evenly strided")
+    keep = torch.empty(B, N, dtype=torch.uint8, device=x.device) if keep is None else keep
+    p = problem(B, N, D // 64, 64, x.dtype, x.stride(1))
+    _check(lib().ragged_keep_topk_l2(ctypes.byref(p), x.data_ptr(), int(k), keep.data_ptr(),
+                                     _stream(stream)), "ragged_keep_topk_l2")
+    return keep
 
 
 def empty_launch(grid: int = 1, block: int = 32, stream=None):

@@ -226,6 +226,18 @@ void ragged_graph_destroy(ragged_graph* graph) {
   delete graph;
 }
 
+ragged_status ragged_keep_topk_l2(const ragged_problem* prob, const void* x, int32_t k,
+                                  uint8_t* keep, void* stream) {
+  RAGGED_TRY(check_problem(prob));
+  if (k < 0) return fail(RAGGED_EINVAL, "k < 0");
+  if (prob->B == 0) return RAGGED_OK;
+  RAGGED_TRY(check_ptr(x, "x"));
+  RAGGED_TRY(check_ptr_any(keep, "keep"));
+  cudaError_t e = ragged::launch_keep_topk_l2(prob->dtype, x, prob->ld, prob->B, prob->N,
+                                              prob->H * prob->d, k, keep, as_stream(stream));
+  return e == cudaSuccess ? RAGGED_OK : cuda_fail(e, "ragged_keep_topk_l2");
+}
+
 ragged_status ragged_empty_launch(int32_t grid, int32_t block, void* stream) {
   if (grid < 1 || block < 1 || block > 1024) return fail(RAGGED_EINVAL, "bad grid/block");
   cudaError_t e = ragged::launch_empty(grid, block, as_stream(stream));

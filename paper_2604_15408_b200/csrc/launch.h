@@ -19,6 +19,8 @@ cudaError_t launch_fused(int dtype, int engine, const uint8_t* keep, const void*
                          const void* v, long long ld, void* o, int32_t* cu_out, int B, int N, int H,
                          cudaStream_t st);
 cudaError_t launch_empty(int grid, int block, cudaStream_t st);
+cudaError_t launch_keep_topk_l2(int dtype, const void* x, long long ld, int B, int N, int D, int k,
+                                uint8_t* keep, cudaStream_t st);
 int fused_smem_bytes(int N);
 #ifdef RAGGED_TIMELINE
 int timeline_copy(void* host, int max_ctas);

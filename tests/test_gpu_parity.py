@@ -298,3 +298,59 @@ def test_fused_cu_with_empty_images(engine, B, N):
     torch.cuda.synchronize()
     assert cu.cpu().numpy().tolist() == oracle.scan(keep)[0].tolist()
     assert torch.all(o[0] == 0) and torch.all(o[-1] == 0)
+
+
+# ------------------------------------------------- N2: on-device prune ----
+
+def _check_l2_mask(x, k, got):
+    """Exact where the decision is unique (score gap at the threshold well above
+    fp32 rounding); otherwise the result must still be a valid top-k."""
+    want = oracle.keep_topk_l2(x, k)
+    s = oracle.l2_scores(x)
+    B, N = want.shape
+    for b in range(B):
+        if np.array_equal(got[b], want[b]):
+            continue
+        srt = np.sort(s[b])[::-1]
+        gap = (srt[k - 1] - srt[k]) / srt[k] if 0 < k < N else np.inf
+        assert gap < 1e-5, f"image {b}: masks differ although the threshold gap is {gap:.2e}"
+        assert got[b].sum() == want[b].sum() and got[b][0] == 1
+        assert s[b][got[b] == 1].min() >= s[b][got[b] == 0].max() * (1 - 1e-5)
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "fp16"])
+@pytest.mark.parametrize("B,N,D,p", [(32, 197, 768, 0.8), (4, 197, 192, 0.5), (7, 33, 64, 0.3),
+                                     (3, 256, 384, 0.9), (2, 1, 64, 0.0)])
+def test_keep_topk_l2_matches_oracle(dtype, B, N, D, p):
+    x = synth.hidden_states(B, N, D, dtype, seed=5)
+    k = synth.kept_tokens(N, p)
+    keep = rb.keep_topk_l2(x.to(DEV), k)
+    torch.cuda.synchronize()
+    _check_l2_mask(x, k, keep.cpu().numpy())
+
+
+def test_keep_topk_l2_ties_and_k_edges():
+    """Exact ties resolve to the lower position; k = 0 keeps nothing, k >= N all."""
+    x = torch.zeros(2, 9, 64, dtype=torch.bfloat16)
+    x[:, 1:, 0] = 1.0                       # all non-CLS scores equal
+    x[1, 5, 0] = 2.0
+    xd = x.to(DEV)
+    got = rb.keep_topk_l2(xd, 4).cpu().numpy()
+    assert got[0].tolist() == [1, 1, 1, 1, 0, 0, 0, 0, 0]
+    assert got[1].tolist() == [1, 1, 1, 0, 0, 1, 0, 0, 0]
+    assert rb.keep_topk_l2(xd, 0).cpu().numpy().sum() == 0
+    assert rb.keep_topk_l2(xd, 50).cpu().numpy().sum() == 18
+
+
+def test_prune_then_fused_path():
+    """N2 -> a5: the on-device mask drives the fused path; equals the oracle end to end."""
+    B, N, H = 8, 197, 12
+    x = synth.hidden_states(B, N, H * 64, "bf16", seed=6)
+    q, k, v = synth.activations(B, N, H, 64, "bf16", seed=6)
+    keep = rb.keep_topk_l2(x.to(DEV), synth.kept_tokens(N, 0.7))
+    o = rb.pack_attend_unpack(*_dev(q, k, v), keep)
+    torch.cuda.synchronize()
+    km = keep.cpu().numpy()
+    _check_l2_mask(x, synth.kept_tokens(N, 0.7), km)
+    ref, _ = oracle.pack_attend_unpack(q, k, v, km)
+    check_attention(to_np(o), ref, torch.bfloat16)
