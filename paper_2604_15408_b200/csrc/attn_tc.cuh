@@ -44,8 +44,8 @@ struct TcSmem {
 __host__ __device__ inline TcSmem tc_smem(int N) {
   TcSmem L;
   L.kv_rows = (N + 15) & ~15;
-  L.off_q = 0;                                     // 64 x 128 B Q tile; O staging later
-  L.off_k = kTcTile * kRowBytes;                   // kv_rows x 128 B
+  L.off_q = 0;                                     // 128 x 128 B: one Q tile or a tile pair; O staging later
+  L.off_k = 2 * kTcTile * kRowBytes;               // kv_rows x 128 B
   L.off_v = L.off_k + L.kv_rows * kRowBytes;
   L.off_small = L.off_v + L.kv_rows * kRowBytes;   // pos, drop, ballots, scan scratch, mbarriers
   L.slot_bytes = L.off_small + 2048;
@@ -77,7 +77,7 @@ __global__ void __launch_bounds__(3 * kTcSlotThreads, 1) attn_tc_kernel(const At
   int16_t* sPos = reinterpret_cast<int16_t*>(small);
   int16_t* sDrop = sPos + kMaxN;
   uint32_t* sWords = reinterpret_cast<uint32_t*>(sDrop + kMaxN);         // 32 B
-  uint64_t* bars = reinterpret_cast<uint64_t*>(small + 1056);            // 2 x 8 B
+  uint64_t* bars = reinterpret_cast<uint64_t*>(small + 1056);            // 4 x 8 B
   uint32_t* tslot = reinterpret_cast<uint32_t*>(smem + nslots * L.slot_bytes);
   auto sync = [slot] { asm volatile("bar.sync %0, %1;" ::"r"(slot + 1), "r"(kTcSlotThreads) : "memory"); };
 
@@ -86,8 +86,10 @@ __global__ void __launch_bounds__(3 * kTcSlotThreads, 1) attn_tc_kernel(const At
   const uint32_t ncols_cta = nslots > 2 ? 512u : (nslots > 1 ? 256u : 128u);
   if (threadIdx.x < 32) tc::alloc(smem_u32(tslot), ncols_cta);  // first thing: see header
   if (tid == 32) {
-    tc::mbar_init(smem_u32(&bars[0]), 1);
-    tc::mbar_init(smem_u32(&bars[1]), 1);
+    tc::mbar_init(smem_u32(&bars[0]), 1);  // single-tile path: S ready
+    tc::mbar_init(smem_u32(&bars[1]), 1);  // single-tile path: P V done
+    tc::mbar_init(smem_u32(&bars[2]), 1);  // pair path: tile A (S_{j+1} ready, P_j V_j done)
+    tc::mbar_init(smem_u32(&bars[3]), 1);  // pair path: tile B
     tc::fence_mbar_init();
   }
   tc::fence_before();
@@ -101,6 +103,8 @@ __global__ void __launch_bounds__(3 * kTcSlotThreads, 1) attn_tc_kernel(const At
   const int g = (tid & 31) >> 2, t4 = tid & 3;                     // fragment row / column pair
   const uint32_t bar_s = smem_u32(&bars[0]), bar_o = smem_u32(&bars[1]);
   uint32_t ph_s = 0, ph_o = 0;
+  const uint32_t bar_x = smem_u32(&bars[2]);  // pair path: tile X uses bar_x + 8 X
+  uint32_t ph_x[2] = {0u, 0u};                // pair path: per-tile barrier parities
   constexpr uint32_t kFmt = std::is_same<T, __nv_bfloat16>::value ? 1u : 0u;
   const uint32_t idesc_o = tc::idesc_f16(kFmt, kTcTile, kHeadDim, 1);
   constexpr float kScaleLog2 = 0.18033688011112042f;  // log2(e) / sqrt(64)
@@ -166,15 +170,15 @@ __global__ void __launch_bounds__(3 * kTcSlotThreads, 1) attn_tc_kernel(const At
     }
     // Q tile rows [0, min(128, n - 128 tile)); rows past n stay unwritten: they
     // only feed their own (discarded) S / O rows.
-    auto load_q_tile = [&](int tile) {
+    auto load_q_rows = [&](int first, int rows) {  // query rows [first, first+rows) -> sQ rows 0..
       const int c = tid & 7, r0 = tid >> 3;
-      const int rows = min(kTcTile, n - tile * kTcTile);
       const char* gsrc = img_q + c * 16;
       uint32_t sdst = smem_u32(sQ) + r0 * kRowBytes + ((c ^ (r0 & 7)) << 4);
       for (int rr = r0; rr < rows; rr += 16, sdst += 16 * kRowBytes)
-        cp_async_16(sdst, gsrc + sPos[tile * kTcTile + rr] * ldb, 16);
+        cp_async_16(sdst, gsrc + sPos[first + rr] * ldb, 16);
     };
-    load_q_tile(0);
+    auto load_q_tile = [&](int tile) { load_q_rows(tile * kTcTile, min(kTcTile, n - tile * kTcTile)); };
+    load_q_rows(0, min(n, 2 * kTcTile));
     cp_async_commit();
     if (cu_here) count_prefix();
     TL(2);
@@ -182,7 +186,185 @@ __global__ void __launch_bounds__(3 * kTcSlotThreads, 1) attn_tc_kernel(const At
     // the others run the softmax; with no idle warp, every thread does it last.
     const int live = n >= kTcTile ? 4 : (n + 15) >> 4;
 
-    for (int tile = 0; tile * kTcTile < n; ++tile) {
+    // n > 64: query tiles processed in PAIRS inside the slot's 128 TMEM columns:
+    // tile A (rows 128p .. +63) uses TMEM lanes 0-15 of each warp quarter, tile B
+    // (rows 128p + 64 ..) lanes 16-31 (M = 64 UMMA at lane offset 16 -- verified,
+    // scripts/micro/m64_lane16.cu).  The warps alternate the two tiles' softmax so
+    // one tile's UMMAs run while the other's softmax executes; each tile's
+    // S_{j+1} is queued right behind its P_j V_j, and one commit per tile and
+    // chunk (tcgen05.commit tracks every prior UMMA of the thread) both signals
+    // S_{j+1} and certifies P_j V_j, so lazy O-rescaling needs no extra wait.
+    auto run_pairs = [&]() {
+      const int npairs = (n + 2 * kTcTile - 1) / (2 * kTcTile);
+      for (int pr = 0; pr < npairs; ++pr) {
+        const int r0p = pr * 2 * kTcTile;
+        const int rowsA = min(kTcTile, n - r0p), rowsB = max(0, min(kTcTile, n - r0p - kTcTile));
+        const int ntl = rowsB > 0 ? 2 : 1;
+        if (pr > 0) load_q_rows(r0p, rowsA + rowsB);
+        cp_async_commit();
+        cp_async_wait_all();
+        tc::fence_proxy_async_smem();
+        tc::fence_before();
+        sync();
+        tc::fence_after();
+        if (pr == 0 && cu_here && tid == 0) write_cu();
+        if (pr == 0) TL(3);
+        float mm[2][2], ll[2][2];
+#pragma unroll
+        for (int X = 0; X < 2; ++X) mm[X][0] = mm[X][1] = -INFINITY, ll[X][0] = ll[X][1] = 0.f;
+        auto issue_s = [&](int X, int jj) {  // S of tile X, chunk jj
+          const int kc = min(kTcChunk, n16 - jj * kTcChunk);
+          const uint64_t qd = tc::sw128_desc(smem_u32(sQ) + X * kTcTile * kRowBytes);
+          const uint64_t kd = tc::sw128_desc(smem_u32(sK) + jj * kTcChunk * kRowBytes);
+          const uint32_t idesc_s = tc::idesc_f16(kFmt, kTcTile, kc, 0);
+          const uint32_t d = tS + ((uint32_t)(16 * X) << 16);
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk) tc::mma_ss(d, qd + 2 * kk, kd + 2 * kk, idesc_s, kk > 0);
+        };
+        if (tid == 0) {
+          for (int X = 0; X < ntl; ++X) {
+            issue_s(X, 0);
+            tc::commit(bar_x + 8u * (uint32_t)X);
+          }
+        }
+        for (int j = 0; j < nchunks; ++j) {
+          for (int X = 0; X < ntl; ++X) {
+            tc::mbar_wait(bar_x + 8u * (uint32_t)X, ph_x[X]);
+            ph_x[X] ^= 1u;
+            tc::fence_after();
+            if (pr == 0 && j == 0 && X == 0) TL(5);
+            const int rowsX = X ? rowsB : rowsA;
+            if (warp * 16 < rowsX) {  // this warp owns real rows of tile X
+              const uint32_t tSx = tS + lane_off + ((uint32_t)(16 * X) << 16);
+              const uint32_t tOx = tO + lane_off + ((uint32_t)(16 * X) << 16);
+              float& m0x = mm[X][0];
+              float& m1x = mm[X][1];
+              const int c0 = j * kTcChunk;
+              const int nv = min(kTcChunk, n - c0);
+              const int ngv = (nv + 7) >> 3;
+              float x[8][4];
+              {
+                uint32_t r[32];
+                tc::ld_16x256b_x8(tSx, r);
+                tc::wait_ld();
+#pragma unroll
+                for (int jg = 0; jg < 8; ++jg)
+#pragma unroll
+                  for (int e = 0; e < 4; ++e) {
+                    const int key = 8 * jg + 2 * t4 + (e & 1);
+                    x[jg][e] = key < nv ? __uint_as_float(r[4 * jg + e]) * kScaleLog2 : -INFINITY;
+                  }
+              }
+              float mx0 = -INFINITY, mx1 = -INFINITY;
+#pragma unroll
+              for (int jg = 0; jg < 8; ++jg) {
+                mx0 = fmaxf(mx0, fmaxf(x[jg][0], x[jg][1]));
+                mx1 = fmaxf(mx1, fmaxf(x[jg][2], x[jg][3]));
+              }
+              mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 1));
+              mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 2));
+              mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 1));
+              mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 2));
+              float al0 = 1.f, al1 = 1.f;
+              if (j == 0) {
+                m0x = mx0;
+                m1x = mx1;
+              } else {
+                if (mx0 - m0x > 8.f) { al0 = ex2(m0x - mx0); m0x = mx0; }
+                if (mx1 - m1x > 8.f) { al1 = ex2(m1x - mx1); m1x = mx1; }
+              }
+              if (j > 0 && __any_sync(0xffffffffu, al0 != 1.f || al1 != 1.f)) {  // P_{j-1} V_{j-1} is done
+                uint32_t o[32];
+                tc::ld_16x256b_x8(tOx, o);
+                tc::wait_ld();
+#pragma unroll
+                for (int jg = 0; jg < 8; ++jg) {
+                  o[4 * jg + 0] = __float_as_uint(__uint_as_float(o[4 * jg + 0]) * al0);
+                  o[4 * jg + 1] = __float_as_uint(__uint_as_float(o[4 * jg + 1]) * al0);
+                  o[4 * jg + 2] = __float_as_uint(__uint_as_float(o[4 * jg + 2]) * al1);
+                  o[4 * jg + 3] = __float_as_uint(__uint_as_float(o[4 * jg + 3]) * al1);
+                }
+                tc::st_16x256b_x8(tOx, o);
+              }
+              ll[X][0] *= al0;
+              ll[X][1] *= al1;
+              uint32_t hi[16], lo[16];
+#pragma unroll
+              for (int jg = 0; jg < 8; ++jg) {
+                float p0 = 0.f, p1 = 0.f, p2 = 0.f, p3 = 0.f;
+                if (jg < ngv) {
+                  p0 = ex2(x[jg][0] - m0x);
+                  p1 = ex2(x[jg][1] - m0x);
+                  p2 = ex2(x[jg][2] - m1x);
+                  p3 = ex2(x[jg][3] - m1x);
+                }
+                ll[X][0] += p0 + p1;
+                ll[X][1] += p2 + p3;
+                split2<T>(p0, p1, hi[2 * jg], lo[2 * jg]);
+                split2<T>(p2, p3, hi[2 * jg + 1], lo[2 * jg + 1]);
+              }
+              tc::st_16x128b_x8(tSx, hi);
+              tc::st_16x128b_x8(tSx + 32, lo);
+              tc::wait_st();
+            }
+            tc::fence_before();
+            sync();
+            if (tid == 0) {  // P_j V_j for tile X, then S_{j+1} behind it; one commit covers both
+              tc::fence_after();
+              const int nk = (min(kTcChunk, n - j * kTcChunk) + 15) >> 4;
+              const uint32_t pa = tS + ((uint32_t)(16 * X) << 16);
+              const uint32_t od = tO + ((uint32_t)(16 * X) << 16);
+              for (int kk = 0; kk < nk; ++kk) {
+                const uint64_t vd = tc::sw128_desc(smem_u32(sV) + (j * kTcChunk + kk * 16) * kRowBytes);
+                tc::mma_ts(od, pa + kk * 8, vd, idesc_o, (j > 0 || kk > 0) ? 1u : 0u);
+                tc::mma_ts(od, pa + 32 + kk * 8, vd, idesc_o, 1u);
+              }
+              if (j + 1 < nchunks) issue_s(X, j + 1);
+              tc::commit(bar_x + 8u * (uint32_t)X);
+            }
+          }
+        }
+        if (pr == 0) TL(8);
+        for (int X = 0; X < ntl; ++X) {  // the last commit certifies the last P V
+          tc::mbar_wait(bar_x + 8u * (uint32_t)X, ph_x[X]);
+          ph_x[X] ^= 1u;
+        }
+        tc::fence_after();
+        if (pr == 0) TL(9);
+        // epilogue: both tiles' O rows -> 16 bit -> SMEM (sQ is free) -> row stores
+        for (int X = 0; X < ntl; ++X) {
+          const int rowsX = X ? rowsB : rowsA;
+          if (warp * 16 >= rowsX) continue;
+          float l0 = ll[X][0], l1 = ll[X][1];
+          l0 += __shfl_xor_sync(0xffffffffu, l0, 1);
+          l0 += __shfl_xor_sync(0xffffffffu, l0, 2);
+          l1 += __shfl_xor_sync(0xffffffffu, l1, 1);
+          l1 += __shfl_xor_sync(0xffffffffu, l1, 2);
+          const float inv0 = 1.f / l0, inv1 = 1.f / l1;
+          uint32_t o[32];
+          tc::ld_16x256b_x8(tO + lane_off + ((uint32_t)(16 * X) << 16), o);
+          tc::wait_ld();
+          const int r0 = X * kTcTile + warp * 16 + g, r1 = r0 + 8;
+#pragma unroll
+          for (int jg = 0; jg < 8; ++jg) {
+            *reinterpret_cast<uint32_t*>(sQ + swz(r0, jg) + 4 * t4) =
+                pack2<T>(__uint_as_float(o[4 * jg + 0]) * inv0, __uint_as_float(o[4 * jg + 1]) * inv0);
+            *reinterpret_cast<uint32_t*>(sQ + swz(r1, jg) + 4 * t4) =
+                pack2<T>(__uint_as_float(o[4 * jg + 2]) * inv1, __uint_as_float(o[4 * jg + 3]) * inv1);
+          }
+        }
+        tc::fence_before();
+        sync();
+        for (int rr = tid >> 3; rr < rowsA + rowsB; rr += kTcSlotThreads / 8) {
+          const uint4 v = *reinterpret_cast<const uint4*>(sQ + rr * kRowBytes + (((tid & 7) ^ (rr & 7)) << 4));
+          st_global_16(img_o + sPos[r0p + rr] * HDb, v);
+        }
+        sync();  // sQ, TMEM reused by the next pair / problem
+        if (pr == 0) TL(6);
+      }
+    };
+    if (n > kTcTile) run_pairs();
+    for (int tile = 0; n <= kTcTile && tile * kTcTile < n; ++tile) {
       if (tile > 0) load_q_tile(tile);
       cp_async_commit();
       cp_async_wait_all();

@@ -1,2 +1,7 @@
-for rep in 1 2; do for v in _old _x _y ""; do RAGGED_LIB=paper_2604_15408_b200/libragged$v.so timeout 300 python bench.py --steps 3000 --warmup 20 --engine 1 --no-extras --e2e-steps 5 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('lib$v e1', round(d['us_per_call'],3))"; done; done
-RAGGED_LIB=paper_2604_15408_b200/libragged_old.so timeout 300 python bench.py --steps 3000 --warmup 20 --engine 1 --no-extras --e2e-steps 5 --no-cu | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('old nocu', round(d['us_per_call'],3))"
+python scripts/timeline.py --config C3 --engine 2 --prune 0.0 --out gpurun_out/tl_p0_e2.json > /dev/null 2>&1
+python -c "
+import json
+d=json.load(open('gpurun_out/tl_p0_e2.json'))
+for m in ('isolated','back_to_back'):
+  t=d[m]; print(m, {k: [round(x,2) for x in v] if isinstance(v,list) else v for k,v in t.items() if v is not None and 'sm_' not in k})
+"
