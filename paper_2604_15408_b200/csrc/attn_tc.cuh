@@ -77,7 +77,7 @@ __global__ void __launch_bounds__(3 * kTcSlotThreads, 1) attn_tc_kernel(const At
   int16_t* sPos = reinterpret_cast<int16_t*>(small);
   int16_t* sDrop = sPos + kMaxN;
   uint32_t* sWords = reinterpret_cast<uint32_t*>(sDrop + kMaxN);         // 32 B
-  uint64_t* bars = reinterpret_cast<uint64_t*>(small + 1056);            // 4 x 8 B
+  uint64_t* bars = reinterpret_cast<uint64_t*>(small + 1056);            // 6 x 8 B
   uint32_t* tslot = reinterpret_cast<uint32_t*>(smem + nslots * L.slot_bytes);
   auto sync = [slot] { asm volatile("bar.sync %0, %1;" ::"r"(slot + 1), "r"(kTcSlotThreads) : "memory"); };
 
@@ -90,6 +90,8 @@ __global__ void __launch_bounds__(3 * kTcSlotThreads, 1) attn_tc_kernel(const At
     tc::mbar_init(smem_u32(&bars[1]), 1);  // single-tile path: P V done
     tc::mbar_init(smem_u32(&bars[2]), 1);  // pair path: tile A (S_{j+1} ready, P_j V_j done)
     tc::mbar_init(smem_u32(&bars[3]), 1);  // pair path: tile B
+    tc::mbar_init(smem_u32(&bars[4]), 4);  // pair path: P of tile A stored (one arrival per warp)
+    tc::mbar_init(smem_u32(&bars[5]), 4);  // pair path: P of tile B stored
     tc::fence_mbar_init();
   }
   tc::fence_before();
@@ -105,6 +107,8 @@ __global__ void __launch_bounds__(3 * kTcSlotThreads, 1) attn_tc_kernel(const At
   uint32_t ph_s = 0, ph_o = 0;
   const uint32_t bar_x = smem_u32(&bars[2]);  // pair path: tile X uses bar_x + 8 X
   uint32_t ph_x[2] = {0u, 0u};                // pair path: per-tile barrier parities
+  const uint32_t bar_p = smem_u32(&bars[4]);  // pair path: "P of tile X ready" = bar_p + 8 X
+  uint32_t ph_p[2] = {0u, 0u};                // (waited by the issuing thread only)
   constexpr uint32_t kFmt = std::is_same<T, __nv_bfloat16>::value ? 1u : 0u;
   const uint32_t idesc_o = tc::idesc_f16(kFmt, kTcTile, kHeadDim, 1);
   constexpr float kScaleLog2 = 0.18033688011112042f;  // log2(e) / sqrt(64)
@@ -307,9 +311,17 @@ __global__ void __launch_bounds__(3 * kTcSlotThreads, 1) attn_tc_kernel(const At
               tc::st_16x128b_x8(tSx + 32, lo);
               tc::wait_st();
             }
+            // hand-off: each warp arrives once its P rows are stored; only the issuing
+            // thread waits, the other warps go straight on to the other tile
             tc::fence_before();
-            sync();
+            __syncwarp();
+            if ((tid & 31) == 0) {
+              asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar_p + 8u * (uint32_t)X)
+                           : "memory");
+            }
             if (tid == 0) {  // P_j V_j for tile X, then S_{j+1} behind it; one commit covers both
+              tc::mbar_wait(bar_p + 8u * (uint32_t)X, ph_p[X]);
+              ph_p[X] ^= 1u;
               tc::fence_after();
               const int nk = (min(kTcChunk, n - j * kTcChunk) + 15) >> 4;
               const uint32_t pa = tS + ((uint32_t)(16 * X) << 16);
