@@ -49,7 +49,10 @@ def parse():
     ap.add_argument("--prune", type=float, default=None, help="override the config's pruning ratio")
     ap.add_argument("--method", default=None)
     ap.add_argument("--engine", type=int, default=0)
-    ap.add_argument("--gather", action="store_true", help="NCCL all-gather of O after every step")
+    ap.add_argument("--gather-variants", default="auto", choices=["auto", "none", "nccl", "all"],
+                    help="SURVEY §8(e) exchange variants measured after the headline: auto = NCCL "
+                         "all-gathers at N>1 and the peer-memory kernels (world 1) at N=1; all = "
+                         "NCCL + fused peer-memory all-gathers at N>1 (torch symmetric memory)")
     ap.add_argument("--no-cu", action="store_true", help="experiment: do not request cu_seqlens")
     ap.add_argument("--no-extras", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
@@ -220,14 +223,11 @@ def main():
         sets.append(dict(q=q.to(dev), k=k.to(dev), v=v.to(dev), keep=keep.to(dev),
                          o=torch.empty(B, N, H, 64, dtype=dt, device=dev),
                          cu=torch.empty(B + 1, dtype=torch.int32, device=dev)))
-    gathered = torch.empty(ws * B, N, H, 64, dtype=dt, device=dev) if args.gather else None
 
     def step(i, stream=None):
         s = sets[i % N_SETS]
         rb.pack_attend_unpack(s["q"], s["k"], s["v"], s["keep"], o=s["o"],
                               cu=None if args.no_cu else s["cu"], stream=stream, engine=args.engine)
-        if gathered is not None:
-            dist.all_gather_into_tensor(gathered, s["o"])
 
     # warm-up: W eager steps
     for i in range(args.warmup):
@@ -265,6 +265,16 @@ def main():
     # e2e through the C ABI with host buffers (pinned): H2D inputs, fused kernel, D2H output
     e2e = measure_e2e(args, rb, torch, dev, q, k, v, keep, ws, B, N, H, dt)
 
+    # the four exchange variants, after the headline (never part of it)
+    gv = None
+    impls = {"auto": ["nccl"] if ws > 1 else ["peer"], "none": [], "nccl": ["nccl"] if ws > 1 else [],
+             "all": (["nccl", "peer"] if ws > 1 else ["peer"])}[args.gather_variants]
+    if impls:
+        try:
+            gv = gather_variants(rb, torch, dev, sets, ws, rank, B, N, H, T, impls)
+        except Exception as ex:  # context only: never lose the headline line
+            gv = {"error": repr(ex)[:300]}
+
     if rank != 0:
         if ws > 1:
             dist.barrier()
@@ -293,9 +303,12 @@ def main():
                        "l2": f"{N_SETS} rotating input/output sets "
                              f"({N_SETS * (4 * B * N * H * 128) / 1e6:.0f} MB > 126 MB L2)",
                        "timing": "K steps in one CUDA graph, CUDA events, max over ranks",
-                       "gather": bool(args.gather)},
+                       "exchange": "none in the headline (compute-only, weak scaling); "
+                                   "all-gather variants under gather_variants"},
             "us_per_call": us_per_call, "images_per_s": value,
             "gpu_launches": args.steps, "clocks": clk.summary(), "roofline": roofline, "e2e": e2e}
+    if gv is not None:
+        line["gather_variants"] = gv
 
     if ws == 1 and not args.no_extras:
         line["cpu_baseline"] = cpu_baseline(args, c, B, N, H)
@@ -357,6 +370,124 @@ def measure_e2e(args, rb, torch, dev, q, k, v, keep, ws, B, N, H, dt):
 
 
 # ----------------------------------------------------------------------------
+def gather_variants(rb, torch, dev, sets, ws, rank, B, N, H, T, impls, reps=200):
+    """per-step device µs (max over ranks) of
+      compute_only  fused pack-attend-unpack into the local padded O;
+      cls           + all-gather of the CLS rows [B_global, H*d] (classifier input, P:367);
+      packed        ragged_pack + ragged_attn + all-gather of the packed O rows
+                    (capacity-padded to the largest rank's T);
+      padded        + all-gather of the padded O [B_global, N, H, d] (BASELINE.json literal).
+    impl "nccl": our kernels, then torch.distributed NCCL all_gather_into_tensor.
+    impl "peer": ONE kernel per step that stores every output row into every
+    rank's gathered buffer over NVLink (ragged_dist.h; torch symmetric memory
+    gives the peer pointers), ending in the in-kernel cross-rank barrier.
+    At N = 1 "peer" runs with world = 1 (local destination): the kernel's own
+    cost of the gather path, no link traffic."""
+    import torch.distributed as dist
+    from paper_2604_15408_b200.shard import max_over_ranks
+    HD, Bg, off = H * 64, ws * B, rank * B
+    dt = sets[0]["q"].dtype
+    esz = 2
+    tcap = int(max_over_ranks(float(T), dev))
+
+    def timed(fns):
+        if ws > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        return max_over_ranks(_graph_time(torch, fns, reps), dev)
+
+    def alloc(shape, dtype, symmetric):
+        """(tensor, per-rank pointers): symmetric memory at N>1, local at N=1."""
+        if ws == 1 or not symmetric:
+            t = torch.empty(shape, dtype=dtype, device=dev)
+            return t, [t.data_ptr()]
+        import torch.distributed._symmetric_memory as symm
+        t = symm.empty(*shape, dtype=dtype, device=dev)
+        h = symm.rendezvous(t, dist.group.WORLD)
+        return t, [int(p) for p in h.buffer_ptrs]
+
+    packed_bufs = []
+    for i in range(2):                       # two alternating packed workspaces
+        mk = lambda: torch.empty(B * N, H, 64, dtype=dt, device=dev)  # noqa: E731
+        packed_bufs.append((mk(), mk(), mk(), torch.empty(B + 1, dtype=torch.int32, device=dev),
+                            torch.empty(B * N, dtype=torch.int32, device=dev),
+                            torch.empty(B * N, dtype=torch.int32, device=dev), mk()))
+    cls_local = torch.empty(B, HD, dtype=dt, device=dev)
+    out = {"steps_per_variant": reps, "T_cap": tcap,
+           "bytes_gathered_per_rank": {"cls": Bg * HD * esz, "packed": ws * tcap * HD * esz,
+                                       "padded": Bg * N * HD * esz}}
+    out["compute_only_us"] = timed([lambda s=s: rb.pack_attend_unpack(s["q"], s["k"], s["v"], s["keep"],
+                                                                      o=s["o"]) for s in sets])
+
+    def pack_fn(s, i):
+        pb = packed_bufs[i % 2]
+        rb.pack(s["q"], s["k"], s["v"], s["keep"], out=pb[:6])
+        return pb
+
+    if "nccl" in impls and ws > 1:
+        res = {}
+        cls_g = torch.empty(Bg, HD, dtype=dt, device=dev)
+        pk_g = torch.empty(ws * tcap, H, 64, dtype=dt, device=dev)
+        pad_g = torch.empty(Bg, N, H, 64, dtype=dt, device=dev)
+        g1 = lambda s: rb.gather_desc(1, 0, out=[s["o"]], cls=[cls_local])  # noqa: E731
+
+        def cls_step(s):
+            rb.pack_attend_unpack_gather(s["q"], s["k"], s["v"], s["keep"], g1(s))
+            dist.all_gather_into_tensor(cls_g, cls_local)
+
+        def packed_step(s, i):
+            pb = pack_fn(s, i)
+            rb.attn(pb[0], pb[1], pb[2], pb[3], N, op=pb[6])
+            dist.all_gather_into_tensor(pk_g, pb[6][:tcap])
+
+        def padded_step(s):
+            rb.pack_attend_unpack(s["q"], s["k"], s["v"], s["keep"], o=s["o"])
+            dist.all_gather_into_tensor(pad_g, s["o"])
+
+        res["cls_us"] = timed([lambda s=s: cls_step(s) for s in sets])
+        res["packed_us"] = timed([lambda s=s, i=i: packed_step(s, i) for i, s in enumerate(sets)])
+        res["padded_us"] = timed([lambda s=s: padded_step(s) for s in sets])
+        out["nccl"] = res
+
+    if "peer" in impls:
+        res = {}
+        cls_g, cls_p = alloc((Bg, HD), dt, True)
+        pk_g, pk_p = alloc((ws * tcap, H, 64), dt, True)
+        pad_g, pad_p = alloc((Bg, N, H, 64), dt, True)
+        sigs = []
+        for _ in range(3):                   # one signal array + state per variant
+            sg, sp = alloc((max(ws, 4),), torch.int32, True)
+            sg.zero_()
+            sigs.append((sg, sp, torch.zeros(2, dtype=torch.int32, device=dev)))
+        torch.cuda.synchronize()
+        if ws > 1:
+            dist.barrier()
+
+        def sig_kw(j):
+            return {"signal": sigs[j][1], "state": sigs[j][2]} if ws > 1 else {}
+
+        def cls_desc(s):
+            return rb.gather_desc(ws, rank, out=[s["o"] if r == rank else None for r in range(ws)],
+                                  cls=[p + off * HD * esz for p in cls_p], **sig_kw(0))
+
+        pk_desc = rb.gather_desc(ws, rank, out=[p + rank * tcap * HD * esz for p in pk_p], **sig_kw(1))
+        pad_desc = rb.gather_desc(ws, rank, out=[p + off * N * HD * esz for p in pad_p], **sig_kw(2))
+        cls_descs = [cls_desc(s) for s in sets]
+
+        def packed_step(s, i):
+            pb = pack_fn(s, i)
+            rb.attn_gather(pb[0], pb[1], pb[2], pb[3], N, pk_desc)
+
+        res["cls_us"] = timed([lambda s=s, d=d: rb.pack_attend_unpack_gather(s["q"], s["k"], s["v"], s["keep"], d)
+                               for s, d in zip(sets, cls_descs)])
+        res["packed_us"] = timed([lambda s=s, i=i: packed_step(s, i) for i, s in enumerate(sets)])
+        res["padded_us"] = timed([lambda s=s: rb.pack_attend_unpack_gather(s["q"], s["k"], s["v"], s["keep"],
+                                                                           pad_desc) for s in sets])
+        res["world"] = ws
+        out["peer"] = res
+    return out
+
+
 def _graph_time(torch, fns, reps):
     """Device µs per call: `reps` calls (rotating over fns) in one CUDA graph."""
     for f in fns:                   # eager first call: one-time attributes outside capture

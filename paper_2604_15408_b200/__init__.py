@@ -41,6 +41,43 @@ class Problem(ctypes.Structure):
                 ("ld", ctypes.c_int64)]
 
 
+MAX_PEERS = 8
+
+
+class Gather(ctypes.Structure):
+    """ragged_gather (include/ragged_dist.h): per-rank destinations of this
+    rank's output shard (device pointers, peer-mapped for other ranks), the
+    ranks' signal arrays and this rank's barrier state."""
+    _fields_ = [("world", ctypes.c_int32), ("rank", ctypes.c_int32),
+                ("out", ctypes.c_void_p * MAX_PEERS), ("cls", ctypes.c_void_p * MAX_PEERS),
+                ("signal", ctypes.c_void_p * MAX_PEERS), ("state", ctypes.c_void_p)]
+
+
+def _addr(x) -> int | None:
+    """A device address: a tensor's data_ptr(), a raw int (e.g. a peer pointer
+    from torch symmetric memory), or None."""
+    if x is None:
+        return None
+    return x.data_ptr() if hasattr(x, "data_ptr") else int(x)
+
+
+def gather_desc(world: int, rank: int, out=None, cls=None, signal=None, state=None) -> Gather:
+    """Build a ragged_gather from per-rank lists (length world; entries are
+    tensors, ints or None)."""
+    g = Gather()
+    g.world, g.rank = world, rank
+    for name, lst in (("out", out), ("cls", cls), ("signal", signal)):
+        if lst is None:
+            continue
+        if len(lst) != world:
+            raise ValueError(f"{name} must have one entry per rank")
+        arr = getattr(g, name)
+        for r, x in enumerate(lst):
+            arr[r] = _addr(x)
+    g.state = _addr(state)
+    return g
+
+
 def _load() -> ctypes.CDLL:
     if not os.path.exists(LIB_PATH):
         raise ImportError(f"{LIB_PATH} is missing: build it with `python -m paper_2604_15408_b200.build` "
@@ -58,6 +95,8 @@ def _load() -> ctypes.CDLL:
         "ragged_empty_launch": [I32, I32, V],
         "ragged_keep_topk_l2": [P, V, I32, V, V],
         "ragged_validate_cu_seqlens": [ctypes.POINTER(I32), I32, I64],
+        "ragged_pack_attend_unpack_gather": [P, V, V, V, V, V, ctypes.POINTER(Gather), V],
+        "ragged_attn_gather": [P, V, V, V, V, ctypes.POINTER(Gather), V],
     }
     for name, args in sigs.items():
         f = getattr(lib, name)
@@ -79,7 +118,7 @@ _lib = None
 EXPORTS = ("ragged_scan", "ragged_pack", "ragged_attn", "ragged_unpack", "ragged_pack_attend_unpack",
            "ragged_graph_create", "ragged_graph_launch", "ragged_graph_destroy", "ragged_empty_launch",
            "ragged_validate_cu_seqlens", "ragged_status_str", "ragged_last_error", "ragged_build_info",
-           "ragged_keep_topk_l2")
+           "ragged_keep_topk_l2", "ragged_pack_attend_unpack_gather", "ragged_attn_gather")
 
 
 def lib() -> ctypes.CDLL:
@@ -217,6 +256,32 @@ def pack_attend_unpack(q, k, v, keep, o=None, cu=None, want_cu=False, stream=Non
                                           v.data_ptr(), o.data_ptr(), _ptr(cu), _stream(stream)),
            "ragged_pack_attend_unpack")
     return (o, cu) if (want_cu or cu is not None) else o
+
+
+def pack_attend_unpack_gather(q, k, v, keep, gather: Gather, cu=None, stream=None,
+                              engine=ENGINE_AUTO):
+    """a5 fused with the §8(e) all-gather: this rank's padded O rows (and/or
+    CLS rows) are stored into every rank's gathered buffer (ragged_dist.h)."""
+    p = _padded_problem(q, k, v, engine)
+    keep = _keep_u8(keep)
+    _check(lib().ragged_pack_attend_unpack_gather(ctypes.byref(p), keep.data_ptr(), q.data_ptr(),
+                                                 k.data_ptr(), v.data_ptr(), _ptr(cu),
+                                                 ctypes.byref(gather), _stream(stream)),
+           "ragged_pack_attend_unpack_gather")
+
+
+def attn_gather(qp, kp, vp, cu, N: int, gather: Gather, stream=None, engine=ENGINE_AUTO):
+    """a3 with the packed all-gather: rows [cu[b], cu[b+1]) of this rank's
+    packed O go to out[r] + row * H * d on every rank r (ragged_dist.h)."""
+    cap, H, d = qp.shape
+    for t in (qp, kp, vp):
+        if not t.is_contiguous() or t.shape != qp.shape:
+            raise ValueError("packed q/k/v must be contiguous [cap, H, d]")
+    B = cu.numel() - 1
+    p = problem(B, N, H, d, qp.dtype, H * d, engine)
+    _check(lib().ragged_attn_gather(ctypes.byref(p), qp.data_ptr(), kp.data_ptr(), vp.data_ptr(),
+                                   cu.data_ptr(), ctypes.byref(gather), _stream(stream)),
+           "ragged_attn_gather")
 
 
 class Graph:

@@ -13,6 +13,7 @@
 
 #include "../../include/ragged.h"
 #include "../../include/ragged_debug.h"
+#include "../../include/ragged_dist.h"
 #include "launch.h"
 
 namespace {
@@ -253,6 +254,69 @@ int32_t ragged_validate_cu_seqlens(const int32_t* cu, int32_t n, int64_t total) 
   return -1;
 }
 
+// ---- ragged_dist.h ----------------------------------------------------------
+static ragged_status to_gather_args(const ragged_problem* prob, const ragged_gather* g, bool fused,
+                                    ragged::GatherArgs& ga) {
+  if (g == nullptr) return fail(RAGGED_EINVAL, "gather is NULL");
+  if (g->world < 1 || g->world > RAGGED_MAX_PEERS) return fail(RAGGED_EINVAL, "world not in 1..8");
+  if (g->rank < 0 || g->rank >= g->world) return fail(RAGGED_EINVAL, "rank not in 0..world-1");
+  if (resolve_engine(prob) != RAGGED_ENGINE_MMA_SYNC)
+    return fail(RAGGED_ENOTSUP, "gather entry points run on the mma.sync engine only");
+  ga.world = g->world;
+  ga.rank = g->rank;
+  int nsig = 0, nout = 0;
+  for (int r = 0; r < g->world; ++r) {
+    if (!aligned16(g->out[r])) return fail(RAGGED_EALIGN, "gather out[r] is not 16-byte aligned");
+    if (!aligned16(g->cls[r])) return fail(RAGGED_EALIGN, "gather cls[r] is not 16-byte aligned");
+    if (!fused && g->cls[r] != nullptr) return fail(RAGGED_EINVAL, "cls[] is fused-only");
+    ga.out[r] = static_cast<char*>(g->out[r]);
+    ga.cls[r] = static_cast<char*>(g->cls[r]);
+    ga.sig[r] = g->signal[r];
+    nsig += g->signal[r] != nullptr;
+    nout += (g->out[r] != nullptr) + (g->cls[r] != nullptr);
+  }
+  if (nout == 0) return fail(RAGGED_EINVAL, "gather has no destination");
+  if (nsig != 0 && (nsig != g->world || g->state == nullptr))
+    return fail(RAGGED_EINVAL, "signal[] must be set for every rank, together with state");
+  ga.state = nsig ? g->state : nullptr;
+  return RAGGED_OK;
+}
+
+ragged_status ragged_pack_attend_unpack_gather(const ragged_problem* prob, const uint8_t* keep,
+                                               const void* q, const void* k, const void* v,
+                                               int32_t* cu_seqlens_or_null, const ragged_gather* g,
+                                               void* stream) {
+  RAGGED_TRY(check_problem(prob));
+  ragged::GatherArgs ga;
+  RAGGED_TRY(to_gather_args(prob, g, true, ga));
+  if (prob->B == 0) return RAGGED_OK;
+  RAGGED_TRY(check_ptr_any(keep, "keep"));
+  RAGGED_TRY(check_ptr(q, "q"));
+  RAGGED_TRY(check_ptr(k, "k"));
+  RAGGED_TRY(check_ptr(v, "v"));
+  if ((long long)prob->B * prob->H + 1 > 0x7fffffffLL) return fail(RAGGED_ENOTSUP, "B*H too large");
+  cudaError_t e = ragged::launch_fused_gather(prob->dtype, keep, q, k, v, prob->ld, cu_seqlens_or_null,
+                                              prob->B, prob->N, prob->H, ga, as_stream(stream));
+  return e == cudaSuccess ? RAGGED_OK : cuda_fail(e, "ragged_pack_attend_unpack_gather");
+}
+
+ragged_status ragged_attn_gather(const ragged_problem* prob, const void* qp, const void* kp,
+                                 const void* vp, const int32_t* cu_seqlens, const ragged_gather* g,
+                                 void* stream) {
+  RAGGED_TRY(check_problem(prob));
+  ragged::GatherArgs ga;
+  RAGGED_TRY(to_gather_args(prob, g, false, ga));
+  if (prob->B == 0) return RAGGED_OK;
+  RAGGED_TRY(check_ptr(qp, "qp"));
+  RAGGED_TRY(check_ptr(kp, "kp"));
+  RAGGED_TRY(check_ptr(vp, "vp"));
+  RAGGED_TRY(check_ptr_any(cu_seqlens, "cu_seqlens"));
+  if ((long long)prob->B * prob->H > 0x7fffffffLL) return fail(RAGGED_ENOTSUP, "B*H too large");
+  cudaError_t e = ragged::launch_attn_gather(prob->dtype, qp, kp, vp, cu_seqlens, prob->B, prob->N,
+                                             prob->H, ga, as_stream(stream));
+  return e == cudaSuccess ? RAGGED_OK : cuda_fail(e, "ragged_attn_gather");
+}
+
 const char* ragged_status_str(ragged_status s) {
   switch (s) {
     case RAGGED_OK: return "RAGGED_OK";
@@ -274,7 +338,7 @@ int32_t ragged_debug_timeline_clear(void) { return ragged::timeline_clear(); }
 #endif
 
 const char* ragged_build_info(void) {
-  return "libragged 0.2 sm_100a engines=mma_sync,tcgen05";
+  return "libragged 0.3 sm_100a engines=mma_sync,tcgen05 gather=peer";
 }
 
 }  // extern "C"

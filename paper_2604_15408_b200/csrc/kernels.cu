@@ -6,6 +6,8 @@
 //                         (image, head) (Alg. 1)
 //   unpack_kernel     a4: packed O -> padded O, +0.0 for dropped rows
 //   attn_kernel<.,1>  a5: fused pack-attend-unpack, one launch
+//   attn_kernel<.,.,1>    §8(e): a3/a5 whose output rows go to every rank's
+//                         gathered buffer over peer memory + cross-rank barrier
 //   empty_kernel          launch-floor probe
 //
 // Design notes (DESIGN.md has the full version):
@@ -385,6 +387,68 @@ __device__ __forceinline__ void zero_rows(char* img_o, const int16_t* sDrop, int
   for (; rr < nd; rr += step) st_global_16(img_o + sDrop[rr] * HDb, z);
 }
 
+// ---- fused all-gather over peer memory --------------------
+// One 16-byte chunk of output row `row` to every destination rank (the local
+// one included); `off` is this thread's byte offset of (image base, head,
+// chunk) inside a destination shard.  CLS rows (padded position 0, fused mode)
+// additionally go to the compact [B, H*d] CLS buffers at `cls_off`.
+template <bool kCls>
+__device__ __forceinline__ void gather_store(const GatherArgs& g, long long off, int row, int HDb,
+                                             long long cls_off, uint4 v) {
+#pragma unroll
+  for (int d = 0; d < kMaxPeers; ++d) {
+    if (d < g.world && g.out[d] != nullptr) st_global_16(g.out[d] + off + (long long)row * HDb, v);
+  }
+  if (kCls && row == 0) {
+#pragma unroll
+    for (int d = 0; d < kMaxPeers; ++d)
+      if (d < g.world && g.cls[d] != nullptr) st_global_16(g.cls[d] + cls_off, v);
+  }
+}
+
+__device__ __forceinline__ void gather_zero_rows(const GatherArgs& g, long long off,
+                                                 const int16_t* sDrop, int first, int nd, int step,
+                                                 int HDb) {
+#pragma unroll 1
+  for (int d = 0; d < kMaxPeers; ++d)
+    if (d < g.world && g.out[d] != nullptr) zero_rows(g.out[d] + off, sDrop, first, nd, step, HDb);
+}
+
+__device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Grid-completion barrier across ranks, called by thread 0 of every CTA after
+// the CTA's stores (preceded by __syncthreads).  Each CTA publishes its stores
+// at system scope and counts itself in; the last CTA of the grid bumps the
+// epoch, writes it into slot `rank` of every rank's signal array (release) and
+// waits until every rank has written the epoch into its own array (acquire).
+// After the kernel completes, every rank's destination buffers hold every
+// rank's shard.  A lost peer traps (launch error) instead of hanging the GPU.
+__device__ __forceinline__ void gather_arrive(const GatherArgs& g) {
+  __threadfence_system();
+  const uint32_t prev = atomicAdd(g.state, 1u);
+  if (prev != gridDim.x * gridDim.y * gridDim.z - 1u) return;
+  __threadfence_system();
+  volatile uint32_t* st = g.state;
+  const uint32_t epoch = st[1] + 1u;
+  st[1] = epoch;
+  st[0] = 0u;
+  for (int d = 0; d < g.world; ++d) st_release_sys(g.sig[d] + g.rank, epoch);
+  const uint32_t* mine = g.sig[g.rank];
+  for (int s = 0; s < g.world; ++s) {
+    for (uint32_t spins = 0; (int)(ld_acquire_sys(mine + s) - epoch) < 0; ++spins) {
+      if (spins > (1u << 24)) __trap();
+      __nanosleep(128);
+    }
+  }
+}
+
 // Kept positions in keep[0, len) -- this thread's share (stride nthr): 16-byte
 // loads when the mask is 16-byte aligned, nonzero bytes counted with __vcmpne4.
 __device__ __forceinline__ int count_kept(const uint8_t* __restrict__ keep, long long len, int t,
@@ -468,8 +532,10 @@ __device__ __forceinline__ void image_rows(const AttnArgs& a, int b, int16_t* sP
   }
 }
 
-template <typename T, bool kFused>
-__global__ void __launch_bounds__(kAttnThreads, 3) attn_kernel(const AttnArgs a) {
+// kGather: outputs go to the GatherArgs destinations (fused all-gather over
+// peer memory) instead of a.o, followed by the cross-rank completion barrier.
+template <typename T, bool kFused, bool kGather>
+__global__ void __launch_bounds__(kAttnThreads, 3) attn_kernel(const AttnArgs a, const GatherArgs ga) {
   extern __shared__ __align__(1024) uint8_t smem[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int rows_cap = attn_rows_cap(a.N);
@@ -488,6 +554,12 @@ __global__ void __launch_bounds__(kAttnThreads, 3) attn_kernel(const AttnArgs a)
     if (a.cu_mode == 1) {
       if (bid == 0) {  // the scan CTA: cu_seqlens only, concurrent with the rest
         scan_cta_cu(a, sK, tid, [] { __syncthreads(); });
+        if constexpr (kGather) {
+          if (ga.state != nullptr) {
+            __syncthreads();
+            if (tid == 0) gather_arrive(ga);
+          }
+        }
         return;
       }
       bid -= 1;
@@ -511,6 +583,16 @@ __global__ void __launch_bounds__(kAttnThreads, 3) attn_kernel(const AttnArgs a)
   const char* img_k = reinterpret_cast<const char*>(gk) + row_base * ldb + h * kRowBytes;
   const char* img_v = reinterpret_cast<const char*>(gv) + row_base * ldb + h * kRowBytes;
   char* img_o = reinterpret_cast<char*>(go) + row_base * HDb + h * kRowBytes + (tid & 7) * 16;
+  // kGather: byte offsets of this thread's chunk inside a destination shard.
+  const long long o_off = kGather ? row_base * HDb + h * kRowBytes + (tid & 7) * 16 : 0;
+  const long long cls_off = kGather ? (long long)b * HDb + h * kRowBytes + (tid & 7) * 16 : 0;
+  if constexpr (kGather && kFused) {  // a dropped CLS token still owns a (+0) CLS row
+    if (tid < 8 && n < a.N && sDrop[0] == 0) {
+#pragma unroll
+      for (int d = 0; d < kMaxPeers; ++d)
+        if (d < ga.world && ga.cls[d] != nullptr) st_global_16(ga.cls[d] + cls_off, make_uint4(0, 0, 0, 0));
+    }
+  }
 
   // ---- stage K, V (rows [0, n16), zero-filled past n) and each warp's first Q slice.
   // Thread -> (chunk c, tensor t, row r0 + 8i): the swizzled chunk c ^ (r & 7) is
@@ -568,7 +650,8 @@ __global__ void __launch_bounds__(kAttnThreads, 3) attn_kernel(const AttnArgs a)
   const int busy = nsl < 4 ? nsl : 4;  // warps [0, busy) own slices
   auto zero_dropped = [&](int t, int nthr) {
 #ifndef RAGGED_ABLATE_ZERO
-    if constexpr (kFused) zero_rows(img_o, sDrop, t >> 3, a.N - n, nthr >> 3, HDb);
+    if constexpr (kFused && kGather) gather_zero_rows(ga, o_off, sDrop, t >> 3, a.N - n, nthr >> 3, HDb);
+    else if constexpr (kFused) zero_rows(img_o, sDrop, t >> 3, a.N - n, nthr >> 3, HDb);
 #endif
   };
   if (busy < 4 && warp >= busy) zero_dropped(tid - busy * 32, (4 - busy) * 32);
@@ -712,7 +795,8 @@ __global__ void __launch_bounds__(kAttnThreads, 3) attn_kernel(const AttnArgs a)
       const int rr = (lane >> 3) + 4 * i, r = slice * 16 + rr;
       if (r < n) {
         const uint4 val = *reinterpret_cast<const uint4*>(qcur + swz(rr, lane & 7));
-        st_global_16(img_o + sPos[r] * HDb, val);
+        if constexpr (kGather) gather_store<kFused>(ga, o_off, sPos[r], HDb, cls_off, val);
+        else st_global_16(img_o + sPos[r] * HDb, val);
       }
     }
     cp_async_wait_all();
@@ -720,6 +804,12 @@ __global__ void __launch_bounds__(kAttnThreads, 3) attn_kernel(const AttnArgs a)
     buf ^= 1;
   }
   if (busy == 4) zero_dropped(tid, kAttnThreads);
+  if constexpr (kGather) {
+    if (ga.state != nullptr) {
+      __syncthreads();
+      if (tid == 0) gather_arrive(ga);
+    }
+  }
 #ifdef RAGGED_TIMELINE
   __syncthreads();
   TL(4);
@@ -866,12 +956,14 @@ static cudaError_t smem_attr_once(Kern kern, int max_bytes, bool (&done)[64]) {
   return e;
 }
 
-template <typename T, bool kFused>
-static cudaError_t launch_attn_mma(const AttnArgs& a, int grid, cudaStream_t st) {
+template <typename T, bool kFused, bool kGather = false>
+static cudaError_t launch_attn_mma(const AttnArgs& a, int grid, cudaStream_t st,
+                                   const GatherArgs& g = GatherArgs{}) {
   static bool done[64] = {false};
-  cudaError_t e = smem_attr_once(attn_kernel<T, kFused>, attn_smem_bytes(kMaxN), done);
+  cudaError_t e = smem_attr_once(attn_kernel<T, kFused, kGather>, attn_smem_bytes(kMaxN), done);
   if (e != cudaSuccess) return e;
-  return launch_pdl(attn_kernel<T, kFused>, dim3(grid), dim3(kAttnThreads), attn_smem_bytes(a.N), st, a);
+  return launch_pdl(attn_kernel<T, kFused, kGather>, dim3(grid), dim3(kAttnThreads),
+                    attn_smem_bytes(a.N), st, a, g);
 }
 
 // tcgen05 engine: persistent grid of min(#SMs, work items) CTAs x nslots slots.
@@ -931,6 +1023,44 @@ cudaError_t launch_fused(int dtype, int engine, const uint8_t* keep, const void*
   a.H = H;
   a.ld = ld;
   return dispatch_attn<true>(dtype, engine, a, B * H + (a.cu_mode == 1 ? 1 : 0), st);
+}
+
+// Fused pack-attend-unpack whose padded output (and/or CLS rows) is written to
+// every rank's gathered buffer (mma.sync engine).  cu_seqlens stays local.
+cudaError_t launch_fused_gather(int dtype, const uint8_t* keep, const void* q, const void* k,
+                                const void* v, long long ld, int32_t* cu_out, int B, int N, int H,
+                                const GatherArgs& g, cudaStream_t st) {
+  AttnArgs a{};
+  a.keep = keep;
+  a.q = q;
+  a.k = k;
+  a.v = v;
+  a.cu_out = cu_out;
+  a.cu_mode = cu_out == nullptr ? 0 : ((long long)B * N <= 65536 ? 2 : 1);
+  a.B = B;
+  a.N = N;
+  a.H = H;
+  a.ld = ld;
+  const int grid = B * H + (a.cu_mode == 1 ? 1 : 0);
+  return dtype == 0 ? launch_attn_mma<__nv_bfloat16, true, true>(a, grid, st, g)
+                    : launch_attn_mma<__half, true, true>(a, grid, st, g);
+}
+
+// ragged_attn whose packed output rows go to every rank's gathered buffer.
+cudaError_t launch_attn_gather(int dtype, const void* qp, const void* kp, const void* vp,
+                               const int32_t* cu, int B, int N, int H, const GatherArgs& g,
+                               cudaStream_t st) {
+  AttnArgs a{};
+  a.q = qp;
+  a.k = kp;
+  a.v = vp;
+  a.cu = cu;
+  a.B = B;
+  a.N = N;
+  a.H = H;
+  a.ld = (long long)H * kHeadDim;
+  return dtype == 0 ? launch_attn_mma<__nv_bfloat16, false, true>(a, B * H, st, g)
+                    : launch_attn_mma<__half, false, true>(a, B * H, st, g);
 }
 
 cudaError_t launch_keep_topk_l2(int dtype, const void* x, long long ld, int B, int N, int D, int k,

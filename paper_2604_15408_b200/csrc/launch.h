@@ -18,6 +18,24 @@ cudaError_t launch_unpack(const void* op, const int32_t* dst, void* o, int B, in
 cudaError_t launch_fused(int dtype, int engine, const uint8_t* keep, const void* q, const void* k,
                          const void* v, long long ld, void* o, int32_t* cu_out, int B, int N, int H,
                          cudaStream_t st);
+// Fused compute + all-gather over peer memory: every output
+// row goes to up to kMaxPeers destinations (device pointers, peer-mapped for
+// other ranks), then the last CTA of the grid signals every rank and waits
+// for all of them (release/acquire at system scope).  See include/ragged.h.
+constexpr int kMaxPeers = 8;
+struct GatherArgs {
+  int world = 0, rank = 0;
+  char* out[kMaxPeers] = {};        // this rank's output shard start in rank r's buffer
+  char* cls[kMaxPeers] = {};        // fused only: this rank's CLS rows [B, H*d] in rank r's buffer
+  uint32_t* sig[kMaxPeers] = {};    // rank r's signal array [world]
+  uint32_t* state = nullptr;        // local [2]: arrival counter, epoch
+};
+cudaError_t launch_fused_gather(int dtype, const uint8_t* keep, const void* q, const void* k,
+                                const void* v, long long ld, int32_t* cu_out, int B, int N, int H,
+                                const GatherArgs& g, cudaStream_t st);
+cudaError_t launch_attn_gather(int dtype, const void* qp, const void* kp, const void* vp,
+                               const int32_t* cu, int B, int N, int H, const GatherArgs& g,
+                               cudaStream_t st);
 cudaError_t launch_empty(int grid, int block, cudaStream_t st);
 cudaError_t launch_keep_topk_l2(int dtype, const void* x, long long ld, int B, int N, int D, int k,
                                 uint8_t* keep, cudaStream_t st);

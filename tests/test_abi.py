@@ -15,7 +15,8 @@ rb = pytest.importorskip("paper_2604_15408_b200")
 
 
 def _declared():
-    src = open(os.path.join(ROOT, "include", "ragged.h")).read()
+    # ragged_debug.h declares the timeline-build-only symbols (libragged_tl.so).
+    src = "".join(open(os.path.join(ROOT, "include", h)).read() for h in ("ragged.h", "ragged_dist.h"))
     return sorted(set(re.findall(r"^\s*RAGGED_API\s+(?:ragged_status|void|int32_t|const char\*)\s+(ragged_\w+)\(",
                                  src, re.M)))
 
@@ -81,6 +82,40 @@ def test_pointer_validation():
     assert rb.lib().ragged_graph_launch(None, None) == rb.EINVAL
     rb.lib().ragged_graph_destroy(None)
     assert rb.lib().ragged_empty_launch(0, 32, None) == rb.EINVAL
+
+
+def _gather_call(p, g, fused=True):
+    if fused:
+        return rb.lib().ragged_pack_attend_unpack_gather(ctypes.byref(p), FAKE, FAKE, FAKE, FAKE, None,
+                                                         ctypes.byref(g) if g is not None else None, None)
+    return rb.lib().ragged_attn_gather(ctypes.byref(p), FAKE, FAKE, FAKE, FAKE,
+                                       ctypes.byref(g) if g is not None else None, None)
+
+
+def test_gather_validation():
+    """ragged_dist.h: every host-checkable gather error, before any CUDA call
+    (B = 0 reaches the no-op return only after the descriptor is valid)."""
+    p = rb.problem(0, 197, 12)
+    ok = rb.gather_desc(2, 1, out=[FAKE, FAKE])
+    assert _gather_call(p, ok) == rb.OK
+    assert _gather_call(p, ok, fused=False) == rb.OK
+    assert _gather_call(p, None) == rb.EINVAL
+    assert _gather_call(p, rb.gather_desc(0, 0)) == rb.EINVAL
+    assert _gather_call(p, rb.gather_desc(9, 0)) == rb.EINVAL
+    assert _gather_call(p, rb.gather_desc(2, 2, out=[FAKE, FAKE])) == rb.EINVAL
+    assert _gather_call(p, rb.gather_desc(2, -1, out=[FAKE, FAKE])) == rb.EINVAL
+    assert _gather_call(p, rb.gather_desc(2, 0)) == rb.EINVAL                       # no destination
+    assert _gather_call(p, rb.gather_desc(2, 0, out=[FAKE, FAKE + 8])) == rb.EALIGN
+    assert _gather_call(p, rb.gather_desc(2, 0, cls=[FAKE + 4, None])) == rb.EALIGN
+    assert _gather_call(p, rb.gather_desc(2, 0, cls=[FAKE, FAKE]), fused=False) == rb.EINVAL
+    # signals must cover every rank and come with state
+    assert _gather_call(p, rb.gather_desc(2, 0, out=[FAKE, FAKE], signal=[FAKE, None], state=FAKE)) == rb.EINVAL
+    assert _gather_call(p, rb.gather_desc(2, 0, out=[FAKE, FAKE], signal=[FAKE, FAKE])) == rb.EINVAL
+    assert _gather_call(p, rb.gather_desc(2, 0, out=[FAKE, FAKE], signal=[FAKE, FAKE], state=FAKE)) == rb.OK
+    p2 = rb.problem(0, 197, 12, engine=rb.ENGINE_TCGEN05)
+    assert _gather_call(p2, ok) == rb.ENOTSUP
+    with pytest.raises(ValueError):
+        rb.gather_desc(2, 0, out=[FAKE])
 
 
 def test_empty_batch_is_noop_without_cuda():
