@@ -28,9 +28,9 @@ N_DEIT = 197          # 196 patches + CLS
 HEAD_DIM = 64         # B_D = d = 64
 
 PRESETS = {
-    "deit_tiny": {"H": 3, "D": 192},
-    "deit_small": {"H": 6, "D": 384},
-    "deit_base": {"H": 12, "D": 768},
+    "deit_tiny": {"H": 3, "D": 192, "MLP": 768},
+    "deit_small": {"H": 6, "D": 384, "MLP": 1536},
+    "deit_base": {"H": 12, "D": 768, "MLP": 3072},
 }
 
 DTYPES = {"bf16": torch.bfloat16, "fp16": torch.float16}
@@ -101,6 +101,47 @@ def hidden_states(B: int, N: int, D: int, dtype=torch.bfloat16, seed: int = 0,
         scale = torch.exp(0.5 * torch.randn(N, 1, generator=g))
         x[b] = (scale * torch.randn(N, D, generator=g)).to(dtype)
     return x
+
+
+VIT_PARAMS = ("ln1_w", "ln1_b", "w_qkv", "b_qkv", "w_proj", "b_proj",
+              "ln2_w", "ln2_b", "w_fc1", "b_fc1", "w_fc2", "b_fc2")
+
+
+def vit_weights(D: int, MLP: int, dtype=torch.bfloat16, seed: int = 0) -> dict:
+    """Random-init weights of one pre-norm ViT block (NEXT row N1; DeiT layout:
+    qkv [3D, D] with output order (q|k|v, head, d), proj [D, D], fc1 [MLP, D],
+    fc2 [D, MLP], LayerNorm weight/bias [D]); there are no trained weights in
+    this build.  Linear weights ~ N(0, 0.02^2) (timm's trunc-normal scale),
+    biases ~ N(0, 0.02^2) (nonzero so a dropped bias is visible), LayerNorm
+    weight ~ 1 + N(0, 0.1^2), bias ~ N(0, 0.05^2).  Rounded once to `dtype`."""
+    if isinstance(dtype, str):
+        dtype = DTYPES[dtype]
+    g = torch.Generator().manual_seed(0x5EED0000 + seed)
+    shapes = {"ln1_w": (D,), "ln1_b": (D,), "w_qkv": (3 * D, D), "b_qkv": (3 * D,),
+              "w_proj": (D, D), "b_proj": (D,), "ln2_w": (D,), "ln2_b": (D,),
+              "w_fc1": (MLP, D), "b_fc1": (MLP,), "w_fc2": (D, MLP), "b_fc2": (D,)}
+    out = {}
+    for name in VIT_PARAMS:
+        r = torch.randn(shapes[name], generator=g)
+        if name in ("ln1_w", "ln2_w"):
+            t = 1.0 + 0.1 * r
+        elif name in ("ln1_b", "ln2_b"):
+            t = 0.05 * r
+        else:
+            t = 0.02 * r
+        out[name] = t.to(dtype)
+    return out
+
+
+def packed_rows(T: int, D: int, dtype=torch.bfloat16, seed: int = 0) -> torch.Tensor:
+    """Packed hidden rows x [T, D] for the N1 block: N(0, 1) per element with a
+    per-row LogNormal(0, 0.5) scale (the prune-point statistics of
+    hidden_states), rounded once to `dtype`."""
+    if isinstance(dtype, str):
+        dtype = DTYPES[dtype]
+    g = torch.Generator().manual_seed(0x9ACC0000 + seed)
+    scale = torch.exp(0.5 * torch.randn(T, 1, generator=g))
+    return (scale * torch.randn(T, D, generator=g)).to(dtype)
 
 
 # --------------------------------------------------------------------------
