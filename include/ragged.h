@@ -107,7 +107,10 @@ RAGGED_API ragged_status ragged_pack(const ragged_problem* prob, const uint8_t* 
  *   op[s:s+n, h, :] = softmax(qp[s:s+n,h,:] kp[s:s+n,h,:]^T / sqrt(d)) vp[s:s+n,h,:]
  * bidirectional, no dropout, no KV cache.  One CTA per (image,
  * head) pair, head fastest (pid -> h = pid mod H, i = pid / H).
- * Packed rows >= cu[B] of op are untouched.  One launch. */
+ * Input rows of qp/kp/vp are prob->ld elements apart (H*d for three packed
+ * [cap, H, d] buffers; 3*H*d for one packed qkv buffer [cap, 3, H, d] with
+ * kp = qp + H*d, vp = qp + 2*H*d -- the N1 block's qkv GEMM output); op rows
+ * are H*d apart.  Packed rows >= cu[B] of op are untouched.  One launch. */
 RAGGED_API ragged_status ragged_attn(const ragged_problem* prob, const void* qp, const void* kp,
                           const void* vp, const int32_t* cu_seqlens, void* op,
                           void* stream);

@@ -78,6 +78,16 @@ def gather_desc(world: int, rank: int, out=None, cls=None, signal=None, state=No
     return g
 
 
+EPI_NONE, EPI_GELU, EPI_RESIDUAL = 0, 1, 2
+VIT_PARAMS = ("ln1_w", "ln1_b", "w_qkv", "b_qkv", "w_proj", "b_proj",
+              "ln2_w", "ln2_b", "w_fc1", "b_fc1", "w_fc2", "b_fc2")
+
+
+class VitWeights(ctypes.Structure):
+    """ragged_vit_weights (include/ragged_block.h)."""
+    _fields_ = [(n, ctypes.c_void_p) for n in VIT_PARAMS] + [("mlp", ctypes.c_int32)]
+
+
 def _load() -> ctypes.CDLL:
     if not os.path.exists(LIB_PATH):
         raise ImportError(f"{LIB_PATH} is missing: build it with `python -m paper_2604_15408_b200.build` "
@@ -97,11 +107,16 @@ def _load() -> ctypes.CDLL:
         "ragged_validate_cu_seqlens": [ctypes.POINTER(I32), I32, I64],
         "ragged_pack_attend_unpack_gather": [P, V, V, V, V, V, ctypes.POINTER(Gather), V],
         "ragged_attn_gather": [P, V, V, V, V, ctypes.POINTER(Gather), V],
+        "ragged_layer_norm": [I32, I32, I32, V, I64, V, V, ctypes.c_float, V, I64, V, V],
+        "ragged_linear": [I32, I32, I32, I32, V, I64, V, V, I32, V, I64, V, I64, V, V],
+        "ragged_vit_block": [P, V, V, ctypes.POINTER(VitWeights), V, I64, V],
     }
     for name, args in sigs.items():
         f = getattr(lib, name)
         f.argtypes = args
         f.restype = ctypes.c_int32
+    lib.ragged_vit_block_workspace.argtypes = [P, I32]
+    lib.ragged_vit_block_workspace.restype = ctypes.c_int64
     lib.ragged_graph_destroy.argtypes = [V]
     lib.ragged_graph_destroy.restype = None
     lib.ragged_status_str.argtypes = [ctypes.c_int32]
@@ -118,7 +133,8 @@ _lib = None
 EXPORTS = ("ragged_scan", "ragged_pack", "ragged_attn", "ragged_unpack", "ragged_pack_attend_unpack",
            "ragged_graph_create", "ragged_graph_launch", "ragged_graph_destroy", "ragged_empty_launch",
            "ragged_validate_cu_seqlens", "ragged_status_str", "ragged_last_error", "ragged_build_info",
-           "ragged_keep_topk_l2", "ragged_pack_attend_unpack_gather", "ragged_attn_gather")
+           "ragged_keep_topk_l2", "ragged_pack_attend_unpack_gather", "ragged_attn_gather",
+           "ragged_layer_norm", "ragged_linear", "ragged_vit_block_workspace", "ragged_vit_block")
 
 
 def lib() -> ctypes.CDLL:
@@ -219,15 +235,27 @@ def pack(q, k, v, keep, out=None, stream=None, engine=ENGINE_AUTO):
     return qp, kp, vp, cu, dst, src
 
 
+def _packed_ld(qp, kp, vp) -> int:
+    """Row stride of packed q/k/v [cap, H, d] views: contiguous buffers (H*d)
+    or slices of one packed qkv buffer [cap, 3, H, d] (3*H*d)."""
+    cap, H, d = qp.shape
+    for t in (qp, kp, vp):
+        if t.shape != qp.shape or t.dtype != qp.dtype or t.stride() != qp.stride():
+            raise ValueError("packed q/k/v must share shape, dtype and strides")
+    if qp.stride(2) != 1 or qp.stride(1) != d:
+        raise ValueError("packed q/k/v must be [cap, H, d] with contiguous heads")
+    return qp.stride(0)
+
+
 def attn(qp, kp, vp, cu, N: int, op=None, stream=None, engine=ENGINE_AUTO):
     """a3 (Alg. 1): packed [cap, H, d] + cu [B+1] -> packed O."""
     cap, H, d = qp.shape
-    for t in (qp, kp, vp):
-        if not t.is_contiguous() or t.shape != qp.shape:
-            raise ValueError("packed q/k/v must be contiguous [cap, H, d]")
+    ld = _packed_ld(qp, kp, vp)
     B = cu.numel() - 1
-    op = torch.empty_like(qp) if op is None else op
-    p = problem(B, N, H, d, qp.dtype, H * d, engine)
+    op = torch.empty(cap, H, d, dtype=qp.dtype, device=qp.device) if op is None else op
+    if not op.is_contiguous() or op.shape != qp.shape:
+        raise ValueError("op must be a contiguous [cap, H, d] tensor")
+    p = problem(B, N, H, d, qp.dtype, ld, engine)
     _check(lib().ragged_attn(ctypes.byref(p), qp.data_ptr(), kp.data_ptr(), vp.data_ptr(), cu.data_ptr(),
                             op.data_ptr(), _stream(stream)), "ragged_attn")
     return op
@@ -274,14 +302,71 @@ def attn_gather(qp, kp, vp, cu, N: int, gather: Gather, stream=None, engine=ENGI
     """a3 with the packed all-gather: rows [cu[b], cu[b+1]) of this rank's
     packed O go to out[r] + row * H * d on every rank r (ragged_dist.h)."""
     cap, H, d = qp.shape
-    for t in (qp, kp, vp):
-        if not t.is_contiguous() or t.shape != qp.shape:
-            raise ValueError("packed q/k/v must be contiguous [cap, H, d]")
     B = cu.numel() - 1
-    p = problem(B, N, H, d, qp.dtype, H * d, engine)
+    p = problem(B, N, H, d, qp.dtype, _packed_ld(qp, kp, vp), engine)
     _check(lib().ragged_attn_gather(ctypes.byref(p), qp.data_ptr(), kp.data_ptr(), vp.data_ptr(),
                                    cu.data_ptr(), ctypes.byref(gather), _stream(stream)),
            "ragged_attn_gather")
+
+
+# ---- NEXT row N1: packed ViT block (include/ragged_block.h) -----------------
+
+def _live(live):
+    return None if live is None else live.data_ptr()
+
+
+def layer_norm(x, w, b, eps: float = 1e-6, y=None, live=None, stream=None):
+    """y = LN(x) over the last dim of x [rows, D] (row stride x.stride(0));
+    live: optional device int32 tensor whose first element is the live row count."""
+    rows, D = x.shape
+    y = torch.empty(rows, D, dtype=x.dtype, device=x.device) if y is None else y
+    _check(lib().ragged_layer_norm(_DTYPE[x.dtype], rows, D, x.data_ptr(), x.stride(0), w.data_ptr(),
+                                  b.data_ptr(), eps, y.data_ptr(), y.stride(0), _live(live), _stream(stream)),
+           "ragged_layer_norm")
+    return y
+
+
+def linear(a, w, bias=None, epi: int = EPI_NONE, residual=None, out=None, live=None, stream=None):
+    """out = epi(a w^T + bias) on tcgen05: a [rows, K], w [N, K] (torch Linear layout)."""
+    rows, K = a.shape
+    N = w.shape[0]
+    if w.shape[1] != K or w.stride(1) != 1 or w.stride(0) != K or a.stride(1) != 1:
+        raise ValueError("a must be [rows, K] with unit column stride and w contiguous [N, K]")
+    out = torch.empty(rows, N, dtype=a.dtype, device=a.device) if out is None else out
+    _check(lib().ragged_linear(_DTYPE[a.dtype], rows, N, K, a.data_ptr(), a.stride(0), w.data_ptr(),
+                              _ptr(bias), epi, _ptr(residual), 0 if residual is None else residual.stride(0),
+                              out.data_ptr(), out.stride(0), _live(live), _stream(stream)), "ragged_linear")
+    return out
+
+
+def vit_weights(params: dict) -> VitWeights:
+    """ragged_vit_weights from a dict of device tensors (names VIT_PARAMS)."""
+    w = VitWeights()
+    for n in VIT_PARAMS:
+        setattr(w, n, params[n].data_ptr())
+    w.mlp = params["w_fc1"].shape[0]
+    return w
+
+
+class VitBlock:
+    """One packed pre-norm ViT block (ragged_vit_block) with its weights and
+    a workspace sized for B*N capacity rows."""
+
+    def __init__(self, params: dict, B: int, N: int, H: int, dtype=torch.bfloat16):
+        self.params = params
+        self.w = vit_weights(params)
+        self.p = problem(B, N, H, 64, dtype)
+        nbytes = lib().ragged_vit_block_workspace(ctypes.byref(self.p), self.w.mlp)
+        if nbytes < 0:
+            raise ValueError("invalid block problem")
+        dev = params["w_qkv"].device
+        self.ws = torch.empty(max(nbytes, 16), dtype=torch.uint8, device=dev)
+
+    def __call__(self, x, cu, stream=None):
+        """In place on packed rows x [B*N, D]; rows [0, cu[B]) live."""
+        _check(lib().ragged_vit_block(ctypes.byref(self.p), x.data_ptr(), cu.data_ptr(), ctypes.byref(self.w),
+                                     self.ws.data_ptr(), self.ws.numel(), _stream(stream)), "ragged_vit_block")
+        return x
 
 
 class Graph:

@@ -16,8 +16,8 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libragged.so")
-SOURCES = ["kernels.cu", "api.cu"]
-HEADERS = ["device.cuh", "launch.h"]
+SOURCES = ["kernels.cu", "block.cu", "api.cu"]
+HEADERS = ["device.cuh", "launch.h", "tcgen05.cuh", "attn_tc.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr", "-Xcompiler", "-fPIC",
          "-Xcompiler", "-fvisibility=hidden", "-I", os.path.join(ROOT, "include")]
@@ -46,8 +46,8 @@ def _stale(variant: str = "") -> bool:
         return True
     t = os.path.getmtime(lib)
     deps = [os.path.join(CSRC, f) for f in SOURCES + HEADERS]
-    deps.append(os.path.join(ROOT, "include", "ragged.h"))
-    deps.append(os.path.join(ROOT, "include", "ragged_debug.h"))
+    for h in ("ragged.h", "ragged_debug.h", "ragged_dist.h", "ragged_block.h"):
+        deps.append(os.path.join(ROOT, "include", h))
     deps.append(os.path.abspath(__file__))
     return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
 

@@ -14,6 +14,7 @@
 #include "../../include/ragged.h"
 #include "../../include/ragged_debug.h"
 #include "../../include/ragged_dist.h"
+#include "../../include/ragged_block.h"
 #include "launch.h"
 
 namespace {
@@ -144,7 +145,7 @@ ragged_status ragged_attn(const ragged_problem* prob, const void* qp, const void
   RAGGED_TRY(check_ptr(op, "op"));
   if ((long long)prob->B * prob->H > 0x7fffffffLL) return fail(RAGGED_ENOTSUP, "B*H too large");
   cudaError_t e = ragged::launch_attn(prob->dtype, resolve_engine(prob), qp, kp, vp, cu_seqlens, op, prob->B, prob->N,
-                                      prob->H, as_stream(stream));
+                                      prob->H, prob->ld, as_stream(stream));
   return e == cudaSuccess ? RAGGED_OK : cuda_fail(e, "ragged_attn");
 }
 
@@ -313,8 +314,141 @@ ragged_status ragged_attn_gather(const ragged_problem* prob, const void* qp, con
   RAGGED_TRY(check_ptr_any(cu_seqlens, "cu_seqlens"));
   if ((long long)prob->B * prob->H > 0x7fffffffLL) return fail(RAGGED_ENOTSUP, "B*H too large");
   cudaError_t e = ragged::launch_attn_gather(prob->dtype, qp, kp, vp, cu_seqlens, prob->B, prob->N,
-                                             prob->H, ga, as_stream(stream));
+                                             prob->H, prob->ld, ga, as_stream(stream));
   return e == cudaSuccess ? RAGGED_OK : cuda_fail(e, "ragged_attn_gather");
+}
+
+// ---- ragged_block.h (NEXT row N1) -------------------------------------------
+static int device_sms() {
+  int dev = 0, v = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+  return v;
+}
+
+static ragged_status check_stride(int64_t ld, int64_t min_ld, const char* name) {
+  static thread_local char buf[96];
+  if (ld < min_ld) {
+    snprintf(buf, sizeof buf, "%s < row width", name);
+    return fail(RAGGED_EINVAL, buf);
+  }
+  if (ld % 8 != 0) {
+    snprintf(buf, sizeof buf, "%s %% 8 != 0", name);
+    return fail(RAGGED_EALIGN, buf);
+  }
+  return RAGGED_OK;
+}
+
+ragged_status ragged_layer_norm(ragged_dtype dtype, int32_t rows, int32_t D, const void* x, int64_t ldx,
+                                const void* w, const void* b, float eps, void* y, int64_t ldy,
+                                const int32_t* live_rows_or_null, void* stream) {
+  if (dtype != RAGGED_BF16 && dtype != RAGGED_FP16) return fail(RAGGED_ENOTSUP, "dtype");
+  if (rows < 0) return fail(RAGGED_EINVAL, "rows < 0");
+  if (D < 8 || D > 1024 || D % 8 != 0) return fail(RAGGED_EINVAL, "D must be a multiple of 8 in [8, 1024]");
+  if (!(eps >= 0.f)) return fail(RAGGED_EINVAL, "eps < 0");
+  if (rows == 0) return RAGGED_OK;
+  RAGGED_TRY(check_ptr(x, "x"));
+  RAGGED_TRY(check_ptr(w, "w"));
+  RAGGED_TRY(check_ptr(b, "b"));
+  RAGGED_TRY(check_ptr(y, "y"));
+  RAGGED_TRY(check_stride(ldx, D, "ldx"));
+  RAGGED_TRY(check_stride(ldy, D, "ldy"));
+  cudaError_t e = ragged::launch_layer_norm(dtype, x, ldx, w, b, eps, y, ldy, rows, live_rows_or_null, D,
+                                            as_stream(stream));
+  return e == cudaSuccess ? RAGGED_OK : cuda_fail(e, "ragged_layer_norm");
+}
+
+static ragged_status linear_impl(ragged_dtype dtype, int32_t rows, int32_t N, int32_t K, const void* a,
+                                 int64_t lda, const void* w, const void* bias, int epi, const void* residual,
+                                 int64_t ldr, void* out, int64_t ldo, const int32_t* live, cudaStream_t st) {
+  ragged::GemmArgs g{};
+  g.bias = bias;
+  g.residual = residual;
+  g.out = out;
+  g.M_cap = rows;
+  g.N = N;
+  g.K = K;
+  g.ldo = ldo;
+  g.ldr = ldr;
+  g.m_dev = live;
+  const int bn = ragged::gemm_pick_bn(rows, N, device_sms());
+  cudaError_t e = ragged::launch_gemm(dtype, a, lda, w, g, epi, bn, st);
+  return e == cudaSuccess ? RAGGED_OK : cuda_fail(e, "ragged_linear");
+}
+
+ragged_status ragged_linear(ragged_dtype dtype, int32_t rows, int32_t N, int32_t K, const void* a, int64_t lda,
+                            const void* w, const void* bias, ragged_epilogue epi, const void* residual,
+                            int64_t ldr, void* out, int64_t ldo, const int32_t* live_rows_or_null,
+                            void* stream) {
+  if (dtype != RAGGED_BF16 && dtype != RAGGED_FP16) return fail(RAGGED_ENOTSUP, "dtype");
+  if (rows < 0) return fail(RAGGED_EINVAL, "rows < 0");
+  if (N < 64 || N % 64 != 0 || N > (1 << 20)) return fail(RAGGED_ENOTSUP, "N must be a multiple of 64");
+  if (K < 64 || K % 64 != 0 || K > (1 << 20)) return fail(RAGGED_ENOTSUP, "K must be a multiple of 64");
+  if (epi != RAGGED_EPI_NONE && epi != RAGGED_EPI_GELU && epi != RAGGED_EPI_RESIDUAL)
+    return fail(RAGGED_EINVAL, "unknown epilogue");
+  if (rows == 0) return RAGGED_OK;
+  RAGGED_TRY(check_ptr(a, "a"));
+  RAGGED_TRY(check_ptr(w, "w"));
+  RAGGED_TRY(check_ptr(out, "out"));
+  if (bias != nullptr) RAGGED_TRY(check_ptr(bias, "bias"));
+  if (epi == RAGGED_EPI_RESIDUAL) {
+    RAGGED_TRY(check_ptr(residual, "residual"));
+    RAGGED_TRY(check_stride(ldr, N, "ldr"));
+  }
+  RAGGED_TRY(check_stride(lda, K, "lda"));
+  RAGGED_TRY(check_stride(ldo, N, "ldo"));
+  return linear_impl(dtype, rows, N, K, a, lda, w, bias, epi, residual, ldr, out, ldo, live_rows_or_null,
+                     as_stream(stream));
+}
+
+int64_t ragged_vit_block_workspace(const ragged_problem* prob, int32_t mlp) {
+  if (prob == nullptr || prob->B < 0 || prob->N < 1 || prob->H < 1 || prob->d != 64 || mlp < 64) return -1;
+  const int64_t D = (int64_t)prob->H * prob->d, rows = (int64_t)prob->B * prob->N;
+  return rows * (5 * D + mlp) * 2;
+}
+
+ragged_status ragged_vit_block(const ragged_problem* prob, void* x, const int32_t* cu_seqlens,
+                               const ragged_vit_weights* w, void* workspace, int64_t ws_bytes, void* stream) {
+  if (prob == nullptr) return fail(RAGGED_EINVAL, "problem is NULL");
+  ragged_problem p = *prob;
+  p.ld = (int64_t)p.H * p.d;
+  p.engine = RAGGED_ENGINE_AUTO;
+  RAGGED_TRY(check_problem(&p));
+  if (w == nullptr) return fail(RAGGED_EINVAL, "weights is NULL");
+  const int D = p.H * p.d, mlp = w->mlp;
+  if (D % 64 != 0 || D > 1024) return fail(RAGGED_ENOTSUP, "D = H*d must be a multiple of 64, <= 1024");
+  if (mlp < 64 || mlp % 64 != 0) return fail(RAGGED_ENOTSUP, "mlp must be a multiple of 64");
+  const int64_t need = ragged_vit_block_workspace(&p, mlp);
+  if (ws_bytes < need) return fail(RAGGED_EINVAL, "workspace too small");
+  if (p.B == 0) return RAGGED_OK;
+  if ((long long)p.B * p.N > (1LL << 30)) return fail(RAGGED_ENOTSUP, "B*N too large");
+  RAGGED_TRY(check_ptr(x, "x"));
+  RAGGED_TRY(check_ptr_any(cu_seqlens, "cu_seqlens"));
+  RAGGED_TRY(check_ptr(workspace, "workspace"));
+  const void* ptrs[12] = {w->ln1_w, w->ln1_b, w->w_qkv, w->b_qkv, w->w_proj, w->b_proj,
+                          w->ln2_w, w->ln2_b, w->w_fc1, w->b_fc1, w->w_fc2, w->b_fc2};
+  for (const void* q : ptrs) RAGGED_TRY(check_ptr(q, "weight"));
+  cudaStream_t st = as_stream(stream);
+  const int rows = p.B * p.N;
+  const int32_t* live = cu_seqlens + p.B;
+  char* ws = static_cast<char*>(workspace);
+  void* y = ws;                                         // [rows, D]   LN outputs
+  void* qkv = ws + (int64_t)rows * D * 2;               // [rows, 3D]
+  void* a = ws + (int64_t)rows * 4 * D * 2;             // [rows, D]   attention output
+  void* f = ws + (int64_t)rows * 5 * D * 2;             // [rows, MLP]
+  const char* qkvb = static_cast<const char*>(qkv);
+  cudaError_t e = ragged::launch_layer_norm(p.dtype, x, D, w->ln1_w, w->ln1_b, 1e-6f, y, D, rows, live, D, st);
+  if (e != cudaSuccess) return cuda_fail(e, "ragged_vit_block/ln1");
+  RAGGED_TRY(linear_impl((ragged_dtype)p.dtype, rows, 3 * D, D, y, D, w->w_qkv, w->b_qkv, 0, nullptr, 0, qkv, 3 * D, live, st));
+  e = ragged::launch_attn(p.dtype, RAGGED_ENGINE_MMA_SYNC, qkvb, qkvb + D * 2, qkvb + 2 * D * 2, cu_seqlens, a,
+                          p.B, p.N, p.H, 3LL * D, st);
+  if (e != cudaSuccess) return cuda_fail(e, "ragged_vit_block/attn");
+  RAGGED_TRY(linear_impl((ragged_dtype)p.dtype, rows, D, D, a, D, w->w_proj, w->b_proj, 2, x, D, x, D, live, st));
+  e = ragged::launch_layer_norm(p.dtype, x, D, w->ln2_w, w->ln2_b, 1e-6f, y, D, rows, live, D, st);
+  if (e != cudaSuccess) return cuda_fail(e, "ragged_vit_block/ln2");
+  RAGGED_TRY(linear_impl((ragged_dtype)p.dtype, rows, mlp, D, y, D, w->w_fc1, w->b_fc1, 1, nullptr, 0, f, mlp, live, st));
+  RAGGED_TRY(linear_impl((ragged_dtype)p.dtype, rows, D, mlp, f, mlp, w->w_fc2, w->b_fc2, 2, x, D, x, D, live, st));
+  return RAGGED_OK;
 }
 
 const char* ragged_status_str(ragged_status s) {

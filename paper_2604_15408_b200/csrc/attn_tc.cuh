@@ -128,7 +128,7 @@ __global__ void __launch_bounds__(3 * kTcSlotThreads, 1) attn_tc_kernel(const At
     long long row_base;
     image_rows<kFused>(a, b, sPos, sDrop, sWords, n, row_base, tid, sync);
 
-    const int ldb = (kFused ? (int)a.ld : (int)HD) * 2;
+    const int ldb = (int)a.ld * 2;
     const char* img_q = static_cast<const char*>(a.q) + row_base * ldb + h * kRowBytes;
     const char* img_k = static_cast<const char*>(a.k) + row_base * ldb + h * kRowBytes;
     const char* img_v = static_cast<const char*>(a.v) + row_base * ldb + h * kRowBytes;

@@ -1,0 +1,394 @@
+// block.cu -- NEXT row N1: the packed ViT block after the prune point
+// ("ragged attention + MLP on packed buffer").
+//
+//   layer_norm_kernel   y = LN(x) row-wise (fp32 statistics), one warp per row
+//   gemm_tc_kernel      out = epi(a W^T + bias): tcgen05 UMMA (M = 128, N = BN,
+//                       K = 16 per instruction) with operands brought into
+//                       SWIZZLE_128B shared memory by TMA, fp32 accumulators
+//                       in TMEM, warp-specialised: warp 0 TMA producer,
+//                       warp 1 MMA issuer (+ TMEM owner), warps 2-5 epilogue
+//                       (bias, exact GELU or residual add, RNE to 16-bit)
+//   the attention step is attn_kernel (kernels.cu) reading the packed qkv
+//   buffer with a 3*H*d row stride.
+//
+// Row counts stay on the device: every kernel takes the capacity (B*N rows)
+// and a device pointer to the live count T = cu[B]; tiles past T exit at
+// once, so the block needs no host synchronisation (the paper's pack does
+// one).
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <type_traits>
+#include <utility>
+
+#include "device.cuh"
+#include "launch.h"
+#include "tcgen05.cuh"
+
+namespace ragged {
+
+// ------------------------------------------------------------ LayerNorm ----
+constexpr int kLnThreads = 256;  // 8 rows (warps) per CTA
+
+template <typename T, int kCPL>  // kCPL: 16-byte chunks per lane (D <= 256 * kCPL)
+__global__ void __launch_bounds__(kLnThreads) layer_norm_kernel(const T* __restrict__ x, long long ldx,
+                                                                 const T* __restrict__ w,
+                                                                 const T* __restrict__ bvec, float eps,
+                                                                 T* __restrict__ y, long long ldy, int M_cap,
+                                                                 const int32_t* __restrict__ m_dev, int D) {
+  pdl_launch_dependents();
+  pdl_wait_prerequisites();
+  const int lane = threadIdx.x & 31;
+  const long long row = (long long)blockIdx.x * (kLnThreads / 32) + (threadIdx.x >> 5);
+  const int M = m_dev ? min(*m_dev, M_cap) : M_cap;
+  if (row >= M) return;
+  const int nch = D >> 3;  // 16-byte chunks per row
+  float v[kCPL][8];
+  float s = 0.f;
+  const T* xr = x + row * ldx;
+#pragma unroll
+  for (int i = 0; i < kCPL; ++i) {
+    const int c = lane + 32 * i;
+    if (c < nch) {
+      const uint4 u = ld_global_nc_16(xr + c * 8);
+      const uint32_t wds[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float2 f = unpack2<T>(wds[j]);
+        v[i][2 * j] = f.x;
+        v[i][2 * j + 1] = f.y;
+        s += f.x + f.y;
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v[i][j] = 0.f;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  const float mean = s / (float)D;
+  float q = 0.f;
+#pragma unroll
+  for (int i = 0; i < kCPL; ++i) {
+    if (lane + 32 * i < nch) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const float t = v[i][j] - mean;
+        q += t * t;
+      }
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) q += __shfl_xor_sync(0xffffffffu, q, o);
+  const float rstd = rsqrtf(q / (float)D + eps);
+  T* yr = y + row * ldy;
+#pragma unroll
+  for (int i = 0; i < kCPL; ++i) {
+    const int c = lane + 32 * i;
+    if (c < nch) {
+      const uint4 wu = ld_global_nc_16(w + c * 8), bu = ld_global_nc_16(bvec + c * 8);
+      const uint32_t ww[4] = {wu.x, wu.y, wu.z, wu.w}, bw[4] = {bu.x, bu.y, bu.z, bu.w};
+      uint32_t o[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float2 gw = unpack2<T>(ww[j]), gb = unpack2<T>(bw[j]);
+        o[j] = pack2<T>((v[i][2 * j] - mean) * rstd * gw.x + gb.x,
+                        (v[i][2 * j + 1] - mean) * rstd * gw.y + gb.y);
+      }
+      st_global_16(yr + c * 8, make_uint4(o[0], o[1], o[2], o[3]));
+    }
+  }
+}
+
+// ------------------------------------------------------------------ GEMM ----
+constexpr int kGemmBM = 128, kGemmBK = 64;
+constexpr int kGemmThreads = 192;  // warp 0 TMA, warp 1 MMA, warps 2-5 epilogue
+
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, uint32_t bar, int c0,
+                                            int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, "
+      "%4}], [%2];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void prefetch_tmap(const CUtensorMap* m) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(m)) : "memory");
+}
+
+__device__ __forceinline__ float gelu_erf(float x) { return 0.5f * x * (1.f + erff(x * 0.70710678118654752f)); }
+
+template <int BN>
+__host__ __device__ constexpr int gemm_stages() {
+  return (196 * 1024) / ((kGemmBM + BN) * kGemmBK * 2) < 8 ? (196 * 1024) / ((kGemmBM + BN) * kGemmBK * 2) : 8;
+}
+template <int BN>
+__host__ __device__ constexpr int gemm_smem_bytes() {
+  return gemm_stages<BN>() * (kGemmBM + BN) * kGemmBK * 2 + 1024 /*align*/ + 256 /*barriers*/;
+}
+
+template <typename T, int BN, int kEpi>
+__global__ void __launch_bounds__(kGemmThreads, 1)
+    gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                   const GemmArgs g) {
+  constexpr int kStages = gemm_stages<BN>();
+  constexpr uint32_t kABytes = kGemmBM * kGemmBK * 2, kBBytes = BN * kGemmBK * 2;
+  constexpr uint32_t kStageBytes = kABytes + kBBytes;
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw = smem_u32(smem_raw);
+  const uint32_t base = (raw + 1023u) & ~1023u;  // SWIZZLE_128B atoms need 1024-B alignment
+  const uint32_t bars = base + kStages * kStageBytes;
+  auto full = [&](int s) { return bars + 8u * (uint32_t)s; };
+  auto empty = [&](int s) { return bars + 8u * (uint32_t)(kStages + s); };
+  const uint32_t tfull = bars + 8u * (uint32_t)(2 * kStages);
+  const uint32_t tslot = tfull + 8u;
+  uint32_t* tslot_ptr = reinterpret_cast<uint32_t*>(smem_raw + (tslot - raw));
+
+  pdl_launch_dependents();
+  pdl_wait_prerequisites();
+  const int m0 = blockIdx.x * kGemmBM, n0 = blockIdx.y * BN;
+  const int M = g.m_dev ? min(*g.m_dev, g.M_cap) : g.M_cap;
+  if (m0 >= M) return;  // uniform per CTA, before any barrier or TMEM use
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      tc::mbar_init(full(s), 1);
+      tc::mbar_init(empty(s), 1);
+    }
+    tc::mbar_init(tfull, 1);
+    tc::fence_mbar_init();
+    prefetch_tmap(&tmA);
+    prefetch_tmap(&tmB);
+  }
+  if (warp == 1) tc::alloc(tslot, BN);
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tmem = *tslot_ptr;
+  const int nk = g.K / kGemmBK;
+
+  if (warp == 0) {
+    if (lane == 0) {  // TMA producer
+      for (int kb = 0; kb < nk; ++kb) {
+        const int s = kb % kStages, r = kb / kStages;
+        if (r > 0) tc::mbar_wait(empty(s), (uint32_t)((r - 1) & 1));
+        const uint32_t sa = base + (uint32_t)s * kStageBytes;
+        mbar_expect_tx(full(s), kStageBytes);
+        tma_load_2d(sa, &tmA, full(s), kb * kGemmBK, m0);
+        tma_load_2d(sa + kABytes, &tmB, full(s), kb * kGemmBK, n0);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // MMA issuer
+      const uint32_t idesc = tc::idesc_f16(std::is_same<T, __half>::value ? 0u : 1u, kGemmBM, BN, 0u);
+      for (int kb = 0; kb < nk; ++kb) {
+        const int s = kb % kStages, r = kb / kStages;
+        tc::mbar_wait(full(s), (uint32_t)(r & 1));
+        tc::fence_after();
+        const uint32_t sa = base + (uint32_t)s * kStageBytes, sb = sa + kABytes;
+#pragma unroll
+        for (int k = 0; k < kGemmBK / 16; ++k)
+          tc::mma_ss(tmem, tc::sw128_desc(sa + 32u * k), tc::sw128_desc(sb + 32u * k), idesc,
+                     (kb | k) != 0 ? 1u : 0u);
+        tc::commit(empty(s));  // frees the stage when these MMAs complete
+      }
+      tc::commit(tfull);
+    }
+  } else {  // epilogue: warp w reads TMEM lanes 32*(w % 4) .. +31 (one row per thread)
+    const int quad = warp & 3;
+    const long long row = (long long)m0 + 32 * quad + lane;
+    const bool live = row < M;
+    tc::mbar_wait(tfull, 0u);
+    tc::fence_after();
+    const T* bias = static_cast<const T*>(g.bias);
+    const T* res = kEpi == 2 ? static_cast<const T*>(g.residual) + row * g.ldr + n0 : nullptr;
+    T* out = static_cast<T*>(g.out) + row * g.ldo + n0;
+#pragma unroll 1
+    for (int c = 0; c < BN; c += 32) {
+      uint32_t r[32];
+      tc::ld_x32(tmem + ((uint32_t)(32 * quad) << 16) + (uint32_t)c, r);
+      tc::wait_ld();
+      if (live) {
+        float acc[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) acc[j] = __uint_as_float(r[j]);
+        if (bias != nullptr) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const uint4 u = ld_global_nc_16(bias + n0 + c + 8 * q);
+            const uint32_t wd[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const float2 f = unpack2<T>(wd[j]);
+              acc[8 * q + 2 * j] += f.x;
+              acc[8 * q + 2 * j + 1] += f.y;
+            }
+          }
+        }
+        if constexpr (kEpi == 1) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) acc[j] = gelu_erf(acc[j]);
+        }
+        if constexpr (kEpi == 2) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const uint4 u = *reinterpret_cast<const uint4*>(res + c + 8 * q);
+            const uint32_t wd[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const float2 f = unpack2<T>(wd[j]);
+              acc[8 * q + 2 * j] += f.x;
+              acc[8 * q + 2 * j + 1] += f.y;
+            }
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          uint4 u;
+          u.x = pack2<T>(acc[8 * q + 0], acc[8 * q + 1]);
+          u.y = pack2<T>(acc[8 * q + 2], acc[8 * q + 3]);
+          u.z = pack2<T>(acc[8 * q + 4], acc[8 * q + 5]);
+          u.w = pack2<T>(acc[8 * q + 6], acc[8 * q + 7]);
+          st_global_16(out + c + 8 * q, u);
+        }
+      }
+    }
+  }
+  tc::fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc::fence_after();
+    tc::dealloc(tmem, BN);
+  }
+}
+
+// ------------------------------------------------------------- launchers ----
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_pdl_b(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                                Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
+cudaError_t launch_layer_norm(int dtype, const void* x, long long ldx, const void* w, const void* b,
+                              float eps, void* y, long long ldy, int M_cap, const int32_t* m_dev, int D,
+                              cudaStream_t st) {
+  const int rows_per = kLnThreads / 32;
+  const dim3 grid((M_cap + rows_per - 1) / rows_per);
+  const int cpl = (D / 8 + 31) / 32;
+#define RAGGED_LN(TT, C)                                                                             \
+  return launch_pdl_b(layer_norm_kernel<TT, C>, grid, dim3(kLnThreads), 0, st, (const TT*)x, ldx,  \
+                      (const TT*)w, (const TT*)b, eps, (TT*)y, ldy, M_cap, m_dev, D)
+  if (dtype == 0) {
+    switch (cpl) {
+      case 1: RAGGED_LN(__nv_bfloat16, 1);
+      case 2: RAGGED_LN(__nv_bfloat16, 2);
+      case 3: RAGGED_LN(__nv_bfloat16, 3);
+      default: RAGGED_LN(__nv_bfloat16, 4);
+    }
+  }
+  switch (cpl) {
+    case 1: RAGGED_LN(__half, 1);
+    case 2: RAGGED_LN(__half, 2);
+    case 3: RAGGED_LN(__half, 3);
+    default: RAGGED_LN(__half, 4);
+  }
+#undef RAGGED_LN
+}
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda).
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (fn == nullptr) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  return fn;
+}
+
+// 2-D row-major [rows, cols] 16-bit tensor, row stride ld elements; box
+// {64 columns (128 B), box_rows}, SWIZZLE_128B, zero fill out of bounds.
+static bool make_tmap(CUtensorMap* m, int dtype, const void* ptr, long long rows, long long cols, long long ld,
+                      int box_rows) {
+  EncodeTiledFn fn = encode_fn();
+  if (fn == nullptr) return false;
+  const cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  const cuuint64_t strides[1] = {(cuuint64_t)ld * 2};
+  const cuuint32_t box[2] = {(cuuint32_t)kGemmBK, (cuuint32_t)box_rows};
+  const cuuint32_t estr[2] = {1, 1};
+  return fn(m, dtype == 0 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2,
+            const_cast<void*>(ptr), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <typename T, int BN, int kEpi>
+static cudaError_t launch_gemm_t(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& g,
+                                 cudaStream_t st) {
+  static bool done[64] = {false};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev >= 0 && dev < 64 && !done[dev]) {
+    cudaError_t e = cudaFuncSetAttribute(gemm_tc_kernel<T, BN, kEpi>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         gemm_smem_bytes<BN>());
+    if (e != cudaSuccess) return e;
+    done[dev] = true;
+  }
+  const dim3 grid((g.M_cap + kGemmBM - 1) / kGemmBM, g.N / BN);
+  return launch_pdl_b(gemm_tc_kernel<T, BN, kEpi>, grid, dim3(kGemmThreads), gemm_smem_bytes<BN>(), st, ta, tb,
+                      g);
+}
+
+template <typename T, int BN>
+static cudaError_t launch_gemm_bn(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& g, int epi,
+                                  cudaStream_t st) {
+  if (epi == 1) return launch_gemm_t<T, BN, 1>(ta, tb, g, st);
+  if (epi == 2) return launch_gemm_t<T, BN, 2>(ta, tb, g, st);
+  return launch_gemm_t<T, BN, 0>(ta, tb, g, st);
+}
+
+// Tile width: the widest of {256, 128, 64} dividing N that still gives at
+// least one CTA per SM, else 64 (more CTAs for small GEMMs).
+int gemm_pick_bn(int M_cap, int N, int sms) {
+  const int mt = (M_cap + kGemmBM - 1) / kGemmBM;
+  for (int bn : {256, 128}) {
+    if (N % bn == 0 && (long long)mt * (N / bn) >= sms) return bn;
+  }
+  return N % 128 == 0 && N < 128 ? 128 : 64;
+}
+
+cudaError_t launch_gemm(int dtype, const void* a, long long lda, const void* w, const GemmArgs& g, int epi,
+                        int bn, cudaStream_t st) {
+  CUtensorMap ta, tb;
+  if (!make_tmap(&ta, dtype, a, g.M_cap, g.K, lda, kGemmBM)) return cudaErrorInvalidValue;
+  if (!make_tmap(&tb, dtype, w, g.N, g.K, g.K, bn)) return cudaErrorInvalidValue;
+  if (dtype == 0) {
+    if (bn == 256) return launch_gemm_bn<__nv_bfloat16, 256>(ta, tb, g, epi, st);
+    if (bn == 128) return launch_gemm_bn<__nv_bfloat16, 128>(ta, tb, g, epi, st);
+    return launch_gemm_bn<__nv_bfloat16, 64>(ta, tb, g, epi, st);
+  }
+  if (bn == 256) return launch_gemm_bn<__half, 256>(ta, tb, g, epi, st);
+  if (bn == 128) return launch_gemm_bn<__half, 128>(ta, tb, g, epi, st);
+  return launch_gemm_bn<__half, 64>(ta, tb, g, epi, st);
+}
+
+}  // namespace ragged

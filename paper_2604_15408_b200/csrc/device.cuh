@@ -103,6 +103,18 @@ __device__ __forceinline__ uint32_t pack2<__half>(float a, float b) {
   return *reinterpret_cast<uint32_t*>(&h);
 }
 
+// Unpack two 16-bit values (lo first) to floats (exact).
+template <typename T>
+__device__ __forceinline__ float2 unpack2(uint32_t w);
+template <>
+__device__ __forceinline__ float2 unpack2<__nv_bfloat16>(uint32_t w) {
+  return __bfloat1622float2(*reinterpret_cast<__nv_bfloat162*>(&w));
+}
+template <>
+__device__ __forceinline__ float2 unpack2<__half>(uint32_t w) {
+  return __half22float2(*reinterpret_cast<__half2*>(&w));
+}
+
 // Split p into hi + lo in the 16-bit type (p ~= hi + lo to ~2^-16 relative):
 // the PV product runs twice (P_hi V + P_lo V) so that rounding P to 16 bits
 // does not cost output accuracy (R2).

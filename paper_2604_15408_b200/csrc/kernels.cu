@@ -577,7 +577,7 @@ __global__ void __launch_bounds__(kAttnThreads, 3) attn_kernel(const AttnArgs a,
   image_rows<kFused>(a, b, sPos, sDrop, sWords, n, row_base, tid, [] { __syncthreads(); });
   // Byte addressing: one 64-bit image base per tensor, then 32-bit row offsets
   // (pos < 256, token stride <= 2^23 bytes -- validated in api.cu).
-  const int ldb = (kFused ? (int)a.ld : (int)HD) * 2;  // input token stride, bytes
+  const int ldb = (int)a.ld * 2;  // input token stride, bytes
   const int HDb = (int)HD * 2;                          // output token stride, bytes
   const char* img_q = reinterpret_cast<const char*>(gq) + row_base * ldb + h * kRowBytes;
   const char* img_k = reinterpret_cast<const char*>(gk) + row_base * ldb + h * kRowBytes;
@@ -990,7 +990,7 @@ static cudaError_t dispatch_attn(int dtype, int engine, const AttnArgs& a, int n
 }
 
 cudaError_t launch_attn(int dtype, int engine, const void* qp, const void* kp, const void* vp,
-                        const int32_t* cu, void* op, int B, int N, int H, cudaStream_t st) {
+                        const int32_t* cu, void* op, int B, int N, int H, long long ld, cudaStream_t st) {
   AttnArgs a{};
   a.q = qp;
   a.k = kp;
@@ -1000,7 +1000,7 @@ cudaError_t launch_attn(int dtype, int engine, const void* qp, const void* kp, c
   a.B = B;
   a.N = N;
   a.H = H;
-  a.ld = (long long)H * kHeadDim;
+  a.ld = ld;
   return dispatch_attn<false>(dtype, engine, a, B * H, st);
 }
 
@@ -1048,8 +1048,8 @@ cudaError_t launch_fused_gather(int dtype, const uint8_t* keep, const void* q, c
 
 // ragged_attn whose packed output rows go to every rank's gathered buffer.
 cudaError_t launch_attn_gather(int dtype, const void* qp, const void* kp, const void* vp,
-                               const int32_t* cu, int B, int N, int H, const GatherArgs& g,
-                               cudaStream_t st) {
+                               const int32_t* cu, int B, int N, int H, long long ld,
+                               const GatherArgs& g, cudaStream_t st) {
   AttnArgs a{};
   a.q = qp;
   a.k = kp;
@@ -1058,7 +1058,7 @@ cudaError_t launch_attn_gather(int dtype, const void* qp, const void* kp, const 
   a.B = B;
   a.N = N;
   a.H = H;
-  a.ld = (long long)H * kHeadDim;
+  a.ld = ld;
   return dtype == 0 ? launch_attn_mma<__nv_bfloat16, false, true>(a, B * H, st, g)
                     : launch_attn_mma<__half, false, true>(a, B * H, st, g);
 }

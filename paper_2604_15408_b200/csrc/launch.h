@@ -12,7 +12,7 @@ cudaError_t launch_pack(const void* q, const void* k, const void* v, long long l
                         cudaStream_t st);
 // engine: 1 = mma.sync, 2 = tcgen05 (api.cu resolves RAGGED_ENGINE_AUTO)
 cudaError_t launch_attn(int dtype, int engine, const void* qp, const void* kp, const void* vp, const int32_t* cu,
-                        void* op, int B, int N, int H, cudaStream_t st);
+                        void* op, int B, int N, int H, long long ld, cudaStream_t st);
 cudaError_t launch_unpack(const void* op, const int32_t* dst, void* o, int B, int N, int H,
                           cudaStream_t st);
 cudaError_t launch_fused(int dtype, int engine, const uint8_t* keep, const void* q, const void* k,
@@ -34,9 +34,26 @@ cudaError_t launch_fused_gather(int dtype, const uint8_t* keep, const void* q, c
                                 const void* v, long long ld, int32_t* cu_out, int B, int N, int H,
                                 const GatherArgs& g, cudaStream_t st);
 cudaError_t launch_attn_gather(int dtype, const void* qp, const void* kp, const void* vp,
-                               const int32_t* cu, int B, int N, int H, const GatherArgs& g,
-                               cudaStream_t st);
+                               const int32_t* cu, int B, int N, int H, long long ld,
+                               const GatherArgs& g, cudaStream_t st);
 cudaError_t launch_empty(int grid, int block, cudaStream_t st);
+
+// ---- NEXT row N1 (block.cu) ----
+struct GemmArgs {
+  const void* bias;        // [N] or null
+  const void* residual;    // [M, ldr] (epilogue 2) or null
+  void* out;               // [M, ldo]
+  int M_cap, N, K;
+  long long ldo, ldr;      // elements
+  const int32_t* m_dev;    // live rows = min(*m_dev, M_cap), or null -> M_cap
+};
+// epi: 0 none, 1 exact GELU, 2 residual add.  bn in {64, 128, 256}, N % bn == 0, K % 64 == 0.
+cudaError_t launch_gemm(int dtype, const void* a, long long lda, const void* w, const GemmArgs& g, int epi,
+                        int bn, cudaStream_t st);
+int gemm_pick_bn(int M_cap, int N, int sms);
+cudaError_t launch_layer_norm(int dtype, const void* x, long long ldx, const void* w, const void* b,
+                              float eps, void* y, long long ldy, int M_cap, const int32_t* m_dev, int D,
+                              cudaStream_t st);
 cudaError_t launch_keep_topk_l2(int dtype, const void* x, long long ld, int B, int N, int D, int k,
                                 uint8_t* keep, cudaStream_t st);
 int fused_smem_bytes(int N);

@@ -16,8 +16,9 @@ rb = pytest.importorskip("paper_2604_15408_b200")
 
 def _declared():
     # ragged_debug.h declares the timeline-build-only symbols (libragged_tl.so).
-    src = "".join(open(os.path.join(ROOT, "include", h)).read() for h in ("ragged.h", "ragged_dist.h"))
-    return sorted(set(re.findall(r"^\s*RAGGED_API\s+(?:ragged_status|void|int32_t|const char\*)\s+(ragged_\w+)\(",
+    src = "".join(open(os.path.join(ROOT, "include", h)).read()
+                  for h in ("ragged.h", "ragged_dist.h", "ragged_block.h"))
+    return sorted(set(re.findall(r"^\s*RAGGED_API\s+(?:ragged_status|void|int32_t|int64_t|const char\*)\s+(ragged_\w+)\(",
                                  src, re.M)))
 
 
@@ -156,3 +157,33 @@ def test_product_package_does_not_import_oracle():
             if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
                 txt = open(os.path.join(dirpath, f)).read()
                 assert "oracle" not in re.sub(r"#.*|//.*", "", txt).replace("oracle/", ""), f
+
+
+def test_block_validation():
+    """ragged_block.h host-checkable errors (no CUDA call)."""
+    L = rb.lib()
+    assert L.ragged_layer_norm(0, 4, 12, FAKE, 12, FAKE, FAKE, 1e-6, FAKE, 12, None, None) == rb.EINVAL  # D % 8
+    assert L.ragged_layer_norm(0, 4, 2048, FAKE, 2048, FAKE, FAKE, 1e-6, FAKE, 2048, None, None) == rb.EINVAL
+    assert L.ragged_layer_norm(0, 4, 64, FAKE, 60, FAKE, FAKE, 1e-6, FAKE, 64, None, None) == rb.EINVAL
+    assert L.ragged_layer_norm(0, 4, 64, FAKE + 2, 64, FAKE, FAKE, 1e-6, FAKE, 64, None, None) == rb.EALIGN
+    assert L.ragged_layer_norm(5, 4, 64, FAKE, 64, FAKE, FAKE, 1e-6, FAKE, 64, None, None) == rb.ENOTSUP
+    assert L.ragged_layer_norm(0, 0, 64, None, 64, None, None, 1e-6, None, 64, None, None) == rb.OK
+    lin = lambda *a: L.ragged_linear(*a, None, None)  # noqa: E731
+    assert lin(0, 4, 100, 64, FAKE, 64, FAKE, None, 0, None, 0, FAKE, 100) == rb.ENOTSUP       # N % 64
+    assert lin(0, 4, 64, 96, FAKE, 96, FAKE, None, 0, None, 0, FAKE, 64) == rb.ENOTSUP         # K % 64
+    assert lin(0, 4, 64, 64, FAKE, 64, FAKE, None, 7, None, 0, FAKE, 64) == rb.EINVAL          # epilogue
+    assert lin(0, 4, 64, 64, FAKE, 64, FAKE, None, 2, None, 64, FAKE, 64) == rb.EINVAL         # residual NULL
+    assert lin(0, 4, 64, 64, FAKE, 64, FAKE, FAKE + 4, 0, None, 0, FAKE, 64) == rb.EALIGN      # bias
+    assert lin(0, 4, 64, 64, FAKE, 60, FAKE, None, 0, None, 0, FAKE, 64) == rb.EINVAL          # lda < K
+    assert lin(0, 0, 64, 64, None, 64, None, None, 0, None, 0, None, 64) == rb.OK
+    p = rb.problem(4, 197, 12)
+    assert L.ragged_vit_block_workspace(ctypes.byref(p), 3072) == 4 * 197 * (5 * 768 + 3072) * 2
+    assert L.ragged_vit_block_workspace(ctypes.byref(rb.problem(4, 197, 12, d=32)), 3072) == -1
+    w = rb.VitWeights()
+    w.mlp = 3072
+    assert L.ragged_vit_block(ctypes.byref(p), FAKE, FAKE, ctypes.byref(w), FAKE, 10, None) == rb.EINVAL  # ws
+    big = 1 << 40
+    assert L.ragged_vit_block(ctypes.byref(p), FAKE, FAKE, ctypes.byref(w), FAKE, big, None) == rb.EINVAL  # NULL w
+    w.mlp = 100
+    assert L.ragged_vit_block(ctypes.byref(p), FAKE, FAKE, ctypes.byref(w), FAKE, big, None) == rb.ENOTSUP
+    assert L.ragged_vit_block(None, FAKE, FAKE, ctypes.byref(w), FAKE, big, None) == rb.EINVAL

@@ -1,0 +1,241 @@
+"""GPU parity of NEXT row N1 (include/ragged_block.h): LayerNorm, the tcgen05
+GEMM with its three epilogues, and the whole packed ViT block, against the
+fp64 oracle (oracle/vit_block.py) on the same 16-bit inputs.
+
+Tolerances (R22), from the arithmetic:
+  * LayerNorm: fp32 statistics, one RNE rounding of the output ->
+    |err| <= 1 ulp_dt(|ref|) + 2^-16 (fp32 statistic error on O(1) values).
+  * GEMM: fp32 accumulation of K products of exact 16-bit operands plus one
+    RNE rounding of the output -> |err| <= ulp_dt(|ref|) + K * 2^-23 *
+    sum_k |a_k w_k| (a deliberately loose form of the standard bound gamma_K).
+    GELU (erff, ~2 ulp fp32) and the residual add (exact inputs) add
+    nothing visible at 16-bit output precision.
+  * Block, stage-local: every stored intermediate of the GPU block is checked
+    against the oracle step applied to the GPU's own previous stored tensor,
+    with the per-kernel bounds above.
+  * Block, end to end vs the oracle run with the same storage rounding:
+    rounding flips at intermediate storage points propagate through later
+    GEMMs and the residual stream, so the bound is relative to the output
+    scale: max-abs <= 2^-7 max|ref| and relative Frobenius <= 2^-9; and the
+    GPU's distance to the pure-fp64 block is within 10 % of the distance the
+    bf16 storage rounding alone causes (measured: DESIGN.md R22).
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+from helpers import MANT, bits, to_np
+
+rb = pytest.importorskip("paper_2604_15408_b200")
+pytestmark = pytest.mark.gpu
+DEV = "cuda"
+DT = {"bf16": torch.bfloat16, "fp16": torch.float16}
+SENT = -12345
+
+
+def ulp(x, dtype):
+    ax = np.maximum(np.abs(x), 2.0 ** -14)
+    return 2.0 ** (np.floor(np.log2(ax)) - MANT[dtype])
+
+
+def store(dtype):
+    return lambda t: torch.from_numpy(np.asarray(t)).to(dtype).double().numpy()
+
+
+def _sentinel(shape, dtype):
+    t = torch.empty(shape, dtype=dtype, device=DEV)
+    t.view(torch.int16).fill_(SENT)
+    return t
+
+
+# ------------------------------------------------------------- LayerNorm ----
+
+@pytest.mark.parametrize("rows,D", [(1, 64), (37, 192), (130, 384), (1248, 768), (9, 1000), (5, 1024)])
+@pytest.mark.parametrize("dt", ["bf16", "fp16"])
+def test_layer_norm(rows, D, dt):
+    dtype = DT[dt]
+    x = (synth.packed_rows(rows, D, dtype, seed=rows) * 3 + 0.5).to(dtype)
+    g = torch.Generator().manual_seed(D)
+    w = (1 + 0.1 * torch.randn(D, generator=g)).to(dtype)
+    b = (0.05 * torch.randn(D, generator=g)).to(dtype)
+    y = rb.layer_norm(x.to(DEV), w.to(DEV), b.to(DEV))
+    torch.cuda.synchronize()
+    ref = oracle.layer_norm(x, w, b)
+    err = np.abs(to_np(y) - ref)
+    assert (err <= ulp(ref, dtype) + 2.0 ** -16).all(), err.max()
+
+
+def test_layer_norm_live_rows_and_strides():
+    """Rows at or past the live count are not written; strided x / y."""
+    rows, D, live = 40, 192, 23
+    xs = synth.packed_rows(rows, 2 * D, seed=1).to(DEV)[:, :D]          # row stride 2D
+    w = torch.ones(D, dtype=torch.bfloat16, device=DEV)
+    b = torch.zeros(D, dtype=torch.bfloat16, device=DEV)
+    ybuf = _sentinel((rows, D + 64), torch.bfloat16)
+    y = ybuf[:, :D]
+    rb.layer_norm(xs, w, b, y=y, live=torch.tensor([live], dtype=torch.int32, device=DEV))
+    torch.cuda.synchronize()
+    ref = oracle.layer_norm(xs[:live].cpu(), w.cpu(), b.cpu())
+    assert (np.abs(to_np(y[:live]) - ref) <= ulp(ref, torch.bfloat16) + 2.0 ** -16).all()
+    assert (bits(ybuf[live:]) == SENT).all() and (bits(ybuf[:, D:]) == SENT).all()
+
+
+# ------------------------------------------------------------------ GEMM ----
+
+def _gemm_case(M, N, K, epi, dtype=torch.bfloat16, live=None, seed=0):
+    g = torch.Generator().manual_seed(seed)
+    a = torch.randn(M, K, generator=g).to(dtype)
+    w = (0.05 * torch.randn(N, K, generator=g)).to(dtype)
+    bias = (0.1 * torch.randn(N, generator=g)).to(dtype)
+    res = torch.randn(M, N, generator=g).to(dtype) if epi == rb.EPI_RESIDUAL else None
+    out = _sentinel((M, N), dtype)
+    lv = None if live is None else torch.tensor([live], dtype=torch.int32, device=DEV)
+    rb.linear(a.to(DEV), w.to(DEV), bias.to(DEV), epi, None if res is None else res.to(DEV), out=out, live=lv)
+    torch.cuda.synchronize()
+    L = M if live is None else min(live, M)
+    ref = oracle.linear(a[:L], w, bias)
+    if epi == rb.EPI_GELU:
+        ref = oracle.gelu(ref)
+    if epi == rb.EPI_RESIDUAL:
+        ref = ref + oracle.as_f64(res[:L])
+    mag = np.abs(oracle.as_f64(a[:L])) @ np.abs(oracle.as_f64(w)).T
+    bound = ulp(ref, dtype) + K * 2.0 ** -23 * mag
+    err = np.abs(to_np(out[:L]) - ref)
+    assert (err <= bound).all(), f"worst ratio {(err / bound).max():.3f}"
+    if L < M:
+        assert (bits(out[L:]) == SENT).all()
+    return err.max(initial=0.0)
+
+
+@pytest.mark.parametrize("M,N,K", [(1, 64, 64), (130, 192, 384), (257, 1536, 384), (300, 768, 3072),
+                                   (1248, 2304, 768), (4100, 256, 128)])
+@pytest.mark.parametrize("epi", [0, 1, 2])
+def test_linear_epilogues(M, N, K, epi):
+    _gemm_case(M, N, K, epi, seed=M + N + K + epi)
+
+
+def test_linear_fp16_and_live_rows():
+    _gemm_case(333, 384, 192, rb.EPI_GELU, dtype=torch.float16, seed=5)
+    _gemm_case(640, 512, 256, rb.EPI_RESIDUAL, live=517, seed=6)     # partial last live tile
+    _gemm_case(640, 512, 256, rb.EPI_NONE, live=0, seed=7)           # nothing live
+
+
+def test_linear_residual_in_place():
+    """out may alias residual (the block's x += proj(a))."""
+    M, N, K = 200, 384, 384
+    g = torch.Generator().manual_seed(9)
+    a = torch.randn(M, K, generator=g).bfloat16().to(DEV)
+    w = (0.05 * torch.randn(N, K, generator=g)).bfloat16().to(DEV)
+    x = torch.randn(M, N, generator=g).bfloat16().to(DEV)
+    x0 = x.clone()
+    rb.linear(a, w, None, rb.EPI_RESIDUAL, x, out=x)
+    torch.cuda.synchronize()
+    ref = oracle.linear(a.cpu(), w.cpu(), np.zeros(N)) + oracle.as_f64(x0.cpu())
+    mag = np.abs(oracle.as_f64(a.cpu())) @ np.abs(oracle.as_f64(w.cpu())).T
+    assert (np.abs(to_np(x) - ref) <= ulp(ref, torch.bfloat16) + K * 2.0 ** -23 * mag).all()
+
+
+# ----------------------------------------------------------------- block ----
+
+def _check_block(got, ref, ref64):
+    """End-to-end bound (R22): vs the oracle with the same storage rounding,
+    max-abs <= 2^-7 max|ref| and relative Frobenius error <= 2^-9 (the bf16
+    unit roundoff); and vs the pure-fp64 block the GPU is no less accurate
+    than exact arithmetic with bf16 storage (relF within 10 %)."""
+    err = np.abs(got - ref)
+    assert err.max() <= 2.0 ** -7 * np.abs(ref).max(), (err.max(), np.abs(ref).max())
+    relf = np.linalg.norm(got - ref) / np.linalg.norm(ref)
+    assert relf <= 2.0 ** -9, relf
+    r_gpu = np.linalg.norm(got - ref64) / np.linalg.norm(ref64)
+    r_sto = np.linalg.norm(ref - ref64) / np.linalg.norm(ref64)
+    assert r_gpu <= 1.1 * r_sto + 1e-6, (r_gpu, r_sto)
+
+
+def _block_inputs(preset, B, p, seed, dtype=torch.bfloat16, method="l2"):
+    pr = synth.PRESETS[preset]
+    D, H, MLP, N = pr["D"], pr["H"], pr["MLP"], 197
+    params = synth.vit_weights(D, MLP, dtype, seed)
+    keep = synth.make_inputs(B, N, H, p, method, "bf16", seed=seed)[3].numpy()
+    cu, _, _ = oracle.scan(keep)
+    T = int(cu[-1])
+    x = synth.packed_rows(T, D, dtype, seed)
+    return params, cu, x, D, H, MLP, N, T
+
+
+@pytest.mark.parametrize("preset,B,p,method", [("deit_tiny", 4, 0.5, "l2"), ("deit_small", 6, 0.0, "l2"),
+                                               ("deit_base", 8, 0.8, "l2"), ("deit_base", 5, 0.7, "ats")])
+def test_vit_block_end_to_end(preset, B, p, method):
+    dtype = torch.bfloat16
+    params, cu, x, D, H, MLP, N, T = _block_inputs(preset, B, p, seed=B, method=method)
+    blk = rb.VitBlock({k: v.to(DEV) for k, v in params.items()}, B, N, H, dtype)
+    xd = _sentinel((B * N, D), dtype)
+    xd[:T] = x.to(DEV)
+    blk(xd, torch.from_numpy(cu.astype(np.int32)).to(DEV))
+    torch.cuda.synchronize()
+    assert (bits(xd[T:]) == SENT).all()            # rows past cu[B] untouched
+    got = to_np(xd[:T])
+    ref = oracle.vit_block(x, cu, params, H, store=store(dtype))
+    _check_block(got, ref, oracle.vit_block(x, cu, params, H))
+
+    # stage-local checks on the stored intermediates left in the workspace
+    ws = blk.ws
+    R = B * N
+    view = lambda off, cols: ws[off * 2: off * 2 + R * cols * 2].view(dtype).view(R, cols)[:T]  # noqa: E731
+    qkv, a, f = view(R * D, 3 * D), view(4 * R * D, D), view(5 * R * D, MLP)
+    z = view(0, D)                                   # LN2 output (LN1's was overwritten)
+    pf = {k: oracle.as_f64(v) for k, v in params.items()}
+    # f = GELU(z Wfc1^T + b) from the GPU's own z
+    ref_f = oracle.gelu(oracle.linear(z.cpu(), pf["w_fc1"], pf["b_fc1"]))
+    mag = np.abs(to_np(z)) @ np.abs(pf["w_fc1"]).T
+    assert (np.abs(to_np(f) - ref_f) <= ulp(ref_f, dtype) + D * 2.0 ** -23 * mag + 2.0 ** -20).all()
+    # a = attention(q, k, v) from the GPU's own qkv: the attention tolerance (R2)
+    q3 = to_np(qkv).reshape(T, 3, H, 64)
+    ref_a = oracle.attention(q3[:, 0], q3[:, 1], q3[:, 2], cu).reshape(T, D)
+    assert np.abs(to_np(a) - ref_a).max() <= 2e-3 * max(1.0, np.abs(q3[:, 2]).max())
+
+
+def test_vit_block_graph_and_determinism():
+    """Two runs (eager and CUDA-graph replay) give bitwise-identical rows."""
+    dtype = torch.bfloat16
+    params, cu, x, D, H, MLP, N, T = _block_inputs("deit_small", 8, 0.7, seed=11)
+    blk = rb.VitBlock({k: v.to(DEV) for k, v in params.items()}, 8, N, H, dtype)
+    cud = torch.from_numpy(cu.astype(np.int32)).to(DEV)
+    x0 = torch.zeros(8 * N, D, dtype=dtype, device=DEV)
+    x0[:T] = x.to(DEV)
+    xa = x0.clone()
+    blk(xa, cud)
+    xb = x0.clone()
+    g = torch.cuda.CUDAGraph()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        blk(xb, cud, stream=s)           # warm (one-time attributes) outside capture
+    torch.cuda.synchronize()
+    xb.copy_(x0)
+    with torch.cuda.graph(g, stream=s):
+        blk(xb, cud, stream=s)
+    g.replay()
+    torch.cuda.synchronize()
+    assert (bits(xa) == bits(xb)).all()
+
+
+def test_vit_block_empty_images_and_all_dropped():
+    dtype = torch.bfloat16
+    pr = synth.PRESETS["deit_tiny"]
+    D, H, MLP, N, B = pr["D"], pr["H"], pr["MLP"], 197, 3
+    params = synth.vit_weights(D, MLP, dtype, 3)
+    for counts in ([0, 5, 0], [0, 0, 0]):
+        cu = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
+        T = int(cu[-1])
+        x = synth.packed_rows(max(T, 1), D, dtype, 3)[:T]
+        blk = rb.VitBlock({k: v.to(DEV) for k, v in params.items()}, B, N, H, dtype)
+        xd = _sentinel((B * N, D), dtype)
+        xd[:T] = x.to(DEV)
+        blk(xd, torch.from_numpy(cu.astype(np.int32)).to(DEV))
+        torch.cuda.synchronize()
+        assert (bits(xd[T:]) == SENT).all()
+        if T:
+            _check_block(to_np(xd[:T]), oracle.vit_block(x, cu, params, H, store=store(dtype)),
+                         oracle.vit_block(x, cu, params, H))
