@@ -634,7 +634,79 @@ def extras(args, rb, torch, dev, sets, c, B, N, H, dt, T):
         rb.keep_topk_l2(xs[i % 4], kk, keep=keeps[i])
         rb.pack_attend_unpack(s["q"], s["k"], s["v"], keeps[i], o=s["o"], cu=s["cu"])
     out["prune_then_fused_us"] = _graph_time(torch, [(lambda i=i: prune_fused(i)) for i in range(N_SETS)], reps)
+    try:
+        out["n1_block"] = n1_block_extras(rb, torch, dev, dt)
+    except Exception as ex:
+        out["n1_block"] = {"error": repr(ex)[:300]}
     return out
+
+
+def n1_block_extras(rb, torch, dev, dt):
+    """NEXT row N1: the packed DeiT-B block (LN, qkv GEMM, ragged
+    attention, proj GEMM + residual, LN, fc1 GEMM + GELU, fc2 GEMM + residual)
+    on the packed rows of B = 32 images, vs the same block with torch ops
+    (cuBLAS linears, torch LayerNorm / GELU) around our ragged_attn; and the
+    paper's layers 5-12 as a pipeline: pack once (ragged_pack) + 8 blocks.
+    Weights stay L2-resident per block (14 MB); graph-replayed device time."""
+    import numpy as np
+    import oracle
+    import synth
+    pr = synth.PRESETS["deit_base"]
+    D, H, MLP, N, B = pr["D"], pr["H"], pr["MLP"], 197, 32
+    res = {}
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    tc_peak = peaks.get("bf16_tflops_sustained", 1365.0)
+    for p in (0.8, 0.0):
+        params = {k: v.to(dev) for k, v in synth.vit_weights(D, MLP, dt, 0).items()}
+        keep = synth.make_inputs(B, N, H, p, "l2", "bf16", seed=0)[3].numpy()
+        cu, _, _ = oracle.scan(keep)
+        T = int(cu[-1])
+        cud = torch.from_numpy(cu.astype(np.int32)).to(dev)
+        blk = rb.VitBlock(params, B, N, H, dt)
+        x = torch.zeros(B * N, D, dtype=dt, device=dev)
+        x[:T] = synth.packed_rows(T, D, dt, 0).to(dev)
+        ours = _graph_time(torch, [lambda: blk(x, cud)], 100)
+        P = params
+        F = torch.nn.functional
+
+        def torch_block(xx=x[:T]):
+            y = F.layer_norm(xx, (D,), P["ln1_w"], P["ln1_b"], 1e-6)
+            qkv = F.linear(y, P["w_qkv"], P["b_qkv"]).view(T, 3, H, 64)
+            a = rb.attn(qkv[:, 0], qkv[:, 1], qkv[:, 2], cud, N)
+            h = xx + F.linear(a.view(T, D), P["w_proj"], P["b_proj"])
+            z = F.layer_norm(h, (D,), P["ln2_w"], P["ln2_b"], 1e-6)
+            return h + F.linear(F.gelu(F.linear(z, P["w_fc1"], P["b_fc1"])), P["w_fc2"], P["b_fc2"])
+
+        tb = _graph_time(torch, [torch_block], 100)
+        flops = 2.0 * T * D * (4 * D + 2 * MLP) + 4.0 * float((np.diff(cu) ** 2).sum()) * 64 * H
+        res[f"p{p}"] = {"T": T, "block_us": ours, "torch_cublas_block_us": tb,
+                        "block_tflops": flops / ours / 1e6, "tensor_frac_of_sustained": flops / ours / 1e6 / tc_peak}
+    # layers 5-12 on the packed buffer: ragged_pack of the hidden states once, then 8 blocks
+    p = 0.8
+    blocks = [rb.VitBlock({k: v.to(dev) for k, v in synth.vit_weights(D, MLP, dt, L).items()}, B, N, H, dt)
+              for L in range(8)]
+    xh = synth.hidden_states(B, N, D, dt, seed=0).to(dev)
+    keep = torch.from_numpy(synth.mask_threshold_l2(B, N, synth.kept_tokens(N, p), 1000, D=D)).to(dev)
+    xp = torch.empty(B * N, D, dtype=dt, device=dev)
+    cu = torch.empty(B + 1, dtype=torch.int32, device=dev)
+    dst = torch.empty(B * N, dtype=torch.int32, device=dev)
+    src = torch.empty(B * N, dtype=torch.int32, device=dev)
+    x3 = xh.view(B, N, H, 64)
+
+    def pipeline():
+        rb.pack(x3, x3, x3, keep, out=(xp.view(B * N, H, 64), xp.view(B * N, H, 64), xp.view(B * N, H, 64),
+                                       cu, dst, src))
+        for bl in blocks:
+            bl(xp, cu)
+
+    us = _graph_time(torch, [pipeline], 20)
+    res["layers5_12_p0.8"] = {"us_per_batch": us, "images_per_s": B / us * 1e6,
+                              "note": "pack once + 8 packed blocks, B=32 DeiT-B, synthetic weights"}
+    return res
 
 
 def config_extras(rb, torch, dev, dt):

@@ -18,6 +18,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include <type_traits>
 #include <utility>
@@ -103,7 +104,8 @@ __global__ void __launch_bounds__(kLnThreads) layer_norm_kernel(const T* __restr
 
 // ------------------------------------------------------------------ GEMM ----
 constexpr int kGemmBM = 128, kGemmBK = 64;
-constexpr int kGemmThreads = 192;  // warp 0 TMA, warp 1 MMA, warps 2-5 epilogue
+constexpr int kEpiWarps = 8;                         // two per TMEM lane quadrant
+constexpr int kGemmThreads = 64 + 32 * kEpiWarps;    // warp 0 TMA, warp 1 MMA, warps 2.. epilogue
 
 __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, uint32_t bar, int c0,
                                             int c1) {
@@ -122,15 +124,23 @@ __device__ __forceinline__ void prefetch_tmap(const CUtensorMap* m) {
 
 __device__ __forceinline__ float gelu_erf(float x) { return 0.5f * x * (1.f + erff(x * 0.70710678118654752f)); }
 
+constexpr int kEpiRowBytes = 80;                               // 64 B of bf16 + 16 B pad
+constexpr int kEpiStageBytes = kEpiWarps * 32 * kEpiRowBytes;  // per warp: 32 rows x 32 columns
+
 template <int BN>
 __host__ __device__ constexpr int gemm_stages() {
-  return (196 * 1024) / ((kGemmBM + BN) * kGemmBK * 2) < 8 ? (196 * 1024) / ((kGemmBM + BN) * kGemmBK * 2) : 8;
+  return (192 * 1024) / ((kGemmBM + BN) * kGemmBK * 2) < 8 ? (192 * 1024) / ((kGemmBM + BN) * kGemmBK * 2) : 8;
 }
 template <int BN>
 __host__ __device__ constexpr int gemm_smem_bytes() {
-  return gemm_stages<BN>() * (kGemmBM + BN) * kGemmBK * 2 + 1024 /*align*/ + 256 /*barriers*/;
+  return gemm_stages<BN>() * (kGemmBM + BN) * kGemmBK * 2 + kEpiStageBytes + 1024 /*align*/ + 256 /*barriers*/;
 }
 
+// Persistent: CTA c takes tiles c, c + gridDim.x, ... of the live tile grid
+// (m-block major, n fastest, so concurrently running CTAs share A row
+// blocks in L2 and every CTA streams the L2-resident weights).  Two TMEM
+// accumulators (2 x BN columns): the epilogue of tile i overlaps the
+// mainloop of tile i + 1.
 template <typename T, int BN, int kEpi>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
@@ -141,81 +151,133 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
   const uint32_t base = (raw + 1023u) & ~1023u;  // SWIZZLE_128B atoms need 1024-B alignment
-  const uint32_t bars = base + kStages * kStageBytes;
+  const uint32_t stage_epi = base + kStages * kStageBytes;
+  const uint32_t bars = stage_epi + kEpiStageBytes;
   auto full = [&](int s) { return bars + 8u * (uint32_t)s; };
   auto empty = [&](int s) { return bars + 8u * (uint32_t)(kStages + s); };
-  const uint32_t tfull = bars + 8u * (uint32_t)(2 * kStages);
-  const uint32_t tslot = tfull + 8u;
+  auto tfull = [&](int a) { return bars + 8u * (uint32_t)(2 * kStages + a); };
+  auto tempty = [&](int a) { return bars + 8u * (uint32_t)(2 * kStages + 2 + a); };
+  const uint32_t tslot = bars + 8u * (uint32_t)(2 * kStages + 4);
   uint32_t* tslot_ptr = reinterpret_cast<uint32_t*>(smem_raw + (tslot - raw));
 
+  // Setup (barriers, TMEM, descriptor prefetch) runs before the PDL wait,
+  // overlapping the previous kernel's tail; the live row count is read after.
   pdl_launch_dependents();
-  pdl_wait_prerequisites();
-  const int m0 = blockIdx.x * kGemmBM, n0 = blockIdx.y * BN;
-  const int M = g.m_dev ? min(*g.m_dev, g.M_cap) : g.M_cap;
-  if (m0 >= M) return;  // uniform per CTA, before any barrier or TMEM use
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
       tc::mbar_init(full(s), 1);
       tc::mbar_init(empty(s), 1);
     }
-    tc::mbar_init(tfull, 1);
+    for (int a = 0; a < 2; ++a) {
+      tc::mbar_init(tfull(a), 1);
+      tc::mbar_init(tempty(a), kEpiWarps);  // one arrival per epilogue warp
+    }
     tc::fence_mbar_init();
     prefetch_tmap(&tmA);
     prefetch_tmap(&tmB);
   }
-  if (warp == 1) tc::alloc(tslot, BN);
+  if (warp == 1) tc::alloc(tslot, 2 * BN);
   tc::fence_before();
   __syncthreads();
   tc::fence_after();
   const uint32_t tmem = *tslot_ptr;
   const int nk = g.K / kGemmBK;
+  pdl_wait_prerequisites();
+  const int M = g.m_dev ? min(*g.m_dev, g.M_cap) : g.M_cap;
+  const int n_tiles = g.N / BN;
+  const int tiles = ((M + kGemmBM - 1) / kGemmBM) * n_tiles;  // CTAs >= tiles skip to teardown
 
   if (warp == 0) {
     if (lane == 0) {  // TMA producer
-      for (int kb = 0; kb < nk; ++kb) {
-        const int s = kb % kStages, r = kb / kStages;
-        if (r > 0) tc::mbar_wait(empty(s), (uint32_t)((r - 1) & 1));
-        const uint32_t sa = base + (uint32_t)s * kStageBytes;
-        mbar_expect_tx(full(s), kStageBytes);
-        tma_load_2d(sa, &tmA, full(s), kb * kGemmBK, m0);
-        tma_load_2d(sa + kABytes, &tmB, full(s), kb * kGemmBK, n0);
+      int it = 0;
+      for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+        const int m0 = (t / n_tiles) * kGemmBM, n0 = (t % n_tiles) * BN;
+        for (int kb = 0; kb < nk; ++kb, ++it) {
+          const int s = it % kStages, r = it / kStages;
+          if (r > 0) tc::mbar_wait(empty(s), (uint32_t)((r - 1) & 1));
+          const uint32_t sa = base + (uint32_t)s * kStageBytes;
+          mbar_expect_tx(full(s), kStageBytes);
+          tma_load_2d(sa, &tmA, full(s), kb * kGemmBK, m0);
+          tma_load_2d(sa + kABytes, &tmB, full(s), kb * kGemmBK, n0);
+        }
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {  // MMA issuer
       const uint32_t idesc = tc::idesc_f16(std::is_same<T, __half>::value ? 0u : 1u, kGemmBM, BN, 0u);
-      for (int kb = 0; kb < nk; ++kb) {
-        const int s = kb % kStages, r = kb / kStages;
-        tc::mbar_wait(full(s), (uint32_t)(r & 1));
+      int it = 0, i = 0;
+      for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++i) {
+        const int acc = i & 1, use = i >> 1;
+        if (use > 0) tc::mbar_wait(tempty(acc), (uint32_t)((use - 1) & 1));
         tc::fence_after();
-        const uint32_t sa = base + (uint32_t)s * kStageBytes, sb = sa + kABytes;
+        const uint32_t d = tmem + (uint32_t)(acc * BN);
+        for (int kb = 0; kb < nk; ++kb, ++it) {
+          const int s = it % kStages, r = it / kStages;
+          tc::mbar_wait(full(s), (uint32_t)(r & 1));
+          tc::fence_after();
+          const uint32_t sa = base + (uint32_t)s * kStageBytes, sb = sa + kABytes;
 #pragma unroll
-        for (int k = 0; k < kGemmBK / 16; ++k)
-          tc::mma_ss(tmem, tc::sw128_desc(sa + 32u * k), tc::sw128_desc(sb + 32u * k), idesc,
-                     (kb | k) != 0 ? 1u : 0u);
-        tc::commit(empty(s));  // frees the stage when these MMAs complete
+          for (int k = 0; k < kGemmBK / 16; ++k)
+            tc::mma_ss(d, tc::sw128_desc(sa + 32u * k), tc::sw128_desc(sb + 32u * k), idesc,
+                       (kb | k) != 0 ? 1u : 0u);
+          tc::commit(empty(s));  // frees the stage when these MMAs complete
+        }
+        tc::commit(tfull(acc));
       }
-      tc::commit(tfull);
     }
-  } else {  // epilogue: warp w reads TMEM lanes 32*(w % 4) .. +31 (one row per thread)
-    const int quad = warp & 3;
-    const long long row = (long long)m0 + 32 * quad + lane;
-    const bool live = row < M;
-    tc::mbar_wait(tfull, 0u);
-    tc::fence_after();
+  } else {
+    // Epilogue: warp w reads TMEM lanes 32*(w % 4) .. +31 (one row per
+    // thread); the two warps of a lane quadrant take alternate 32-column
+    // chunks.  Per chunk: residual row segment prefetched, TMEM -> registers,
+    // + bias (+ GELU | + residual) in fp32, one RNE rounding, bf16 staged in
+    // smem, then written back transposed (4 threads per 64-byte row segment).
+    const int quad = warp & 3, half = (warp - 2) >> 2;
+    uint8_t* stg = smem_raw + (stage_epi - raw) + (warp - 2) * 32 * kEpiRowBytes;
     const T* bias = static_cast<const T*>(g.bias);
-    const T* res = kEpi == 2 ? static_cast<const T*>(g.residual) + row * g.ldr + n0 : nullptr;
-    T* out = static_cast<T*>(g.out) + row * g.ldo + n0;
-#pragma unroll 1
-    for (int c = 0; c < BN; c += 32) {
-      uint32_t r[32];
-      tc::ld_x32(tmem + ((uint32_t)(32 * quad) << 16) + (uint32_t)c, r);
-      tc::wait_ld();
-      if (live) {
-        float acc[32];
+    int i = 0;
+    for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++i) {
+      const int acc = i & 1;
+      const int m0 = (t / n_tiles) * kGemmBM, n0 = (t % n_tiles) * BN;
+      const long long my_row = (long long)m0 + 32 * quad + lane;
+      const bool live = my_row < M;
+      // residual segments are independent of the accumulator: the first is
+      // fetched before waiting for it, each next one a chunk ahead.
+      const uint4* rrow = kEpi == 2 ? reinterpret_cast<const uint4*>(static_cast<const T*>(g.residual) +
+                                                                       my_row * g.ldr + n0)
+                                    : nullptr;
+      uint4 nres[4];
+      if constexpr (kEpi == 2) {
+        if (live) {
 #pragma unroll
-        for (int j = 0; j < 32; ++j) acc[j] = __uint_as_float(r[j]);
+          for (int q = 0; q < 4; ++q) nres[q] = rrow[(32 * half) / 8 + q];
+        }
+      }
+      tc::mbar_wait(tfull(acc), (uint32_t)((i >> 1) & 1));
+      tc::fence_after();
+      const uint32_t tbase = tmem + ((uint32_t)(32 * quad) << 16) + (uint32_t)(acc * BN);
+#pragma unroll 1
+      for (int c = 32 * half; c < BN; c += 64) {
+        uint4 res[4];
+        if constexpr (kEpi == 2) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) res[q] = nres[q];
+          if (live && c + 64 < BN) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) nres[q] = rrow[(c + 64) / 8 + q];
+          }
+        }
+        uint32_t r[32];
+        tc::ld_x32(tbase + (uint32_t)c, r);
+        tc::wait_ld();
+        if (c + 64 >= BN) {  // this warp's last chunk of the accumulator: hand it back
+          tc::fence_before();
+          __syncwarp();
+          if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tempty(acc)) : "memory");
+        }
+        float v[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
         if (bias != nullptr) {
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
@@ -224,37 +286,43 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
               const float2 f = unpack2<T>(wd[j]);
-              acc[8 * q + 2 * j] += f.x;
-              acc[8 * q + 2 * j + 1] += f.y;
+              v[8 * q + 2 * j] += f.x;
+              v[8 * q + 2 * j + 1] += f.y;
             }
           }
         }
         if constexpr (kEpi == 1) {
 #pragma unroll
-          for (int j = 0; j < 32; ++j) acc[j] = gelu_erf(acc[j]);
+          for (int j = 0; j < 32; ++j) v[j] = gelu_erf(v[j]);
         }
         if constexpr (kEpi == 2) {
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
-            const uint4 u = *reinterpret_cast<const uint4*>(res + c + 8 * q);
-            const uint32_t wd[4] = {u.x, u.y, u.z, u.w};
+            const uint32_t wd[4] = {res[q].x, res[q].y, res[q].z, res[q].w};
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
               const float2 f = unpack2<T>(wd[j]);
-              acc[8 * q + 2 * j] += f.x;
-              acc[8 * q + 2 * j + 1] += f.y;
+              v[8 * q + 2 * j] += f.x;
+              v[8 * q + 2 * j + 1] += f.y;
             }
           }
         }
+        uint8_t* my = stg + lane * kEpiRowBytes;
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          uint4 u;
-          u.x = pack2<T>(acc[8 * q + 0], acc[8 * q + 1]);
-          u.y = pack2<T>(acc[8 * q + 2], acc[8 * q + 3]);
-          u.z = pack2<T>(acc[8 * q + 4], acc[8 * q + 5]);
-          u.w = pack2<T>(acc[8 * q + 6], acc[8 * q + 7]);
-          st_global_16(out + c + 8 * q, u);
+        for (int q = 0; q < 4; ++q)
+          *reinterpret_cast<uint4*>(my + 16 * q) =
+              make_uint4(pack2<T>(v[8 * q], v[8 * q + 1]), pack2<T>(v[8 * q + 2], v[8 * q + 3]),
+                         pack2<T>(v[8 * q + 4], v[8 * q + 5]), pack2<T>(v[8 * q + 6], v[8 * q + 7]));
+        __syncwarp();
+        const int part = lane & 3;
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+          const int rr = 8 * h + (lane >> 2);
+          const long long row = (long long)m0 + 32 * quad + rr;
+          const uint4 o = *reinterpret_cast<const uint4*>(stg + rr * kEpiRowBytes + 16 * part);
+          if (row < M) st_global_16(static_cast<T*>(g.out) + row * g.ldo + n0 + c + 8 * part, o);
         }
+        __syncwarp();  // staging is rewritten by the next chunk
       }
     }
   }
@@ -262,7 +330,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   __syncthreads();
   if (warp == 1) {
     tc::fence_after();
-    tc::dealloc(tmem, BN);
+    tc::dealloc(tmem, 2 * BN);
   }
 }
 
@@ -353,7 +421,12 @@ static cudaError_t launch_gemm_t(const CUtensorMap& ta, const CUtensorMap& tb, c
     if (e != cudaSuccess) return e;
     done[dev] = true;
   }
-  const dim3 grid((g.M_cap + kGemmBM - 1) / kGemmBM, g.N / BN);
+  // Persistent grid sized for the capacity; CTAs beyond the live tile count exit at once.
+  const long long tiles = (long long)((g.M_cap + kGemmBM - 1) / kGemmBM) * (g.N / BN);
+  static int sms[64] = {0};
+  if (dev >= 0 && dev < 64 && sms[dev] == 0) cudaDeviceGetAttribute(&sms[dev], cudaDevAttrMultiProcessorCount, dev);
+  const int nsm = (dev >= 0 && dev < 64 && sms[dev] > 0) ? sms[dev] : 148;
+  const dim3 grid((unsigned)(tiles < nsm ? tiles : nsm));
   return launch_pdl_b(gemm_tc_kernel<T, BN, kEpi>, grid, dim3(kGemmThreads), gemm_smem_bytes<BN>(), st, ta, tb,
                       g);
 }
@@ -366,14 +439,30 @@ static cudaError_t launch_gemm_bn(const CUtensorMap& ta, const CUtensorMap& tb, 
   return launch_gemm_t<T, BN, 0>(ta, tb, g, st);
 }
 
-// Tile width: the widest of {256, 128, 64} dividing N that still gives at
-// least one CTA per SM, else 64 (more CTAs for small GEMMs).
+// Tile width from {256, 128, 64} (dividing N) minimising the estimated time
+// rounds * (BN + 64): rounds of the persistent grid over the full-capacity
+// tile count, the +64 standing for per-tile fixed cost (epilogue drain,
+// pipeline refill) in units of N columns.
 int gemm_pick_bn(int M_cap, int N, int sms) {
-  const int mt = (M_cap + kGemmBM - 1) / kGemmBM;
-  for (int bn : {256, 128}) {
-    if (N % bn == 0 && (long long)mt * (N / bn) >= sms) return bn;
+  static const int forced = [] {
+    const char* e = getenv("RAGGED_GEMM_BN");  // tuning experiments only
+    return e ? atoi(e) : 0;
+  }();
+  if ((forced == 64 || forced == 128 || forced == 256) && N % forced == 0) return forced;
+  const long long mt = (M_cap + kGemmBM - 1) / kGemmBM;
+  int best = 64;
+  long long best_cost = -1;
+  for (int bn : {256, 128, 64}) {
+    if (N % bn != 0) continue;
+    const long long tiles = mt * (N / bn);
+    const long long rounds = (tiles + sms - 1) / sms;
+    const long long cost = rounds * (bn + 64);
+    if (best_cost < 0 || cost < best_cost) {
+      best_cost = cost;
+      best = bn;
+    }
   }
-  return N % 128 == 0 && N < 128 ? 128 : 64;
+  return best;
 }
 
 cudaError_t launch_gemm(int dtype, const void* a, long long lda, const void* w, const GemmArgs& g, int epi,
