@@ -90,8 +90,8 @@ __global__ void __launch_bounds__(3 * kTcSlotThreads, 1) attn_tc_kernel(const At
     tc::mbar_init(smem_u32(&bars[1]), 1);  // single-tile path: P V done
     tc::mbar_init(smem_u32(&bars[2]), 1);  // pair path: tile A (S_{j+1} ready, P_j V_j done)
     tc::mbar_init(smem_u32(&bars[3]), 1);  // pair path: tile B
-    tc::mbar_init(smem_u32(&bars[4]), 4);  // pair path: P of tile A stored (one arrival per warp)
-    tc::mbar_init(smem_u32(&bars[5]), 4);  // pair path: P of tile B stored
+    bars[4] = 0ull;  // pair path: warps that stored P of tile A (atomic count, mod 4)
+    bars[5] = 0ull;  // pair path: same for tile B
     tc::fence_mbar_init();
   }
   tc::fence_before();
@@ -107,8 +107,7 @@ __global__ void __launch_bounds__(3 * kTcSlotThreads, 1) attn_tc_kernel(const At
   uint32_t ph_s = 0, ph_o = 0;
   const uint32_t bar_x = smem_u32(&bars[2]);  // pair path: tile X uses bar_x + 8 X
   uint32_t ph_x[2] = {0u, 0u};                // pair path: per-tile barrier parities
-  const uint32_t bar_p = smem_u32(&bars[4]);  // pair path: "P of tile X ready" = bar_p + 8 X
-  uint32_t ph_p[2] = {0u, 0u};                // (waited by the issuing thread only)
+  const uint32_t cnt_p = smem_u32(&bars[4]);  // pair path: P-stored counter of tile X at cnt_p + 8 X
   constexpr uint32_t kFmt = std::is_same<T, __nv_bfloat16>::value ? 1u : 0u;
   const uint32_t idesc_o = tc::idesc_f16(kFmt, kTcTile, kHeadDim, 1);
   constexpr float kScaleLog2 = 0.18033688011112042f;  // log2(e) / sqrt(64)
@@ -213,17 +212,17 @@ __global__ void __launch_bounds__(3 * kTcSlotThreads, 1) attn_tc_kernel(const At
         tc::fence_after();
         if (pr == 0 && cu_here && tid == 0) write_cu();
         if (pr == 0) TL(3);
+        if (pr == 0 && slot == 0) PT(0);
         float mm[2][2], ll[2][2];
 #pragma unroll
         for (int X = 0; X < 2; ++X) mm[X][0] = mm[X][1] = -INFINITY, ll[X][0] = ll[X][1] = 0.f;
+        // descriptors advance by bytes >> 4: a 64-row block of 128-byte rows = +512
+        const uint64_t qd0 = tc::sw128_desc(smem_u32(sQ)), kd0 = tc::sw128_desc(smem_u32(sK));
+        const uint64_t vd0 = tc::sw128_desc(smem_u32(sV));
         auto issue_s = [&](int X, int jj) {  // S of tile X, chunk jj
           const int kc = min(kTcChunk, n16 - jj * kTcChunk);
-          const uint64_t qd = tc::sw128_desc(smem_u32(sQ) + X * kTcTile * kRowBytes);
-          const uint64_t kd = tc::sw128_desc(smem_u32(sK) + jj * kTcChunk * kRowBytes);
-          const uint32_t idesc_s = tc::idesc_f16(kFmt, kTcTile, kc, 0);
-          const uint32_t d = tS + ((uint32_t)(16 * X) << 16);
-#pragma unroll
-          for (int kk = 0; kk < 4; ++kk) tc::mma_ss(d, qd + 2 * kk, kd + 2 * kk, idesc_s, kk > 0);
+          tc::mma_ss_k64(tS + ((uint32_t)(16 * X) << 16), qd0 + 512ull * (uint64_t)X, kd0 + 512ull * (uint64_t)jj,
+                         tc::idesc_f16(kFmt, kTcTile, kc, 0));
         };
         if (tid == 0) {
           for (int X = 0; X < ntl; ++X) {
@@ -237,6 +236,7 @@ __global__ void __launch_bounds__(3 * kTcSlotThreads, 1) attn_tc_kernel(const At
             ph_x[X] ^= 1u;
             tc::fence_after();
             if (pr == 0 && j == 0 && X == 0) TL(5);
+            if (pr == 0 && slot == 0 && j < 4) PT(1 + 6 * j + 3 * X);
             const int rowsX = X ? rowsB : rowsA;
             if (warp * 16 < rowsX) {  // this warp owns real rows of tile X
               const uint32_t tSx = tS + lane_off + ((uint32_t)(16 * X) << 16);
@@ -311,28 +311,29 @@ __global__ void __launch_bounds__(3 * kTcSlotThreads, 1) attn_tc_kernel(const At
               tc::st_16x128b_x8(tSx + 32, lo);
               tc::wait_st();
             }
-            // hand-off: each warp arrives once its P rows are stored; only the issuing
-            // thread waits, the other warps go straight on to the other tile
+            if (pr == 0 && slot == 0 && j < 4) PT(2 + 6 * j + 3 * X);
+            // hand-off without waiting: each warp counts itself in once its P rows
+            // are stored; the LAST warp to arrive issues P_j V_j (+ S_{j+1}) and
+            // commits, so no warp ever blocks on the others' softmax and the
+            // warps go straight on to the other tile.
             tc::fence_before();
             __syncwarp();
+            uint32_t prev = 0;
             if ((tid & 31) == 0) {
-              asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar_p + 8u * (uint32_t)X)
+              asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], 1;"
+                           : "=r"(prev)
+                           : "r"(cnt_p + 8u * (uint32_t)X)
                            : "memory");
             }
-            if (tid == 0) {  // P_j V_j for tile X, then S_{j+1} behind it; one commit covers both
-              tc::mbar_wait(bar_p + 8u * (uint32_t)X, ph_p[X]);
-              ph_p[X] ^= 1u;
+            prev = __shfl_sync(0xffffffffu, prev, 0);
+            if ((prev & 3u) == 3u && (tid & 31) == 0) {  // P_j V_j for tile X, then S_{j+1} behind it
               tc::fence_after();
               const int nk = (min(kTcChunk, n - j * kTcChunk) + 15) >> 4;
-              const uint32_t pa = tS + ((uint32_t)(16 * X) << 16);
-              const uint32_t od = tO + ((uint32_t)(16 * X) << 16);
-              for (int kk = 0; kk < nk; ++kk) {
-                const uint64_t vd = tc::sw128_desc(smem_u32(sV) + (j * kTcChunk + kk * 16) * kRowBytes);
-                tc::mma_ts(od, pa + kk * 8, vd, idesc_o, (j > 0 || kk > 0) ? 1u : 0u);
-                tc::mma_ts(od, pa + 32 + kk * 8, vd, idesc_o, 1u);
-              }
+              tc::mma_ts_pv(tO + ((uint32_t)(16 * X) << 16), tS + ((uint32_t)(16 * X) << 16),
+                            vd0 + 512ull * (uint64_t)j, idesc_o, nk, j > 0 ? 1u : 0u);
               if (j + 1 < nchunks) issue_s(X, j + 1);
               tc::commit(bar_x + 8u * (uint32_t)X);
+              if (pr == 0 && slot == 0 && j < 4) PT(3 + 6 * j + 3 * X);
             }
           }
         }
@@ -343,6 +344,7 @@ __global__ void __launch_bounds__(3 * kTcSlotThreads, 1) attn_tc_kernel(const At
         }
         tc::fence_after();
         if (pr == 0) TL(9);
+        if (pr == 0 && slot == 0) PT(25);
         // epilogue: both tiles' O rows -> 16 bit -> SMEM (sQ is free) -> row stores
         for (int X = 0; X < ntl; ++X) {
           const int rowsX = X ? rowsB : rowsA;
@@ -373,6 +375,8 @@ __global__ void __launch_bounds__(3 * kTcSlotThreads, 1) attn_tc_kernel(const At
         }
         sync();  // sQ, TMEM reused by the next pair / problem
         if (pr == 0) TL(6);
+        if (pr == 0 && slot == 0) PT(26);
+        if (pr == 1 && slot == 0) PT(27);
       }
     };
     if (n > kTcTile) run_pairs();
@@ -406,11 +410,8 @@ __global__ void __launch_bounds__(3 * kTcSlotThreads, 1) attn_tc_kernel(const At
         // ---- S_j = Q K_j^T: 4 UMMA of K = 16 (+32 B along the SW128 rows each)
         if (tid == 0) {
           tc::fence_after();
-          const uint64_t qd = tc::sw128_desc(smem_u32(sQ));
-          const uint64_t kd = tc::sw128_desc(smem_u32(sK) + j * kTcChunk * kRowBytes);
-          const uint32_t idesc_s = tc::idesc_f16(kFmt, kTcTile, kc, 0);
-#pragma unroll
-          for (int kk = 0; kk < 4; ++kk) tc::mma_ss(tS, qd + 2 * kk, kd + 2 * kk, idesc_s, kk > 0);
+          tc::mma_ss_k64(tS, tc::sw128_desc(smem_u32(sQ)), tc::sw128_desc(smem_u32(sK)) + 512ull * (uint64_t)j,
+                         tc::idesc_f16(kFmt, kTcTile, kc, 0));
           tc::commit(bar_s);
         }
         tc::mbar_wait(bar_s, ph_s);
@@ -497,11 +498,8 @@ __global__ void __launch_bounds__(3 * kTcSlotThreads, 1) attn_tc_kernel(const At
         if (tid == 0) {
           tc::fence_after();
           const int nk = (min(kTcChunk, n - j * kTcChunk) + 15) >> 4;
-          for (int kk = 0; kk < nk; ++kk) {
-            const uint64_t vd = tc::sw128_desc(smem_u32(sV) + (j * kTcChunk + kk * 16) * kRowBytes);
-            tc::mma_ts(tO, tS + kk * 8, vd, idesc_o, (j > 0 || kk > 0) ? 1u : 0u);
-            tc::mma_ts(tO, tS + 32 + kk * 8, vd, idesc_o, 1u);
-          }
+          tc::mma_ts_pv(tO, tS, tc::sw128_desc(smem_u32(sV)) + 512ull * (uint64_t)j, idesc_o, nk,
+                        j > 0 ? 1u : 0u);
           tc::commit(bar_o);
         }
         tc::mbar_wait(bar_o, ph_o);  // before S_{j+1} overwrites P_j, and before the epilogue

@@ -51,9 +51,20 @@ __device__ __forceinline__ void tl_stamp(int slot) {
   }
 }
 #define TL(slot) tl_stamp(slot)
+// pair-path probe (tcgen05 engine, n > 64): clock64 of slot 0, thread 0, pass 0
+constexpr int kPtSlots = 32;
+__device__ unsigned long long g_pairs_tl[kTlMaxCtas * kPtSlots];
+#define PT(i)                                                                              \
+  do {                                                                                     \
+    if (threadIdx.x == 0 && blockIdx.x < kTlMaxCtas && (i) < kPtSlots)                     \
+      g_pairs_tl[blockIdx.x * kPtSlots + (i)] = clock64();                                 \
+  } while (0)
 #else
 #define TL(slot) \
   do {           \
+  } while (0)
+#define PT(i) \
+  do {        \
   } while (0)
 #endif
 
@@ -1083,6 +1094,10 @@ int fused_smem_bytes(int N) { return attn_smem_bytes(N); }
 int timeline_copy(void* host, int max_ctas) {
   const int n = max_ctas < kTlMaxCtas ? max_ctas : kTlMaxCtas;
   return cudaMemcpyFromSymbol(host, g_timeline, (size_t)n * kTlSlots * 8) == cudaSuccess ? n : -1;
+}
+int pairs_timeline_copy(void* host, int max_ctas) {
+  const int n = max_ctas < kTlMaxCtas ? max_ctas : kTlMaxCtas;
+  return cudaMemcpyFromSymbol(host, g_pairs_tl, (size_t)n * kPtSlots * 8) == cudaSuccess ? n : -1;
 }
 int timeline_clear() {
   void* p = nullptr;

@@ -59,6 +59,7 @@ cudaError_t launch_keep_topk_l2(int dtype, const void* x, long long ld, int B, i
 int fused_smem_bytes(int N);
 #ifdef RAGGED_TIMELINE
 int timeline_copy(void* host, int max_ctas);
+int pairs_timeline_copy(void* host, int max_ctas);
 int timeline_clear();
 #endif
 

@@ -58,6 +58,79 @@ __device__ __forceinline__ void mma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_
       "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate));
 }
 
+// ---- issue bursts with precomputed operands --------------------------------
+// Small UMMAs cost ~50 cycles of tensor pipe each (scripts/micro/umma_issue.cu),
+// but the single issuing thread pays for every dependent ALU op between them
+// (a descriptor rebuild + predicate per UMMA measured ~130-210 cycles per UMMA):
+// these helpers issue back-to-back with operands computed up front.
+
+// D = A B over K = 64: 4 UMMAs of K = 16, descriptors +2 (32 B) per step; the
+// first overwrites D.
+__device__ __forceinline__ void mma_ss_k64(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc) {
+  asm volatile(
+      "{\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %4, %5, %3, 1;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %6, %7, %3, 1;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %8, %9, %3, 1;\n\t"
+      "}\n" ::"r"(d),
+      "l"(a), "l"(b), "r"(idesc), "l"(a + 2ull), "l"(b + 2ull), "l"(a + 4ull), "l"(b + 4ull), "l"(a + 6ull),
+      "l"(b + 6ull));
+}
+
+// O (+)= P V over nk (1..4) steps of 16 keys: P hi at TMEM column pa + 8k, P lo
+// at pa + 32 + 8k (two 16-bit values per column), V rows +16 per step (SW128
+// MN-major: +2048 B = +128 in the descriptor).  acc = 0 overwrites O.
+__device__ __forceinline__ void mma_ts_pv(uint32_t o, uint32_t pa, uint64_t vd, uint32_t idesc, int nk,
+                                          uint32_t acc) {
+  switch (nk) {
+    case 4:
+      asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %3, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%8], %4, %1, p;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%9], %4, %1, 1;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%10], %5, %1, 1;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%11], %5, %1, 1;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%12], %6, %1, 1;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%13], %6, %1, 1;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%14], %7, %1, 1;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%15], %7, %1, 1;\n\t"
+      "}\n"
+      ::"r"(o), "r"(idesc), "r"(pa), "r"(acc), "l"(vd + 0ull), "l"(vd + 128ull), "l"(vd + 256ull), "l"(vd + 384ull), "r"(pa + 0u), "r"(pa + 32u), "r"(pa + 8u), "r"(pa + 40u), "r"(pa + 16u), "r"(pa + 48u), "r"(pa + 24u), "r"(pa + 56u));
+      break;
+    case 3:
+      asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %3, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%7], %4, %1, p;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%8], %4, %1, 1;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%9], %5, %1, 1;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%10], %5, %1, 1;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%11], %6, %1, 1;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%12], %6, %1, 1;\n\t"
+      "}\n"
+      ::"r"(o), "r"(idesc), "r"(pa), "r"(acc), "l"(vd + 0ull), "l"(vd + 128ull), "l"(vd + 256ull), "r"(pa + 0u), "r"(pa + 32u), "r"(pa + 8u), "r"(pa + 40u), "r"(pa + 16u), "r"(pa + 48u));
+      break;
+    case 2:
+      asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %3, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%6], %4, %1, p;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%7], %4, %1, 1;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%8], %5, %1, 1;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%9], %5, %1, 1;\n\t"
+      "}\n"
+      ::"r"(o), "r"(idesc), "r"(pa), "r"(acc), "l"(vd + 0ull), "l"(vd + 128ull), "r"(pa + 0u), "r"(pa + 32u), "r"(pa + 8u), "r"(pa + 40u));
+      break;
+    default:
+      asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %3, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%5], %4, %1, p;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%6], %4, %1, 1;\n\t"
+      "}\n"
+      ::"r"(o), "r"(idesc), "r"(pa), "r"(acc), "l"(vd + 0ull), "r"(pa + 0u), "r"(pa + 32u));
+      break;
+  }
+}
+
 // Arrive on an mbarrier when all previously issued tcgen05 ops of this thread complete.
 __device__ __forceinline__ void commit(uint32_t bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
