@@ -728,7 +728,50 @@ def extras(args, rb, torch, dev, sets, c, B, N, H, dt, T):
         out["n1_block"] = n1_block_extras(rb, torch, dev, dt)
     except Exception as ex:
         out["n1_block"] = {"error": repr(ex)[:300]}
+    try:
+        out["n4_general_attn"] = n4_general_extras(rb, torch, dev, dt)
+    except Exception as ex:
+        out["n4_general_attn"] = {"error": repr(ex)[:300]}
     return out
+
+
+def n4_general_extras(rb, torch, dev, dt):
+    """NEXT row N4: ragged_attn beyond DeiT (attn_general.cu): longer sequences
+    (K/V streamed, Alg. 1's outer loops) and other head dims; FA2 varlen on the
+    same packed buffers for context.  Roofline: HBM bytes 4*T*H*d*2 and tensor
+    flops 4*sum(n^2)*d*H (hi+lo PV executes 1.5x that)."""
+    import numpy as np
+    import synth
+    res = {}
+    cases = [("vit_l16_384_B8_N577_H16_d64_p0", 8, 577, 16, 64, 0.0),
+             ("vit_l16_384_B8_N577_H16_d64_p0.7", 8, 577, 16, 64, 0.7),
+             ("seq1024_B8_H12_d64_p0.5", 8, 1024, 12, 64, 0.5),
+             ("deit_shape_B32_N197_H6_d128_p0.8", 32, 197, 6, 128, 0.8),
+             ("B32_N197_H8_d80_p0.5", 32, 197, 8, 80, 0.5),
+             ("B32_N197_H24_d32_p0.5", 32, 197, 24, 32, 0.5)]
+    for name, B, N, H, d, p in cases:
+        q, k, v = synth.activations(B, N, H, d, dt, seed=1)
+        keep = synth.mask_random(B, N, synth.kept_tokens(N, p), seed=1001)
+        keep_t = torch.from_numpy(keep)
+        idx = torch.nonzero(keep_t.view(-1)).view(-1)
+        lens = keep.sum(1).astype(np.int64)
+        cu = torch.from_numpy(np.concatenate([[0], np.cumsum(lens)]).astype(np.int32)).to(dev)
+        T = int(lens.sum())
+        qp, kp, vp = (t.reshape(B * N, H, d)[idx].contiguous().to(dev) for t in (q, k, v))
+        op = torch.empty_like(qp)
+        us = _graph_time(torch, [lambda: rb.attn(qp, kp, vp, cu, N, op=op)], 100)
+        flops = 4.0 * float((lens.astype(np.float64) ** 2).sum()) * d * H
+        hbm = 4.0 * T * H * d * 2
+        r = {"T": T, "us": us, "tflops": flops / us / 1e6, "hbm_GBps": hbm / us / 1e3}
+        try:
+            from flash_attn import flash_attn_varlen_func
+            nmax = int(lens.max())
+            r["fa2_varlen_us"] = _graph_time(torch, [lambda: flash_attn_varlen_func(qp, kp, vp, cu, cu, nmax, nmax)],
+                                             100)
+        except Exception as ex:
+            r["fa2_varlen_error"] = repr(ex)[:120]
+        res[name] = r
+    return res
 
 
 def n1_block_extras(rb, torch, dev, dt):

@@ -107,6 +107,11 @@ RAGGED_API ragged_status ragged_pack(const ragged_problem* prob, const uint8_t* 
  *   op[s:s+n, h, :] = softmax(qp[s:s+n,h,:] kp[s:s+n,h,:]^T / sqrt(d)) vp[s:s+n,h,:]
  * bidirectional, no dropout, no KV cache.  One CTA per (image,
  * head) pair, head fastest (pid -> h = pid mod H, i = pid / H).
+ * Shapes: the DeiT path takes d = 64, N <= 256 (one-stage K/V in shared
+ * memory).  Other shapes (NEXT row N4) run a streaming kernel: d in {32, 64,
+ * 80, 128} and N up to 2^20, K/V in 64-key chunks with Alg. 1's online
+ * softmax; rows are prob->ld elements apart as below, op rows
+ * H*d apart.  Other d -> RAGGED_ENOTSUP.
  * Input rows of qp/kp/vp are prob->ld elements apart (H*d for three packed
  * [cap, H, d] buffers; 3*H*d for one packed qkv buffer [cap, 3, H, d] with
  * kp = qp + H*d, vp = qp + 2*H*d -- the N1 block's qkv GEMM output); op rows

@@ -33,21 +33,27 @@ ragged_status cuda_fail(cudaError_t e, const char* where) {
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
-// Shape / dtype / stride checks shared by every entry point.
-ragged_status check_problem(const ragged_problem* p) {
+// Shape / dtype / stride checks shared by every entry point.  `general`
+// (ragged_attn only, NEXT row N4): N up to 2^20 and d in {32, 64, 80, 128}.
+ragged_status check_problem(const ragged_problem* p, bool general = false) {
   if (p == nullptr) return fail(RAGGED_EINVAL, "problem is NULL");
   if (p->B < 0) return fail(RAGGED_EINVAL, "B < 0");
   if (p->N < 1) return fail(RAGGED_EINVAL, "N < 1");
   if (p->H < 1) return fail(RAGGED_EINVAL, "H < 1");
-  if (p->N > 256) return fail(RAGGED_ENOTSUP, "N > 256 (one-stage sequence cap, DESIGN.md R12)");
-  if (p->d != 64) return fail(RAGGED_ENOTSUP, "head_dim must be 64 (P:330-331)");
+  if (general) {
+    if (p->N > (1 << 20)) return fail(RAGGED_ENOTSUP, "N > 2^20");
+    if (!ragged::attn_general_supports(p->d)) return fail(RAGGED_ENOTSUP, "head_dim must be 32, 64, 80 or 128");
+  } else {
+    if (p->N > 256) return fail(RAGGED_ENOTSUP, "N > 256 (one-stage sequence cap, DESIGN.md R12)");
+    if (p->d != 64) return fail(RAGGED_ENOTSUP, "head_dim must be 64 (P:330-331)");
+  }
   if (p->dtype != RAGGED_BF16 && p->dtype != RAGGED_FP16)
     return fail(RAGGED_ENOTSUP, "dtype must be RAGGED_BF16 or RAGGED_FP16");
   if (p->engine != RAGGED_ENGINE_AUTO && p->engine != RAGGED_ENGINE_MMA_SYNC &&
       p->engine != RAGGED_ENGINE_TCGEN05)
     return fail(RAGGED_ENOTSUP, "unknown engine");
   if ((long long)p->B * p->N > 0x7fffffffLL) return fail(RAGGED_ENOTSUP, "B*N exceeds int32 indices");
-  if ((long long)p->H * 64 > (1LL << 22)) return fail(RAGGED_ENOTSUP, "H*d > 2^22");
+  if ((long long)p->H * p->d > (1LL << 22)) return fail(RAGGED_ENOTSUP, "H*d > 2^22");
   if (p->ld > (1LL << 22)) return fail(RAGGED_ENOTSUP, "ld > 2^22 elements");
   if (p->ld < (int64_t)p->H * p->d) return fail(RAGGED_EINVAL, "ld < H*d");
   if (p->ld % 8 != 0) return fail(RAGGED_EALIGN, "ld % 8 != 0 (rows must be 16-byte aligned)");
@@ -136,7 +142,7 @@ ragged_status ragged_pack(const ragged_problem* prob, const uint8_t* keep, const
 
 ragged_status ragged_attn(const ragged_problem* prob, const void* qp, const void* kp,
                           const void* vp, const int32_t* cu_seqlens, void* op, void* stream) {
-  RAGGED_TRY(check_problem(prob));
+  RAGGED_TRY(check_problem(prob, true));
   if (prob->B == 0) return RAGGED_OK;
   RAGGED_TRY(check_ptr(qp, "qp"));
   RAGGED_TRY(check_ptr(kp, "kp"));
@@ -144,6 +150,13 @@ ragged_status ragged_attn(const ragged_problem* prob, const void* qp, const void
   RAGGED_TRY(check_ptr_any(cu_seqlens, "cu_seqlens"));
   RAGGED_TRY(check_ptr(op, "op"));
   if ((long long)prob->B * prob->H > 0x7fffffffLL) return fail(RAGGED_ENOTSUP, "B*H too large");
+  if (prob->N > 256 || prob->d != 64) {  // NEXT row N4: the streaming kernel (attn_general.cu)
+    if ((long long)prob->B * prob->H * ((prob->N + 63) / 64) > 0x7fffffffLL)
+      return fail(RAGGED_ENOTSUP, "too many query blocks");
+    cudaError_t e = ragged::launch_attn_general(prob->dtype, prob->d, qp, kp, vp, cu_seqlens, op, prob->B,
+                                                prob->N, prob->H, prob->ld, as_stream(stream));
+    return e == cudaSuccess ? RAGGED_OK : cuda_fail(e, "ragged_attn/general");
+  }
   cudaError_t e = ragged::launch_attn(prob->dtype, resolve_engine(prob), qp, kp, vp, cu_seqlens, op, prob->B, prob->N,
                                       prob->H, prob->ld, as_stream(stream));
   return e == cudaSuccess ? RAGGED_OK : cuda_fail(e, "ragged_attn");

@@ -38,6 +38,11 @@ cudaError_t launch_attn_gather(int dtype, const void* qp, const void* kp, const 
                                const GatherArgs& g, cudaStream_t st);
 cudaError_t launch_empty(int grid, int block, cudaStream_t st);
 
+// ---- NEXT row N4 (attn_general.cu): d in {32, 64, 80, 128}, any N ----
+bool attn_general_supports(int d);
+cudaError_t launch_attn_general(int dtype, int d, const void* qp, const void* kp, const void* vp, const int32_t* cu,
+                                void* op, int B, int N, int H, long long ld, cudaStream_t st);
+
 // ---- NEXT row N1 (block.cu) ----
 struct GemmArgs {
   const void* bias;        // [N] or null

@@ -159,6 +159,20 @@ def test_product_package_does_not_import_oracle():
                 assert "oracle" not in re.sub(r"#.*|//.*", "", txt).replace("oracle/", ""), f
 
 
+def test_general_attn_validation():
+    """ragged_attn's widened shapes (NEXT row N4) pass validation; the fused /
+    pack / unpack paths keep the DeiT caps."""
+    L = rb.lib()
+    for d in (32, 80, 128):
+        p = rb.problem(0, 1000, 4, d=d)
+        assert L.ragged_attn(ctypes.byref(p), None, None, None, None, None, None) == rb.OK
+    assert L.ragged_attn(ctypes.byref(rb.problem(0, 197, 4, d=96)), None, None, None, None, None, None) == rb.ENOTSUP
+    assert L.ragged_attn(ctypes.byref(rb.problem(0, (1 << 20) + 1, 1)), None, None, None, None, None,
+                         None) == rb.ENOTSUP
+    assert _call_fused(rb.problem(0, 300, 4)) == rb.ENOTSUP
+    assert _call_fused(rb.problem(0, 197, 4, d=128)) == rb.ENOTSUP
+
+
 def test_block_validation():
     """ragged_block.h host-checkable errors (no CUDA call)."""
     L = rb.lib()

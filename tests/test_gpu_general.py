@@ -1,0 +1,96 @@
+"""GPU parity of NEXT row N4 (csrc/attn_general.cu): ragged_attn for head dims
+d in {32, 64, 80, 128} and sequences longer than the one-stage cap (N > 256),
+against the fp64 oracle (oracle.attention, which is shape-generic).  Same
+tolerance as the DeiT path (R2): max-abs <= 2e-3 (bf16) / 5e-4 (fp16) with
+V ~ U(-1, 1), plus the secondary bound ulp(|ref|) + 2^-12 max|V|."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+from helpers import TOL, check_attention, to_np
+
+rb = pytest.importorskip("paper_2604_15408_b200")
+pytestmark = pytest.mark.gpu
+DEV = "cuda"
+DT = {"bf16": torch.bfloat16, "fp16": torch.float16}
+
+
+def _packed_case(lengths, H, d, dt, seed, dist="standard"):
+    lengths = np.asarray(lengths)
+    B, N = len(lengths), max(1, int(lengths.max()))
+    q, k, v = synth.activations(B, N, H, d, DT[dt], seed, dist)
+    keep = np.zeros((B, N), np.uint8)
+    for b, n in enumerate(lengths):
+        keep[b, :n] = 1
+    cu, _, src = oracle.scan(keep)
+    T = int(cu[-1])
+    flat = lambda t: t.reshape(B * N, H, d)[torch.from_numpy(src[:T])]  # noqa: E731
+    qp, kp, vp = (flat(t) for t in (q, k, v))
+    return qp, kp, vp, cu, N, T
+
+
+@pytest.mark.parametrize("d", [32, 64, 80, 128])
+@pytest.mark.parametrize("dt", ["bf16", "fp16"])
+def test_general_head_dims(d, dt):
+    lengths = [197, 1, 0, 63, 64, 65, 130, 39, 256]
+    H = 3
+    qp, kp, vp, cu, N, T = _packed_case(lengths, H, d, dt, seed=d)
+    cud = torch.from_numpy(cu.astype(np.int32)).to(DEV)
+    got = rb.attn(qp.to(DEV), kp.to(DEV), vp.to(DEV), cud, N)
+    torch.cuda.synchronize()
+    ref = oracle.attention(qp, kp, vp, cu)
+    check_attention(to_np(got[:T]), ref, DT[dt])
+
+
+@pytest.mark.parametrize("dt", ["bf16", "fp16"])
+def test_general_long_sequences(dt):
+    """N > 256: Alg. 1's K/V streaming (ViT-L/16 @ 384: 577 tokens; 1000; a
+    ragged mix)."""
+    lengths = [577, 1000, 300, 257, 5]
+    qp, kp, vp, cu, N, T = _packed_case(lengths, 2, 64, dt, seed=7)
+    got = rb.attn(qp.to(DEV), kp.to(DEV), vp.to(DEV), torch.from_numpy(cu.astype(np.int32)).to(DEV), N)
+    torch.cuda.synchronize()
+    check_attention(to_np(got[:T]), oracle.attention(qp, kp, vp, cu), DT[dt])
+
+
+@pytest.mark.parametrize("dist", ["peaked", "heavy"])
+def test_general_distributions(dist):
+    lengths = [400, 77, 129]
+    qp, kp, vp, cu, N, T = _packed_case(lengths, 2, 128, "bf16", seed=9, dist=dist)
+    got = rb.attn(qp.to(DEV), kp.to(DEV), vp.to(DEV), torch.from_numpy(cu.astype(np.int32)).to(DEV), N)
+    torch.cuda.synchronize()
+    vmax = float(vp.abs().max()) if dist == "heavy" else None
+    check_attention(to_np(got[:T]), oracle.attention(qp, kp, vp, cu), torch.bfloat16, vmax=vmax, dist=dist)
+
+
+def test_general_strided_qkv_and_untouched_rows():
+    """Packed qkv buffer [cap, 3, H, d] (row stride 3*H*d), d = 80; output rows
+    past cu[B] keep their contents."""
+    lengths = [300, 45, 0, 260]
+    H, d = 2, 80
+    qp, kp, vp, cu, N, T = _packed_case(lengths, H, d, "bf16", seed=11)
+    cap = T + 37
+    qkv = torch.zeros(cap, 3, H, d, dtype=torch.bfloat16)
+    qkv[:T, 0], qkv[:T, 1], qkv[:T, 2] = qp, kp, vp
+    qkv = qkv.to(DEV)
+    op = torch.full((cap, H, d), 7.0, dtype=torch.bfloat16, device=DEV)
+    rb.attn(qkv[:, 0], qkv[:, 1], qkv[:, 2], torch.from_numpy(cu.astype(np.int32)).to(DEV), N, op=op)
+    torch.cuda.synchronize()
+    check_attention(to_np(op[:T]), oracle.attention(qp, kp, vp, cu), torch.bfloat16)
+    assert (op[T:] == 7.0).all()
+
+
+def test_general_deterministic_and_isolated():
+    lengths = [333, 90]
+    qp, kp, vp, cu, N, T = _packed_case(lengths, 2, 128, "bf16", seed=13)
+    cud = torch.from_numpy(cu.astype(np.int32)).to(DEV)
+    a = rb.attn(qp.to(DEV), kp.to(DEV), vp.to(DEV), cud, N)
+    b = rb.attn(qp.to(DEV), kp.to(DEV), vp.to(DEV), cud, N)
+    kp2 = kp.clone()
+    kp2[333:] += 1.0                       # perturb image 1 only
+    c = rb.attn(qp.to(DEV), kp2.to(DEV), vp.to(DEV), cud, N)
+    torch.cuda.synchronize()
+    assert torch.equal(a.view(torch.int16), b.view(torch.int16))
+    assert torch.equal(a[:333].view(torch.int16), c[:333].view(torch.int16))
