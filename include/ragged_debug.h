@@ -20,6 +20,8 @@ __attribute__((visibility("default"))) int32_t ragged_debug_timeline_clear(void)
 /* clock64 stamps of the tcgen05 pair path (slot 0, thread 0, first pass):
  * 32 x uint64 per CTA (scripts/pairs_probe.py documents the slots). */
 __attribute__((visibility("default"))) int32_t ragged_debug_pairs_timeline(void* host, int32_t max_ctas);
+/* %globaltimer stamps of the tcgen05 GEMM (8 x uint64 per CTA, block.cu GT slots). */
+__attribute__((visibility("default"))) int32_t ragged_debug_gemm_timeline(void* host, int32_t max_ctas);
 #endif
 #ifdef __cplusplus
 }

@@ -485,6 +485,9 @@ int32_t ragged_debug_timeline_clear(void) { return ragged::timeline_clear(); }
 int32_t ragged_debug_pairs_timeline(void* host, int32_t max_ctas) {
   return ragged::pairs_timeline_copy(host, max_ctas);
 }
+int32_t ragged_debug_gemm_timeline(void* host, int32_t max_ctas) {
+  return ragged::gemm_timeline_copy(host, max_ctas);
+}
 #endif
 
 const char* ragged_build_info(void) {

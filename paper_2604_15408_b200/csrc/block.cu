@@ -103,6 +103,28 @@ __global__ void __launch_bounds__(kLnThreads) layer_norm_kernel(const T* __restr
 }
 
 // ------------------------------------------------------------------ GEMM ----
+// Optional per-CTA probe (timeline debug build only): %globaltimer at
+// 0 entry, 1 after setup, 2 after the PDL wait, 3 first stage landed (MMA
+// thread), 4 first tile's last MMA issued, 5 first tile's accumulator ready
+// (epilogue), 6 first tile stored, 7 exit.
+#ifdef RAGGED_TIMELINE
+constexpr int kGtSlots = 8;
+__device__ unsigned long long g_gemm_tl[1024 * kGtSlots];
+#define GT(i)                                                        \
+  do {                                                               \
+    unsigned long long _t;                                           \
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(_t));           \
+    if (blockIdx.x < 1024) g_gemm_tl[blockIdx.x * kGtSlots + (i)] = _t; \
+  } while (0)
+int gemm_timeline_copy(void* host, int max_ctas) {
+  const int n = max_ctas < 1024 ? max_ctas : 1024;
+  return cudaMemcpyFromSymbol(host, g_gemm_tl, (size_t)n * kGtSlots * 8) == cudaSuccess ? n : -1;
+}
+#else
+#define GT(i) \
+  do {        \
+  } while (0)
+#endif
 constexpr int kGemmBM = 128, kGemmBK = 64;
 constexpr int kEpiWarps = 8;                         // two per TMEM lane quadrant
 constexpr int kGemmThreads = 64 + 32 * kEpiWarps;    // warp 0 TMA, warp 1 MMA, warps 2.. epilogue
@@ -164,6 +186,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   // overlapping the previous kernel's tail; the live row count is read after.
   pdl_launch_dependents();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) GT(0);
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
       tc::mbar_init(full(s), 1);
@@ -183,7 +206,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   tc::fence_after();
   const uint32_t tmem = *tslot_ptr;
   const int nk = g.K / kGemmBK;
+  if (threadIdx.x == 0) GT(1);
   pdl_wait_prerequisites();
+  if (threadIdx.x == 0) GT(2);
   const int M = g.m_dev ? min(*g.m_dev, g.M_cap) : g.M_cap;
   const int n_tiles = g.N / BN;
   const int tiles = ((M + kGemmBM - 1) / kGemmBM) * n_tiles;  // CTAs >= tiles skip to teardown
@@ -206,6 +231,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   } else if (warp == 1) {
     if (lane == 0) {  // MMA issuer
       const uint32_t idesc = tc::idesc_f16(std::is_same<T, __half>::value ? 0u : 1u, kGemmBM, BN, 0u);
+      const uint64_t adesc0 = tc::sw128_desc(base), bdesc0 = tc::sw128_desc(base + kABytes);
       int it = 0, i = 0;
       for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++i) {
         const int acc = i & 1, use = i >> 1;
@@ -216,14 +242,14 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           const int s = it % kStages, r = it / kStages;
           tc::mbar_wait(full(s), (uint32_t)(r & 1));
           tc::fence_after();
-          const uint32_t sa = base + (uint32_t)s * kStageBytes, sb = sa + kABytes;
-#pragma unroll
-          for (int k = 0; k < kGemmBK / 16; ++k)
-            tc::mma_ss(d, tc::sw128_desc(sa + 32u * k), tc::sw128_desc(sb + 32u * k), idesc,
-                       (kb | k) != 0 ? 1u : 0u);
+          if (it == 0) GT(3);
+          // one burst of 4 UMMAs with precomputed descriptors (stage offset >> 4)
+          const uint64_t soff = (uint64_t)((s * kStageBytes) >> 4);
+          tc::mma_ss_k64_acc(d, adesc0 + soff, bdesc0 + soff, idesc, kb != 0 ? 1u : 0u);
           tc::commit(empty(s));  // frees the stage when these MMAs complete
         }
         tc::commit(tfull(acc));
+        if (i == 0) GT(4);
       }
     }
   } else {
@@ -255,6 +281,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       }
       tc::mbar_wait(tfull(acc), (uint32_t)((i >> 1) & 1));
       tc::fence_after();
+      if (i == 0 && warp == 2 && lane == 0) GT(5);
       const uint32_t tbase = tmem + ((uint32_t)(32 * quad) << 16) + (uint32_t)(acc * BN);
 #pragma unroll 1
       for (int c = 32 * half; c < BN; c += 64) {
@@ -324,6 +351,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         }
         __syncwarp();  // staging is rewritten by the next chunk
       }
+      if (i == 0 && warp == 2 && lane == 0) GT(6);
     }
   }
   tc::fence_before();
@@ -332,6 +360,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     tc::fence_after();
     tc::dealloc(tmem, 2 * BN);
   }
+  if (threadIdx.x == 0) GT(7);
 }
 
 // ------------------------------------------------------------- launchers ----

@@ -65,6 +65,7 @@ int fused_smem_bytes(int N);
 #ifdef RAGGED_TIMELINE
 int timeline_copy(void* host, int max_ctas);
 int pairs_timeline_copy(void* host, int max_ctas);
+int gemm_timeline_copy(void* host, int max_ctas);
 int timeline_clear();
 #endif
 

@@ -78,6 +78,20 @@ __device__ __forceinline__ void mma_ss_k64(uint32_t d, uint64_t a, uint64_t b, u
       "l"(b + 6ull));
 }
 
+// D (+)= A B over K = 64 with a runtime accumulate flag for the first step
+// (GEMM k-blocks after the first accumulate).
+__device__ __forceinline__ void mma_ss_k64_acc(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %10, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %4, %5, %3, 1;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %6, %7, %3, 1;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %8, %9, %3, 1;\n\t"
+      "}\n" ::"r"(d),
+      "l"(a), "l"(b), "r"(idesc), "l"(a + 2ull), "l"(b + 2ull), "l"(a + 4ull), "l"(b + 4ull), "l"(a + 6ull),
+      "l"(b + 6ull), "r"(acc));
+}
+
 // O (+)= P V over nk (1..4) steps of 16 keys: P hi at TMEM column pa + 8k, P lo
 // at pa + 32 + 8k (two 16-bit values per column), V rows +16 per step (SW128
 // MN-major: +2048 B = +128 in the descriptor).  acc = 0 overwrites O.

@@ -1,3 +1,1 @@
-for c in "2 12 0.8 1 host" "3 6 0.5 2 host" "2 12 0.8 1 host_long" "3 6 0.5 2 host_long" "2 12 0.8 1 sleep_default"; do
-  timeout 120 python scripts/dbg/gather_cases.py $c 2>&1 | grep CASE
-done > gpurun_out/dbg.log
+for c in "1248 2304 768 0" "1248 768 3072 2" "6304 2304 768 0" "50000 2304 768 0"; do timeout 120 python scripts/gemm_probe.py $c; done > gpurun_out/gemm_probe.txt 2>&1
