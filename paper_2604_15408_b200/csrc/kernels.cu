@@ -709,7 +709,8 @@ __global__ void __launch_bounds__(kAttnThreads, 3) attn_kernel(const AttnArgs a,
         }
       }
       // scale to log2 units, mask key columns >= n (R4), row max over the quad
-      float mx0 = -INFINITY, mx1 = -INFINITY;
+      // (tree reductions: short dependency chains, the warp has little else to hide them)
+      float t0[8], t1[8];
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
 #pragma unroll
@@ -718,9 +719,17 @@ __global__ void __launch_bounds__(kAttnThreads, 3) attn_kernel(const AttnArgs a,
           const float val = (j < nt && col < n) ? s[j][e] * kScaleLog2 : -INFINITY;
           s[j][e] = val;
         }
-        mx0 = fmaxf(mx0, fmaxf(s[j][0], s[j][1]));
-        mx1 = fmaxf(mx1, fmaxf(s[j][2], s[j][3]));
+        t0[j] = fmaxf(s[j][0], s[j][1]);
+        t1[j] = fmaxf(s[j][2], s[j][3]);
       }
+#pragma unroll
+      for (int w = 4; w > 0; w >>= 1)
+#pragma unroll
+        for (int j = 0; j < w; ++j) {
+          t0[j] = fmaxf(t0[j], t0[j + w]);
+          t1[j] = fmaxf(t1[j], t1[j + w]);
+        }
+      float mx0 = t0[0], mx1 = t1[0];
       mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 1));
       mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 2));
       mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 1));
@@ -750,12 +759,21 @@ __global__ void __launch_bounds__(kAttnThreads, 3) attn_kernel(const AttnArgs a,
           s[j][1] = ex2(s[j][1] - mn0);
           s[j][2] = ex2(s[j][2] - mn1);
           s[j][3] = ex2(s[j][3] - mn1);
-          l0 += s[j][0] + s[j][1];
-          l1 += s[j][2] + s[j][3];
         } else {
           s[j][0] = s[j][1] = s[j][2] = s[j][3] = 0.f;
         }
+        t0[j] = s[j][0] + s[j][1];
+        t1[j] = s[j][2] + s[j][3];
       }
+#pragma unroll
+      for (int w = 4; w > 0; w >>= 1)
+#pragma unroll
+        for (int j = 0; j < w; ++j) {
+          t0[j] += t0[j + w];
+          t1[j] += t1[j + w];
+        }
+      l0 += t0[0];
+      l1 += t1[0];
       // O += P_hi V + P_lo V
 #ifdef RAGGED_ABLATE_PV
       const int nk = 0;
