@@ -1,0 +1,10 @@
+# Round-end validation: GPU tests, smoke, full bench, ncu launch list + full capture of the fused kernel.
+NCU=/usr/local/cuda/bin/ncu
+timeout 1200 python -m pytest tests -m gpu -q 2>&1 | tail -3 > gpurun_out/final_pytest.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/final_smoke.log 2>&1
+timeout 1500 python bench.py > gpurun_out/final_bench.json 2> gpurun_out/final_bench.err
+timeout 600 $NCU --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/final_launches.csv \
+  python bench.py --steps 2 --warmup 1 --no-extras --gather-variants none > /dev/null 2>&1
+timeout 600 $NCU --set full --clock-control none --import-source on -k regex:attn_kernel -s 4 -c 2 \
+  -o gpurun_out/final_prof_fused -f python scripts/prof_kernels.py --config C3 --what fused --iters 8 > /dev/null 2>&1
+echo done > gpurun_out/final_done.txt
