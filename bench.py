@@ -858,6 +858,15 @@ def n1_block_extras(rb, torch, dev, dt):
     us = _graph_time(torch, [pipeline], 20)
     res["layers5_12_p0.8"] = {"us_per_batch": us, "images_per_s": B / us * 1e6,
                               "note": "pack once + 8 packed blocks, B=32 DeiT-B, synthetic weights"}
+    # dispatch study for the block pipeline (paper protocol, host-synced medians):
+    # 56 eager launches through the C ABI vs one ragged_vit_pipeline_graph launch
+    pipeline()
+    torch.cuda.synchronize()
+    gr = rb.VitPipelineGraph(blocks, xp, cu)
+    res["layers5_12_host_sync_us"] = {
+        "eager_8_blocks": _host_time(torch, lambda: [bl(xp, cu) for bl in blocks], warm=5, iters=100),
+        "one_graph_launch": _host_time(torch, gr.launch, warm=5, iters=100)}
+    gr.close()
     return res
 
 

@@ -81,6 +81,20 @@ RAGGED_API ragged_status ragged_vit_block(const ragged_problem* prob, void* x, c
                                           const ragged_vit_weights* w, void* workspace, int64_t ws_bytes,
                                           void* stream);
 
+/* Layers 5-12 as one replayable unit (P:364-367 and the paper's thesis that
+ * dispatch, not arithmetic, bounds ViT-length work): capture
+ * `layers` consecutive ragged_vit_block calls on the same packed rows x and
+ * cu_seqlens (weights[i] for layer i) into a CUDA graph; every launch of the
+ * returned handle replays all 7*layers kernels with one host call.  Pointers
+ * are fixed at creation; the workspace (>= ragged_vit_block_workspace,
+ * zero-initialised) is shared by the layers.  Destroy with
+ * ragged_graph_destroy (ragged.h); launch with ragged_graph_launch. */
+RAGGED_API ragged_status ragged_vit_pipeline_graph_create(const ragged_problem* prob, void* x,
+                                                          const int32_t* cu_seqlens,
+                                                          const ragged_vit_weights* weights, int32_t layers,
+                                                          void* workspace, int64_t ws_bytes,
+                                                          ragged_graph** out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -110,6 +110,7 @@ def _load() -> ctypes.CDLL:
         "ragged_layer_norm": [I32, I32, I32, V, I64, V, V, ctypes.c_float, V, I64, V, V],
         "ragged_linear": [I32, I32, I32, I32, V, I64, V, V, I32, V, I64, V, I64, V, V],
         "ragged_vit_block": [P, V, V, ctypes.POINTER(VitWeights), V, I64, V],
+        "ragged_vit_pipeline_graph_create": [P, V, V, ctypes.POINTER(VitWeights), I32, V, I64, ctypes.POINTER(V)],
     }
     for name, args in sigs.items():
         f = getattr(lib, name)
@@ -134,7 +135,8 @@ EXPORTS = ("ragged_scan", "ragged_pack", "ragged_attn", "ragged_unpack", "ragged
            "ragged_graph_create", "ragged_graph_launch", "ragged_graph_destroy", "ragged_empty_launch",
            "ragged_validate_cu_seqlens", "ragged_status_str", "ragged_last_error", "ragged_build_info",
            "ragged_keep_topk_l2", "ragged_pack_attend_unpack_gather", "ragged_attn_gather",
-           "ragged_layer_norm", "ragged_linear", "ragged_vit_block_workspace", "ragged_vit_block")
+           "ragged_layer_norm", "ragged_linear", "ragged_vit_block_workspace", "ragged_vit_block",
+           "ragged_vit_pipeline_graph_create")
 
 
 def lib() -> ctypes.CDLL:
@@ -367,6 +369,37 @@ class VitBlock:
         _check(lib().ragged_vit_block(ctypes.byref(self.p), x.data_ptr(), cu.data_ptr(), ctypes.byref(self.w),
                                      self.ws.data_ptr(), self.ws.numel(), _stream(stream)), "ragged_vit_block")
         return x
+
+
+class VitPipelineGraph:
+    """ragged_vit_pipeline_graph_create: `len(blocks)` packed blocks (VitBlock
+    objects sharing B, N, H, dtype) captured as one replayable graph over the
+    fixed buffers x [B*N, D] and cu [B+1]; launch() replays every layer."""
+
+    def __init__(self, blocks, x, cu):
+        b0 = blocks[0]
+        self._refs = (blocks, x, cu)
+        arr = (VitWeights * len(blocks))(*[bl.w for bl in blocks])
+        self._arr = arr
+        h = ctypes.c_void_p()
+        _check(lib().ragged_vit_pipeline_graph_create(ctypes.byref(b0.p), x.data_ptr(), cu.data_ptr(), arr,
+                                                     len(blocks), b0.ws.data_ptr(), b0.ws.numel(),
+                                                     ctypes.byref(h)), "ragged_vit_pipeline_graph_create")
+        self._h = h
+
+    def launch(self, stream=None):
+        _check(lib().ragged_graph_launch(self._h, _stream(stream)), "ragged_graph_launch")
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().ragged_graph_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 class Graph:

@@ -464,6 +464,47 @@ ragged_status ragged_vit_block(const ragged_problem* prob, void* x, const int32_
   return RAGGED_OK;
 }
 
+ragged_status ragged_vit_pipeline_graph_create(const ragged_problem* prob, void* x, const int32_t* cu_seqlens,
+                                               const ragged_vit_weights* weights, int32_t layers, void* workspace,
+                                               int64_t ws_bytes, ragged_graph** out) {
+  if (out == nullptr) return fail(RAGGED_EINVAL, "out is NULL");
+  *out = nullptr;
+  if (weights == nullptr) return fail(RAGGED_EINVAL, "weights is NULL");
+  if (layers < 1 || layers > 1024) return fail(RAGGED_EINVAL, "layers not in 1..1024");
+  cudaStream_t st = nullptr;
+  cudaError_t e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+  if (e != cudaSuccess) return cuda_fail(e, "ragged_vit_pipeline_graph_create/stream");
+  ragged_graph* g = new ragged_graph();
+  e = cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal);
+  if (e != cudaSuccess) {
+    cudaStreamDestroy(st);
+    delete g;
+    return cuda_fail(e, "ragged_vit_pipeline_graph_create/begin");
+  }
+  ragged_status s = RAGGED_OK;
+  for (int32_t i = 0; i < layers && s == RAGGED_OK; ++i)
+    s = ragged_vit_block(prob, x, cu_seqlens, weights + i, workspace, ws_bytes, st);
+  e = cudaStreamEndCapture(st, &g->graph);
+  cudaStreamDestroy(st);
+  if (s != RAGGED_OK) {
+    if (g->graph) cudaGraphDestroy(g->graph);
+    delete g;
+    return s;
+  }
+  if (e != cudaSuccess) {
+    delete g;
+    return cuda_fail(e, "ragged_vit_pipeline_graph_create/end");
+  }
+  e = cudaGraphInstantiate(&g->exec, g->graph, 0);
+  if (e != cudaSuccess) {
+    cudaGraphDestroy(g->graph);
+    delete g;
+    return cuda_fail(e, "ragged_vit_pipeline_graph_create/instantiate");
+  }
+  *out = g;
+  return RAGGED_OK;
+}
+
 const char* ragged_status_str(ragged_status s) {
   switch (s) {
     case RAGGED_OK: return "RAGGED_OK";

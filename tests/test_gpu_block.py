@@ -239,3 +239,33 @@ def test_vit_block_empty_images_and_all_dropped():
         if T:
             _check_block(to_np(xd[:T]), oracle.vit_block(x, cu, params, H, store=store(dtype)),
                          oracle.vit_block(x, cu, params, H))
+
+
+def test_vit_pipeline_graph_equals_eager():
+    """ragged_vit_pipeline_graph_create: 3 layers replayed as one graph give
+    the same bits as 3 eager ragged_vit_block calls."""
+    dtype = torch.bfloat16
+    B, N = 6, 197
+    pr = synth.PRESETS["deit_small"]
+    D, H, MLP = pr["D"], pr["H"], pr["MLP"]
+    keep = synth.make_inputs(B, N, H, 0.7, "l2", "bf16", seed=21)[3].numpy()
+    cu, _, _ = oracle.scan(keep)
+    T = int(cu[-1])
+    cud = torch.from_numpy(cu.astype(np.int32)).to(DEV)
+    blocks = [rb.VitBlock({k: v.to(DEV) for k, v in synth.vit_weights(D, MLP, dtype, 30 + L).items()}, B, N, H, dtype)
+              for L in range(3)]
+    x0 = torch.zeros(B * N, D, dtype=dtype, device=DEV)
+    x0[:T] = synth.packed_rows(T, D, dtype, 21).to(DEV)
+    xe = x0.clone()
+    for bl in blocks:
+        bl(xe, cud)
+    xg = x0.clone()
+    g = rb.VitPipelineGraph(blocks, xg, cud)
+    g.launch()
+    torch.cuda.synchronize()
+    assert (bits(xe) == bits(xg)).all()
+    xg.copy_(x0)
+    g.launch()                                   # replays are repeatable
+    torch.cuda.synchronize()
+    assert (bits(xe) == bits(xg)).all()
+    g.close()
