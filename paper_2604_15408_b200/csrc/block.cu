@@ -126,8 +126,16 @@ int gemm_timeline_copy(void* host, int max_ctas) {
   } while (0)
 #endif
 constexpr int kGemmBM = 128, kGemmBK = 64;
-constexpr int kEpiWarps = 8;                         // two per TMEM lane quadrant
-constexpr int kGemmThreads = 64 + 32 * kEpiWarps;    // warp 0 TMA, warp 1 MMA, warps 2.. epilogue
+// Epilogue warps: 8 (two per TMEM lane quadrant), 16 for the GELU epilogue
+// whose erf evaluation is issue-bound; warp 0 TMA, warp 1 MMA.
+template <int kEpi>
+__host__ __device__ constexpr int epi_warps() {
+  return kEpi == 1 ? 16 : 8;
+}
+template <int kEpi>
+__host__ __device__ constexpr int gemm_threads() {
+  return 64 + 32 * epi_warps<kEpi>();
+}
 
 __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, uint32_t bar, int c0,
                                             int c1) {
@@ -147,15 +155,21 @@ __device__ __forceinline__ void prefetch_tmap(const CUtensorMap* m) {
 __device__ __forceinline__ float gelu_erf(float x) { return 0.5f * x * (1.f + erff(x * 0.70710678118654752f)); }
 
 constexpr int kEpiRowBytes = 80;                               // 64 B of bf16 + 16 B pad
-constexpr int kEpiStageBytes = kEpiWarps * 32 * kEpiRowBytes;  // per warp: 32 rows x 32 columns
-
-template <int BN>
-__host__ __device__ constexpr int gemm_stages() {
-  return (192 * 1024) / ((kGemmBM + BN) * kGemmBK * 2) < 8 ? (192 * 1024) / ((kGemmBM + BN) * kGemmBK * 2) : 8;
+template <int kEpi>
+__host__ __device__ constexpr int epi_stage_bytes() {  // per warp: 32 rows x 32 columns
+  return epi_warps<kEpi>() * 32 * kEpiRowBytes;
 }
-template <int BN>
+
+template <int BN, int kEpi>
+__host__ __device__ constexpr int gemm_stages() {
+  return (226 * 1024 - epi_stage_bytes<kEpi>() - 1280) / ((kGemmBM + BN) * kGemmBK * 2) < 8
+             ? (226 * 1024 - epi_stage_bytes<kEpi>() - 1280) / ((kGemmBM + BN) * kGemmBK * 2)
+             : 8;
+}
+template <int BN, int kEpi>
 __host__ __device__ constexpr int gemm_smem_bytes() {
-  return gemm_stages<BN>() * (kGemmBM + BN) * kGemmBK * 2 + kEpiStageBytes + 1024 /*align*/ + 256 /*barriers*/;
+  return gemm_stages<BN, kEpi>() * (kGemmBM + BN) * kGemmBK * 2 + epi_stage_bytes<kEpi>() + 1024 /*align*/ +
+         256 /*barriers*/;
 }
 
 // Persistent: CTA c takes tiles c, c + gridDim.x, ... of the live tile grid
@@ -164,10 +178,12 @@ __host__ __device__ constexpr int gemm_smem_bytes() {
 // accumulators (2 x BN columns): the epilogue of tile i overlaps the
 // mainloop of tile i + 1.
 template <typename T, int BN, int kEpi>
-__global__ void __launch_bounds__(kGemmThreads, 1)
+__global__ void __launch_bounds__(gemm_threads<kEpi>(), 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const GemmArgs g) {
-  constexpr int kStages = gemm_stages<BN>();
+  constexpr int kStages = gemm_stages<BN, kEpi>();
+  constexpr int kEpiWarps = epi_warps<kEpi>();
+  constexpr int kEpiStageBytes = epi_stage_bytes<kEpi>();
   constexpr uint32_t kABytes = kGemmBM * kGemmBK * 2, kBBytes = BN * kGemmBK * 2;
   constexpr uint32_t kStageBytes = kABytes + kBBytes;
   extern __shared__ uint8_t smem_raw[];
@@ -258,6 +274,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     // chunks.  Per chunk: residual row segment prefetched, TMEM -> registers,
     // + bias (+ GELU | + residual) in fp32, one RNE rounding, bf16 staged in
     // smem, then written back transposed (4 threads per 64-byte row segment).
+    constexpr int kEp = kEpiWarps / 4;  // warps per TMEM lane quadrant: alternate 32-column chunks
     const int quad = warp & 3, half = (warp - 2) >> 2;
     uint8_t* stg = smem_raw + (stage_epi - raw) + (warp - 2) * 32 * kEpiRowBytes;
     const T* bias = static_cast<const T*>(g.bias);
@@ -276,28 +293,32 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       if constexpr (kEpi == 2) {
         if (live) {
 #pragma unroll
-          for (int q = 0; q < 4; ++q) nres[q] = rrow[(32 * half) / 8 + q];
+          for (int q = 0; q < 4; ++q) nres[q] = rrow[(32 * half) / 8 + q];  // half = this warp's first chunk
         }
       }
       tc::mbar_wait(tfull(acc), (uint32_t)((i >> 1) & 1));
       tc::fence_after();
       if (i == 0 && warp == 2 && lane == 0) GT(5);
+      if (32 * half >= BN) {  // no chunk for this warp at this tile width: just count in
+        if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tempty(acc)) : "memory");
+        continue;
+      }
       const uint32_t tbase = tmem + ((uint32_t)(32 * quad) << 16) + (uint32_t)(acc * BN);
 #pragma unroll 1
-      for (int c = 32 * half; c < BN; c += 64) {
+      for (int c = 32 * half; c < BN; c += 32 * kEp) {
         uint4 res[4];
         if constexpr (kEpi == 2) {
 #pragma unroll
           for (int q = 0; q < 4; ++q) res[q] = nres[q];
-          if (live && c + 64 < BN) {
+          if (live && c + 32 * kEp < BN) {
 #pragma unroll
-            for (int q = 0; q < 4; ++q) nres[q] = rrow[(c + 64) / 8 + q];
+            for (int q = 0; q < 4; ++q) nres[q] = rrow[(c + 32 * kEp) / 8 + q];
           }
         }
         uint32_t r[32];
         tc::ld_x32(tbase + (uint32_t)c, r);
         tc::wait_ld();
-        if (c + 64 >= BN) {  // this warp's last chunk of the accumulator: hand it back
+        if (c + 32 * kEp >= BN) {  // this warp's last chunk of the accumulator: hand it back
           tc::fence_before();
           __syncwarp();
           if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tempty(acc)) : "memory");
@@ -446,7 +467,7 @@ static cudaError_t launch_gemm_t(const CUtensorMap& ta, const CUtensorMap& tb, c
   cudaGetDevice(&dev);
   if (dev >= 0 && dev < 64 && !done[dev]) {
     cudaError_t e = cudaFuncSetAttribute(gemm_tc_kernel<T, BN, kEpi>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         gemm_smem_bytes<BN>());
+                                         gemm_smem_bytes<BN, kEpi>());
     if (e != cudaSuccess) return e;
     done[dev] = true;
   }
@@ -456,7 +477,8 @@ static cudaError_t launch_gemm_t(const CUtensorMap& ta, const CUtensorMap& tb, c
   if (dev >= 0 && dev < 64 && sms[dev] == 0) cudaDeviceGetAttribute(&sms[dev], cudaDevAttrMultiProcessorCount, dev);
   const int nsm = (dev >= 0 && dev < 64 && sms[dev] > 0) ? sms[dev] : 148;
   const dim3 grid((unsigned)(tiles < nsm ? tiles : nsm));
-  return launch_pdl_b(gemm_tc_kernel<T, BN, kEpi>, grid, dim3(kGemmThreads), gemm_smem_bytes<BN>(), st, ta, tb,
+  return launch_pdl_b(gemm_tc_kernel<T, BN, kEpi>, grid, dim3(gemm_threads<kEpi>()), gemm_smem_bytes<BN, kEpi>(), st,
+                      ta, tb,
                       g);
 }
 
