@@ -262,9 +262,9 @@ __global__ void __launch_bounds__(kScanThreads, 1)
       }
     }
     // cu[b] at every image boundary b*N inside [p0, p0 + 16)
-    if (p0 < total) {
-      long long b = (p0 + N - 1) / N;
-      for (long long pos = b * N; pos < p0 + kScanRun && pos < total; pos += N, ++b)
+    if (p0 < total) {  // (B*N < 2^31, validated): 32-bit division
+      int b = (int)(((unsigned)p0 + (unsigned)N - 1u) / (unsigned)N);
+      for (long long pos = (long long)b * N; pos < p0 + kScanRun && pos < total; pos += N, ++b)
         cu[b] = excl + __popc(flags & ((1u << (int)(pos - p0)) - 1u));
     }
     __syncthreads();
@@ -278,9 +278,13 @@ __global__ void __launch_bounds__(kScanThreads, 1)
 // Gather form over packed rows r < T = cu[B] (read on the device): each row
 // is 3 tensors x (H*d*2 / 16) 16-byte chunks; a grid-stride loop over rows in
 // groups of kPackRows, U chunks in flight per thread.
-constexpr int kCopyThreads = 256;
-constexpr int kPackRows = 4;
-constexpr int kCopyUnroll = 4;
+// One warp per row: lane l moves the row's 16-byte chunks l, l + 32, ... of
+// all three tensors, every load of the row in flight before its stores; the
+// row's index is one broadcast load.  (Replaces a 4-rows-per-CTA flat loop:
+// fewer dependent index loads and integer divisions per byte moved.)
+constexpr int kCopyThreads = 256;              // 8 warps, one row each per step
+constexpr int kCopyWarps = kCopyThreads / 32;
+constexpr int kCopyU = 3;                      // chunks per lane per tensor per pass
 
 __global__ void __launch_bounds__(kCopyThreads)
     pack_kernel(const uint8_t* __restrict__ q, const uint8_t* __restrict__ k,
@@ -289,70 +293,65 @@ __global__ void __launch_bounds__(kCopyThreads)
                 uint8_t* __restrict__ vp, int B, long long ld_bytes, int row_bytes) {
   pdl_launch_dependents();
   pdl_wait_prerequisites();
+  const int lane = threadIdx.x & 31;
   const int T = cu[B];
   const int cpr = row_bytes >> 4;  // chunks per tensor row
-  const int per_row = 3 * cpr;
-  for (long long r0 = (long long)blockIdx.x * kPackRows; r0 < T;
-       r0 += (long long)gridDim.x * kPackRows) {
-    const int rows = (int)(kPackRows < (T - r0) ? (long long)(kPackRows) : (long long)(T - r0));
-    const int total = rows * per_row;
-    for (int f0 = threadIdx.x; f0 < total; f0 += kCopyThreads * kCopyUnroll) {
-      uint4 val[kCopyUnroll];
-      uint8_t* dptr[kCopyUnroll];
+  for (long long r = (long long)blockIdx.x * kCopyWarps + (threadIdx.x >> 5); r < T;
+       r += (long long)gridDim.x * kCopyWarps) {
+    const long long so = (long long)src[r] * ld_bytes;
+    const long long dof = r * row_bytes;
+    for (int c0 = 0; c0 < cpr; c0 += 32 * kCopyU) {
+      uint4 vq[kCopyU], vk[kCopyU], vv[kCopyU];
 #pragma unroll
-      for (int u = 0; u < kCopyUnroll; ++u) {
-        const int f = f0 + u * kCopyThreads;
-        dptr[u] = nullptr;
-        if (f < total) {
-          const int rl = f / per_row, rem = f - rl * per_row;
-          const int t = rem / cpr, c = rem - t * cpr;
-          const long long r = r0 + rl;
-          const long long s = src[r];
-          const uint8_t* g = t == 0 ? q : (t == 1 ? k : v);
-          uint8_t* p = t == 0 ? qp : (t == 1 ? kp : vp);
-          val[u] = ld_global_nc_16(g + s * ld_bytes + c * 16);
-          dptr[u] = p + r * row_bytes + c * 16;
+      for (int u = 0; u < kCopyU; ++u) {
+        const int c = c0 + lane + 32 * u;
+        if (c < cpr) {
+          vq[u] = ld_global_nc_16(q + so + c * 16);
+          vk[u] = ld_global_nc_16(k + so + c * 16);
+          vv[u] = ld_global_nc_16(v + so + c * 16);
         }
       }
 #pragma unroll
-      for (int u = 0; u < kCopyUnroll; ++u)
-        if (dptr[u]) st_global_16(dptr[u], val[u]);
+      for (int u = 0; u < kCopyU; ++u) {
+        const int c = c0 + lane + 32 * u;
+        if (c < cpr) {
+          st_global_16(qp + dof + c * 16, vq[u]);
+          st_global_16(kp + dof + c * 16, vk[u]);
+          st_global_16(vp + dof + c * 16, vv[u]);
+        }
+      }
     }
   }
 }
 
 // -------------------------------------------------------------- unpack ----
-constexpr int kUnpackRows = 4;
+// One warp per padded row: a kept row copies packed row dst[i], a dropped
+// row (dst = -1) writes +0.0.
+constexpr int kUnpackU = 4;
 
 __global__ void __launch_bounds__(kCopyThreads)
     unpack_kernel(const uint8_t* __restrict__ op, const int32_t* __restrict__ dst,
                   uint8_t* __restrict__ o, long long BN, int row_bytes) {
   pdl_launch_dependents();
   pdl_wait_prerequisites();
+  const int lane = threadIdx.x & 31;
   const int cpr = row_bytes >> 4;
-  for (long long r0 = (long long)blockIdx.x * kUnpackRows; r0 < BN;
-       r0 += (long long)gridDim.x * kUnpackRows) {
-    const int rows = (int)(kUnpackRows < (BN - r0) ? (long long)(kUnpackRows) : (long long)(BN - r0));
-    const int total = rows * cpr;
-    for (int f0 = threadIdx.x; f0 < total; f0 += kCopyThreads * kCopyUnroll) {
-      uint4 val[kCopyUnroll];
-      uint8_t* dptr[kCopyUnroll];
+  for (long long i = (long long)blockIdx.x * kCopyWarps + (threadIdx.x >> 5); i < BN;
+       i += (long long)gridDim.x * kCopyWarps) {
+    const int j = dst[i];
+    const long long so = (long long)j * row_bytes, dof = i * row_bytes;
+    for (int c0 = 0; c0 < cpr; c0 += 32 * kUnpackU) {
+      uint4 val[kUnpackU];
 #pragma unroll
-      for (int u = 0; u < kCopyUnroll; ++u) {
-        const int f = f0 + u * kCopyThreads;
-        dptr[u] = nullptr;
-        if (f < total) {
-          const int rl = f / cpr, c = f - rl * cpr;
-          const long long i = r0 + rl;
-          const int j = dst[i];
-          val[u] = j >= 0 ? ld_global_nc_16(op + (long long)j * row_bytes + c * 16)
-                          : make_uint4(0u, 0u, 0u, 0u);
-          dptr[u] = o + i * row_bytes + c * 16;
-        }
+      for (int u = 0; u < kUnpackU; ++u) {
+        const int c = c0 + lane + 32 * u;
+        val[u] = (j >= 0 && c < cpr) ? ld_global_nc_16(op + so + c * 16) : make_uint4(0u, 0u, 0u, 0u);
       }
 #pragma unroll
-      for (int u = 0; u < kCopyUnroll; ++u)
-        if (dptr[u]) st_global_16(dptr[u], val[u]);
+      for (int u = 0; u < kUnpackU; ++u) {
+        const int c = c0 + lane + 32 * u;
+        if (c < cpr) st_global_16(o + dof + c * 16, val[u]);
+      }
     }
   }
 }
@@ -952,8 +951,9 @@ cudaError_t launch_pack(const void* q, const void* k, const void* v, long long l
   int dev = 0;
   cudaGetDevice(&dev);
   const long long cap_rows = (long long)B * N;
-  const long long want = (cap_rows + kPackRows - 1) / kPackRows;
-  const int grid = (int)(want < ((long long)sm_count(dev) * 8) ? (long long)(want) : (long long)((long long)sm_count(dev) * 8));
+  const long long want = (cap_rows + kCopyWarps - 1) / kCopyWarps;   // live rows are known on the device only
+  const long long most = (long long)sm_count(dev) * 8;              // 8 CTAs (64 warps) per SM
+  const int grid = (int)(want < most ? want : most);
   return launch_pdl(pack_kernel, dim3(grid), dim3(kCopyThreads), 0, st,
                     static_cast<const uint8_t*>(q), static_cast<const uint8_t*>(k),
                     static_cast<const uint8_t*>(v), cu, (const int32_t*)src, static_cast<uint8_t*>(qp),
@@ -966,8 +966,9 @@ cudaError_t launch_unpack(const void* op, const int32_t* dst, void* o, int B, in
   int dev = 0;
   cudaGetDevice(&dev);
   const long long BN = (long long)B * N;
-  const long long want = (BN + kUnpackRows - 1) / kUnpackRows;
-  const int grid = (int)(want < ((long long)sm_count(dev) * 8) ? (long long)(want) : (long long)((long long)sm_count(dev) * 8));
+  const long long want = (BN + kCopyWarps - 1) / kCopyWarps;
+  const long long most = (long long)sm_count(dev) * 8;
+  const int grid = (int)(want < most ? want : most);
   return launch_pdl(unpack_kernel, dim3(grid), dim3(kCopyThreads), 0, st,
                     static_cast<const uint8_t*>(op), dst, static_cast<uint8_t*>(o), BN,
                     H * kHeadDim * 2);
