@@ -612,6 +612,9 @@ __global__ void __launch_bounds__(kAttnThreads, 3) attn_kernel(const AttnArgs a,
     const int c = tid & 7, t = (tid >> 3) & 1, r0 = tid >> 4;
     const char* gsrc = (t ? img_v : img_k) + c * 16;
     uint32_t sdst = smem_u32(t ? sV : sK) + r0 * kRowBytes + ((c ^ r0) << 4);
+    // unrolled by 4: the shared-memory position loads of 4 rows issue together
+    // instead of one dependent LDS -> cp.async pair per row
+#pragma unroll 4
     for (int r = r0; r < n16; r += 8, sdst += 8 * kRowBytes) {
       const bool valid = r < n;
       cp_async_16(sdst, gsrc + (valid ? sPos[r] * ldb : 0), valid ? 16 : 0);
