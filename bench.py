@@ -743,6 +743,17 @@ def extras(args, rb, torch, dev, sets, c, B, N, H, dt, T):
         rb.keep_topk_l2(xs[i % 4], kk, keep=keeps[i])
         rb.pack_attend_unpack(s["q"], s["k"], s["v"], keeps[i], o=s["o"], cu=s["cu"])
     out["prune_then_fused_us"] = _graph_time(torch, [(lambda i=i: prune_fused(i)) for i in range(N_SETS)], reps)
+    # the paper's dispatch study through the C ABI with no Python in the loop
+    # (SURVEY §8(d) timing modes M1/M2/M3): tools/ragged_bench, if built
+    try:
+        import subprocess
+        tool = os.path.join(ROOT, "tools", "ragged_bench")
+        if os.path.exists(tool):
+            r = subprocess.run([tool, str(B), str(N), str(H), str(c["p"])], capture_output=True, text=True,
+                               timeout=120)
+            out["native_timing_modes"] = json.loads(r.stdout.strip().splitlines()[-1])
+    except Exception as ex:
+        out["native_timing_modes"] = {"error": repr(ex)[:200]}
     try:
         out["n1_block"] = n1_block_extras(rb, torch, dev, dt)
     except Exception as ex:

@@ -83,9 +83,27 @@ def build(force: bool = False, verbose: bool = False, variant: str = "") -> str:
     return lib
 
 
+TOOL_SRC = os.path.join(ROOT, "tools", "ragged_bench.cu")
+TOOL_BIN = os.path.join(ROOT, "tools", "ragged_bench")
+
+
+def build_tool(verbose: bool = False) -> str:
+    """tools/ragged_bench: the native timing driver (links libragged.so)."""
+    build(verbose=verbose)
+    cmd = [nvcc(), *ARCH, "-O2", "-std=c++17", "-I", os.path.join(ROOT, "include"), TOOL_SRC, "-o", TOOL_BIN,
+           "-L", PKG, "-lragged", "-Xlinker", "-rpath", "-Xlinker", "$ORIGIN/../paper_2604_15408_b200"]
+    r = subprocess.run(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT)
+    if r.returncode != 0:
+        sys.stderr.write(r.stdout.decode(errors="replace"))
+        raise RuntimeError("ragged_bench build failed")
+    return TOOL_BIN
+
+
 if __name__ == "__main__":
     print(build(force=True, verbose="--verbose" in sys.argv))
     if "--tl" in sys.argv:
         print(build(force=True, variant="tl"))
     if "--tlz" in sys.argv:
         print(build(force=True, variant="tlz"))
+    if "--tool" in sys.argv:
+        print(build_tool())
