@@ -649,6 +649,7 @@ __global__ void __launch_bounds__(kAttnThreads, 3) attn_kernel(const AttnArgs a,
   cp_async_wait_all();
   __syncthreads();
   TL(3);
+  PT(0);
   if (cu_here && tid == 0) {
     const int pre = (int)(sWords[0] + sWords[1] + sWords[2] + sWords[3]);
     a.cu_out[b] = pre;
@@ -737,6 +738,7 @@ __global__ void __launch_bounds__(kAttnThreads, 3) attn_kernel(const AttnArgs a,
       mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 1));
       mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 2));
       TL(5);
+      PT(1);
       const float mn0 = fmaxf(m0, mx0), mn1 = fmaxf(m1, mx1);
       const float al0 = ex2(m0 - mn0), al1 = ex2(m1 - mn1);  // alpha = e^{m - m'}
       m0 = mn0;
@@ -821,6 +823,7 @@ __global__ void __launch_bounds__(kAttnThreads, 3) attn_kernel(const AttnArgs a,
     }
     __syncwarp();
     TL(6);
+    PT(2);
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       const int rr = (lane >> 3) + 4 * i, r = slice * 16 + rr;
