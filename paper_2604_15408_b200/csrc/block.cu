@@ -289,11 +289,21 @@ __global__ void __launch_bounds__(gemm_threads<kEpi>(), 1)
       const uint4* rrow = kEpi == 2 ? reinterpret_cast<const uint4*>(static_cast<const T*>(g.residual) +
                                                                        my_row * g.ldr + n0)
                                     : nullptr;
-      uint4 nres[4];
+      // residual row segments do not depend on the accumulator: every chunk of
+      // this warp is fetched before waiting for it, so their DRAM latency
+      // hides behind the tile's mainloop (the epilogue warps are idle there)
+      constexpr int kCh = (BN / 32 + kEp - 1) / kEp;  // chunks per warp
+      uint4 rall[kEpi == 2 ? kCh : 1][4];
       if constexpr (kEpi == 2) {
         if (live) {
 #pragma unroll
-          for (int q = 0; q < 4; ++q) nres[q] = rrow[(32 * half) / 8 + q];  // half = this warp's first chunk
+          for (int ci = 0; ci < kCh; ++ci) {
+            const int c = 32 * half + 32 * kEp * ci;
+            if (c < BN) {
+#pragma unroll
+              for (int q = 0; q < 4; ++q) rall[ci][q] = rrow[c / 8 + q];
+            }
+          }
         }
       }
       tc::mbar_wait(tfull(acc), (uint32_t)((i >> 1) & 1));
@@ -304,16 +314,14 @@ __global__ void __launch_bounds__(gemm_threads<kEpi>(), 1)
         continue;
       }
       const uint32_t tbase = tmem + ((uint32_t)(32 * quad) << 16) + (uint32_t)(acc * BN);
-#pragma unroll 1
-      for (int c = 32 * half; c < BN; c += 32 * kEp) {
+#pragma unroll
+      for (int ci = 0; ci < kCh; ++ci) {
+        const int c = 32 * half + 32 * kEp * ci;
+        if (c >= BN) break;
         uint4 res[4];
         if constexpr (kEpi == 2) {
 #pragma unroll
-          for (int q = 0; q < 4; ++q) res[q] = nres[q];
-          if (live && c + 32 * kEp < BN) {
-#pragma unroll
-            for (int q = 0; q < 4; ++q) nres[q] = rrow[(c + 32 * kEp) / 8 + q];
-          }
+          for (int q = 0; q < 4; ++q) res[q] = rall[ci][q];
         }
         uint32_t r[32];
         tc::ld_x32(tbase + (uint32_t)c, r);
