@@ -448,11 +448,11 @@ def gather_variants(rb, torch, dev, sets, ws, rank, B, N, H, T, impls, reps=200)
     esz = 2
     tcap = int(max_over_ranks(float(T), dev))
 
-    def timed(fns):
+    def timed(fns, graph=True):
         if ws > 1:
             dist.barrier()
         torch.cuda.synchronize()
-        return max_over_ranks(_graph_time(torch, fns, reps), dev)
+        return max_over_ranks(_graph_time(torch, fns, reps) if graph else _eager_time(torch, fns, reps), dev)
 
     def alloc(shape, dtype, symmetric):
         """(tensor, per-rank pointers): symmetric memory at N>1, local at N=1."""
@@ -502,9 +502,12 @@ def gather_variants(rb, torch, dev, sets, ws, rank, B, N, H, T, impls, reps=200)
             rb.pack_attend_unpack(s["q"], s["k"], s["v"], s["keep"], o=s["o"])
             dist.all_gather_into_tensor(pad_g, s["o"])
 
-        res["cls_us"] = timed([lambda s=s: cls_step(s) for s in sets])
-        res["packed_us"] = timed([lambda s=s, i=i: packed_step(s, i) for i, s in enumerate(sets)])
-        res["padded_us"] = timed([lambda s=s: padded_step(s) for s in sets])
+        # NCCL collectives are timed eagerly (device events around `reps` steps),
+        # not graph-captured: robust on every NCCL / PyTorch build
+        res["cls_us"] = timed([lambda s=s: cls_step(s) for s in sets], graph=False)
+        res["packed_us"] = timed([lambda s=s, i=i: packed_step(s, i) for i, s in enumerate(sets)], graph=False)
+        res["padded_us"] = timed([lambda s=s: padded_step(s) for s in sets], graph=False)
+        res["timing"] = "eager launches, CUDA events, max over ranks"
         out["nccl"] = res
 
     if "peer" in impls:
@@ -544,6 +547,20 @@ def gather_variants(rb, torch, dev, sets, ws, rank, B, N, H, T, impls, reps=200)
         res["world"] = ws
         out["peer"] = res
     return out
+
+
+def _eager_time(torch, fns, reps):
+    """Device µs per call of `reps` eager calls (rotating over fns), CUDA events."""
+    for f in fns:
+        f()
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for i in range(reps):
+        fns[i % len(fns)]()
+    e.record()
+    torch.cuda.synchronize()
+    return 1e3 * s.elapsed_time(e) / reps
 
 
 def _graph_time(torch, fns, reps):
