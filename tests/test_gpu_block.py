@@ -196,6 +196,31 @@ def test_vit_block_end_to_end(preset, B, p, method):
     assert np.abs(to_np(a) - ref_a).max() <= 2e-3 * max(1.0, np.abs(q3[:, 2]).max())
 
 
+def test_vit_block_fp16():
+    """The block in fp16 (storage rounding to fp16 in the oracle)."""
+    dtype = torch.float16
+    pr = synth.PRESETS["deit_small"]
+    D, H, MLP, N, B = pr["D"], pr["H"], pr["MLP"], 197, 4
+    params = synth.vit_weights(D, MLP, dtype, 7)
+    keep = synth.make_inputs(B, N, H, 0.6, "l2", "bf16", seed=7)[3].numpy()
+    cu, _, _ = oracle.scan(keep)
+    T = int(cu[-1])
+    x = synth.packed_rows(T, D, dtype, 7)
+    blk = rb.VitBlock({k: v.to(DEV) for k, v in params.items()}, B, N, H, dtype)
+    xd = _sentinel((B * N, D), dtype)
+    xd[:T] = x.to(DEV)
+    blk(xd, torch.from_numpy(cu.astype(np.int32)).to(DEV))
+    torch.cuda.synchronize()
+    assert (bits(xd[T:]) == SENT).all()
+    got = to_np(xd[:T])
+    ref = oracle.vit_block(x, cu, params, H, store=store(dtype))
+    err = np.abs(got - ref)
+    assert err.max() <= 2.0 ** -9 * np.abs(ref).max(), (err.max(), np.abs(ref).max())   # fp16: 3 more mantissa bits
+    r_gpu = np.linalg.norm(got - oracle.vit_block(x, cu, params, H)) / np.linalg.norm(ref)
+    r_sto = np.linalg.norm(ref - oracle.vit_block(x, cu, params, H)) / np.linalg.norm(ref)
+    assert r_gpu <= 1.1 * r_sto + 1e-6
+
+
 def test_vit_block_graph_and_determinism():
     """Two runs (eager and CUDA-graph replay) give bitwise-identical rows."""
     dtype = torch.bfloat16
