@@ -306,7 +306,7 @@ __global__ void __launch_bounds__(gemm_threads<kEpi>(), 1)
           }
         }
       }
-      tc::mbar_wait(tfull(acc), (uint32_t)((i >> 1) & 1));
+      tc::mbar_wait_sleep(tfull(acc), (uint32_t)((i >> 1) & 1), 256);  // don't steal issue slots from TMA / MMA
       tc::fence_after();
       if (i == 0 && warp == 2 && lane == 0) GT(5);
       if (32 * half >= BN) {  // no chunk for this warp at this tile width: just count in
@@ -484,7 +484,12 @@ static cudaError_t launch_gemm_t(const CUtensorMap& ta, const CUtensorMap& tb, c
   static int sms[64] = {0};
   if (dev >= 0 && dev < 64 && sms[dev] == 0) cudaDeviceGetAttribute(&sms[dev], cudaDevAttrMultiProcessorCount, dev);
   const int nsm = (dev >= 0 && dev < 64 && sms[dev] > 0) ? sms[dev] : 148;
-  const dim3 grid((unsigned)(tiles < nsm ? tiles : nsm));
+  static const int grid_cap = [] {
+    const char* e = getenv("RAGGED_GEMM_GRID");  // tuning experiments only
+    return e ? atoi(e) : 0;
+  }();
+  const int cap = grid_cap > 0 && grid_cap < nsm ? grid_cap : nsm;
+  const dim3 grid((unsigned)(tiles < cap ? tiles : cap));
   return launch_pdl_b(gemm_tc_kernel<T, BN, kEpi>, grid, dim3(gemm_threads<kEpi>()), gemm_smem_bytes<BN, kEpi>(), st,
                       ta, tb,
                       g);
