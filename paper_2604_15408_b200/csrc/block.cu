@@ -42,17 +42,30 @@ __global__ void __launch_bounds__(kLnThreads) layer_norm_kernel(const T* __restr
   pdl_wait_prerequisites();
   const int lane = threadIdx.x & 31;
   const long long row = (long long)blockIdx.x * (kLnThreads / 32) + (threadIdx.x >> 5);
-  const int M = m_dev ? min(*m_dev, M_cap) : M_cap;
-  if (row >= M) return;
+  if (row >= M_cap) return;
+  // The row (inside the capacity, so always addressable), gamma and beta are
+  // loaded together with the live count: one memory round trip, not two.
   const int nch = D >> 3;  // 16-byte chunks per row
-  float v[kCPL][8];
-  float s = 0.f;
   const T* xr = x + row * ldx;
+  uint4 raw[kCPL], wraw[kCPL], braw[kCPL];
 #pragma unroll
   for (int i = 0; i < kCPL; ++i) {
     const int c = lane + 32 * i;
     if (c < nch) {
-      const uint4 u = ld_global_nc_16(xr + c * 8);
+      raw[i] = *reinterpret_cast<const uint4*>(xr + c * 8);
+      wraw[i] = ld_global_nc_16(w + c * 8);
+      braw[i] = ld_global_nc_16(bvec + c * 8);
+    }
+  }
+  const int M = m_dev ? min(*m_dev, M_cap) : M_cap;
+  if (row >= M) return;
+  float v[kCPL][8];
+  float s = 0.f;
+#pragma unroll
+  for (int i = 0; i < kCPL; ++i) {
+    const int c = lane + 32 * i;
+    if (c < nch) {
+      const uint4 u = raw[i];
       const uint32_t wds[4] = {u.x, u.y, u.z, u.w};
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
@@ -88,7 +101,7 @@ __global__ void __launch_bounds__(kLnThreads) layer_norm_kernel(const T* __restr
   for (int i = 0; i < kCPL; ++i) {
     const int c = lane + 32 * i;
     if (c < nch) {
-      const uint4 wu = ld_global_nc_16(w + c * 8), bu = ld_global_nc_16(bvec + c * 8);
+      const uint4 wu = wraw[i], bu = braw[i];
       const uint32_t ww[4] = {wu.x, wu.y, wu.z, wu.w}, bw[4] = {bu.x, bu.y, bu.z, bu.w};
       uint32_t o[4];
 #pragma unroll
