@@ -188,7 +188,8 @@ def cpu_baseline(args, c, B, N, H):
     dt = time.perf_counter() - t0
     out = {"value": B * calls / dt, "unit": "images/s", "cores": 1, "kind": "oracle",
            "sample": f"{calls} full {args.config} batches ({B} images) in {dt:.1f} s, "
-                     f"fp64 numpy oracle, 1 BLAS thread, host {os.cpu_count()} cores"}
+                     f"fp64 numpy oracle, 1 BLAS thread, host {os.cpu_count()} cores",
+           "host_cpu": _cpu_model(), "wall_s": dt}
     # all host cores: one process per core, images split across processes (the
     # oracle is per image, so results are identical to the 1-thread run)
     try:
@@ -196,6 +197,16 @@ def cpu_baseline(args, c, B, N, H):
     except Exception as ex:
         out["all_cores"] = {"error": repr(ex)[:200]}
     return out
+
+
+def _cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
 
 
 def _oracle_worker(payload):
