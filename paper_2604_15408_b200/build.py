@@ -33,7 +33,11 @@ def nvcc() -> str:
 VARIANTS = {"": [], "tl": ["-DRAGGED_TIMELINE"],
             # timing experiments only: ablations of the mma.sync engine
             "tlz": ["-DRAGGED_TIMELINE", "-DRAGGED_ABLATE_QK", "-DRAGGED_ABLATE_PV", "-DRAGGED_ABLATE_EXP",
-                    "-DRAGGED_ABLATE_ZERO"]}
+                    "-DRAGGED_ABLATE_ZERO"],
+            "abz": ["-DRAGGED_ABLATE_ZERO"],
+            "abc": ["-DRAGGED_ABLATE_QK", "-DRAGGED_ABLATE_PV", "-DRAGGED_ABLATE_EXP"],
+            "aball": ["-DRAGGED_ABLATE_QK", "-DRAGGED_ABLATE_PV", "-DRAGGED_ABLATE_EXP",
+                      "-DRAGGED_ABLATE_ZERO"]}
 
 
 def lib_path(variant: str = "") -> str:
@@ -105,5 +109,8 @@ if __name__ == "__main__":
         print(build(force=True, variant="tl"))
     if "--tlz" in sys.argv:
         print(build(force=True, variant="tlz"))
+    for v in VARIANTS:
+        if v and f"--{v}" in sys.argv and v not in ("tl", "tlz"):
+            print(build(force=True, variant=v))
     if "--tool" in sys.argv:
         print(build_tool())

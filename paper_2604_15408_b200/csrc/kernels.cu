@@ -363,7 +363,7 @@ constexpr int kQAreaBytes = (kAttnThreads / 32) * 2 * kQBufBytes;  // double-buf
 
 __host__ __device__ inline int attn_rows_cap(int N) { return (N + 15) & ~15; }
 __host__ __device__ inline int attn_smem_bytes(int N) {
-  return 2 * attn_rows_cap(N) * kRowBytes + kQAreaBytes + 2 * kMaxN * 2 + 8 * 4;
+  return 2 * attn_rows_cap(N) * kRowBytes + kQAreaBytes + 2 * kMaxN * 2 + 16 * 4;
 }
 
 struct AttnArgs {
@@ -459,6 +459,45 @@ __device__ __forceinline__ void gather_arrive(const GatherArgs& g) {
   }
 }
 
+// Kept positions in keep[0, len), this thread's share (stride nthr), in two
+// halves so the first loads can be issued early: prefix_loads() issues up to
+// kCntU 16-byte loads, prefix_count() counts them plus the rest of the share.
+constexpr int kCntU = 4;
+struct PrefixLoads {
+  uint4 v[kCntU];
+  bool aligned;
+};
+__device__ __forceinline__ void prefix_loads(PrefixLoads& L, const uint8_t* __restrict__ keep,
+                                             long long len, int t, int nthr) {
+  L.aligned = (reinterpret_cast<uintptr_t>(keep) & 15) == 0;
+  const long long nfull = len >> 4;
+#pragma unroll
+  for (int i = 0; i < kCntU; ++i) {
+    const long long c = t + (long long)i * nthr;
+    L.v[i] = (L.aligned && c < nfull) ? __ldg(reinterpret_cast<const uint4*>(keep) + c)
+                                      : make_uint4(0u, 0u, 0u, 0u);
+  }
+}
+__device__ __forceinline__ int popc_nonzero16(uint4 v) {
+  return (__popc(__vcmpne4(v.x, 0u)) + __popc(__vcmpne4(v.y, 0u)) + __popc(__vcmpne4(v.z, 0u)) +
+          __popc(__vcmpne4(v.w, 0u))) >> 3;
+}
+__device__ __forceinline__ int prefix_count(const PrefixLoads& L, const uint8_t* __restrict__ keep,
+                                            long long len, int t, int nthr) {
+  int cnt = 0;
+  long long p = t;
+  if (L.aligned) {
+#pragma unroll
+    for (int i = 0; i < kCntU; ++i) cnt += popc_nonzero16(L.v[i]);
+    const long long nfull = len >> 4;
+    for (long long c = t + (long long)kCntU * nthr; c < nfull; c += nthr)
+      cnt += popc_nonzero16(*reinterpret_cast<const uint4*>(keep + (c << 4)));
+    p = (nfull << 4) + t;
+  }
+  for (; p < len; p += nthr) cnt += keep[p] != 0 ? 1 : 0;
+  return cnt;
+}
+
 // Kept positions in keep[0, len) -- this thread's share (stride nthr): 16-byte
 // loads when the mask is 16-byte aligned, nonzero bytes counted with __vcmpne4.
 __device__ __forceinline__ int count_kept(const uint8_t* __restrict__ keep, long long len, int t,
@@ -495,16 +534,24 @@ __device__ __forceinline__ void scan_cta_cu(const AttnArgs& a, uint8_t* scratch,
 //           row_base = b * N (padded rows).
 //   packed: n = cu[b+1] - cu[b], sPos[r] = r; row_base = cu[b] (packed rows).
 // Ends with __syncthreads().  Requires blockDim.x == kAttnThreads, N <= 256.
-template <bool kFused, typename Sync>
+// `mid` runs after the keep-row loads are issued and before their values are
+// used: work placed there overlaps the mask's memory round trip.
+struct NoMid {
+  __device__ __forceinline__ void operator()() const {}
+};
+
+template <bool kFused, typename Sync, typename Mid = NoMid>
 __device__ __forceinline__ void image_rows(const AttnArgs& a, int b, int16_t* sPos, int16_t* sDrop,
                                            uint32_t* sWords, int& n, long long& row_base, int tid,
-                                           Sync sync) {
+                                           Sync sync, Mid mid = Mid()) {
   const int warp = tid >> 5, lane = tid & 31;
   if constexpr (kFused) {
     const uint8_t* km = a.keep + (long long)b * a.N;
     const int p0 = tid, p1 = tid + kAttnThreads;
-    const bool k0 = p0 < a.N && km[p0] != 0;
-    const bool k1 = p1 < a.N && km[p1] != 0;
+    const uint8_t m0 = p0 < a.N ? km[p0] : (uint8_t)0;
+    const uint8_t m1 = p1 < a.N ? km[p1] : (uint8_t)0;
+    mid();
+    const bool k0 = m0 != 0, k1 = m1 != 0;
     const uint32_t w0 = __ballot_sync(0xffffffffu, k0);
     const uint32_t w1 = __ballot_sync(0xffffffffu, k1);
     if (lane == 0) {
@@ -582,13 +629,30 @@ __global__ void __launch_bounds__(kAttnThreads, 3) attn_kernel(const AttnArgs a,
   const T* gv = static_cast<const T*>(a.v);
   T* go = static_cast<T*>(a.o);
 
-  int n;
-  long long row_base;
-  image_rows<kFused>(a, b, sPos, sDrop, sWords, n, row_base, tid, [] { __syncthreads(); });
   // Byte addressing: one 64-bit image base per tensor, then 32-bit row offsets
   // (pos < 256, token stride <= 2^23 bytes -- validated in api.cu).
   const int ldb = (int)a.ld * 2;  // input token stride, bytes
   const int HDb = (int)HD * 2;                          // output token stride, bytes
+
+  // cu_mode 2: the head-0 CTA of image b issues the loads of the keeps of images
+  // [0, b) (its cu_seqlens entry) while its own keep row is in flight -- one DRAM
+  // round trip for both (C3: cu_seqlens cost 0.45 -> 0.08 us).
+  //  (Measured and rejected: zeroing all of the head's padded rows here, kept
+  //  rows overwritten later -- C3 6.8 -> 7.5 us: the 25 KB of stores per CTA
+  //  queue ahead of the gathers; the dropped rows are zeroed during the compute.)
+  const bool cu_here = kFused && a.cu_mode == 2 && h == 0;
+  PrefixLoads pl;
+  int n;
+  long long row_base;
+  image_rows<kFused>(a, b, sPos, sDrop, sWords, n, row_base, tid, [] { __syncthreads(); }, [&] {
+    if (cu_here) prefix_loads(pl, a.keep, (long long)b * a.N, tid, kAttnThreads);
+    if (cu_here) {
+      int c = prefix_count(pl, a.keep, (long long)b * a.N, tid, kAttnThreads);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+      if (lane == 0) sWords[8 + warp] = (uint32_t)c;
+    }
+  });
   const char* img_q = reinterpret_cast<const char*>(gq) + row_base * ldb + h * kRowBytes;
   const char* img_k = reinterpret_cast<const char*>(gk) + row_base * ldb + h * kRowBytes;
   const char* img_v = reinterpret_cast<const char*>(gv) + row_base * ldb + h * kRowBytes;
@@ -635,15 +699,6 @@ __global__ void __launch_bounds__(kAttnThreads, 3) attn_kernel(const AttnArgs a,
   };
   if (warp * 16 < n) load_q(qwarp, warp);
   cp_async_commit();
-  // cu_mode 2: the head-0 CTA of image b counts the keeps of images [0, b) while
-  // its gathers are in flight (L2-hot mask bytes); reduced at the barrier below.
-  const bool cu_here = kFused && a.cu_mode == 2 && h == 0;
-  if (cu_here) {
-    int c = count_kept(a.keep, (long long)b * a.N, tid, kAttnThreads);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
-    if (lane == 0) sWords[warp] = (uint32_t)c;  // ballot words are dead after image_rows
-  }
 
   TL(2);
   cp_async_wait_all();
@@ -651,7 +706,7 @@ __global__ void __launch_bounds__(kAttnThreads, 3) attn_kernel(const AttnArgs a,
   TL(3);
   PT(0);
   if (cu_here && tid == 0) {
-    const int pre = (int)(sWords[0] + sWords[1] + sWords[2] + sWords[3]);
+    const int pre = (int)(sWords[8] + sWords[9] + sWords[10] + sWords[11]);
     a.cu_out[b] = pre;
     if (b == a.B - 1) a.cu_out[a.B] = pre + n;
   }
