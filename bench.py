@@ -432,10 +432,81 @@ def measure_e2e(args, rb, torch, dev, q, k, v, keep, ws, B, N, H, dt):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     h2d = sum(t.numel() * t.element_size() for t in (q, k, v, keep))
+    copy_engine = {"value": ws * B * args.e2e_steps / (ms * 1e-3), "unit": "images/s",
+                   "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": ohs[0].numel() * ohs[0].element_size(),
+                   "us_per_step": 1e3 * ms / args.e2e_steps, "mode": "copy_engine",
+                   "pipelining": f"{nst} streams, independent batches (H2D / kernel / D2H overlap)"}
+    del bufs
+    variants = {"copy_engine": copy_engine}
+    for name, out_host in (("zero_copy", False), ("zero_copy_out", True)):
+        try:
+            variants[name] = measure_e2e_zero_copy(args, rb, torch, dev, q, k, v, keep, ws, B, N, H, dt,
+                                                   out_host)
+        except Exception as ex:  # never lose the copy-engine number
+            variants[name] = {"error": repr(ex)[:300]}
+    best = max((x for x in variants.values() if "value" in x), key=lambda x: x["value"])
+    best = dict(best)
+    best["variants"] = variants
+    return best
+
+
+def measure_e2e_zero_copy(args, rb, torch, dev, q, k, v, keep, ws, B, N, H, dt, out_host=False):
+    """e2e with the inputs read IN PLACE from pinned host memory by the fused
+    kernel (ragged_pack_attend_unpack_host): only the keep mask and the kept
+    q/k/v rows cross the host link.  The padded output goes back through a
+    D2H copy (copy engine) of the device O, or (out_host) the kernel stores
+    the padded O straight into pinned host memory.  Every step uses a different host
+    input set (enough sets that their kept rows exceed 2x L2, so no step is
+    served from cache); 3 streams pipeline the independent steps."""
+    import math
+    nst = 3
+    T = int(keep.numpy().astype(bool).sum())
+    kept = keep.numel() + 3 * T * H * 64 * q.element_size()
+    set_bytes = sum(t.numel() * t.element_size() for t in (q, k, v, keep))
+    nsets = max(1, min(48, math.ceil(2 * 126e6 / max(kept, 1)), int(4e9 // set_bytes)))
+    hosts = [tuple(t.pin_memory() for t in (q, k, v, keep)) for _ in range(nsets)]
+    ohs = [torch.empty(B, N, H, 64, dtype=dt).pin_memory() for _ in range(nst)]
+    obufs = [torch.empty(B, N, H, 64, dtype=dt, device=dev) for _ in range(nst)]
+    streams = [torch.cuda.Stream() for _ in range(nst)]
+
+    def one(i):
+        j = i % nst
+        hq, hk, hv, hkeep = hosts[i % nsets]
+        with torch.cuda.stream(streams[j]):
+            if out_host:
+                rb.pack_attend_unpack_host(hq, hk, hv, hkeep, ohs[j], stream=streams[j])
+            else:
+                rb.pack_attend_unpack_host(hq, hk, hv, hkeep, obufs[j], stream=streams[j])
+                ohs[j].copy_(obufs[j], non_blocking=True)
+
+    for i in range(max(2 * nst, nsets)):
+        one(i)
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    cur = torch.cuda.current_stream()
+    s.record(cur)
+    for st in streams:
+        st.wait_stream(cur)
+    for i in range(args.e2e_steps):
+        one(i)
+    for st in streams:
+        cur.wait_stream(st)
+    e.record(cur)
+    torch.cuda.synchronize()
+    ms = s.elapsed_time(e)
+    if ws > 1:
+        import torch.distributed as dist
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
     return {"value": ws * B * args.e2e_steps / (ms * 1e-3), "unit": "images/s",
-            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": ohs[0].numel() * ohs[0].element_size(),
-            "us_per_step": 1e3 * ms / args.e2e_steps,
-            "pipelining": f"{nst} streams, independent batches (H2D / kernel / D2H overlap)"}
+            "h2d_bytes_per_step": kept, "d2h_bytes_per_step": ohs[0].numel() * ohs[0].element_size(),
+            "us_per_step": 1e3 * ms / args.e2e_steps, "mode": "zero_copy_out" if out_host else "zero_copy",
+            "host_input_sets": nsets,
+            "pipelining": f"{nst} streams, independent batches (kernel reads host / D2H overlap); "
+                          "h2d bytes = keep mask + kept q/k/v rows read in place by the kernel; "
+                          + ("the kernel writes the padded O into pinned host memory" if out_host else
+                             "padded O copied D2H by the copy engine")}
 
 
 # ----------------------------------------------------------------------------

@@ -135,6 +135,24 @@ RAGGED_API ragged_status ragged_pack_attend_unpack(const ragged_problem* prob, c
                                         void* o, int32_t* cu_seqlens_or_null,
                                         void* stream);
 
+/* a5, end to end from HOST memory (bench.py "e2e"): the same fused launch, but
+ * keep, q, k, v (and optionally o) may be page-locked host buffers mapped into
+ * the device address space (cudaHostAlloc / cudaHostRegister with mapping;
+ * every pinned allocation under UVA).  The kernel reads the keep mask and only
+ * the KEPT q/k/v rows across PCIe / C2C (zero-copy: B*N + 3*T*H*d*e bytes
+ * instead of the 3*B*N*H*d*e of copying the padded inputs), so host->device
+ * traffic scales with the kept fraction, as the on-device path's HBM traffic
+ * does.  Each pointer may also be a device pointer.  Host pointers are
+ * translated with cudaHostGetDevicePointer.  Errors: as
+ * ragged_pack_attend_unpack, plus RAGGED_EINVAL for pageable (unregistered)
+ * host memory or a pinned buffer without a device mapping.  Asynchronous on
+ * `stream`; the caller keeps host buffers alive and unmodified until the
+ * stream reaches this call's completion. */
+RAGGED_API ragged_status ragged_pack_attend_unpack_host(const ragged_problem* prob, const uint8_t* keep,
+                                             const void* q, const void* k, const void* v,
+                                             void* o, int32_t* cu_seqlens_or_null,
+                                             void* stream);
+
 /* a5 -- CUDA-graph capture of one ragged_pack_attend_unpack with fixed
  * pointers: ragged_graph_launch replays it as a single graph launch with no
  * argument marshalling.  The handle owns its cudaGraphExec; destroy it with

@@ -100,6 +100,7 @@ def _load() -> ctypes.CDLL:
         "ragged_attn": [P, V, V, V, V, V, V],
         "ragged_unpack": [P, V, V, V, V],
         "ragged_pack_attend_unpack": [P, V, V, V, V, V, V, V],
+        "ragged_pack_attend_unpack_host": [P, V, V, V, V, V, V, V],
         "ragged_graph_create": [P, V, V, V, V, V, V, ctypes.POINTER(V)],
         "ragged_graph_launch": [V, V],
         "ragged_empty_launch": [I32, I32, V],
@@ -132,6 +133,7 @@ def _load() -> ctypes.CDLL:
 _lib = None
 
 EXPORTS = ("ragged_scan", "ragged_pack", "ragged_attn", "ragged_unpack", "ragged_pack_attend_unpack",
+           "ragged_pack_attend_unpack_host",
            "ragged_graph_create", "ragged_graph_launch", "ragged_graph_destroy", "ragged_empty_launch",
            "ragged_validate_cu_seqlens", "ragged_status_str", "ragged_last_error", "ragged_build_info",
            "ragged_keep_topk_l2", "ragged_pack_attend_unpack_gather", "ragged_attn_gather",
@@ -286,6 +288,23 @@ def pack_attend_unpack(q, k, v, keep, o=None, cu=None, want_cu=False, stream=Non
                                           v.data_ptr(), o.data_ptr(), _ptr(cu), _stream(stream)),
            "ragged_pack_attend_unpack")
     return (o, cu) if (want_cu or cu is not None) else o
+
+
+def pack_attend_unpack_host(q, k, v, keep, o, cu=None, stream=None, engine=ENGINE_AUTO):
+    """a5 end to end from host memory: q, k, v, keep are PINNED CPU tensors
+    (tensor.pin_memory()); the kernel reads the mask and only the kept rows
+    over the host link (ragged_pack_attend_unpack_host).  o (and cu) are
+    device tensors or pinned CPU tensors.  Returns o."""
+    for t in (q, k, v, keep):
+        if t.device.type != "cpu" or not t.is_pinned():
+            raise ValueError("q, k, v, keep must be pinned CPU tensors")
+    p = _padded_problem(q, k, v, engine)
+    keep = _keep_u8(keep)
+    _check(lib().ragged_pack_attend_unpack_host(ctypes.byref(p), keep.data_ptr(), q.data_ptr(),
+                                               k.data_ptr(), v.data_ptr(), o.data_ptr(), _ptr(cu),
+                                               _stream(stream)),
+           "ragged_pack_attend_unpack_host")
+    return o
 
 
 def pack_attend_unpack_gather(q, k, v, keep, gather: Gather, cu=None, stream=None,

@@ -190,6 +190,56 @@ ragged_status ragged_pack_attend_unpack(const ragged_problem* prob, const uint8_
   return e == cudaSuccess ? RAGGED_OK : cuda_fail(e, "ragged_pack_attend_unpack");
 }
 
+namespace {
+// A pointer the device can dereference: device memory as is, page-locked host
+// memory through its device mapping; pageable host memory is rejected.
+ragged_status device_view(const void* p, const char* name, const void** out) {
+  static thread_local char buf[128];
+  cudaPointerAttributes at{};
+  cudaError_t e = cudaPointerGetAttributes(&at, p);
+  if (e != cudaSuccess) return cuda_fail(e, name);
+  if (at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged) {
+    *out = p;
+    return RAGGED_OK;
+  }
+  if (at.type == cudaMemoryTypeHost) {
+    void* d = nullptr;
+    e = cudaHostGetDevicePointer(&d, const_cast<void*>(p), 0);
+    if (e != cudaSuccess || d == nullptr) {
+      cudaGetLastError();
+      snprintf(buf, sizeof buf, "%s: page-locked host buffer has no device mapping", name);
+      return fail(RAGGED_EINVAL, buf);
+    }
+    *out = d;
+    return RAGGED_OK;
+  }
+  snprintf(buf, sizeof buf, "%s: pageable host memory (use page-locked, mapped memory)", name);
+  return fail(RAGGED_EINVAL, buf);
+}
+}  // namespace
+
+ragged_status ragged_pack_attend_unpack_host(const ragged_problem* prob, const uint8_t* keep,
+                                             const void* q, const void* k, const void* v, void* o,
+                                             int32_t* cu_seqlens_or_null, void* stream) {
+  RAGGED_TRY(check_problem(prob));
+  if (prob->B == 0) return RAGGED_OK;
+  RAGGED_TRY(check_ptr_any(keep, "keep"));
+  RAGGED_TRY(check_ptr(q, "q"));
+  RAGGED_TRY(check_ptr(k, "k"));
+  RAGGED_TRY(check_ptr(v, "v"));
+  RAGGED_TRY(check_ptr(o, "o"));
+  const void *dkeep, *dq, *dk, *dv, *dov, *dcu = nullptr;
+  RAGGED_TRY(device_view(keep, "keep", &dkeep));
+  RAGGED_TRY(device_view(q, "q", &dq));
+  RAGGED_TRY(device_view(k, "k", &dk));
+  RAGGED_TRY(device_view(v, "v", &dv));
+  RAGGED_TRY(device_view(o, "o", &dov));
+  if (cu_seqlens_or_null != nullptr) RAGGED_TRY(device_view(cu_seqlens_or_null, "cu_seqlens", &dcu));
+  return ragged_pack_attend_unpack(prob, static_cast<const uint8_t*>(dkeep), dq, dk, dv,
+                                   const_cast<void*>(dov),
+                                   static_cast<int32_t*>(const_cast<void*>(dcu)), stream);
+}
+
 ragged_status ragged_graph_create(const ragged_problem* prob, const uint8_t* keep, const void* q,
                                   const void* k, const void* v, void* o,
                                   int32_t* cu_seqlens_or_null, ragged_graph** out) {

@@ -8,6 +8,7 @@ import re
 import subprocess
 
 import pytest
+import torch
 
 from conftest import GOLDEN, ROOT
 
@@ -83,6 +84,22 @@ def test_pointer_validation():
     assert rb.lib().ragged_graph_launch(None, None) == rb.EINVAL
     rb.lib().ragged_graph_destroy(None)
     assert rb.lib().ragged_empty_launch(0, 32, None) == rb.EINVAL
+
+
+def test_host_entry_validation():
+    """ragged_pack_attend_unpack_host: host-checkable errors before any CUDA call."""
+    f = rb.lib().ragged_pack_attend_unpack_host
+    p = rb.problem(4, 197, 12)
+    assert f(ctypes.byref(p), FAKE, 0, FAKE, FAKE, FAKE, None, None) == rb.EINVAL
+    assert f(ctypes.byref(p), 0, FAKE, FAKE, FAKE, FAKE, None, None) == rb.EINVAL
+    assert f(ctypes.byref(p), FAKE, FAKE, FAKE + 8, FAKE, FAKE, None, None) == rb.EALIGN
+    assert f(None, FAKE, FAKE, FAKE, FAKE, FAKE, None, None) == rb.EINVAL
+    p.d = 32
+    assert f(ctypes.byref(p), FAKE, FAKE, FAKE, FAKE, FAKE, None, None) == rb.ENOTSUP
+    assert f(ctypes.byref(rb.problem(0, 197, 12)), None, None, None, None, None, None, None) == rb.OK
+    with pytest.raises(ValueError):   # the binding takes pinned CPU tensors only
+        t = torch.zeros(1, 197, 12, 64, dtype=torch.bfloat16)
+        rb.pack_attend_unpack_host(t, t, t, torch.ones(1, 197, dtype=torch.uint8), t)
 
 
 def _gather_call(p, g, fused=True):

@@ -354,3 +354,40 @@ def test_prune_then_fused_path():
     _check_l2_mask(x, synth.kept_tokens(N, 0.7), km)
     ref, _ = oracle.pack_attend_unpack(q, k, v, km)
     check_attention(to_np(o), ref, torch.bfloat16)
+
+
+# ------------------------------------------- a5 from host memory (e2e) ----
+
+@pytest.mark.parametrize("engine", ENGINES)
+@pytest.mark.parametrize("dtype", ["bf16", "fp16"])
+@pytest.mark.parametrize("B,H,p,method", [(32, 12, 0.8, "l2"), (5, 3, 0.0, "all"), (9, 6, 0.5, "ats")])
+def test_fused_host_inputs_bitwise(engine, dtype, B, H, p, method):
+    """ragged_pack_attend_unpack_host (pinned host q/k/v/keep read in place by
+    the kernel) == the device-resident call, bit for bit, for a device and a
+    pinned-host o; cu_seqlens exact; within tolerance of the fp64 oracle."""
+    q, k, v, keep = synth.make_inputs(B, 197, H, p, method, dtype, seed=21)
+    qh, kh, vh, keeph = (t.pin_memory() for t in (q, k, v, keep))
+    qd, kd, vd, keepd = _dev(q, k, v, keep)
+    ref, cu_ref = rb.pack_attend_unpack(qd, kd, vd, keepd, want_cu=True, engine=engine)
+    o_dev = torch.full_like(ref, 7.0)
+    cu_dev = torch.full((B + 1,), -1, dtype=torch.int32, device=DEV)
+    rb.pack_attend_unpack_host(qh, kh, vh, keeph, o_dev, cu=cu_dev, engine=engine)
+    o_host = torch.full(ref.shape, 7.0, dtype=ref.dtype).pin_memory()
+    rb.pack_attend_unpack_host(qh, kh, vh, keeph, o_host, engine=engine)
+    torch.cuda.synchronize()
+    assert torch.equal(cu_dev, cu_ref)
+    assert np.array_equal(bits(o_dev), bits(ref))
+    assert np.array_equal(bits(o_host), bits(ref))
+    ref64, rcu = fused_oracle(q, k, v, keep)
+    assert cu_dev.cpu().numpy().tolist() == np.asarray(rcu).tolist()
+    check_attention(to_np(o_dev), ref64, DT[dtype])
+
+
+def test_fused_host_rejects_pageable():
+    q, k, v, keep = synth.make_inputs(2, 197, 3, 0.5, "l2", "bf16", seed=1)
+    o = torch.empty(2, 197, 3, 64, dtype=torch.bfloat16, device=DEV)
+    p = rb.problem(2, 197, 3)
+    st = rb.lib().ragged_pack_attend_unpack_host(
+        __import__("ctypes").byref(p), keep.data_ptr(), q.data_ptr(), k.data_ptr(), v.data_ptr(),
+        o.data_ptr(), None, None)
+    assert st == rb.EINVAL and "pageable" in rb.last_error()
