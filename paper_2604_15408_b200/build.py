@@ -35,6 +35,7 @@ VARIANTS = {"": [], "tl": ["-DRAGGED_TIMELINE"],
             "tlz": ["-DRAGGED_TIMELINE", "-DRAGGED_ABLATE_QK", "-DRAGGED_ABLATE_PV", "-DRAGGED_ABLATE_EXP",
                     "-DRAGGED_ABLATE_ZERO"],
             "abz": ["-DRAGGED_ABLATE_ZERO"],
+            "tlnz": ["-DRAGGED_TIMELINE", "-DRAGGED_ABLATE_ZERO"],
             "abc": ["-DRAGGED_ABLATE_QK", "-DRAGGED_ABLATE_PV", "-DRAGGED_ABLATE_EXP"],
             "aball": ["-DRAGGED_ABLATE_QK", "-DRAGGED_ABLATE_PV", "-DRAGGED_ABLATE_EXP",
                       "-DRAGGED_ABLATE_ZERO"]}
@@ -110,7 +111,7 @@ if __name__ == "__main__":
     if "--tlz" in sys.argv:
         print(build(force=True, variant="tlz"))
     for v in VARIANTS:
-        if v and f"--{v}" in sys.argv and v not in ("tl", "tlz"):
+        if v and f"--{v}" in sys.argv and v not in ("tl", "tlz"):  # noqa: E501
             print(build(force=True, variant=v))
     if "--tool" in sys.argv:
         print(build_tool())
