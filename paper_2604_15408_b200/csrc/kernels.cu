@@ -79,7 +79,8 @@ __device__ unsigned long long g_pairs_tl[kTlMaxCtas * kPtSlots];
 template <int kThreads, int kIPW, bool kWriteIdx, typename Sync>
 __device__ void scan_cta(const uint8_t* __restrict__ keep, int B, int N, int32_t* __restrict__ cu,
                          int32_t* __restrict__ dst, int32_t* __restrict__ src, uint32_t* s_words,
-                         int32_t* s_cnt, int32_t* s_off, int32_t* s_carry_p, int tid, Sync sync) {
+                         int32_t* s_cnt, int32_t* s_off, int32_t* s_carry_p, int tid, Sync sync,
+                         int carry0 = 0, bool write_first = true) {
   constexpr int kWarps = kThreads / 32;
   constexpr int CH = kWarps * kIPW;
   const int warp = tid >> 5, lane = tid & 31;
@@ -87,8 +88,8 @@ __device__ void scan_cta(const uint8_t* __restrict__ keep, int B, int N, int32_t
   const uint32_t lt = (1u << lane) - 1u;
   int32_t& s_carry = *s_carry_p;
   if (tid == 0) {
-    cu[0] = 0;
-    s_carry = 0;
+    if (write_first) cu[0] = carry0;
+    s_carry = carry0;
   }
   for (int base = 0; base < B; base += CH) {
     // phase A: load keep bytes of kIPW images per warp (all loads in flight), ballot.
@@ -378,6 +379,7 @@ struct AttnArgs {
                            // 2: every head-0 CTA counts the keeps before its image
   int B, N, H;
   long long ld;            // input token stride in elements
+  int cu_groups;           // cu_mode 1: scan items (mma engine: one per 128 images; tcgen05: 1)
 };
 
 // Zero (+0.0) the 128-byte head slices of dropped rows sDrop[first], [first +
@@ -528,6 +530,50 @@ __device__ __forceinline__ void scan_cta_cu(const AttnArgs& a, uint8_t* scratch,
                                    c + 2 * CH, tid, sync);
 }
 
+// Kept bytes of keep[0, len): count_kept with eight 16-byte loads per thread in
+// flight (bandwidth-bound on long prefixes).
+__device__ __forceinline__ int count_kept_wide(const uint8_t* __restrict__ keep, long long len, int t,
+                                               int nthr) {
+  if ((reinterpret_cast<uintptr_t>(keep) & 15) != 0) return count_kept(keep, len, t, nthr);
+  const uint4* k4 = reinterpret_cast<const uint4*>(keep);
+  const long long nfull = len >> 4;
+  int cnt = 0;
+  long long c = t;
+  for (; c + 7LL * nthr < nfull; c += 8LL * nthr) {
+    uint4 v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = __ldg(k4 + c + (long long)u * nthr);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) cnt += popc_nonzero16(v[u]);
+  }
+  for (; c < nfull; c += nthr) cnt += popc_nonzero16(__ldg(k4 + c));
+  for (long long p = (nfull << 4) + t; p < len; p += nthr) cnt += keep[p] != 0 ? 1 : 0;
+  return cnt;
+}
+
+// cu_mode 1 on the mma.sync engine: scan item g of a.cu_groups writes cu_seqlens
+// for images [g0, g1): its offset cu[g0] is the count of keeps in images [0, g0)
+// (one streaming pass over that prefix), then scan_cta continues from it.  The
+// groups run concurrently with the attention items instead of one CTA walking
+// the whole mask (B = 4096: one scan CTA was the kernel's critical path).
+__device__ __forceinline__ void scan_group_cu(const AttnArgs& a, int g, uint8_t* scratch, int tid) {
+  constexpr int CH = kAttnThreads / 32 * 8;
+  const int G = a.cu_groups;
+  const int g0 = (int)((long long)a.B * g / G), g1 = (int)((long long)a.B * (g + 1) / G);
+  uint32_t* w = reinterpret_cast<uint32_t*>(scratch);
+  int32_t* c = reinterpret_cast<int32_t*>(w + CH * 8);
+  int32_t* red = c + 3 * CH + 1;
+  int cnt = count_kept_wide(a.keep, (long long)g0 * a.N, tid, kAttnThreads);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+  if ((tid & 31) == 0) red[tid >> 5] = cnt;
+  __syncthreads();
+  const int offset = red[0] + red[1] + red[2] + red[3];
+  scan_cta<kAttnThreads, 8, false>(a.keep + (long long)g0 * a.N, g1 - g0, a.N, a.cu_out + g0, nullptr,
+                                   nullptr, w, c, c + CH, c + 2 * CH, tid, [] { __syncthreads(); },
+                                   offset, g == 0);
+}
+
 // The rows of problem (image b, one head): kept positions sPos[0, n) (ascending,
 // R7) and dropped positions sDrop[0, N - n).
 //   fused:  ballots of the keep row + popc ranks (no cross-image prefix needed);
@@ -609,8 +655,8 @@ __global__ void __launch_bounds__(kAttnThreads, 3) attn_kernel(const AttnArgs a,
   int bid = blockIdx.x;
   if constexpr (kFused) {
     if (a.cu_mode == 1) {
-      if (bid == 0) {  // the scan CTA: cu_seqlens only, concurrent with the rest
-        scan_cta_cu(a, sK, tid, [] { __syncthreads(); });
+      if (bid < a.cu_groups) {  // scan CTAs: cu_seqlens only, concurrent with the rest
+        scan_group_cu(a, bid, sK, tid);
         if constexpr (kGather) {
           if (ga.state != nullptr) {
             __syncthreads();
@@ -619,7 +665,7 @@ __global__ void __launch_bounds__(kAttnThreads, 3) attn_kernel(const AttnArgs a,
         }
         return;
       }
-      bid -= 1;
+      bid -= a.cu_groups;
     }
   }
   const int b = bid / a.H, h = bid - b * a.H;   // head fastest
@@ -1108,12 +1154,13 @@ cudaError_t launch_fused(int dtype, int engine, const uint8_t* keep, const void*
   // Small batches: each head-0 CTA derives its own cu[b] (no extra CTA on the
   // critical path); large: one extra scan CTA / work item, hidden by the rest.
   a.cu_mode = cu_out == nullptr ? 0 : ((long long)B * N <= 65536 ? 2 : 1);
+  a.cu_groups = a.cu_mode != 1 ? 0 : (engine == 2 ? 1 : (B + 127) / 128);
 
   a.B = B;
   a.N = N;
   a.H = H;
   a.ld = ld;
-  return dispatch_attn<true>(dtype, engine, a, B * H + (a.cu_mode == 1 ? 1 : 0), st);
+  return dispatch_attn<true>(dtype, engine, a, B * H + a.cu_groups, st);
 }
 
 // Fused pack-attend-unpack whose padded output (and/or CLS rows) is written to
@@ -1128,11 +1175,12 @@ cudaError_t launch_fused_gather(int dtype, const uint8_t* keep, const void* q, c
   a.v = v;
   a.cu_out = cu_out;
   a.cu_mode = cu_out == nullptr ? 0 : ((long long)B * N <= 65536 ? 2 : 1);
+  a.cu_groups = a.cu_mode == 1 ? (B + 127) / 128 : 0;
   a.B = B;
   a.N = N;
   a.H = H;
   a.ld = ld;
-  const int grid = B * H + (a.cu_mode == 1 ? 1 : 0);
+  const int grid = B * H + a.cu_groups;
   return dtype == 0 ? launch_attn_mma<__nv_bfloat16, true, true>(a, grid, st, g)
                     : launch_attn_mma<__half, true, true>(a, grid, st, g);
 }

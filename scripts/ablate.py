@@ -24,6 +24,7 @@ ap.add_argument("--steps", type=int, default=1000)
 ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--no-cu", action="store_true")
 ap.add_argument("--tag", default="")
+ap.add_argument("--sets", type=int, default=16)
 a = ap.parse_args()
 c = synth.CONFIGS[a.config]
 p = c["p"] if a.prune is None else a.prune
@@ -31,7 +32,7 @@ H = synth.PRESETS[c["preset"]]["H"]
 B, N = c["B"], 197
 q, k, v, keep = synth.make_inputs(B, N, H, p, c["method"], "bf16", seed=0)
 dev = torch.device("cuda")
-S = 16
+S = a.sets
 sets = [[t.to(dev) for t in (q, k, v, keep)] for _ in range(S)]
 outs = [torch.empty(B, N, H, 64, dtype=q.dtype, device=dev) for _ in range(S)]
 cus = [torch.empty(B + 1, dtype=torch.int32, device=dev) for _ in range(S)]
