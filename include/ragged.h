@@ -88,7 +88,9 @@ typedef struct {
  *   dst[b*N+n] = cu[b] + #{n' < n : keep[b,n'] != 0} if keep[b,n] != 0, else -1
  *   src[dst[i]] = i for every kept i (stable: ascending position within an
  *   image, image-major -- DESIGN.md R7); src[r] for r >= cu[B] is untouched.
- * Deterministic, bit-exact.  One launch. */
+ * Deterministic, bit-exact.  One launch: for B*N <= 65536 one CTA per image
+ * (cu[b] from a count of the keeps of images [0, b), ranks by warp ballots);
+ * larger batches one CTA walking the mask as a flat prefix sum. */
 RAGGED_API ragged_status ragged_scan(const ragged_problem* prob, const uint8_t* keep,
                           int32_t* cu_seqlens, int32_t* dst_index, int32_t* src_index,
                           void* stream);
@@ -96,7 +98,10 @@ RAGGED_API ragged_status ragged_scan(const ragged_problem* prob, const uint8_t* 
 /* a1 + a2 -- pack.  Runs ragged_scan, then gathers the kept rows:
  *   qp[r] = q[src[r]], kp[r] = k[src[r]], vp[r] = v[src[r]] for r < cu[B]
  * (bit copies; whole H*d rows).  Rows >= cu[B] of the
- * packed buffers are untouched.  Two launches (scan, gather). */
+ * packed buffers are untouched.  For B*N <= 65536 ONE launch (one CTA per
+ * (image, head): the scan of its image as in ragged_scan, written by the head-0
+ * CTA, then the head's 128-byte row slices); larger batches two launches
+ * (ragged_scan's flat scan, then a row gather). */
 RAGGED_API ragged_status ragged_pack(const ragged_problem* prob, const uint8_t* keep,
                           const void* q, const void* k, const void* v,
                           int32_t* cu_seqlens, int32_t* dst_index, int32_t* src_index,

@@ -133,11 +133,9 @@ ragged_status ragged_pack(const ragged_problem* prob, const uint8_t* keep, const
   RAGGED_TRY(check_ptr(kp, "kp"));
   RAGGED_TRY(check_ptr(vp, "vp"));
   cudaStream_t st = as_stream(stream);
-  cudaError_t e = ragged::launch_scan(keep, prob->B, prob->N, cu_seqlens, dst_index, src_index, st);
-  if (e != cudaSuccess) return cuda_fail(e, "ragged_pack/scan");
-  e = ragged::launch_pack(q, k, v, prob->ld, prob->B, prob->N, prob->H, cu_seqlens, src_index, qp,
-                          kp, vp, st);
-  return e == cudaSuccess ? RAGGED_OK : cuda_fail(e, "ragged_pack/gather");
+  cudaError_t e = ragged::launch_scan_pack(keep, q, k, v, prob->ld, prob->B, prob->N, prob->H, cu_seqlens,
+                                           dst_index, src_index, qp, kp, vp, st);
+  return e == cudaSuccess ? RAGGED_OK : cuda_fail(e, "ragged_pack");
 }
 
 ragged_status ragged_attn(const ragged_problem* prob, const void* qp, const void* kp,

@@ -492,8 +492,16 @@ __device__ __forceinline__ int prefix_count(const PrefixLoads& L, const uint8_t*
 #pragma unroll
     for (int i = 0; i < kCntU; ++i) cnt += popc_nonzero16(L.v[i]);
     const long long nfull = len >> 4;
-    for (long long c = t + (long long)kCntU * nthr; c < nfull; c += nthr)
-      cnt += popc_nonzero16(*reinterpret_cast<const uint4*>(keep + (c << 4)));
+    const uint4* k4 = reinterpret_cast<const uint4*>(keep);
+    long long c = t + (long long)kCntU * nthr;
+    for (; c + 7LL * nthr < nfull; c += 8LL * nthr) {  // long prefixes: 8 loads in flight
+      uint4 v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = __ldg(k4 + c + (long long)u * nthr);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) cnt += popc_nonzero16(v[u]);
+    }
+    for (; c < nfull; c += nthr) cnt += popc_nonzero16(__ldg(k4 + c));
     p = (nfull << 4) + t;
   }
   for (; p < len; p += nthr) cnt += keep[p] != 0 ? 1 : 0;
@@ -572,6 +580,110 @@ __device__ __forceinline__ void scan_group_cu(const AttnArgs& a, int g, uint8_t*
   scan_cta<kAttnThreads, 8, false>(a.keep + (long long)g0 * a.N, g1 - g0, a.N, a.cu_out + g0, nullptr,
                                    nullptr, w, c, c + CH, c + 2 * CH, tid, [] { __syncthreads(); },
                                    offset, g == 0);
+}
+
+// a1 / a2 for small batches (B*N <= 65536) in ONE launch, one CTA per image
+// (scan) or per (image, head) (pack = scan + gather).  The definition
+// per image: cu[b] = #keeps in images [0, b) -- a streaming count of that
+// prefix issued together with the image's own keep row (one memory round
+// trip) -- and the kept positions' ranks by warp ballots (R7 order).  The
+// head-0 CTA writes cu[b] (cu[B] by the last image), dst and src for the
+// image; with kPack every CTA then copies its head's 128-byte slices of the
+// kept q/k/v rows to packed rows cu[b] + rank.  No global scan pass, no second
+// launch.  Larger batches use scan_kernel + pack_kernel (the prefix count
+// would grow with B).
+constexpr int kImgThreads = 128;
+
+template <bool kPack>
+__global__ void __launch_bounds__(kImgThreads)
+    image_scan_kernel(const uint8_t* __restrict__ keep, int B, int N, int H, int32_t* __restrict__ cu,
+                      int32_t* __restrict__ dst, int32_t* __restrict__ src, const uint8_t* __restrict__ q,
+                      const uint8_t* __restrict__ k, const uint8_t* __restrict__ v, long long ld_bytes,
+                      uint8_t* __restrict__ qp, uint8_t* __restrict__ kp, uint8_t* __restrict__ vp) {
+  __shared__ int16_t sPos[kMaxN];
+  __shared__ uint32_t sWords[16];
+  pdl_launch_dependents();
+  pdl_wait_prerequisites();
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int b = kPack ? (int)(blockIdx.x / H) : (int)blockIdx.x;
+  const int h = kPack ? (int)(blockIdx.x - (unsigned)b * H) : 0;
+  const long long img0 = (long long)b * N;
+  const uint8_t* km = keep + img0;
+  const int p0 = tid, p1 = tid + kImgThreads;
+  const uint8_t m0 = p0 < N ? km[p0] : (uint8_t)0;
+  const uint8_t m1 = p1 < N ? km[p1] : (uint8_t)0;
+  PrefixLoads pl;
+  prefix_loads(pl, keep, img0, tid, kImgThreads);
+  int c = prefix_count(pl, keep, img0, tid, kImgThreads);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  const bool k0 = m0 != 0, k1 = m1 != 0;
+  const uint32_t w0 = __ballot_sync(0xffffffffu, k0);
+  const uint32_t w1 = __ballot_sync(0xffffffffu, k1);
+  if (lane == 0) {
+    sWords[warp] = w0;
+    sWords[4 + warp] = w1;
+    sWords[8 + warp] = (uint32_t)c;
+  }
+  __syncthreads();
+  const int base = (int)(sWords[8] + sWords[9] + sWords[10] + sWords[11]);
+  int pre0 = 0, pre1 = 0, n = 0;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const int cj = __popc(sWords[j]);
+    pre0 += j < warp ? cj : 0;
+    pre1 += j < 4 + warp ? cj : 0;
+    n += cj;
+  }
+  const uint32_t lt = (1u << lane) - 1u;
+  const int r0 = pre0 + __popc(w0 & lt), r1 = pre1 + __popc(w1 & lt);
+  if (h == 0) {
+    if (p0 < N) {
+      dst[img0 + p0] = k0 ? base + r0 : -1;
+      if (k0) src[base + r0] = (int32_t)(img0 + p0);
+    }
+    if (p1 < N) {
+      dst[img0 + p1] = k1 ? base + r1 : -1;
+      if (k1) src[base + r1] = (int32_t)(img0 + p1);
+    }
+    if (tid == 0) {
+      cu[b] = base;
+      if (b == B - 1) cu[B] = base + n;
+    }
+  }
+  if constexpr (kPack) {
+    if (k0) sPos[r0] = (int16_t)p0;
+    if (k1) sPos[r1] = (int16_t)p1;
+    __syncthreads();
+    // 8 threads per 128-byte head slice, 16 rows per pass, 4 passes' loads in flight
+    const int ch = (tid & 7) * 16, rr = tid >> 3;
+    const long long row_bytes = (long long)H * kRowBytes;
+    const long long soff = img0 * ld_bytes + h * kRowBytes + ch;
+    const long long doff = (long long)base * row_bytes + h * kRowBytes + ch;
+    for (int r = rr; r < n; r += 64) {
+      uint4 vq[4], vk[4], vv[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int ru = r + 16 * u;
+        if (ru < n) {
+          const long long so = soff + sPos[ru] * ld_bytes;
+          vq[u] = ld_global_nc_16(q + so);
+          vk[u] = ld_global_nc_16(k + so);
+          vv[u] = ld_global_nc_16(v + so);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int ru = r + 16 * u;
+        if (ru < n) {
+          const long long d = doff + ru * row_bytes;
+          st_global_16(qp + d, vq[u]);
+          st_global_16(kp + d, vk[u]);
+          st_global_16(vp + d, vv[u]);
+        }
+      }
+    }
+  }
 }
 
 // The rows of problem (image b, one head): kept positions sPos[0, n) (ascending,
@@ -1047,9 +1159,33 @@ static cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, siz
   return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 
+// Batches whose prefix counts stay short run one CTA per image (a1 in one
+// memory round trip); larger ones the single-CTA flat scan.
+constexpr long long kImageScanMaxBN = 65536;
+
 cudaError_t launch_scan(const uint8_t* keep, int B, int N, int32_t* cu, int32_t* dst, int32_t* src,
                         cudaStream_t st) {
+  if ((long long)B * N <= kImageScanMaxBN)
+    return launch_pdl(image_scan_kernel<false>, dim3(B), dim3(kImgThreads), 0, st, keep, B, N, 1, cu,
+                      dst, src, (const uint8_t*)nullptr, (const uint8_t*)nullptr,
+                      (const uint8_t*)nullptr, 0LL, (uint8_t*)nullptr, (uint8_t*)nullptr,
+                      (uint8_t*)nullptr);
   return launch_pdl(scan_kernel, dim3(1), dim3(kScanThreads), 0, st, keep, B, N, cu, dst, src);
+}
+
+// a1 + a2: one launch (one CTA per (image, head)) for small batches, else
+// scan_kernel then pack_kernel.  Returns the first failing launch's error.
+cudaError_t launch_scan_pack(const uint8_t* keep, const void* q, const void* k, const void* v,
+                             long long ld_elems, int B, int N, int H, int32_t* cu, int32_t* dst,
+                             int32_t* src, void* qp, void* kp, void* vp, cudaStream_t st) {
+  if ((long long)B * N <= kImageScanMaxBN && (long long)B * H <= 0x7fffffffLL)
+    return launch_pdl(image_scan_kernel<true>, dim3(B * H), dim3(kImgThreads), 0, st, keep, B, N, H,
+                      cu, dst, src, static_cast<const uint8_t*>(q), static_cast<const uint8_t*>(k),
+                      static_cast<const uint8_t*>(v), ld_elems * 2, static_cast<uint8_t*>(qp),
+                      static_cast<uint8_t*>(kp), static_cast<uint8_t*>(vp));
+  cudaError_t e = launch_scan(keep, B, N, cu, dst, src, st);
+  if (e != cudaSuccess) return e;
+  return launch_pack(q, k, v, ld_elems, B, N, H, cu, src, qp, kp, vp, st);
 }
 
 cudaError_t launch_pack(const void* q, const void* k, const void* v, long long ld_elems, int B, int N,

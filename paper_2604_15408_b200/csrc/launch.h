@@ -10,6 +10,10 @@ cudaError_t launch_scan(const uint8_t* keep, int B, int N, int32_t* cu, int32_t*
 cudaError_t launch_pack(const void* q, const void* k, const void* v, long long ld_elems, int B, int N,
                         int H, const int32_t* cu, const int32_t* src, void* qp, void* kp, void* vp,
                         cudaStream_t st);
+// a1 + a2 (ragged_pack): one launch for B*N <= 65536, else launch_scan + launch_pack
+cudaError_t launch_scan_pack(const uint8_t* keep, const void* q, const void* k, const void* v,
+                             long long ld_elems, int B, int N, int H, int32_t* cu, int32_t* dst,
+                             int32_t* src, void* qp, void* kp, void* vp, cudaStream_t st);
 // engine: 1 = mma.sync, 2 = tcgen05 (api.cu resolves RAGGED_ENGINE_AUTO)
 cudaError_t launch_attn(int dtype, int engine, const void* qp, const void* kp, const void* vp, const int32_t* cu,
                         void* op, int B, int N, int H, long long ld, cudaStream_t st);
