@@ -872,7 +872,8 @@ def n4_general_extras(rb, torch, dev, dt):
     import numpy as np
     import synth
     res = {}
-    cases = [("vit_l16_384_B8_N577_H16_d64_p0", 8, 577, 16, 64, 0.0),
+    cases = [("deit_b_C3_B32_N197_H12_d64_p0.8", 32, 197, 12, 64, 0.8),
+             ("vit_l16_384_B8_N577_H16_d64_p0", 8, 577, 16, 64, 0.0),
              ("vit_l16_384_B8_N577_H16_d64_p0.7", 8, 577, 16, 64, 0.7),
              ("seq1024_B8_H12_d64_p0.5", 8, 1024, 12, 64, 0.5),
              ("deit_shape_B32_N197_H6_d128_p0.8", 32, 197, 6, 128, 0.8),
@@ -899,6 +900,15 @@ def n4_general_extras(rb, torch, dev, dt):
                                              100)
         except Exception as ex:
             r["fa2_varlen_error"] = repr(ex)[:120]
+        # fp8 (E4M3) inputs, per-tensor scales (ragged_attn_fp8): half the input bytes
+        try:
+            q8, k8, v8 = ((t.float() / (float(t.abs().max()) / 448.0)).to(torch.float8_e4m3fn) for t in (qp, kp, vp))
+            o8 = torch.empty_like(qp)
+            r["fp8_us"] = _graph_time(torch, [lambda: rb.attn_fp8(q8, k8, v8, cu, N, (1.0, 1.0, 1.0),
+                                                                  out_dtype=dt, op=o8)], 100)
+            r["fp8_hbm_GBps"] = (3.0 * T * H * d + T * H * d * 2) / r["fp8_us"] / 1e3
+        except Exception as ex:
+            r["fp8_error"] = repr(ex)[:120]
         res[name] = r
     return res
 

@@ -125,6 +125,21 @@ RAGGED_API ragged_status ragged_attn(const ragged_problem* prob, const void* qp,
                           const void* vp, const int32_t* cu_seqlens, void* op,
                           void* stream);
 
+/* NEXT row N4 -- fp8 inputs.  ragged_attn with q/k/v stored as FP8 E4M3
+ * bytes (OCP e4m3fn: bias 7, 3 mantissa bits, max 448, no infinities) and
+ * per-tensor dequantisation scales: with Qd = descale_q * q (exact value of
+ * each byte times the scale), likewise Kd, Vd, for every image i and head h:
+ *   op[s:s+n, h, :] = softmax(Qd Kd^T / sqrt(d)) Vd       (as ragged_attn)
+ * Inputs rows are prob->ld BYTES apart (multiple of 16; H*d for packed
+ * [cap, H, d] buffers); prob->d in {32, 64, 80, 128}; N up to 2^20.  The output
+ * type is prob->dtype (RAGGED_BF16 / RAGGED_FP16), rows H*d elements apart.
+ * The bytes are widened exactly to fp16 in shared memory; QK^T and PV run on
+ * the fp16 tensor-core path (fp32 accumulation, P split hi + lo, R2).
+ * Non-finite scales -> RAGGED_EINVAL.  One launch. */
+RAGGED_API ragged_status ragged_attn_fp8(const ragged_problem* prob, const uint8_t* qp, const uint8_t* kp,
+                              const uint8_t* vp, float descale_q, float descale_k, float descale_v,
+                              const int32_t* cu_seqlens, void* op, void* stream);
+
 /* a4 -- unpack.  o[i] = op[dst[i]] if dst[i] >= 0, else +0.0 (bit pattern 0)
  * for every padded row i < B*N (R10).  One launch. */
 RAGGED_API ragged_status ragged_unpack(const ragged_problem* prob, const void* op,

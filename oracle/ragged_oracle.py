@@ -28,6 +28,11 @@ Passages followed (PAPER.md line numbers):
              dropped positions hold +0.0 (reading R10; not in the paper).
   fused      pack_attend_unpack = unpack o attention o pack (BASELINE.json).
 
+  fp8        (NEXT row N4) ragged attention over FP8 E4M3 inputs with
+             per-tensor scales: the bytes are decoded by the OCP E4M3 formula
+             (reading R23; not in the paper) and the plain attention above is
+             applied to the dequantised values.
+
   prune      (NEXT row N2) Threshold-l2 keep mask: l2 norm of each token's
              hidden state, CLS + top-(k-1) (R20).
 
@@ -174,3 +179,26 @@ def attention_image_head(q, k, v, keep, b: int, h: int):
     pos = np.flatnonzero(np.asarray(keep[b]) != 0)
     qb, kb, vb = (as_f64(t[b, pos, h]) for t in (q, k, v))
     return pos, attention_one(qb, kb, vb)
+
+
+def e4m3_decode(b) -> np.ndarray:
+    """FP8 E4M3 (OCP "e4m3fn") bytes -> exact float64 values (reading R23):
+    sign s = bit 7, exponent e = bits 6..3 (bias 7), mantissa m = bits 2..0;
+    e = 0: (-1)^s * m/8 * 2^-6 (subnormal); e = 15 and m = 7: NaN; otherwise
+    (-1)^s * (1 + m/8) * 2^(e-7).  No infinities; max finite 448."""
+    b = np.asarray(b, dtype=np.uint8).astype(np.int64)
+    s = np.where(b >> 7 == 1, -1.0, 1.0)
+    e = (b >> 3) & 0xF
+    m = (b & 0x7).astype(np.float64)
+    val = np.where(e == 0, m / 8.0 * 2.0 ** -6, (1.0 + m / 8.0) * np.power(2.0, (e - 7).astype(np.float64)))
+    val = np.where((e == 15) & (b & 0x7 == 7), np.nan, val)
+    return s * val
+
+
+def attention_fp8(q8, k8, v8, descale, cu) -> np.ndarray:
+    """NEXT row N4: packed FP8 E4M3 q/k/v bytes (uint8 arrays [T, H, d]) with
+    per-tensor descale factors (dq, dk, dv): attention() of dq*decode(q),
+    dk*decode(k), dv*decode(v)."""
+    dq, dk, dv = (float(x) for x in descale)
+    return attention(e4m3_decode(q8) * dq, e4m3_decode(k8) * dk, e4m3_decode(v8) * dv, cu)
+

@@ -99,6 +99,7 @@ def _load() -> ctypes.CDLL:
         "ragged_pack": [P, V, V, V, V, V, V, V, V, V, V, V],
         "ragged_attn": [P, V, V, V, V, V, V],
         "ragged_unpack": [P, V, V, V, V],
+        "ragged_attn_fp8": [P, V, V, V, ctypes.c_float, ctypes.c_float, ctypes.c_float, V, V, V],
         "ragged_pack_attend_unpack": [P, V, V, V, V, V, V, V],
         "ragged_pack_attend_unpack_host": [P, V, V, V, V, V, V, V],
         "ragged_graph_create": [P, V, V, V, V, V, V, ctypes.POINTER(V)],
@@ -133,7 +134,7 @@ def _load() -> ctypes.CDLL:
 _lib = None
 
 EXPORTS = ("ragged_scan", "ragged_pack", "ragged_attn", "ragged_unpack", "ragged_pack_attend_unpack",
-           "ragged_pack_attend_unpack_host",
+           "ragged_pack_attend_unpack_host", "ragged_attn_fp8",
            "ragged_graph_create", "ragged_graph_launch", "ragged_graph_destroy", "ragged_empty_launch",
            "ragged_validate_cu_seqlens", "ragged_status_str", "ragged_last_error", "ragged_build_info",
            "ragged_keep_topk_l2", "ragged_pack_attend_unpack_gather", "ragged_attn_gather",
@@ -262,6 +263,27 @@ def attn(qp, kp, vp, cu, N: int, op=None, stream=None, engine=ENGINE_AUTO):
     p = problem(B, N, H, d, qp.dtype, ld, engine)
     _check(lib().ragged_attn(ctypes.byref(p), qp.data_ptr(), kp.data_ptr(), vp.data_ptr(), cu.data_ptr(),
                             op.data_ptr(), _stream(stream)), "ragged_attn")
+    return op
+
+
+def attn_fp8(qp, kp, vp, cu, N: int, descale=(1.0, 1.0, 1.0), out_dtype=torch.bfloat16, op=None,
+             stream=None):
+    """NEXT row N4: ragged_attn over packed FP8 E4M3 q/k/v ([cap, H, d],
+    torch.float8_e4m3fn or uint8 bytes) with per-tensor descale factors
+    (descale_q, descale_k, descale_v); output in out_dtype (bf16 / fp16)."""
+    if qp.dim() != 3:
+        raise ValueError("qp/kp/vp must be packed [cap, H, d]")
+    cap, H, d = qp.shape
+    for t in (qp, kp, vp):
+        if t.dtype not in (torch.float8_e4m3fn, torch.uint8) or t.shape != qp.shape or not t.is_contiguous():
+            raise ValueError("qp/kp/vp must be contiguous float8_e4m3fn/uint8 [cap, H, d] of one shape")
+    if out_dtype not in _DTYPE:
+        raise ValueError("out_dtype must be bf16 or fp16")
+    op = torch.empty(cap, H, d, dtype=out_dtype, device=qp.device) if op is None else op
+    p = problem(len(cu) - 1, N, H, d, out_dtype, H * d)
+    dq, dk, dv = (float(x) for x in descale)
+    _check(lib().ragged_attn_fp8(ctypes.byref(p), qp.data_ptr(), kp.data_ptr(), vp.data_ptr(), dq, dk, dv,
+                                 cu.data_ptr(), op.data_ptr(), _stream(stream)), "ragged_attn_fp8")
     return op
 
 

@@ -4,6 +4,7 @@
 // attribute setting after the first call, no device->host traffic): the
 // paper's diagnosis is that this host path is the bottleneck at ViT lengths
 // (P:336-345).
+#include <cmath>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -158,6 +159,27 @@ ragged_status ragged_attn(const ragged_problem* prob, const void* qp, const void
   cudaError_t e = ragged::launch_attn(prob->dtype, resolve_engine(prob), qp, kp, vp, cu_seqlens, op, prob->B, prob->N,
                                       prob->H, prob->ld, as_stream(stream));
   return e == cudaSuccess ? RAGGED_OK : cuda_fail(e, "ragged_attn");
+}
+
+ragged_status ragged_attn_fp8(const ragged_problem* prob, const uint8_t* qp, const uint8_t* kp,
+                              const uint8_t* vp, float descale_q, float descale_k, float descale_v,
+                              const int32_t* cu_seqlens, void* op, void* stream) {
+  RAGGED_TRY(check_problem(prob, true));
+  if (prob->ld % 16 != 0) return fail(RAGGED_EALIGN, "fp8: ld % 16 != 0 (rows must be 16-byte aligned)");
+  if (!std::isfinite(descale_q) || !std::isfinite(descale_k) || !std::isfinite(descale_v))
+    return fail(RAGGED_EINVAL, "fp8: descale factors must be finite");
+  if (prob->B == 0) return RAGGED_OK;
+  RAGGED_TRY(check_ptr(qp, "qp"));
+  RAGGED_TRY(check_ptr(kp, "kp"));
+  RAGGED_TRY(check_ptr(vp, "vp"));
+  RAGGED_TRY(check_ptr_any(cu_seqlens, "cu_seqlens"));
+  RAGGED_TRY(check_ptr(op, "op"));
+  if ((long long)prob->B * prob->H * ((prob->N + 63) / 64) > 0x7fffffffLL)
+    return fail(RAGGED_ENOTSUP, "too many query blocks");
+  cudaError_t e = ragged::launch_attn_general_f8(prob->dtype, prob->d, qp, kp, vp, descale_q, descale_k,
+                                                 descale_v, cu_seqlens, op, prob->B, prob->N, prob->H, prob->ld,
+                                                 as_stream(stream));
+  return e == cudaSuccess ? RAGGED_OK : cuda_fail(e, "ragged_attn_fp8");
 }
 
 ragged_status ragged_unpack(const ragged_problem* prob, const void* op, const int32_t* dst_index,

@@ -10,9 +10,11 @@
 //
 // The DeiT path (d = 64, N <= 256) keeps the specialised kernels of
 // kernels.cu; this kernel serves the shapes they reject.
+#include <cuda_fp8.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <type_traits>
 #include <utility>
 
 #include "device.cuh"
@@ -32,17 +34,55 @@ template <int D>
 __host__ __device__ constexpr int gen_smem_bytes() {
   return (kGenQRows + 4 * kGenChunk) * gen_row_stride<D>();  // Q + K[2] + V[2]
 }
+// kF8: + raw e4m3 staging rows for Q and one K / V chunk (D bytes per row)
+template <int D>
+__host__ __device__ constexpr int gen_smem_bytes_f8() {
+  return gen_smem_bytes<D>() + (kGenQRows + 2 * kGenChunk) * D;
+}
+
+// `rows` raw e4m3 rows (D bytes, contiguous in `raw`) -> fp16 rows of `dst`
+// (row stride RS); exact (every e4m3 value is an fp16 value).
+template <int D>
+__device__ __forceinline__ void f8_rows_to_f16(const uint8_t* raw, uint8_t* dst, int rows, int tid) {
+  constexpr int CH8 = D / 16;  // 16-byte raw chunks per row
+  for (int i = tid; i < rows * CH8; i += kGenThreads) {
+    const int r = i / CH8, c = i - r * CH8;
+    const uint4 v = *reinterpret_cast<const uint4*>(raw + r * D + c * 16);
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+    uint32_t h[8];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const __half2_raw lo = __nv_cvt_fp8x2_to_halfraw2((__nv_fp8x2_storage_t)(w[e] & 0xffffu), __NV_E4M3);
+      const __half2_raw hi = __nv_cvt_fp8x2_to_halfraw2((__nv_fp8x2_storage_t)(w[e] >> 16), __NV_E4M3);
+      h[2 * e] = (uint32_t)lo.x | ((uint32_t)lo.y << 16);
+      h[2 * e + 1] = (uint32_t)hi.x | ((uint32_t)hi.y << 16);
+    }
+    uint8_t* d = dst + r * gen_row_stride<D>() + c * 32;
+    *reinterpret_cast<uint4*>(d) = make_uint4(h[0], h[1], h[2], h[3]);
+    *reinterpret_cast<uint4*>(d + 16) = make_uint4(h[4], h[5], h[6], h[7]);
+  }
+}
 
 __device__ __forceinline__ void ldmatrix_x2(uint32_t addr, uint32_t& r0, uint32_t& r1) {
   asm volatile("ldmatrix.sync.aligned.m8n8.x2.shared.b16 {%0, %1}, [%2];\n" : "=r"(r0), "=r"(r1) : "r"(addr));
 }
 
-template <typename T, int D>
-__global__ void __launch_bounds__(kGenThreads) attn_general_kernel(const T* __restrict__ qp, const T* __restrict__ kp,
-                                                                  const T* __restrict__ vp,
-                                                                  const int32_t* __restrict__ cu, T* __restrict__ op,
-                                                                  int H, int qblocks, long long ld) {
+// kF8 (NEXT row N4, fp8 inputs): q/k/v hold e4m3 bytes (row stride ld
+// bytes); rows are staged raw and widened to fp16 in shared memory (T =
+// __half), scores are scaled by descale_q * descale_k, the output by descale_v
+// and rounded to TO.  Otherwise q/k/v/o are T (= TO), descales unused.
+template <typename T, int D, bool kF8 = false, typename TO = T>
+__global__ void __launch_bounds__(kGenThreads) attn_general_kernel(const void* __restrict__ qp_, const void* __restrict__ kp_,
+                                                                  const void* __restrict__ vp_,
+                                                                  const int32_t* __restrict__ cu, TO* __restrict__ op,
+                                                                  int H, int qblocks, long long ld, float dq, float dk,
+                                                                  float dv) {
+  using TI = typename std::conditional<kF8, uint8_t, T>::type;
+  const TI* qp = static_cast<const TI*>(qp_);
+  const TI* kp = static_cast<const TI*>(kp_);
+  const TI* vp = static_cast<const TI*>(vp_);
   constexpr int RS = gen_row_stride<D>();
+  constexpr int EPC = 16 / sizeof(TI);  // input elements per 16-byte chunk
   constexpr int CH = D / 8;        // 16-byte chunks per row
   constexpr int KS = D / 16;       // k16 steps of S = Q K^T
   constexpr int NT = D / 8;        // n8 tiles of O
@@ -50,6 +90,9 @@ __global__ void __launch_bounds__(kGenThreads) attn_general_kernel(const T* __re
   uint8_t* sQ = smem;
   uint8_t* sK = sQ + kGenQRows * RS;             // [2][64][RS]
   uint8_t* sV = sK + 2 * kGenChunk * RS;         // [2][64][RS]
+  uint8_t* rQ = sV + 2 * kGenChunk * RS;         // kF8: raw [64][D], K [64][D], V [64][D]
+  uint8_t* rK = rQ + kGenQRows * D;
+  uint8_t* rV = rK + kGenChunk * D;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, t4 = lane & 3;
 
@@ -63,33 +106,37 @@ __global__ void __launch_bounds__(kGenThreads) attn_general_kernel(const T* __re
   const int q0 = qb * kGenQRows;
   if (q0 >= n) return;
   const long long HD = (long long)H * D;
-  const T* gq = qp + (long long)s0 * ld + (long long)h * D;
-  const T* gk = kp + (long long)s0 * ld + (long long)h * D;
-  const T* gv = vp + (long long)s0 * ld + (long long)h * D;
+  const TI* gq = qp + (long long)s0 * ld + (long long)h * D;
+  const TI* gk = kp + (long long)s0 * ld + (long long)h * D;
+  const TI* gv = vp + (long long)s0 * ld + (long long)h * D;
+  constexpr int ICH = D / EPC;                 // 16-byte input chunks per row
+  constexpr int IRS = kF8 ? D : RS;            // destination row stride of the copies
+  uint8_t* const qdst = kF8 ? rQ : sQ;
 
   // Q block rows [q0, q0 + 64) (zero past n)
-  for (int i = tid; i < kGenQRows * CH; i += kGenThreads) {
-    const int r = i / CH, c = i - r * CH;
+  for (int i = tid; i < kGenQRows * ICH; i += kGenThreads) {
+    const int r = i / ICH, c = i - r * ICH;
     const bool ok = q0 + r < n;
-    cp_async_16(smem_u32(sQ + r * RS + c * 16), gq + (ok ? (long long)(q0 + r) * ld + c * 8 : 0), ok ? 16 : 0);
+    cp_async_16(smem_u32(qdst + r * IRS + c * 16), gq + (ok ? (long long)(q0 + r) * ld + c * EPC : 0),
+                ok ? 16 : 0);
   }
   auto load_kv = [&](int chunk, int buf) {
     const int k0 = chunk * kGenChunk;
-    uint8_t* dk = sK + buf * kGenChunk * RS;
-    uint8_t* dv = sV + buf * kGenChunk * RS;
-    for (int i = tid; i < kGenChunk * CH; i += kGenThreads) {
-      const int r = i / CH, c = i - r * CH;
+    uint8_t* dk = kF8 ? rK : sK + buf * kGenChunk * RS;
+    uint8_t* dv = kF8 ? rV : sV + buf * kGenChunk * RS;
+    for (int i = tid; i < kGenChunk * ICH; i += kGenThreads) {
+      const int r = i / ICH, c = i - r * ICH;
       const bool ok = k0 + r < n;
-      const long long off = ok ? (long long)(k0 + r) * ld + c * 8 : 0;
-      cp_async_16(smem_u32(dk + r * RS + c * 16), gk + off, ok ? 16 : 0);
-      cp_async_16(smem_u32(dv + r * RS + c * 16), gv + off, ok ? 16 : 0);
+      const long long off = ok ? (long long)(k0 + r) * ld + c * EPC : 0;
+      cp_async_16(smem_u32(dk + r * IRS + c * 16), gk + off, ok ? 16 : 0);
+      cp_async_16(smem_u32(dv + r * IRS + c * 16), gv + off, ok ? 16 : 0);
     }
   };
   const int nchunks = (n + kGenChunk - 1) / kGenChunk;
   load_kv(0, 0);
   cp_async_commit();
 
-  const float scale_log2 = 1.4426950408889634f * rsqrtf((float)D);
+  const float scale_log2 = 1.4426950408889634f * rsqrtf((float)D) * (kF8 ? dq * dk : 1.f);
   const bool warp_live = q0 + warp * 16 < n;
   uint32_t qf[KS][4];
   float o[NT][4];
@@ -100,6 +147,12 @@ __global__ void __launch_bounds__(kGenThreads) attn_general_kernel(const T* __re
   for (int c = 0; c < nchunks; ++c) {
     cp_async_wait_all();
     __syncthreads();  // chunk c (and Q) landed; every warp is done with chunk c - 1
+    if constexpr (kF8) {  // widen the raw e4m3 rows; the raw buffers are then free
+      if (c == 0) f8_rows_to_f16<D>(rQ, sQ, kGenQRows, tid);
+      f8_rows_to_f16<D>(rK, sK + (c & 1) * kGenChunk * RS, kGenChunk, tid);
+      f8_rows_to_f16<D>(rV, sV + (c & 1) * kGenChunk * RS, kGenChunk, tid);
+      __syncthreads();
+    }
     if (c + 1 < nchunks) load_kv(c + 1, (c + 1) & 1);
     cp_async_commit();
     if (c == 0 && warp_live) {
@@ -195,17 +248,17 @@ __global__ void __launch_bounds__(kGenThreads) attn_general_kernel(const T* __re
   l0 += __shfl_xor_sync(0xffffffffu, l0, 2);
   l1 += __shfl_xor_sync(0xffffffffu, l1, 1);
   l1 += __shfl_xor_sync(0xffffffffu, l1, 2);
-  const float inv0 = 1.f / l0, inv1 = 1.f / l1;
+  const float inv0 = (kF8 ? dv : 1.f) / l0, inv1 = (kF8 ? dv : 1.f) / l1;
   // epilogue: this warp's 16 Q rows in smem are dead -> stage O there, then
   // 16-byte row stores (rows past n are not written)
   uint8_t* stg = sQ + warp * 16 * RS;
 #pragma unroll
   for (int j = 0; j < NT; ++j) {
-    *reinterpret_cast<uint32_t*>(stg + g * RS + j * 16 + 4 * t4) = pack2<T>(o[j][0] * inv0, o[j][1] * inv0);
-    *reinterpret_cast<uint32_t*>(stg + (g + 8) * RS + j * 16 + 4 * t4) = pack2<T>(o[j][2] * inv1, o[j][3] * inv1);
+    *reinterpret_cast<uint32_t*>(stg + g * RS + j * 16 + 4 * t4) = pack2<TO>(o[j][0] * inv0, o[j][1] * inv0);
+    *reinterpret_cast<uint32_t*>(stg + (g + 8) * RS + j * 16 + 4 * t4) = pack2<TO>(o[j][2] * inv1, o[j][3] * inv1);
   }
   __syncwarp();
-  T* go = op + (long long)s0 * HD + (long long)h * D;
+  TO* go = op + (long long)s0 * HD + (long long)h * D;
   for (int i = lane; i < 16 * CH; i += 32) {
     const int r = i / CH, cc = i - r * CH;
     const int row = q0 + warp * 16 + r;
@@ -214,15 +267,17 @@ __global__ void __launch_bounds__(kGenThreads) attn_general_kernel(const T* __re
   }
 }
 
-template <typename T, int D>
+template <typename T, int D, bool kF8 = false, typename TO = T>
 static cudaError_t launch_general_t(const void* qp, const void* kp, const void* vp, const int32_t* cu, void* op,
-                                   int B, int N, int H, long long ld, cudaStream_t st) {
+                                   int B, int N, int H, long long ld, cudaStream_t st, float dq = 1.f,
+                                   float dk = 1.f, float dv = 1.f) {
   static bool done[64] = {false};
   int dev = 0;
   cudaGetDevice(&dev);
+  const int smem = kF8 ? gen_smem_bytes_f8<D>() : gen_smem_bytes<D>();
   if (dev >= 0 && dev < 64 && !done[dev]) {
-    cudaError_t e = cudaFuncSetAttribute(attn_general_kernel<T, D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         gen_smem_bytes<D>());
+    cudaError_t e = cudaFuncSetAttribute(attn_general_kernel<T, D, kF8, TO>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     done[dev] = true;
   }
@@ -230,15 +285,15 @@ static cudaError_t launch_general_t(const void* qp, const void* kp, const void* 
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)((long long)B * H * qblocks));
   cfg.blockDim = dim3(kGenThreads);
-  cfg.dynamicSmemBytes = gen_smem_bytes<D>();
+  cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, attn_general_kernel<T, D>, static_cast<const T*>(qp), static_cast<const T*>(kp),
-                            static_cast<const T*>(vp), cu, static_cast<T*>(op), H, qblocks, ld);
+  return cudaLaunchKernelEx(&cfg, attn_general_kernel<T, D, kF8, TO>, qp, kp, vp, cu, static_cast<TO*>(op), H,
+                            qblocks, ld, dq, dk, dv);
 }
 
 bool attn_general_supports(int d) { return d == 32 || d == 64 || d == 80 || d == 128; }
@@ -258,6 +313,25 @@ cudaError_t launch_attn_general(int dtype, int d, const void* qp, const void* kp
   }
   RAGGED_GEN(__half)
 #undef RAGGED_GEN
+}
+
+// fp8 (e4m3) inputs: out_dtype 0 = bf16, 1 = fp16 output
+cudaError_t launch_attn_general_f8(int out_dtype, int d, const void* qp, const void* kp, const void* vp,
+                                   float dq, float dk, float dv, const int32_t* cu, void* op, int B, int N, int H,
+                                   long long ld, cudaStream_t st) {
+#define RAGGED_GEN8(TO)                                                                                       \
+  switch (d) {                                                                                                \
+    case 32: return launch_general_t<__half, 32, true, TO>(qp, kp, vp, cu, op, B, N, H, ld, st, dq, dk, dv);   \
+    case 64: return launch_general_t<__half, 64, true, TO>(qp, kp, vp, cu, op, B, N, H, ld, st, dq, dk, dv);   \
+    case 80: return launch_general_t<__half, 80, true, TO>(qp, kp, vp, cu, op, B, N, H, ld, st, dq, dk, dv);   \
+    case 128: return launch_general_t<__half, 128, true, TO>(qp, kp, vp, cu, op, B, N, H, ld, st, dq, dk, dv); \
+    default: return cudaErrorInvalidValue;                                                                    \
+  }
+  if (out_dtype == 0) {
+    RAGGED_GEN8(__nv_bfloat16)
+  }
+  RAGGED_GEN8(__half)
+#undef RAGGED_GEN8
 }
 
 }  // namespace ragged

@@ -43,6 +43,10 @@ cudaError_t launch_attn_gather(int dtype, const void* qp, const void* kp, const 
 cudaError_t launch_empty(int grid, int block, cudaStream_t st);
 
 // ---- NEXT row N4 (attn_general.cu): d in {32, 64, 80, 128}, any N ----
+// NEXT row N4, fp8 (e4m3) inputs for ragged_attn (out_dtype 0 = bf16, 1 = fp16)
+cudaError_t launch_attn_general_f8(int out_dtype, int d, const void* qp, const void* kp, const void* vp,
+                                   float dq, float dk, float dv, const int32_t* cu, void* op, int B, int N, int H,
+                                   long long ld, cudaStream_t st);
 bool attn_general_supports(int d);
 cudaError_t launch_attn_general(int dtype, int d, const void* qp, const void* kp, const void* vp, const int32_t* cu,
                                 void* op, int B, int N, int H, long long ld, cudaStream_t st);

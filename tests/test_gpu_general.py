@@ -94,3 +94,42 @@ def test_general_deterministic_and_isolated():
     torch.cuda.synchronize()
     assert torch.equal(a.view(torch.int16), b.view(torch.int16))
     assert torch.equal(a[:333].view(torch.int16), c[:333].view(torch.int16))
+
+
+def _quant_e4m3(x):
+    """Per-tensor FP8 E4M3 quantisation with scale amax / 448 (an fp32 value)."""
+    s = float(np.float32(float(x.abs().max()) / 448.0))
+    return (x.float() / s).to(torch.float8_e4m3fn), s
+
+
+@pytest.mark.parametrize("d", [32, 64, 80, 128])
+@pytest.mark.parametrize("out", ["bf16", "fp16"])
+def test_general_fp8_inputs(d, out):
+    """NEXT row N4, fp8 inputs: packed E4M3 q/k/v + per-tensor descales
+    (ragged_attn_fp8) vs the oracle on the dequantised values (R23); ragged
+    lengths incl. empty, 1, tile edges and N > 256; output bf16 / fp16 within
+    the output type's tolerance."""
+    lengths = [197, 1, 0, 63, 64, 65, 130, 39, 300]
+    H = 3
+    qp, kp, vp, cu, N, T = _packed_case(lengths, H, d, "fp16", seed=100 + d)
+    (q8, sq), (k8, sk), (v8, sv) = (_quant_e4m3(t) for t in (qp, kp, vp))
+    cud = torch.from_numpy(cu.astype(np.int32)).to(DEV)
+    got = rb.attn_fp8(q8.to(DEV), k8.to(DEV), v8.to(DEV), cud, N, (sq, sk, sv), out_dtype=DT[out])
+    torch.cuda.synchronize()
+    u8 = lambda t: t.view(torch.uint8).numpy()  # noqa: E731
+    ref = oracle.attention_fp8(u8(q8), u8(k8), u8(v8), (sq, sk, sv), cu)
+    check_attention(to_np(got[:T]), ref, DT[out])
+
+
+def test_general_fp8_deit_shape_and_peaked():
+    """DeiT-B packing at 80 % (39 tokens/image, H = 12, d = 64) with peaked
+    scores (Q, K x 3 before quantisation)."""
+    lengths = [39] * 32
+    qp, kp, vp, cu, N, T = _packed_case(lengths, 12, 64, "bf16", seed=5, dist="peaked")
+    (q8, sq), (k8, sk), (v8, sv) = (_quant_e4m3(t) for t in (qp, kp, vp))
+    got = rb.attn_fp8(q8.to(DEV), k8.to(DEV), v8.to(DEV), torch.from_numpy(cu.astype(np.int32)).to(DEV), 197,
+                      (sq, sk, sv))
+    torch.cuda.synchronize()
+    u8 = lambda t: t.view(torch.uint8).numpy()  # noqa: E731
+    check_attention(to_np(got[:T]), oracle.attention_fp8(u8(q8), u8(k8), u8(v8), (sq, sk, sv), cu),
+                    torch.bfloat16)

@@ -337,3 +337,35 @@ def test_keep_topk_l2_invariants_and_table1_counts():
             kept, dropped = s[b][keep[b] == 1], s[b][keep[b] == 0]
             if dropped.size:
                 assert kept.min() >= dropped.max()                      # threshold property
+
+
+# ---------------------------------------------- N4: FP8 E4M3 decode (R23) ----
+
+def test_e4m3_decode_matches_torch_for_every_byte():
+    """The oracle's formula decode vs torch.float8_e4m3fn (library routine),
+    all 256 bytes (NaN at 0x7f / 0xff)."""
+    b = np.arange(256, dtype=np.uint8)
+    ref = torch.from_numpy(b).view(torch.float8_e4m3fn).double().numpy()
+    got = oracle.e4m3_decode(b)
+    assert np.array_equal(np.isnan(got), np.isnan(ref)) and np.isnan(got).sum() == 2
+    ok = ~np.isnan(ref)
+    assert np.array_equal(got[ok], ref[ok])
+
+
+def test_e4m3_decode_closed_forms():
+    d = oracle.e4m3_decode(np.array([0x00, 0x80, 0x38, 0xB8, 0x7E, 0x01, 0x08, 0x07, 0x40], np.uint8))
+    assert d.tolist() == [0.0, -0.0, 1.0, -1.0, 448.0, 2.0 ** -9, 2.0 ** -6, 7 * 2.0 ** -9, 2.0]
+
+
+def test_attention_fp8_is_attention_of_dequantised_inputs():
+    """attention_fp8 == attention on the decoded, scaled values; scaling V by
+    c scales O by c exactly (the oracle's fp64 arithmetic on dyadic scales)."""
+    rng = np.random.default_rng(3)
+    q8, k8, v8 = (rng.integers(0, 0x7E, size=(7, 2, 32), dtype=np.uint8) for _ in range(3))
+    cu = np.array([0, 3, 7])
+    a = oracle.attention_fp8(q8, k8, v8, (0.5, 0.25, 2.0), cu)
+    b = oracle.attention(oracle.e4m3_decode(q8) * 0.5, oracle.e4m3_decode(k8) * 0.25,
+                         oracle.e4m3_decode(v8) * 2.0, cu)
+    assert np.array_equal(a, b)
+    c = oracle.attention_fp8(q8, k8, v8, (0.5, 0.25, 4.0), cu)
+    assert np.array_equal(c, 2.0 * a)
