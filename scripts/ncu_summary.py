@@ -47,20 +47,28 @@ def rep_summary(rep):
     return launches
 
 
-def launches_summary(path):
+def launches_summary(path, split_ns=None):
+    """Per-kernel launch counts, mean duration and share of GPU time.  With
+    split_ns, launches longer than split_ns are reported as a separate group
+    (bench.py's zero-copy e2e launches read their inputs over PCIe and run
+    ~30x longer than the device-resident steps)."""
     rows = [r for r in csv.reader(open(path)) if len(r) > 5]
     hdr = rows[0]
-    ki, mi, vi, ui = (hdr.index(x) for x in ("Kernel Name", "Metric Name", "Metric Value", "Metric Unit"))
+    ki, mi, vi, ui, ii = (hdr.index(x) for x in ("Kernel Name", "Metric Name", "Metric Value", "Metric Unit", "ID"))
+    dur = {r[ii]: float(r[vi].replace(",", "")) for r in rows[1:] if r[mi] == "gpu__time_duration.sum"}
     d = defaultdict(lambda: defaultdict(list))
     units = {}
     for r in rows[1:]:
-        d[r[ki]][r[mi]].append(float(r[vi].replace(",", "")))
+        name = r[ki]
+        if split_ns is not None and dur.get(r[ii], 0.0) > split_ns:
+            name += f"  [launches > {split_ns / 1e3:g} us: pinned-host inputs (zero-copy e2e)]"
+        d[name][r[mi]].append(float(r[vi].replace(",", "")))
         units[r[mi]] = r[ui]
     total = sum(sum(m.get("gpu__time_duration.sum", [])) for m in d.values())
     out = []
     for k, m in d.items():
         t = m.get("gpu__time_duration.sum", [])
-        out.append({"kernel": k[:120], "launches": len(t), "mean_" + units.get("gpu__time_duration.sum", ""):
+        out.append({"kernel": k[:200], "launches": len(t), "mean_" + units.get("gpu__time_duration.sum", ""):
                     sum(t) / max(len(t), 1), "share_of_time": sum(t) / total if total else None,
                     **{f"mean_{mm}": sum(v) / len(v) for mm, v in m.items() if mm != "gpu__time_duration.sum"}})
     return sorted(out, key=lambda x: -(x["share_of_time"] or 0))
@@ -72,6 +80,7 @@ if __name__ == "__main__":
     ap.add_argument("--launches")
     ap.add_argument("--name", required=True)
     ap.add_argument("--note", default="")
+    ap.add_argument("--split-us", type=float, default=None)
     a = ap.parse_args()
     os.makedirs(PROF, exist_ok=True)
     res = {"note": a.note}
@@ -82,7 +91,7 @@ if __name__ == "__main__":
     if a.launches:
         res["source"] = os.path.basename(a.launches)
         res["ncu"] = "ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none"
-        res["kernels"] = launches_summary(a.launches)
+        res["kernels"] = launches_summary(a.launches, None if a.split_us is None else a.split_us * 1e3)
     with open(os.path.join(PROF, a.name + ".json"), "w") as f:
         json.dump(res, f, indent=1)
     print(json.dumps(res, indent=1)[:3000])
