@@ -393,10 +393,11 @@ def test_fused_host_rejects_pageable():
     assert st == rb.EINVAL and "pageable" in rb.last_error()
 
 
+@pytest.mark.parametrize("engine", ENGINES)
 @pytest.mark.parametrize("dtype", ["bf16", "fp16"])
 @pytest.mark.parametrize("B,H,p,method", [(64, 12, 0.5, "ats"), (200, 12, 0.7, "l2"), (150, 3, 0.0, "all"),
                                           (1000, 6, 0.9, "evit")])
-def test_fused_large_batch_bitwise(dtype, B, H, p, method):
+def test_fused_large_batch_bitwise(engine, dtype, B, H, p, method):
     """Multi-wave fused launches (more (image, head) problems than resident
     CTAs) equal the composed path (pack -> attn -> unpack) bit for bit; with
     B*N > 65536 cu_seqlens comes from ceil(B/128) concurrent scan items (each
@@ -404,9 +405,9 @@ def test_fused_large_batch_bitwise(dtype, B, H, p, method):
     must be exact."""
     q, k, v, keep = synth.make_inputs(B, 197, H, p, method, dtype, seed=31)
     qd, kd, vd, keepd = _dev(q, k, v, keep)
-    o1, cu1 = rb.pack_attend_unpack(qd, kd, vd, keepd, want_cu=True)
+    o1, cu1 = rb.pack_attend_unpack(qd, kd, vd, keepd, want_cu=True, engine=engine)
     qp, kp, vp, cu, dst, src = rb.pack(qd, kd, vd, keepd)
-    o2 = rb.unpack(rb.attn(qp, kp, vp, cu, 197), dst, B, 197)
+    o2 = rb.unpack(rb.attn(qp, kp, vp, cu, 197, engine=engine), dst, B, 197)
     torch.cuda.synchronize()
     assert torch.equal(cu1, cu)
     assert cu1.cpu().tolist() == oracle.scan(keep.numpy())[0].tolist()
