@@ -276,7 +276,8 @@ def main():
     def step(i, stream=None):
         s = sets[i % N_SETS]
         rb.pack_attend_unpack(s["q"], s["k"], s["v"], s["keep"], o=s["o"],
-                              cu=None if args.no_cu else s["cu"], stream=stream, engine=args.engine)
+                              cu=None if args.no_cu else s["cu"], stream=stream, engine=args.engine,
+                              n_hint=T // max(B, 1))
 
     # warm-up: W eager steps
     for i in range(args.warmup):
@@ -800,8 +801,8 @@ def extras(args, rb, torch, dev, sets, c, B, N, H, dt, T):
     for p, r in cells:
         for s in sets:
             s["keep"].copy_(keeps_p[p])
-        fused_t[p].append(_graph_time(torch, [(lambda s=s: rb.pack_attend_unpack(
-            s["q"], s["k"], s["v"], s["keep"], o=s["o"], cu=s["cu"])) for s in sets], reps))
+        fused_t[p].append(_graph_time(torch, [(lambda s=s, kp=synth.kept_tokens(N, p): rb.pack_attend_unpack(
+            s["q"], s["k"], s["v"], s["keep"], o=s["o"], cu=s["cu"], n_hint=kp)) for s in sets], reps))
         if r < 2:   # padded SDPA is flat in p (it never looks at the mask's density)
             try:
                 sdpa_t[p].append(_graph_time(torch, sdpa_fns, reps // 10))
@@ -997,8 +998,9 @@ def config_extras(rb, torch, dev, dt):
     F = torch.nn.functional
     res = {}
 
-    def fused_fn(s):
-        return lambda: rb.pack_attend_unpack(s["q"], s["k"], s["v"], s["keep"], o=s["o"])
+    def fused_fn(s, hint=0):
+        """n_hint: the config's expected kept tokens per image (its pruning ratio)."""
+        return lambda: rb.pack_attend_unpack(s["q"], s["k"], s["v"], s["keep"], o=s["o"], n_hint=hint)
 
     def sdpa_fn(s):
         m = s["keep"].bool()[:, None, None, :]
@@ -1014,7 +1016,7 @@ def config_extras(rb, torch, dev, dt):
 
     # C1: DeiT-Ti single layer, B = 4, l2 keep 50 %
     sets, T = make_sets(4, 3, 0.5, "l2", 64)
-    us = _graph_time(torch, [fused_fn(s) for s in sets], 500)
+    us = _graph_time(torch, [fused_fn(s, T // 4) for s in sets], 500)
     res["C1"] = {"fused_us": us, "images_per_s": 4 / (us * 1e-6), "tok_per_img": T // 4,
                  "padded_sdpa_us": _graph_time(torch, [sdpa_fn(s) for s in sets[:8]], 200)}
     # C2: DeiT-S 12 layers, B = 32: layers 1-4 all kept, 5-12 l2 mask at p
@@ -1026,9 +1028,9 @@ def config_extras(rb, torch, dev, dt):
         keep_all = torch.ones(32, 197, dtype=torch.uint8, device=dev)
         layers = [dict(base[L], keep=(keep_all if L < 4 else keep_p)) for L in range(12)]
 
-        def step(layers=layers):
-            for s in layers:
-                rb.pack_attend_unpack(s["q"], s["k"], s["v"], s["keep"], o=s["o"])
+        def step(layers=layers, kp=synth.kept_tokens(197, p)):
+            for L, s in enumerate(layers):
+                rb.pack_attend_unpack(s["q"], s["k"], s["v"], s["keep"], o=s["o"], n_hint=197 if L < 4 else kp)
         us = _graph_time(torch, [step], 50)
 
         def step_sdpa(layers=layers):
@@ -1044,7 +1046,7 @@ def config_extras(rb, torch, dev, dt):
     for method in ("l2", "dynamicvit", "evit", "ats"):
         for p in (0.5, 0.7, 0.9):
             sets, T = make_sets(64, 12, p, method, 8)
-            us = _graph_time(torch, [fused_fn(s) for s in sets], 200)
+            us = _graph_time(torch, [fused_fn(s, T // 64) for s in sets], 200)
             c4.append({"method": method, "p": p, "mean_tok": T / 64, "fused_us": us,
                        "padded_sdpa_us": _graph_time(torch, [sdpa_fn(s) for s in sets], 40)})
     res["C4"] = c4

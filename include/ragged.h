@@ -80,6 +80,13 @@ typedef struct {
   int32_t dtype;   /* ragged_dtype                                        */
   int32_t engine;  /* ragged_engine (0 = auto)                            */
   int64_t ld;      /* token stride of padded q/k/v in elements, >= H*d, % 8 == 0 */
+  int32_t n_hint;  /* expected kept tokens per image (the caller's pruning
+                      schedule); 0 = unknown.  Performance only: with the
+                      mma.sync engine, n_hint > 64 selects the kernel variant
+                      built for long sequences (exact per-chunk tile counts);
+                      both variants meet the same tolerance (R2) and are
+                      deterministic, but their bits may differ (different
+                      multiply-add contraction).  >= 0. */
 } ragged_problem;
 
 /* a1 -- scan.  Per-image cumulative sums produce cu_seqlens and per-token

@@ -35,10 +35,11 @@ class RaggedError(RuntimeError):
 
 class Problem(ctypes.Structure):
     """ragged_problem: B images, N padded tokens (incl. CLS), H heads, d = 64,
-    dtype, engine, ld = token stride of padded q/k/v in elements."""
+    dtype, engine, ld = token stride of padded q/k/v in elements, n_hint =
+    expected kept tokens per image (0 = unknown; performance only)."""
     _fields_ = [("B", ctypes.c_int32), ("N", ctypes.c_int32), ("H", ctypes.c_int32),
                 ("d", ctypes.c_int32), ("dtype", ctypes.c_int32), ("engine", ctypes.c_int32),
-                ("ld", ctypes.c_int64)]
+                ("ld", ctypes.c_int64), ("n_hint", ctypes.c_int32)]
 
 
 MAX_PEERS = 8
@@ -178,12 +179,12 @@ def _stream(stream) -> int | None:
 
 
 def problem(B: int, N: int, H: int, d: int = 64, dtype=torch.bfloat16, ld: int | None = None,
-            engine: int = ENGINE_AUTO) -> Problem:
+            engine: int = ENGINE_AUTO, n_hint: int = 0) -> Problem:
     dt = _DTYPE[dtype] if isinstance(dtype, torch.dtype) else int(dtype)
-    return Problem(B, N, H, d, dt, engine, H * d if ld is None else ld)
+    return Problem(B, N, H, d, dt, engine, H * d if ld is None else ld, n_hint)
 
 
-def _padded_problem(q, k, v, engine):
+def _padded_problem(q, k, v, engine, n_hint=0):
     """Problem for padded q/k/v [B, N, H, d] views sharing one token stride."""
     if q.dim() != 4:
         raise ValueError("q/k/v must be [B, N, H, d]")
@@ -195,7 +196,7 @@ def _padded_problem(q, k, v, engine):
         raise ValueError("q/k/v must be token-major [B, N, H, d] with unit head-dim stride")
     if q.dtype not in _DTYPE:
         raise ValueError("dtype must be bf16 or fp16")
-    return problem(B, N, H, d, q.dtype, q.stride(1), engine)
+    return problem(B, N, H, d, q.dtype, q.stride(1), engine, n_hint)
 
 
 def _keep_u8(keep):
@@ -252,15 +253,16 @@ def _packed_ld(qp, kp, vp) -> int:
     return qp.stride(0)
 
 
-def attn(qp, kp, vp, cu, N: int, op=None, stream=None, engine=ENGINE_AUTO):
-    """a3 (Alg. 1): packed [cap, H, d] + cu [B+1] -> packed O."""
+def attn(qp, kp, vp, cu, N: int, op=None, stream=None, engine=ENGINE_AUTO, n_hint=0):
+    """a3 (Alg. 1): packed [cap, H, d] + cu [B+1] -> packed O.
+    n_hint: expected kept tokens per image (performance only)."""
     cap, H, d = qp.shape
     ld = _packed_ld(qp, kp, vp)
     B = cu.numel() - 1
     op = torch.empty(cap, H, d, dtype=qp.dtype, device=qp.device) if op is None else op
     if not op.is_contiguous() or op.shape != qp.shape:
         raise ValueError("op must be a contiguous [cap, H, d] tensor")
-    p = problem(B, N, H, d, qp.dtype, ld, engine)
+    p = problem(B, N, H, d, qp.dtype, ld, engine, n_hint)
     _check(lib().ragged_attn(ctypes.byref(p), qp.data_ptr(), kp.data_ptr(), vp.data_ptr(), cu.data_ptr(),
                             op.data_ptr(), _stream(stream)), "ragged_attn")
     return op
@@ -298,9 +300,10 @@ def unpack(op, dst, B: int, N: int, o=None, stream=None):
 
 
 def pack_attend_unpack(q, k, v, keep, o=None, cu=None, want_cu=False, stream=None,
-                       engine=ENGINE_AUTO):
-    """a5: the fused single-launch path.  Returns o (and cu if requested)."""
-    p = _padded_problem(q, k, v, engine)
+                       engine=ENGINE_AUTO, n_hint=0):
+    """a5: the fused single-launch path.  Returns o (and cu if requested).
+    n_hint: expected kept tokens per image (performance only)."""
+    p = _padded_problem(q, k, v, engine, n_hint)
     keep = _keep_u8(keep)
     B, N, H, d = q.shape
     o = torch.empty(B, N, H, d, dtype=q.dtype, device=q.device) if o is None else o
@@ -446,8 +449,8 @@ class VitPipelineGraph:
 class Graph:
     """ragged_graph: one captured pack_attend_unpack with fixed pointers."""
 
-    def __init__(self, q, k, v, keep, o, cu=None, engine=ENGINE_AUTO):
-        self._p = _padded_problem(q, k, v, engine)
+    def __init__(self, q, k, v, keep, o, cu=None, engine=ENGINE_AUTO, n_hint=0):
+        self._p = _padded_problem(q, k, v, engine, n_hint)
         keep = _keep_u8(keep)
         self._refs = (q, k, v, keep, o, cu)     # keep the buffers alive
         h = ctypes.c_void_p()

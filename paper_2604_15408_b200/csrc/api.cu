@@ -58,6 +58,7 @@ ragged_status check_problem(const ragged_problem* p, bool general = false) {
   if (p->ld > (1LL << 22)) return fail(RAGGED_ENOTSUP, "ld > 2^22 elements");
   if (p->ld < (int64_t)p->H * p->d) return fail(RAGGED_EINVAL, "ld < H*d");
   if (p->ld % 8 != 0) return fail(RAGGED_EALIGN, "ld % 8 != 0 (rows must be 16-byte aligned)");
+  if (p->n_hint < 0) return fail(RAGGED_EINVAL, "n_hint < 0");
   return RAGGED_OK;
 }
 
@@ -91,9 +92,12 @@ ragged_status check_ptr_any(const void* p, const char* name) {  // 1-byte / 4-by
 
 cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
 
-// RAGGED_ENGINE_AUTO -> the engine measured fastest.
+// RAGGED_ENGINE_AUTO -> the engine measured fastest; the
+// mma.sync engine's long-sequence variant when the caller expects > 64 kept
+// tokens per image (ragged_problem.n_hint).
 int resolve_engine(const ragged_problem* p) {
-  return p->engine == RAGGED_ENGINE_AUTO ? RAGGED_ENGINE_MMA_SYNC : p->engine;
+  const int e = p->engine == RAGGED_ENGINE_AUTO ? RAGGED_ENGINE_MMA_SYNC : p->engine;
+  return (e == RAGGED_ENGINE_MMA_SYNC && p->n_hint > 64) ? ragged::kEngineMmaLong : e;
 }
 
 }  // namespace
@@ -344,7 +348,7 @@ static ragged_status to_gather_args(const ragged_problem* prob, const ragged_gat
   if (g == nullptr) return fail(RAGGED_EINVAL, "gather is NULL");
   if (g->world < 1 || g->world > RAGGED_MAX_PEERS) return fail(RAGGED_EINVAL, "world not in 1..8");
   if (g->rank < 0 || g->rank >= g->world) return fail(RAGGED_EINVAL, "rank not in 0..world-1");
-  if (resolve_engine(prob) != RAGGED_ENGINE_MMA_SYNC)
+  if (resolve_engine(prob) == RAGGED_ENGINE_TCGEN05)
     return fail(RAGGED_ENOTSUP, "gather entry points run on the mma.sync engine only");
   ga.world = g->world;
   ga.rank = g->rank;

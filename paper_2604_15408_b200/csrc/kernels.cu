@@ -747,9 +747,141 @@ __device__ __forceinline__ void image_rows(const AttnArgs& a, int b, int16_t* sP
   }
 }
 
+// kLargeN variant of one 64-key chunk (Alg. 1) for one warp's
+// 16-row query slice: the same arithmetic in the same order as the generic
+// chunk loop of attn_kernel (bits may differ where the compiler contracts a
+// multiply-add across what are separate blocks there), with the chunk's
+// 8-key tile count NT a template argument -- straight-line code whose tile MMA
+// chains the scheduler interleaves (the generic loop tests `j < nt` per tile).
+template <typename T, int NT>
+__device__ __forceinline__ void attn_chunk(const uint8_t* sK, const uint8_t* sV, int cb, int n,
+                                           int lane, const uint32_t (&qf)[4][4], float (&o)[8][4],
+                                           float& m0, float& m1, float& l0, float& l1) {
+  const int t4 = lane & 3;
+  constexpr float kScaleLog2 = 0.18033688011112042f;  // log2(e) / sqrt(64)
+  float s[8][4];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) s[j][0] = s[j][1] = s[j][2] = s[j][3] = 0.f;
+  // head dims [0, 32) then [32, 64): per half one ldmatrix per key tile and
+  // two MMAs (per-element accumulation order unchanged), NT independent chains
+#pragma unroll
+  for (int kp = 0; kp < 2; ++kp) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+#ifdef RAGGED_ABLATE_QK
+      if (false) {
+#else
+      if (j < NT) {
+#endif
+        uint32_t kb[4];
+        const int kr = cb + 8 * j + (lane & 7);
+        ldmatrix_x4(smem_u32(sK + swz(kr, 4 * kp + (lane >> 3))), kb[0], kb[1], kb[2], kb[3]);
+        mma_16816<T>(s[j], qf[2 * kp], kb[0], kb[1]);
+        mma_16816<T>(s[j], qf[2 * kp + 1], kb[2], kb[3]);
+      }
+    }
+  }
+  // scale to log2 units, mask key columns >= n (R4), row max over the quad
+  // (tree reductions: short dependency chains, the warp has little else to hide them)
+  float t0[8], t1[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int col = cb + 8 * j + 2 * t4 + (e & 1);
+      const float val = (j < NT && col < n) ? s[j][e] * kScaleLog2 : -INFINITY;
+      s[j][e] = val;
+    }
+    t0[j] = fmaxf(s[j][0], s[j][1]);
+    t1[j] = fmaxf(s[j][2], s[j][3]);
+  }
+#pragma unroll
+  for (int w = 4; w > 0; w >>= 1)
+#pragma unroll
+    for (int j = 0; j < w; ++j) {
+      t0[j] = fmaxf(t0[j], t0[j + w]);
+      t1[j] = fmaxf(t1[j], t1[j + w]);
+    }
+  float mx0 = t0[0], mx1 = t1[0];
+  mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 1));
+  mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 2));
+  mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 1));
+  mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 2));
+  TL(5);
+  PT(1);
+  const float mn0 = fmaxf(m0, mx0), mn1 = fmaxf(m1, mx1);
+  const float al0 = ex2(m0 - mn0), al1 = ex2(m1 - mn1);  // alpha = e^{m - m'}
+  m0 = mn0;
+  m1 = mn1;
+  l0 *= al0;
+  l1 *= al1;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    o[j][0] *= al0;
+    o[j][1] *= al0;
+    o[j][2] *= al1;
+    o[j][3] *= al1;
+  }
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {  // P = e^{S - m'}; key tiles past n skipped (exp2 unit)
+#ifdef RAGGED_ABLATE_EXP
+    if (false) {
+#else
+    if (j < NT) {
+#endif
+      s[j][0] = ex2(s[j][0] - mn0);
+      s[j][1] = ex2(s[j][1] - mn0);
+      s[j][2] = ex2(s[j][2] - mn1);
+      s[j][3] = ex2(s[j][3] - mn1);
+    } else {
+      s[j][0] = s[j][1] = s[j][2] = s[j][3] = 0.f;
+    }
+    t0[j] = s[j][0] + s[j][1];
+    t1[j] = s[j][2] + s[j][3];
+  }
+#pragma unroll
+  for (int w = 4; w > 0; w >>= 1)
+#pragma unroll
+    for (int j = 0; j < w; ++j) {
+      t0[j] += t0[j + w];
+      t1[j] += t1[j + w];
+    }
+  l0 += t0[0];
+  l1 += t1[0];
+  // O += P_hi V + P_lo V
+#ifdef RAGGED_ABLATE_PV
+  constexpr int nk = 0;
+#else
+  constexpr int nk = (NT + 1) / 2;  // = ceil(valid keys / 16)
+#endif
+#pragma unroll
+  for (int kk = 0; kk < 4; ++kk) {
+    if (kk < nk) {
+      uint32_t ah[4], al[4];
+      split2<T>(s[2 * kk][0], s[2 * kk][1], ah[0], al[0]);
+      split2<T>(s[2 * kk][2], s[2 * kk][3], ah[1], al[1]);
+      split2<T>(s[2 * kk + 1][0], s[2 * kk + 1][1], ah[2], al[2]);
+      split2<T>(s[2 * kk + 1][2], s[2 * kk + 1][3], ah[3], al[3]);
+#pragma unroll
+      for (int jp = 0; jp < 4; ++jp) {
+        uint32_t vb[4];
+        ldmatrix_x4_trans(smem_u32(sV + swz(cb + 16 * kk + (lane & 15), 2 * jp + (lane >> 4))),
+                          vb[0], vb[1], vb[2], vb[3]);
+        mma_16816<T>(o[2 * jp], ah, vb[0], vb[1]);
+        mma_16816<T>(o[2 * jp], al, vb[0], vb[1]);
+        mma_16816<T>(o[2 * jp + 1], ah, vb[2], vb[3]);
+        mma_16816<T>(o[2 * jp + 1], al, vb[2], vb[3]);
+      }
+    }
+  }
+}
+
 // kGather: outputs go to the GatherArgs destinations (fused all-gather over
 // peer memory) instead of a.o, followed by the cross-rank completion barrier.
-template <typename T, bool kFused, bool kGather>
+// kLargeN: the chunk loop with exact tile counts (attn_chunk), chosen on the host
+// from the caller's expected kept tokens per image (ragged_problem.n_hint > 64):
+// a separate kernel so the short-sequence kernel keeps its register allocation.
+template <typename T, bool kFused, bool kGather, bool kLargeN = false>
 __global__ void __launch_bounds__(kAttnThreads, 3) attn_kernel(const AttnArgs a, const GatherArgs ga) {
   extern __shared__ __align__(1024) uint8_t smem[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -902,6 +1034,20 @@ __global__ void __launch_bounds__(kAttnThreads, 3) attn_kernel(const AttnArgs a,
     for (int j = 0; j < 8; ++j) o[j][0] = o[j][1] = o[j][2] = o[j][3] = 0.f;
     float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
 
+    if constexpr (kLargeN) {
+      for (int cb = 0; cb < n; cb += 64) {
+        switch ((min(64, n - cb) + 7) >> 3) {
+          case 1: attn_chunk<T, 1>(sK, sV, cb, n, lane, qf, o, m0, m1, l0, l1); break;
+          case 2: attn_chunk<T, 2>(sK, sV, cb, n, lane, qf, o, m0, m1, l0, l1); break;
+          case 3: attn_chunk<T, 3>(sK, sV, cb, n, lane, qf, o, m0, m1, l0, l1); break;
+          case 4: attn_chunk<T, 4>(sK, sV, cb, n, lane, qf, o, m0, m1, l0, l1); break;
+          case 5: attn_chunk<T, 5>(sK, sV, cb, n, lane, qf, o, m0, m1, l0, l1); break;
+          case 6: attn_chunk<T, 6>(sK, sV, cb, n, lane, qf, o, m0, m1, l0, l1); break;
+          case 7: attn_chunk<T, 7>(sK, sV, cb, n, lane, qf, o, m0, m1, l0, l1); break;
+          default: attn_chunk<T, 8>(sK, sV, cb, n, lane, qf, o, m0, m1, l0, l1); break;
+        }
+      }
+    } else
     for (int cb = 0; cb < n; cb += 64) {
       const int nv = min(64, n - cb);
       const int nt = (nv + 7) >> 3;
@@ -1229,13 +1375,13 @@ static cudaError_t smem_attr_once(Kern kern, int max_bytes, bool (&done)[64]) {
   return e;
 }
 
-template <typename T, bool kFused, bool kGather = false>
+template <typename T, bool kFused, bool kGather = false, bool kLargeN = false>
 static cudaError_t launch_attn_mma(const AttnArgs& a, int grid, cudaStream_t st,
                                    const GatherArgs& g = GatherArgs{}) {
   static bool done[64] = {false};
-  cudaError_t e = smem_attr_once(attn_kernel<T, kFused, kGather>, attn_smem_bytes(kMaxN), done);
+  cudaError_t e = smem_attr_once(attn_kernel<T, kFused, kGather, kLargeN>, attn_smem_bytes(kMaxN), done);
   if (e != cudaSuccess) return e;
-  return launch_pdl(attn_kernel<T, kFused, kGather>, dim3(grid), dim3(kAttnThreads),
+  return launch_pdl(attn_kernel<T, kFused, kGather, kLargeN>, dim3(grid), dim3(kAttnThreads),
                     attn_smem_bytes(a.N), st, a, g);
 }
 
@@ -1258,6 +1404,9 @@ static cudaError_t dispatch_attn(int dtype, int engine, const AttnArgs& a, int n
   if (engine == 2)
     return dtype == 0 ? launch_attn_tc<__nv_bfloat16, kFused>(a, nwork, st)
                       : launch_attn_tc<__half, kFused>(a, nwork, st);
+  if (engine == kEngineMmaLong)
+    return dtype == 0 ? launch_attn_mma<__nv_bfloat16, kFused, false, true>(a, nwork, st)
+                      : launch_attn_mma<__half, kFused, false, true>(a, nwork, st);
   return dtype == 0 ? launch_attn_mma<__nv_bfloat16, kFused>(a, nwork, st)
                     : launch_attn_mma<__half, kFused>(a, nwork, st);
 }

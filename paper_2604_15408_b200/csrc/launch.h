@@ -14,7 +14,9 @@ cudaError_t launch_pack(const void* q, const void* k, const void* v, long long l
 cudaError_t launch_scan_pack(const uint8_t* keep, const void* q, const void* k, const void* v,
                              long long ld_elems, int B, int N, int H, int32_t* cu, int32_t* dst,
                              int32_t* src, void* qp, void* kp, void* vp, cudaStream_t st);
-// engine: 1 = mma.sync, 2 = tcgen05 (api.cu resolves RAGGED_ENGINE_AUTO)
+// engine: 1 = mma.sync, 2 = tcgen05 (api.cu resolves RAGGED_ENGINE_AUTO),
+// kEngineMmaLong = mma.sync with the long-sequence chunk loop (n_hint > 64)
+constexpr int kEngineMmaLong = 3;
 cudaError_t launch_attn(int dtype, int engine, const void* qp, const void* kp, const void* vp, const int32_t* cu,
                         void* op, int B, int N, int H, long long ld, cudaStream_t st);
 cudaError_t launch_unpack(const void* op, const int32_t* dst, void* o, int B, int N, int H,

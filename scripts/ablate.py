@@ -25,6 +25,7 @@ ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--no-cu", action="store_true")
 ap.add_argument("--tag", default="")
 ap.add_argument("--sets", type=int, default=16)
+ap.add_argument("--n-hint", type=int, default=0)
 a = ap.parse_args()
 c = synth.CONFIGS[a.config]
 p = c["p"] if a.prune is None else a.prune
@@ -37,14 +38,15 @@ sets = [[t.to(dev) for t in (q, k, v, keep)] for _ in range(S)]
 outs = [torch.empty(B, N, H, 64, dtype=q.dtype, device=dev) for _ in range(S)]
 cus = [torch.empty(B + 1, dtype=torch.int32, device=dev) for _ in range(S)]
 for i in range(20):
-    rb.pack_attend_unpack(*sets[i % S], o=outs[i % S], cu=None if a.no_cu else cus[i % S], engine=a.engine)
+    rb.pack_attend_unpack(*sets[i % S], o=outs[i % S], cu=None if a.no_cu else cus[i % S], engine=a.engine,
+                          n_hint=a.n_hint)
 torch.cuda.synchronize()
 g = torch.cuda.CUDAGraph()
 cap = torch.cuda.Stream()
 with torch.cuda.graph(g, stream=cap):
     for i in range(a.steps):
         rb.pack_attend_unpack(*sets[i % S], o=outs[i % S], cu=None if a.no_cu else cus[i % S],
-                              engine=a.engine)
+                              engine=a.engine, n_hint=a.n_hint)
 g.replay()
 torch.cuda.synchronize()
 us = []

@@ -58,7 +58,7 @@ def _call_fused(p, keep=FAKE, q=FAKE, k=FAKE, v=FAKE, o=FAKE):
 @pytest.mark.parametrize("field,value,status", [
     ("B", -1, rb.EINVAL), ("N", 0, rb.EINVAL), ("H", 0, rb.EINVAL), ("N", 257, rb.ENOTSUP),
     ("d", 128, rb.ENOTSUP), ("dtype", 7, rb.ENOTSUP), ("engine", 9, rb.ENOTSUP),
-    ("ld", 100, rb.EINVAL), ("ld", 772, rb.EALIGN),
+    ("ld", 100, rb.EINVAL), ("ld", 772, rb.EALIGN), ("n_hint", -1, rb.EINVAL),
 ])
 def test_problem_validation(field, value, status):
     p = rb.problem(4, 197, 12)
