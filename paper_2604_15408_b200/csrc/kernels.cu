@@ -748,17 +748,26 @@ __device__ __forceinline__ void image_rows(const AttnArgs& a, int b, int16_t* sP
 }
 
 // kLargeN variant of one 64-key chunk (Alg. 1) for one warp's
-// 16-row query slice: the same arithmetic in the same order as the generic
-// chunk loop of attn_kernel (bits may differ where the compiler contracts a
-// multiply-add across what are separate blocks there), with the chunk's
-// 8-key tile count NT a template argument -- straight-line code whose tile MMA
-// chains the scheduler interleaves (the generic loop tests `j < nt` per tile).
-template <typename T, int NT>
+// 16-row query slice, with the chunk's 8-key tile count NT a template argument
+// -- straight-line code whose tile MMA chains the scheduler interleaves (the
+// generic loop tests `j < nt` per tile).  Differences from the generic loop,
+// all exact reformulations of the same softmax (bits may differ, R2 holds):
+//  * kFull (every one of the NT*8 keys is < n): no per-column mask;
+//  * the row max is taken on the raw scores (x -> x*log2(e)/8 is monotonic)
+//    and the scale is folded into the exponent, P = ex2(fma(S, c, -m)): one
+//    FFMA per score instead of FMUL + FADD;
+//  * lazy rescaling: the running reference m is raised (and O, l rescaled by
+//    e^{m - m'}) only when some row of the warp sees its chunk max exceed m by
+//    more than kLazy (log2 units); otherwise m stays and P <= 2^kLazy.  O/l is
+//    invariant to the reference, and P's hi+lo split is relative, so the
+//    tolerance argument of R2 is unchanged.  The first chunk always sets m.
+template <typename T, int NT, bool kFull>
 __device__ __forceinline__ void attn_chunk(const uint8_t* sK, const uint8_t* sV, int cb, int n,
                                            int lane, const uint32_t (&qf)[4][4], float (&o)[8][4],
                                            float& m0, float& m1, float& l0, float& l1) {
   const int t4 = lane & 3;
   constexpr float kScaleLog2 = 0.18033688011112042f;  // log2(e) / sqrt(64)
+  constexpr float kLazy = 8.f;
   float s[8][4];
 #pragma unroll
   for (int j = 0; j < 8; ++j) s[j][0] = s[j][1] = s[j][2] = s[j][3] = 0.f;
@@ -781,16 +790,19 @@ __device__ __forceinline__ void attn_chunk(const uint8_t* sK, const uint8_t* sV,
       }
     }
   }
-  // scale to log2 units, mask key columns >= n (R4), row max over the quad
+  // mask key columns >= n (R4; tail chunks only), raw row max over the quad
   // (tree reductions: short dependency chains, the warp has little else to hide them)
   float t0[8], t1[8];
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
+    if (j >= NT) {
+      s[j][0] = s[j][1] = s[j][2] = s[j][3] = -INFINITY;
+    } else if constexpr (!kFull) {
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const int col = cb + 8 * j + 2 * t4 + (e & 1);
-      const float val = (j < NT && col < n) ? s[j][e] * kScaleLog2 : -INFINITY;
-      s[j][e] = val;
+      for (int e = 0; e < 4; ++e) {
+        const int col = cb + 8 * j + 2 * t4 + (e & 1);
+        if (col >= n) s[j][e] = -INFINITY;
+      }
     }
     t0[j] = fmaxf(s[j][0], s[j][1]);
     t1[j] = fmaxf(s[j][2], s[j][3]);
@@ -809,30 +821,36 @@ __device__ __forceinline__ void attn_chunk(const uint8_t* sK, const uint8_t* sV,
   mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 2));
   TL(5);
   PT(1);
-  const float mn0 = fmaxf(m0, mx0), mn1 = fmaxf(m1, mx1);
-  const float al0 = ex2(m0 - mn0), al1 = ex2(m1 - mn1);  // alpha = e^{m - m'}
-  m0 = mn0;
-  m1 = mn1;
-  l0 *= al0;
-  l1 *= al1;
+  mx0 *= kScaleLog2;
+  mx1 *= kScaleLog2;
+  // m = -inf on the first chunk: the difference is +inf, so it always rescales
+  if (__any_sync(0xffffffffu, mx0 - m0 > kLazy || mx1 - m1 > kLazy)) {
+    const float mn0 = fmaxf(m0, mx0), mn1 = fmaxf(m1, mx1);
+    const float al0 = ex2(m0 - mn0), al1 = ex2(m1 - mn1);  // alpha = e^{m - m'}
+    m0 = mn0;
+    m1 = mn1;
+    l0 *= al0;
+    l1 *= al1;
 #pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    o[j][0] *= al0;
-    o[j][1] *= al0;
-    o[j][2] *= al1;
-    o[j][3] *= al1;
+    for (int j = 0; j < 8; ++j) {
+      o[j][0] *= al0;
+      o[j][1] *= al0;
+      o[j][2] *= al1;
+      o[j][3] *= al1;
+    }
   }
+  const float nm0 = -m0, nm1 = -m1;
 #pragma unroll
-  for (int j = 0; j < 8; ++j) {  // P = e^{S - m'}; key tiles past n skipped (exp2 unit)
+  for (int j = 0; j < 8; ++j) {  // P = e^{S/sqrt(d) - m}; key tiles past n skipped (exp2 unit)
 #ifdef RAGGED_ABLATE_EXP
     if (false) {
 #else
     if (j < NT) {
 #endif
-      s[j][0] = ex2(s[j][0] - mn0);
-      s[j][1] = ex2(s[j][1] - mn0);
-      s[j][2] = ex2(s[j][2] - mn1);
-      s[j][3] = ex2(s[j][3] - mn1);
+      s[j][0] = ex2(fmaf(s[j][0], kScaleLog2, nm0));
+      s[j][1] = ex2(fmaf(s[j][1], kScaleLog2, nm0));
+      s[j][2] = ex2(fmaf(s[j][2], kScaleLog2, nm1));
+      s[j][3] = ex2(fmaf(s[j][3], kScaleLog2, nm1));
     } else {
       s[j][0] = s[j][1] = s[j][2] = s[j][3] = 0.f;
     }
@@ -1036,15 +1054,25 @@ __global__ void __launch_bounds__(kAttnThreads, 3) attn_kernel(const AttnArgs a,
 
     if constexpr (kLargeN) {
       for (int cb = 0; cb < n; cb += 64) {
-        switch ((min(64, n - cb) + 7) >> 3) {
-          case 1: attn_chunk<T, 1>(sK, sV, cb, n, lane, qf, o, m0, m1, l0, l1); break;
-          case 2: attn_chunk<T, 2>(sK, sV, cb, n, lane, qf, o, m0, m1, l0, l1); break;
-          case 3: attn_chunk<T, 3>(sK, sV, cb, n, lane, qf, o, m0, m1, l0, l1); break;
-          case 4: attn_chunk<T, 4>(sK, sV, cb, n, lane, qf, o, m0, m1, l0, l1); break;
-          case 5: attn_chunk<T, 5>(sK, sV, cb, n, lane, qf, o, m0, m1, l0, l1); break;
-          case 6: attn_chunk<T, 6>(sK, sV, cb, n, lane, qf, o, m0, m1, l0, l1); break;
-          case 7: attn_chunk<T, 7>(sK, sV, cb, n, lane, qf, o, m0, m1, l0, l1); break;
-          default: attn_chunk<T, 8>(sK, sV, cb, n, lane, qf, o, m0, m1, l0, l1); break;
+        const int nv = min(64, n - cb);
+        // case 2*NT - 2 + full: NT 8-key tiles, full = no key column >= n
+        switch (2 * ((nv + 7) >> 3) - ((nv & 7) == 0 ? 1 : 2)) {
+          case 0: attn_chunk<T, 1, false>(sK, sV, cb, n, lane, qf, o, m0, m1, l0, l1); break;
+          case 1: attn_chunk<T, 1, true>(sK, sV, cb, n, lane, qf, o, m0, m1, l0, l1); break;
+          case 2: attn_chunk<T, 2, false>(sK, sV, cb, n, lane, qf, o, m0, m1, l0, l1); break;
+          case 3: attn_chunk<T, 2, true>(sK, sV, cb, n, lane, qf, o, m0, m1, l0, l1); break;
+          case 4: attn_chunk<T, 3, false>(sK, sV, cb, n, lane, qf, o, m0, m1, l0, l1); break;
+          case 5: attn_chunk<T, 3, true>(sK, sV, cb, n, lane, qf, o, m0, m1, l0, l1); break;
+          case 6: attn_chunk<T, 4, false>(sK, sV, cb, n, lane, qf, o, m0, m1, l0, l1); break;
+          case 7: attn_chunk<T, 4, true>(sK, sV, cb, n, lane, qf, o, m0, m1, l0, l1); break;
+          case 8: attn_chunk<T, 5, false>(sK, sV, cb, n, lane, qf, o, m0, m1, l0, l1); break;
+          case 9: attn_chunk<T, 5, true>(sK, sV, cb, n, lane, qf, o, m0, m1, l0, l1); break;
+          case 10: attn_chunk<T, 6, false>(sK, sV, cb, n, lane, qf, o, m0, m1, l0, l1); break;
+          case 11: attn_chunk<T, 6, true>(sK, sV, cb, n, lane, qf, o, m0, m1, l0, l1); break;
+          case 12: attn_chunk<T, 7, false>(sK, sV, cb, n, lane, qf, o, m0, m1, l0, l1); break;
+          case 13: attn_chunk<T, 7, true>(sK, sV, cb, n, lane, qf, o, m0, m1, l0, l1); break;
+          case 14: attn_chunk<T, 8, false>(sK, sV, cb, n, lane, qf, o, m0, m1, l0, l1); break;
+          default: attn_chunk<T, 8, true>(sK, sV, cb, n, lane, qf, o, m0, m1, l0, l1); break;
         }
       }
     } else
