@@ -55,6 +55,8 @@ def parse():
                          "NCCL + fused peer-memory all-gathers at N>1 (torch symmetric memory)")
     ap.add_argument("--no-cu", action="store_true", help="experiment: do not request cu_seqlens")
     ap.add_argument("--no-extras", action="store_true")
+    ap.add_argument("--n-hint", type=int, default=None,
+                    help="experiment: override ragged_problem.n_hint (default: the config's kept tokens per image)")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--e2e-steps", type=int, default=50)
     return ap.parse_args()
@@ -165,7 +167,10 @@ def run_reference(args):
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * dt / args.steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"{args.config}: {c['name']}", "images_per_step": nb},
+            "config": {"workload": f"{args.config}: {c['name']}", "B_per_gpu": B, "N": N, "H": H,
+                       "d": 64, "prune": c["p"], "method": c["method"],
+                       "tok_per_img": synth.kept_tokens(N, c["p"]), "global_batch": B,
+                       "images_per_step": nb},
             "cpu_baseline": {"value": value, "unit": "images/s", "cores": 1, "kind": "oracle",
                              "sample": sample},
             "e2e": {"value": value, "unit": "images/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -277,7 +282,7 @@ def main():
         s = sets[i % N_SETS]
         rb.pack_attend_unpack(s["q"], s["k"], s["v"], s["keep"], o=s["o"],
                               cu=None if args.no_cu else s["cu"], stream=stream, engine=args.engine,
-                              n_hint=T // max(B, 1))
+                              n_hint=T // max(B, 1) if args.n_hint is None else args.n_hint)
 
     # warm-up: W eager steps
     for i in range(args.warmup):
