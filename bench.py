@@ -453,7 +453,61 @@ def measure_e2e(args, rb, torch, dev, q, k, v, keep, ws, B, N, H, dt):
     best = max((x for x in variants.values() if "value" in x), key=lambda x: x["value"])
     best = dict(best)
     best["variants"] = variants
+    try:
+        best["link_bound"] = pcie_bound(torch, dev, best["h2d_bytes_per_step"], best["d2h_bytes_per_step"],
+                                        best["us_per_step"])
+    except Exception as ex:
+        best["link_bound"] = {"error": repr(ex)[:300]}
     return best
+
+
+def pcie_bound(torch, dev, h2d_bytes, d2h_bytes, us_per_step, reps=20):
+    """The host link's bound on e2e: copy-engine bandwidth of pinned H2D and D2H
+    copies of one step's byte counts (each direction alone, events on the copy
+    stream), and the step time they imply when both directions overlap (PCIe
+    is full duplex): max(h2d / bw_h2d, d2h / bw_d2h)."""
+    st = torch.cuda.Stream()
+    out = {}
+    for name, nbytes, h2d in (("h2d", h2d_bytes, True), ("d2h", d2h_bytes, False)):
+        hb = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
+        db = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+        with torch.cuda.stream(st):
+            for _ in range(3):
+                (db.copy_(hb, non_blocking=True) if h2d else hb.copy_(db, non_blocking=True))
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record(st)
+            for _ in range(reps):
+                (db.copy_(hb, non_blocking=True) if h2d else hb.copy_(db, non_blocking=True))
+            e.record(st)
+        torch.cuda.synchronize()
+        out[name + "_gbs"] = nbytes * reps / (s.elapsed_time(e) * 1e-3) / 1e9
+    # both directions at once (two streams), as the pipelined e2e steps run them
+    hh = torch.empty(h2d_bytes, dtype=torch.uint8).pin_memory()
+    dh = torch.empty(h2d_bytes, dtype=torch.uint8, device=dev)
+    hd = torch.empty(d2h_bytes, dtype=torch.uint8).pin_memory()
+    dd = torch.empty(d2h_bytes, dtype=torch.uint8, device=dev)
+    st2 = torch.cuda.Stream()
+    cur = torch.cuda.current_stream()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record(cur)
+    st.wait_stream(cur)
+    st2.wait_stream(cur)
+    for _ in range(reps):
+        with torch.cuda.stream(st):
+            dh.copy_(hh, non_blocking=True)
+        with torch.cuda.stream(st2):
+            hd.copy_(dd, non_blocking=True)
+    cur.wait_stream(st)
+    cur.wait_stream(st2)
+    e.record(cur)
+    torch.cuda.synchronize()
+    duplex_us = s.elapsed_time(e) * 1e3 / reps
+    bound_us = max(h2d_bytes / out["h2d_gbs"], d2h_bytes / out["d2h_gbs"]) / 1e3
+    out.update({"bound_us_per_step": bound_us, "frac": bound_us / us_per_step,
+                "duplex_us_per_step": duplex_us, "frac_duplex": duplex_us / us_per_step,
+                "how": f"pinned copy-engine copies of one step's bytes, {reps} reps per direction alone "
+                       "(bound_us) and with both directions concurrently on two streams (duplex_us)"})
+    return out
 
 
 def measure_e2e_zero_copy(args, rb, torch, dev, q, k, v, keep, ws, B, N, H, dt, out_host=False):
