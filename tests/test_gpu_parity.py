@@ -442,3 +442,37 @@ def test_long_sequence_variant(dtype, B, N, H, p, method):
     assert np.array_equal(bits(o_long), bits(again))
     check_attention(to_np(o_long), ref, DT[dtype])
     assert np.all(bits(o_long)[~keep_np.astype(bool)] == 0)
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "fp16"])
+@pytest.mark.parametrize("ramp", [0.0, 5.0, 40.0, -40.0])
+def test_long_variant_running_max_paths(dtype, ramp):
+    """Scores that rise across the 64-key chunks exercise both branches of the
+    long kernel's lazy rescaling (Alg. 1 lines 10-13): ramp 5 keeps
+    every later chunk max within 2^8 of the first (no rescale after chunk 0,
+    P up to ~2^5), ramp 40 raises the max by ~13 nats per chunk (rescale every
+    chunk), -40 puts the max in chunk 0.  q = 8e, k_n = ramp*(n/N)*e + noise with
+    e.e = 1, so the score of key n is ~ramp*n/N nats.  Both kernels within
+    tolerance of the fp64 oracle; fused == composed bitwise under the hint."""
+    B, N, H = 6, 197, 3
+    q, k, v, keep = synth.make_inputs(B, N, H, 0.0, "all", dtype, seed=77)
+    e = torch.full((64,), 1.0 / 8.0)
+    g = torch.Generator().manual_seed(5)
+    pos = (torch.arange(N, dtype=torch.float32) / N).view(1, N, 1, 1)
+    tdt = q.dtype
+    qf = 8.0 * e.view(1, 1, 1, 64) + 0.3 * torch.randn(B, N, H, 64, generator=g)
+    kf = ramp * pos * e.view(1, 1, 1, 64) + 0.3 * torch.randn(B, N, H, 64, generator=g)
+    q, k = qf.to(tdt), kf.to(tdt)
+    keep_np = keep.numpy().copy()
+    keep_np[1, 150:] = 0                       # ragged tail chunk in one image
+    keep = torch.from_numpy(keep_np)
+    qd, kd, vd, keepd = _dev(q, k, v, keep)
+    ref, _ = fused_oracle(q, k, v, keep)
+    o_long = rb.pack_attend_unpack(qd, kd, vd, keepd, n_hint=N)
+    o_short = rb.pack_attend_unpack(qd, kd, vd, keepd)
+    qp, kp, vp, cu, dst, src = rb.pack(qd, kd, vd, keepd)
+    o_comp = rb.unpack(rb.attn(qp, kp, vp, cu, N, n_hint=N), dst, B, N)
+    torch.cuda.synchronize()
+    assert np.array_equal(bits(o_long), bits(o_comp))
+    check_attention(to_np(o_long), ref, DT[dtype], dist="peaked")
+    check_attention(to_np(o_short), ref, DT[dtype], dist="peaked")
