@@ -418,7 +418,7 @@ def test_fused_large_batch_bitwise(engine, dtype, B, H, p, method):
 @pytest.mark.parametrize("dtype", ["bf16", "fp16"])
 @pytest.mark.parametrize("B,N,H,p,method", [(32, 197, 12, 0.0, "all"), (16, 197, 6, 0.3, "l2"), (9, 197, 4, 0.5, "ats"),
                                             (8, 197, 12, 0.8, "l2"), (5, 256, 2, 0.1, "dynamicvit"),
-                                            (7, 100, 3, 0.6, "evit")])
+                                            (7, 100, 3, 0.6, "evit"), (400, 197, 2, 0.3, "l2")])
 def test_long_sequence_variant(dtype, B, N, H, p, method):
     """ragged_problem.n_hint > 64 selects the mma.sync kernel built for long
     sequences (exact per-chunk tile counts; its straight-line code lets the
