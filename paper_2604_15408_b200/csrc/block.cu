@@ -185,6 +185,12 @@ __host__ __device__ constexpr int gemm_smem_bytes() {
          256 /*barriers*/;
 }
 
+// TMEM columns for two BN-wide accumulators, rounded up to a power of two (allocation unit)
+template <int BN>
+__host__ __device__ constexpr uint32_t tmem_cols() {
+  return 2 * BN <= 128 ? 128u : (2 * BN <= 256 ? 256u : 512u);
+}
+
 // Persistent: CTA c takes tiles c, c + gridDim.x, ... of the live tile grid
 // (m-block major, n fastest, so concurrently running CTAs share A row
 // blocks in L2 and every CTA streams the L2-resident weights).  Two TMEM
@@ -229,7 +235,7 @@ __global__ void __launch_bounds__(gemm_threads<kEpi>(), 1)
     prefetch_tmap(&tmA);
     prefetch_tmap(&tmB);
   }
-  if (warp == 1) tc::alloc(tslot, 2 * BN);
+  if (warp == 1) tc::alloc(tslot, tmem_cols<BN>());
   tc::fence_before();
   __syncthreads();
   tc::fence_after();
@@ -400,7 +406,7 @@ __global__ void __launch_bounds__(gemm_threads<kEpi>(), 1)
   __syncthreads();
   if (warp == 1) {
     tc::fence_after();
-    tc::dealloc(tmem, 2 * BN);
+    tc::dealloc(tmem, tmem_cols<BN>());
   }
   if (threadIdx.x == 0) GT(7);
 }
@@ -525,11 +531,11 @@ int gemm_pick_bn(int M_cap, int N, int sms) {
     const char* e = getenv("RAGGED_GEMM_BN");  // tuning experiments only
     return e ? atoi(e) : 0;
   }();
-  if ((forced == 64 || forced == 128 || forced == 256) && N % forced == 0) return forced;
+  if ((forced == 64 || forced == 128 || forced == 192 || forced == 256) && N % forced == 0) return forced;
   const long long mt = (M_cap + kGemmBM - 1) / kGemmBM;
   int best = 64;
   long long best_cost = -1;
-  for (int bn : {256, 128, 64}) {
+  for (int bn : {256, 192, 128, 64}) {
     if (N % bn != 0) continue;
     const long long tiles = mt * (N / bn);
     const long long rounds = (tiles + sms - 1) / sms;
@@ -549,10 +555,12 @@ cudaError_t launch_gemm(int dtype, const void* a, long long lda, const void* w, 
   if (!make_tmap(&tb, dtype, w, g.N, g.K, g.K, bn)) return cudaErrorInvalidValue;
   if (dtype == 0) {
     if (bn == 256) return launch_gemm_bn<__nv_bfloat16, 256>(ta, tb, g, epi, st);
+    if (bn == 192) return launch_gemm_bn<__nv_bfloat16, 192>(ta, tb, g, epi, st);
     if (bn == 128) return launch_gemm_bn<__nv_bfloat16, 128>(ta, tb, g, epi, st);
     return launch_gemm_bn<__nv_bfloat16, 64>(ta, tb, g, epi, st);
   }
   if (bn == 256) return launch_gemm_bn<__half, 256>(ta, tb, g, epi, st);
+  if (bn == 192) return launch_gemm_bn<__half, 192>(ta, tb, g, epi, st);
   if (bn == 128) return launch_gemm_bn<__half, 128>(ta, tb, g, epi, st);
   return launch_gemm_bn<__half, 64>(ta, tb, g, epi, st);
 }
