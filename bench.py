@@ -998,7 +998,7 @@ def n1_block_extras(rb, torch, dev, dt):
         cu, _, _ = oracle.scan(keep)
         T = int(cu[-1])
         cud = torch.from_numpy(cu.astype(np.int32)).to(dev)
-        blk = rb.VitBlock(params, B, N, H, dt)
+        blk = rb.VitBlock(params, B, N, H, dt, n_hint=T // B)
         x = torch.zeros(B * N, D, dtype=dt, device=dev)
         x[:T] = synth.packed_rows(T, D, dt, 0).to(dev)
         ours = _graph_time(torch, [lambda: blk(x, cud)], 100)
@@ -1019,7 +1019,8 @@ def n1_block_extras(rb, torch, dev, dt):
                         "block_tflops": flops / ours / 1e6, "tensor_frac_of_sustained": flops / ours / 1e6 / tc_peak}
     # layers 5-12 on the packed buffer: ragged_pack of the hidden states once, then 8 blocks
     p = 0.8
-    blocks = [rb.VitBlock({k: v.to(dev) for k, v in synth.vit_weights(D, MLP, dt, L).items()}, B, N, H, dt)
+    blocks = [rb.VitBlock({k: v.to(dev) for k, v in synth.vit_weights(D, MLP, dt, L).items()}, B, N, H, dt,
+                          n_hint=synth.kept_tokens(N, p))
               for L in range(8)]
     xh = synth.hidden_states(B, N, D, dt, seed=0).to(dev)
     keep = torch.from_numpy(synth.mask_threshold_l2(B, N, synth.kept_tokens(N, p), 1000, D=D)).to(dev)

@@ -75,8 +75,10 @@ RAGGED_API int64_t ragged_vit_block_workspace(const ragged_problem* prob, int32_
  * ragged_pack).  prob: B, N (<= 256), H, d = 64, dtype; prob->ld ignored.
  * D = H*64 must be a multiple of 64 and <= 1024.  Seven launches (LN, qkv
  * GEMM, attention, proj GEMM + residual, LN, fc1 GEMM + GELU, fc2 GEMM +
- * residual), PDL-chained, CUDA-graph capturable.  Errors: as above, plus
- * EINVAL if ws_bytes < ragged_vit_block_workspace. */
+ * residual), PDL-chained, CUDA-graph capturable.  prob->n_hint (expected kept
+ * tokens per image, 0 = unknown) is performance only: GEMM tile widths are chosen
+ * for ~B*n_hint live rows and the long-sequence attention kernel above 64.
+ * Errors: as above, plus EINVAL if ws_bytes < ragged_vit_block_workspace. */
 RAGGED_API ragged_status ragged_vit_block(const ragged_problem* prob, void* x, const int32_t* cu_seqlens,
                                           const ragged_vit_weights* w, void* workspace, int64_t ws_bytes,
                                           void* stream);

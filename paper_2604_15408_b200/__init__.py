@@ -398,10 +398,11 @@ class VitBlock:
     """One packed pre-norm ViT block (ragged_vit_block) with its weights and
     a workspace sized for B*N capacity rows."""
 
-    def __init__(self, params: dict, B: int, N: int, H: int, dtype=torch.bfloat16):
+    def __init__(self, params: dict, B: int, N: int, H: int, dtype=torch.bfloat16, n_hint: int = 0):
+        """n_hint: expected kept tokens per image (performance only)."""
         self.params = params
         self.w = vit_weights(params)
-        self.p = problem(B, N, H, 64, dtype)
+        self.p = problem(B, N, H, 64, dtype, n_hint=n_hint)
         nbytes = lib().ragged_vit_block_workspace(ctypes.byref(self.p), self.w.mlp)
         if nbytes < 0:
             raise ValueError("invalid block problem")

@@ -4,6 +4,7 @@
 // attribute setting after the first call, no device->host traffic): the
 // paper's diagnosis is that this host path is the bottleneck at ViT lengths
 // (P:336-345).
+#include <algorithm>
 #include <cmath>
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -447,7 +448,8 @@ ragged_status ragged_layer_norm(ragged_dtype dtype, int32_t rows, int32_t D, con
 
 static ragged_status linear_impl(ragged_dtype dtype, int32_t rows, int32_t N, int32_t K, const void* a,
                                  int64_t lda, const void* w, const void* bias, int epi, const void* residual,
-                                 int64_t ldr, void* out, int64_t ldo, const int32_t* live, cudaStream_t st) {
+                                 int64_t ldr, void* out, int64_t ldo, const int32_t* live, cudaStream_t st,
+                                 int32_t rows_hint = 0) {
   ragged::GemmArgs g{};
   g.bias = bias;
   g.residual = residual;
@@ -458,7 +460,9 @@ static ragged_status linear_impl(ragged_dtype dtype, int32_t rows, int32_t N, in
   g.ldo = ldo;
   g.ldr = ldr;
   g.m_dev = live;
-  const int bn = ragged::gemm_pick_bn(rows, N, device_sms());
+  // tile width from the expected live rows when the caller knows them (performance only;
+  // the grid still covers the capacity and the kernel reads the live count on the device)
+  const int bn = ragged::gemm_pick_bn(rows_hint > 0 && rows_hint < rows ? rows_hint : rows, N, device_sms());
   cudaError_t e = ragged::launch_gemm(dtype, a, lda, w, g, epi, bn, st);
   return e == cudaSuccess ? RAGGED_OK : cuda_fail(e, "ragged_linear");
 }
@@ -526,15 +530,18 @@ ragged_status ragged_vit_block(const ragged_problem* prob, void* x, const int32_
   const char* qkvb = static_cast<const char*>(qkv);
   cudaError_t e = ragged::launch_layer_norm(p.dtype, x, D, w->ln1_w, w->ln1_b, 1e-6f, y, D, rows, live, D, st);
   if (e != cudaSuccess) return cuda_fail(e, "ragged_vit_block/ln1");
-  RAGGED_TRY(linear_impl((ragged_dtype)p.dtype, rows, 3 * D, D, y, D, w->w_qkv, w->b_qkv, 0, nullptr, 0, qkv, 3 * D, live, st));
-  e = ragged::launch_attn(p.dtype, RAGGED_ENGINE_MMA_SYNC, qkvb, qkvb + D * 2, qkvb + 2 * D * 2, cu_seqlens, a,
+  // n_hint (expected kept tokens per image, performance only): GEMM tile widths
+  // for ~B*n_hint live rows, and the long-sequence attention kernel above 64
+  const int32_t rh = p.n_hint > 0 ? (int32_t)std::min<long long>((long long)p.B * p.n_hint, rows) : 0;
+  RAGGED_TRY(linear_impl((ragged_dtype)p.dtype, rows, 3 * D, D, y, D, w->w_qkv, w->b_qkv, 0, nullptr, 0, qkv, 3 * D, live, st, rh));
+  e = ragged::launch_attn(p.dtype, resolve_engine(&p), qkvb, qkvb + D * 2, qkvb + 2 * D * 2, cu_seqlens, a,
                           p.B, p.N, p.H, 3LL * D, st);
   if (e != cudaSuccess) return cuda_fail(e, "ragged_vit_block/attn");
-  RAGGED_TRY(linear_impl((ragged_dtype)p.dtype, rows, D, D, a, D, w->w_proj, w->b_proj, 2, x, D, x, D, live, st));
+  RAGGED_TRY(linear_impl((ragged_dtype)p.dtype, rows, D, D, a, D, w->w_proj, w->b_proj, 2, x, D, x, D, live, st, rh));
   e = ragged::launch_layer_norm(p.dtype, x, D, w->ln2_w, w->ln2_b, 1e-6f, y, D, rows, live, D, st);
   if (e != cudaSuccess) return cuda_fail(e, "ragged_vit_block/ln2");
-  RAGGED_TRY(linear_impl((ragged_dtype)p.dtype, rows, mlp, D, y, D, w->w_fc1, w->b_fc1, 1, nullptr, 0, f, mlp, live, st));
-  RAGGED_TRY(linear_impl((ragged_dtype)p.dtype, rows, D, mlp, f, mlp, w->w_fc2, w->b_fc2, 2, x, D, x, D, live, st));
+  RAGGED_TRY(linear_impl((ragged_dtype)p.dtype, rows, mlp, D, y, D, w->w_fc1, w->b_fc1, 1, nullptr, 0, f, mlp, live, st, rh));
+  RAGGED_TRY(linear_impl((ragged_dtype)p.dtype, rows, D, mlp, f, mlp, w->w_fc2, w->b_fc2, 2, x, D, x, D, live, st, rh));
   return RAGGED_OK;
 }
 

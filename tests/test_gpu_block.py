@@ -164,12 +164,15 @@ def _block_inputs(preset, B, p, seed, dtype=torch.bfloat16, method="l2"):
     return params, cu, x, D, H, MLP, N, T
 
 
+@pytest.mark.parametrize("n_hint", [0, 1, 197])
 @pytest.mark.parametrize("preset,B,p,method", [("deit_tiny", 4, 0.5, "l2"), ("deit_small", 6, 0.0, "l2"),
                                                ("deit_base", 8, 0.8, "l2"), ("deit_base", 5, 0.7, "ats")])
-def test_vit_block_end_to_end(preset, B, p, method):
+def test_vit_block_end_to_end(preset, B, p, method, n_hint):
+    """n_hint (performance only) changes GEMM tile widths and the attention
+    kernel variant; the block meets the same bounds for every hint."""
     dtype = torch.bfloat16
     params, cu, x, D, H, MLP, N, T = _block_inputs(preset, B, p, seed=B, method=method)
-    blk = rb.VitBlock({k: v.to(DEV) for k, v in params.items()}, B, N, H, dtype)
+    blk = rb.VitBlock({k: v.to(DEV) for k, v in params.items()}, B, N, H, dtype, n_hint=n_hint)
     xd = _sentinel((B * N, D), dtype)
     xd[:T] = x.to(DEV)
     blk(xd, torch.from_numpy(cu.astype(np.int32)).to(DEV))
