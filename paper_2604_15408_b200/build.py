@@ -38,7 +38,8 @@ VARIANTS = {"": [], "tl": ["-DRAGGED_TIMELINE"],
             "tlnz": ["-DRAGGED_TIMELINE", "-DRAGGED_ABLATE_ZERO"],
             "abc": ["-DRAGGED_ABLATE_QK", "-DRAGGED_ABLATE_PV", "-DRAGGED_ABLATE_EXP"],
             "aball": ["-DRAGGED_ABLATE_QK", "-DRAGGED_ABLATE_PV", "-DRAGGED_ABLATE_EXP",
-                      "-DRAGGED_ABLATE_ZERO"]}
+                      "-DRAGGED_ABLATE_ZERO"],
+            "nopf": ["-DRAGGED_NO_KEEP_PREFETCH"]}  # A/B of the keep-row L2 prefetch
 
 
 def lib_path(variant: str = "") -> str:

@@ -913,6 +913,16 @@ __global__ void __launch_bounds__(kAttnThreads, 3) attn_kernel(const AttnArgs a,
 
   TL(0);
   pdl_launch_dependents();
+#ifndef RAGGED_NO_KEEP_PREFETCH
+  if constexpr (kFused) {
+    // Before the grid-dependency wait: pull this image's keep row into L2
+    // (prefetch.global.L2 consumes no value, and L2 is the device's point of
+    // coherence, so a producer still writing the mask cannot be bypassed); the
+    // row's DRAM latency overlaps the previous launch's tail.
+    const int pb = (a.cu_mode == 1 ? (int)blockIdx.x - a.cu_groups : (int)blockIdx.x) / a.H;
+    if (pb >= 0 && tid * 128 < a.N) prefetch_l2(a.keep + (long long)pb * a.N + tid * 128);
+  }
+#endif
   pdl_wait_prerequisites();
   int bid = blockIdx.x;
   if constexpr (kFused) {
