@@ -39,7 +39,10 @@ VARIANTS = {"": [], "tl": ["-DRAGGED_TIMELINE"],
             "abc": ["-DRAGGED_ABLATE_QK", "-DRAGGED_ABLATE_PV", "-DRAGGED_ABLATE_EXP"],
             "aball": ["-DRAGGED_ABLATE_QK", "-DRAGGED_ABLATE_PV", "-DRAGGED_ABLATE_EXP",
                       "-DRAGGED_ABLATE_ZERO"],
-            "nopf": ["-DRAGGED_NO_KEEP_PREFETCH"]}  # A/B of the keep-row L2 prefetch
+            # A/B of the fused kernel's pre-wait prefetch: none / keep row only (default: keep row
+            # read + kept q/k/v rows prefetched)
+            "nopf": ["-DRAGGED_NO_KEEP_PREFETCH"],
+            "keeppf": ["-DRAGGED_KEEP_PREFETCH_ONLY"]}
 
 
 def lib_path(variant: str = "") -> str:

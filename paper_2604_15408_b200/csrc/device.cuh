@@ -83,6 +83,12 @@ __device__ __forceinline__ void mma_16816<__half>(float (&d)[4], const uint32_t 
       : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
 
+// One byte through L2 only (.cg: nothing is left in L1 for a later load to hit).
+__device__ __forceinline__ uint32_t ld_global_cg_u8(const void* p) {
+  uint16_t v;
+  asm volatile("ld.global.cg.u8 %0, [%1];" : "=h"(v) : "l"(p));
+  return v;
+}
 __device__ __forceinline__ void prefetch_l2(const void* p) {
   asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
 }

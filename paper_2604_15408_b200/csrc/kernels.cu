@@ -915,12 +915,42 @@ __global__ void __launch_bounds__(kAttnThreads, 3) attn_kernel(const AttnArgs a,
   pdl_launch_dependents();
 #ifndef RAGGED_NO_KEEP_PREFETCH
   if constexpr (kFused) {
-    // Before the grid-dependency wait: pull this image's keep row into L2
-    // (prefetch.global.L2 consumes no value, and L2 is the device's point of
-    // coherence, so a producer still writing the mask cannot be bypassed); the
-    // row's DRAM latency overlaps the previous launch's tail.
-    const int pb = (a.cu_mode == 1 ? (int)blockIdx.x - a.cu_groups : (int)blockIdx.x) / a.H;
-    if (pb >= 0 && tid * 128 < a.N) prefetch_l2(a.keep + (long long)pb * a.N + tid * 128);
+    // Before the grid-dependency wait (PDL: this CTA may be resident while the
+    // previous kernel in the stream still runs): read this image's keep row
+    // through L2 (.cg: nothing is left in L1) and prefetch the kept rows' q/k/v
+    // head slices into L2.  Nothing read here reaches a result: the values
+    // only pick prefetch addresses, and the mask is read again after the wait.
+    // A prefetch consumes no value and L2 is the device's point of coherence,
+    // so if the previous kernel is still producing the mask or q/k/v, the
+    // result is unchanged and only prefetches are wasted.  The DRAM round trips
+    // of the mask and the kept rows then overlap the previous launch's tail.
+    const int pbid = a.cu_mode == 1 ? (int)blockIdx.x - a.cu_groups : (int)blockIdx.x;
+#ifndef RAGGED_KEEP_PREFETCH_ONLY
+    if (pbid >= 0) {
+      const int pb = pbid / a.H, ph = pbid - pb * a.H;
+      const uint8_t* km = a.keep + (long long)pb * a.N;
+      const long long ldb2 = a.ld * 2;
+      const char* base_q = static_cast<const char*>(a.q) + (long long)pb * a.N * ldb2 + ph * kRowBytes;
+      const char* base_k = static_cast<const char*>(a.k) + (long long)pb * a.N * ldb2 + ph * kRowBytes;
+      const char* base_v = static_cast<const char*>(a.v) + (long long)pb * a.N * ldb2 + ph * kRowBytes;
+      const int p0 = tid, p1 = tid + kAttnThreads;  // N <= 256: both loads in flight together
+      const uint32_t m0 = p0 < a.N ? ld_global_cg_u8(km + p0) : 0u;
+      const uint32_t m1 = p1 < a.N ? ld_global_cg_u8(km + p1) : 0u;
+      if (m0 != 0) {
+        prefetch_l2(base_q + p0 * ldb2);
+        prefetch_l2(base_k + p0 * ldb2);
+        prefetch_l2(base_v + p0 * ldb2);
+      }
+      if (m1 != 0) {
+        prefetch_l2(base_q + p1 * ldb2);
+        prefetch_l2(base_k + p1 * ldb2);
+        prefetch_l2(base_v + p1 * ldb2);
+      }
+    }
+#else
+    const int pb = pbid / a.H;
+    if (pbid >= 0 && tid * 128 < a.N) prefetch_l2(a.keep + (long long)pb * a.N + tid * 128);
+#endif
   }
 #endif
   pdl_wait_prerequisites();
