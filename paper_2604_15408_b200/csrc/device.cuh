@@ -89,6 +89,11 @@ __device__ __forceinline__ uint32_t ld_global_cg_u8(const void* p) {
   asm volatile("ld.global.cg.u8 %0, [%1];" : "=h"(v) : "l"(p));
   return v;
 }
+__device__ __forceinline__ int ld_global_cg_i32(const void* p) {
+  int v;
+  asm volatile("ld.global.cg.s32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
 __device__ __forceinline__ void prefetch_l2(const void* p) {
   asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
 }

@@ -951,6 +951,22 @@ __global__ void __launch_bounds__(kAttnThreads, 3) attn_kernel(const AttnArgs a,
     const int pb = pbid / a.H;
     if (pbid >= 0 && tid * 128 < a.N) prefetch_l2(a.keep + (long long)pb * a.N + tid * 128);
 #endif
+  } else {
+    // Packed inputs: the same speculation on cu_seqlens -- cu[b], cu[b+1] read
+    // through L2, the image's packed q/k/v rows of this head prefetched; the
+    // range is clamped to the B*N-row capacity, and cu is read again after the wait.
+    const int pb = (int)blockIdx.x / a.H, ph = (int)blockIdx.x - pb * a.H;
+    const int c0 = ld_global_cg_i32(a.cu + pb), c1 = ld_global_cg_i32(a.cu + pb + 1);
+    const int pn = min(max(c1 - c0, 0), a.N);
+    if (c0 >= 0 && (long long)c0 + pn <= (long long)a.B * a.N) {
+      const long long ldb2 = a.ld * 2;
+      const long long off = (long long)c0 * ldb2 + ph * kRowBytes;
+      for (int r = tid; r < pn; r += kAttnThreads) {
+        prefetch_l2(static_cast<const char*>(a.q) + off + r * ldb2);
+        prefetch_l2(static_cast<const char*>(a.k) + off + r * ldb2);
+        prefetch_l2(static_cast<const char*>(a.v) + off + r * ldb2);
+      }
+    }
   }
 #endif
   pdl_wait_prerequisites();
