@@ -476,3 +476,33 @@ def test_long_variant_running_max_paths(dtype, ramp):
     assert np.array_equal(bits(o_long), bits(o_comp))
     check_attention(to_np(o_long), ref, DT[dtype], dist="peaked")
     check_attention(to_np(o_short), ref, DT[dtype], dist="peaked")
+
+
+@pytest.mark.parametrize("n_hint", [0, 197])
+def test_mask_rewritten_by_previous_kernel(n_hint):
+    """The fused kernel reads the keep row (and prefetches kept rows) BEFORE its
+    PDL grid-dependency wait; only the post-wait read may reach results.  Here
+    the N2 mask kernel rewrites ONE keep buffer right before every fused call
+    (both PDL-launched on one stream, no host sync), alternating two hidden-
+    state batches whose masks differ, so every speculative read can see the
+    previous iteration's mask or a half-written one.  Every output must equal,
+    bit for bit, the output computed with a synchronised mask."""
+    B, N, H = 16, 197, 12
+    kk = synth.kept_tokens(N, 0.7)
+    xs = [synth.hidden_states(B, N, H * 64, "bf16", seed=s).to(DEV) for s in (11, 12)]
+    q, k, v = _dev(*synth.activations(B, N, H, 64, "bf16", seed=11))
+    ref = []
+    for x in xs:
+        km = rb.keep_topk_l2(x, kk)
+        torch.cuda.synchronize()
+        ref.append(rb.pack_attend_unpack(q, k, v, km, n_hint=n_hint))
+        torch.cuda.synchronize()
+    assert not torch.equal(rb.keep_topk_l2(xs[0], kk), rb.keep_topk_l2(xs[1], kk))
+    keep = torch.empty(B, N, dtype=torch.uint8, device=DEV)
+    outs = [torch.empty_like(ref[0]) for _ in range(40)]
+    for i, o in enumerate(outs):
+        rb.keep_topk_l2(xs[i % 2], kk, keep=keep)
+        rb.pack_attend_unpack(q, k, v, keep, o=o, n_hint=n_hint)
+    torch.cuda.synchronize()
+    for i, o in enumerate(outs):
+        assert np.array_equal(bits(o), bits(ref[i % 2])), f"call {i}"
