@@ -603,6 +603,33 @@ __global__ void __launch_bounds__(kImgThreads)
   __shared__ int16_t sPos[kMaxN];
   __shared__ uint32_t sWords[16];
   pdl_launch_dependents();
+#ifndef RAGGED_NO_KEEP_PREFETCH
+  {  // as attn_kernel: keep row read through L2 before the wait, only to choose
+     // prefetch addresses (the image's keep row; with kPack its kept rows)
+    const int sb = kPack ? (int)(blockIdx.x / H) : (int)blockIdx.x;
+    const uint8_t* skm = keep + (long long)sb * N;
+    const int s0 = threadIdx.x, s1 = threadIdx.x + kImgThreads;
+    if constexpr (kPack) {
+      const int sh = (int)(blockIdx.x - (unsigned)sb * H);
+      const uint32_t m0 = s0 < N ? ld_global_cg_u8(skm + s0) : 0u;
+      const uint32_t m1 = s1 < N ? ld_global_cg_u8(skm + s1) : 0u;
+      const long long o0 = ((long long)sb * N + s0) * ld_bytes + sh * kRowBytes;
+      const long long o1 = ((long long)sb * N + s1) * ld_bytes + sh * kRowBytes;
+      if (m0 != 0) {
+        prefetch_l2(q + o0);
+        prefetch_l2(k + o0);
+        prefetch_l2(v + o0);
+      }
+      if (m1 != 0) {
+        prefetch_l2(q + o1);
+        prefetch_l2(k + o1);
+        prefetch_l2(v + o1);
+      }
+    } else if (threadIdx.x * 128 < N) {
+      prefetch_l2(skm + threadIdx.x * 128);
+    }
+  }
+#endif
   pdl_wait_prerequisites();
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int b = kPack ? (int)(blockIdx.x / H) : (int)blockIdx.x;
