@@ -1339,6 +1339,17 @@ __global__ void __launch_bounds__(kPruneThreads, 1)
                         uint8_t* __restrict__ keep) {
   __shared__ float s_score[kMaxN];
   pdl_launch_dependents();
+#ifndef RAGGED_NO_KEEP_PREFETCH
+  {  // the image's hidden rows into L2 before the grid-dependency wait (prefetch
+     // only: every value is read after the wait; L2 is the point of coherence)
+    const char* ib = reinterpret_cast<const char*>(x + (long long)blockIdx.x * N * ld);
+    const int lpr = D >> 6;  // 128-byte lines per row (D % 64 == 0)
+    for (int i = threadIdx.x; i < N * lpr; i += kPruneThreads) {
+      const int rn = i / lpr, l = i - rn * lpr;
+      prefetch_l2(ib + (long long)rn * ld * 2 + l * 128);
+    }
+  }
+#endif
   pdl_wait_prerequisites();
   const int b = blockIdx.x, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int cpr = D >> 3;  // 16-byte chunks per row
