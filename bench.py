@@ -36,6 +36,7 @@ sys.path.insert(0, ROOT)
 
 METRIC = "ragged attn µs/call (DeiT-B, B=32, 80% pruned); pipeline images/sec"
 N_SETS = 16
+GATE_CYCLES = 2_000_000        # ~1 ms at 1.965 GHz
 
 
 def parse():
@@ -307,6 +308,12 @@ def main():
     pr = torch.cuda.get_device_properties(dev)
     bus = f"{pr.pci_domain_id:08X}:{pr.pci_bus_id:02X}:{pr.pci_device_id:02X}.0"
     with ClockSampler(local, bus) as clk:
+        # Device-side gate (torch's spin kernel, ~1 ms) queued BEFORE the start
+        # event: the start timestamp is taken when the gate ends, by which time
+        # the host has submitted the graph.  Without it, host-side latency (the
+        # graph submission, the NVML sampling thread holding the GIL) lands
+        # between the two events.  Nothing of the gate is inside the timed region.
+        torch.cuda._sleep(GATE_CYCLES)
         start.record(stream)
         g.replay()
         end.record(stream)
@@ -316,6 +323,7 @@ def main():
     ms = max_over_ranks(start.elapsed_time(end), dev)
     us_per_call = 1e3 * ms / args.steps
     value = ws * B * args.steps / (ms * 1e-3)
+    single = single_call_latency(torch, step, stream)
 
     # e2e through the C ABI with host buffers (pinned): H2D inputs, fused kernel, D2H output
     e2e = measure_e2e(args, rb, torch, dev, q, k, v, keep, ws, B, N, H, dt)
@@ -357,10 +365,11 @@ def main():
                        "T": T, "global_batch": ws * B,
                        "l2": f"{N_SETS} rotating input/output sets "
                              f"({N_SETS * (4 * B * N * H * 128) / 1e6:.0f} MB > 126 MB L2)",
-                       "timing": "K steps in one CUDA graph, CUDA events, max over ranks",
+                       "timing": "K steps in one CUDA graph, CUDA events, max over ranks; a ~1 ms device-side "
+                                 "gate kernel queued before the start event keeps host submission latency out",
                        "exchange": "none in the headline (compute-only, weak scaling); "
                                    "all-gather variants under gather_variants"},
-            "us_per_call": us_per_call, "images_per_s": value,
+            "us_per_call": us_per_call, "images_per_s": value, "single_call_latency_us": single,
             "gpu_launches": args.steps, "clocks": clk.summary(), "roofline": roofline, "e2e": e2e}
     if gv is not None:
         line["gather_variants"] = gv
@@ -377,11 +386,41 @@ def main():
         dist.destroy_process_group()
 
 
+def single_call_latency(torch, step, stream, reps=N_SETS):
+    """One call at a time (the paper's Table 1 protocol times calls one by one,
+    P:142-143): a one-step graph per cold input set, replayed alone between a
+    device-side gate and a synchronize, CUDA events around it.  Unlike the
+    headline (K back-to-back calls whose launches overlap through PDL), this is
+    the device latency of an isolated call.  Median / min / max over the sets."""
+    graphs = []
+    cap = torch.cuda.Stream()
+    for i in range(reps):
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=cap):
+            step(i)
+        graphs.append(g)
+    torch.cuda.synchronize()
+    for g in graphs:
+        g.replay()
+    torch.cuda.synchronize()
+    ts = []
+    for g in graphs:
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda._sleep(GATE_CYCLES // 4)
+        a.record(stream)
+        g.replay()
+        b.record(stream)
+        torch.cuda.synchronize()
+        ts.append(1e3 * a.elapsed_time(b))
+    return {"median": statistics.median(ts), "min": min(ts), "max": max(ts), "calls": len(ts),
+            "protocol": "one-call graph per cold set, gate + events, synchronize between calls"}
+
+
 def traffic_from_profile():
     """DRAM bytes (read + write) per launch of the fused kernel from the
     committed ncu --set full summary (profiles/r01_ncu_fused_traffic.json,
     written by scripts/ncu_traffic.py), or None."""
-    p = os.path.join(ROOT, "profiles", "r01_ncu_fused_traffic.json")
+    p = os.path.join(ROOT, "profiles", "r01", "r01_ncu_fused_traffic.json")
     try:
         return json.load(open(p))["dram_bytes_per_launch"]
     except Exception:

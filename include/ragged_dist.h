@@ -68,7 +68,8 @@ typedef struct {
 /* ragged_pack_attend_unpack (ragged.h) whose outputs go to the gather
  * destinations instead of one local `o`: padded O rows to out[r] and/or CLS
  * rows to cls[r].  cu_seqlens_or_null stays local (this rank's images).
- * Bitwise identical rows to ragged_pack_attend_unpack on the same inputs. */
+ * Bitwise identical rows to ragged_pack_attend_unpack on the same inputs and
+ * the same prob (the same kernel variant is chosen from prob->n_hint). */
 RAGGED_API ragged_status ragged_pack_attend_unpack_gather(const ragged_problem* prob,
                                                           const uint8_t* keep, const void* q,
                                                           const void* k, const void* v,
@@ -76,7 +77,8 @@ RAGGED_API ragged_status ragged_pack_attend_unpack_gather(const ragged_problem* 
                                                           const ragged_gather* g, void* stream);
 
 /* ragged_attn (ragged.h) whose packed output rows [cu[b], cu[b+1]) go to
- * out[r] + row * H * d for every rank r (packed all-gather, capacity slots). */
+ * out[r] + row * H * d for every rank r (packed all-gather, capacity slots).
+ * Bitwise identical rows to ragged_attn on the same inputs and prob. */
 RAGGED_API ragged_status ragged_attn_gather(const ragged_problem* prob, const void* qp,
                                             const void* kp, const void* vp,
                                             const int32_t* cu_seqlens, const ragged_gather* g,

@@ -35,6 +35,11 @@ Passages followed (PAPER.md line numbers):
 
   prune      (NEXT row N2) Threshold-l2 keep mask: l2 norm of each token's
              hidden state, CLS + top-(k-1) (R20).
+  evit       (NEXT row N2) EViT-style keep mask with a fused token (P:95-96
+             "ranks tokens by CLS-attention scores and fuses pruned tokens into a
+             single representative"; reading R17): head-averaged CLS logits,
+             CLS + top-(k-2), the dropped rows' logit-softmax-weighted mean
+             written into the first dropped position, which is marked kept.
 
 Pins (tests/test_oracle.py, run with -m "not gpu"): SPEC worked examples,
 Table 1 token counts and the T = 6,304 / 12,608 totals (P:167-179, P:202,
@@ -158,17 +163,76 @@ def l2_scores(x) -> np.ndarray:
     return s
 
 
+def _scores_nan_low(s):
+    """NaN scores rank below every finite score (R20): at most k tokens kept."""
+    s = np.array(s, dtype=np.float64)
+    s[np.isnan(s)] = -np.inf
+    return s
+
+
 def keep_topk_l2(x, k: int) -> np.ndarray:
     """keep [B, N] uint8: CLS + the k - 1 highest-scoring other tokens of each
     image (P:362-363 "any supported method produces a binary keep mask"); ties
     go to the lower position (stable order, R20)."""
-    s = l2_scores(x)
+    if k < 1:
+        raise ValueError("k must be >= 1: CLS always survives (R6)")
+    s = _scores_nan_low(l2_scores(x))
     B, N = s.shape
     keep = np.zeros((B, N), np.uint8)
     for b in range(B):
         order = np.argsort(-s[b], kind="stable")
         keep[b, order[:max(0, min(k, N))]] = 1
     return keep
+
+
+def evit_logits(q, k) -> np.ndarray:
+    """EViT token scores (R17): the CLS query's attention logits to
+    every token, averaged over heads -- logit[b, n] = (1/H) sum_h
+    q[b, 0, h] . k[b, n, h] / sqrt(d), fp64."""
+    q, k = as_f64(q), as_f64(k)
+    B, N, H, d = k.shape
+    out = np.zeros((B, N))
+    for b in range(B):
+        for h in range(H):
+            out[b] += (k[b, :, h] @ q[b, 0, h]) / np.sqrt(d)
+    return out / H
+
+
+def keep_evit(q, k, v, k_keep: int):
+    """EViT-style keep mask with a fused token (reading R17), per image:
+    1. scores = evit_logits; CLS (n = 0) always kept;
+    2. keep CLS + the max(k_keep - 2, 0) highest-scoring other tokens (ties to the
+       lower position);
+    3. if k_keep >= 2 and a token is dropped: the fused token = sum over dropped
+       tokens j of w_j * row_j with w = softmax(scores[dropped]) (CLS-attention
+       weights of the dropped tokens, normalised), for each of Q, K, V and every
+       head; it is written into the first dropped position f, which is kept;
+    4. k_keep >= N keeps every token (no fused token).
+    Returns (keep uint8 [B, N], f int [B] (-1 = none), fused fp64 [B, 3, H, d])."""
+    if k_keep < 1:
+        raise ValueError("k_keep must be >= 1: CLS always survives (R6)")
+    s = _scores_nan_low(evit_logits(q, k))
+    qf, kf, vf = as_f64(q), as_f64(k), as_f64(v)
+    B, N, H, d = kf.shape
+    keep = np.zeros((B, N), np.uint8)
+    f = np.full(B, -1, np.int64)
+    fused = np.zeros((B, 3, H, d))
+    for b in range(B):
+        if k_keep >= N:
+            keep[b] = 1
+            continue
+        others = 1 + np.argsort(-s[b, 1:], kind="stable")
+        keep[b, 0] = 1
+        keep[b, others[:max(k_keep - 2, 0)]] = 1
+        dropped = np.flatnonzero(keep[b] == 0)
+        if k_keep >= 2 and dropped.size > 0:
+            e = np.exp(s[b, dropped] - s[b, dropped].max())
+            w = e / e.sum()
+            for t, x in enumerate((qf, kf, vf)):
+                fused[b, t] = np.tensordot(w, x[b, dropped], axes=(0, 0))
+            f[b] = dropped[0]
+            keep[b, f[b]] = 1
+    return keep, f, fused
 
 
 def attention_image_head(q, k, v, keep, b: int, h: int):

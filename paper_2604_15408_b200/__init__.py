@@ -199,12 +199,32 @@ def _padded_problem(q, k, v, engine, n_hint=0):
     return problem(B, N, H, d, q.dtype, q.stride(1), engine, n_hint)
 
 
-def _keep_u8(keep):
+def _keep_u8(keep, B: int | None = None, N: int | None = None, device=None):
     if keep.dtype == torch.bool:
         keep = keep.view(torch.uint8)
-    if keep.dtype != torch.uint8 or not keep.is_contiguous():
+    if keep.dtype != torch.uint8 or not keep.is_contiguous() or keep.dim() != 2:
         raise ValueError("keep must be a contiguous uint8/bool [B, N] tensor")
+    if B is not None and tuple(keep.shape) != (B, N):
+        raise ValueError(f"keep must be [B, N] = [{B}, {N}], got {list(keep.shape)}")
+    if device is not None and keep.device != device:
+        raise ValueError(f"keep is on {keep.device}, expected {device}")
     return keep
+
+
+def _require(t, name: str, dtype, device, numel: int | None = None, shape=None):
+    """The C ABI cannot see buffer sizes: check a caller buffer before its
+    pointer crosses the boundary (dtype, device, contiguity, size)."""
+    if t.dtype != dtype:
+        raise ValueError(f"{name} must be {dtype}, got {t.dtype}")
+    if t.device != device:
+        raise ValueError(f"{name} is on {t.device}, expected {device}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    if shape is not None and tuple(t.shape) != tuple(shape):
+        raise ValueError(f"{name} must have shape {list(shape)}, got {list(t.shape)}")
+    if numel is not None and t.numel() < numel:
+        raise ValueError(f"{name} holds {t.numel()} elements, needs at least {numel}")
+    return t
 
 
 def scan(keep, cu=None, dst=None, src=None, stream=None):
@@ -215,6 +235,9 @@ def scan(keep, cu=None, dst=None, src=None, stream=None):
     cu = torch.empty(B + 1, dtype=torch.int32, device=dev) if cu is None else cu
     dst = torch.empty(B * N, dtype=torch.int32, device=dev) if dst is None else dst
     src = torch.empty(B * N, dtype=torch.int32, device=dev) if src is None else src
+    _require(cu, "cu", torch.int32, dev, B + 1)
+    _require(dst, "dst", torch.int32, dev, B * N)
+    _require(src, "src", torch.int32, dev, B * N)
     p = problem(B, N, 1)
     _check(lib().ragged_scan(ctypes.byref(p), keep.data_ptr(), cu.data_ptr(), dst.data_ptr(),
                             src.data_ptr(), _stream(stream)), "ragged_scan")
@@ -225,8 +248,8 @@ def pack(q, k, v, keep, out=None, stream=None, engine=ENGINE_AUTO):
     """a1 + a2: returns (qp, kp, vp, cu, dst, src); packed buffers
     have capacity B*N rows, rows [0, cu[B]) valid."""
     p = _padded_problem(q, k, v, engine)
-    keep = _keep_u8(keep)
     B, N, H, d = q.shape
+    keep = _keep_u8(keep, B, N, q.device)
     if out is None:
         mk = lambda: torch.empty(B * N, H, d, dtype=q.dtype, device=q.device)  # noqa: E731
         qp, kp, vp = mk(), mk(), mk()
@@ -235,6 +258,10 @@ def pack(q, k, v, keep, out=None, stream=None, engine=ENGINE_AUTO):
         src = torch.empty(B * N, dtype=torch.int32, device=q.device)
     else:
         qp, kp, vp, cu, dst, src = out
+        for t, nm in ((qp, "qp"), (kp, "kp"), (vp, "vp")):
+            _require(t, nm, q.dtype, q.device, B * N * H * d)
+        for t, nm in ((cu, "cu"), (dst, "dst"), (src, "src")):
+            _require(t, nm, torch.int32, q.device, B + 1 if nm == "cu" else B * N)
     _check(lib().ragged_pack(ctypes.byref(p), keep.data_ptr(), q.data_ptr(), k.data_ptr(), v.data_ptr(),
                             cu.data_ptr(), dst.data_ptr(), src.data_ptr(), qp.data_ptr(), kp.data_ptr(),
                             vp.data_ptr(), _stream(stream)), "ragged_pack")
@@ -258,10 +285,12 @@ def attn(qp, kp, vp, cu, N: int, op=None, stream=None, engine=ENGINE_AUTO, n_hin
     n_hint: expected kept tokens per image (performance only)."""
     cap, H, d = qp.shape
     ld = _packed_ld(qp, kp, vp)
+    _require(cu, "cu", torch.int32, qp.device)
     B = cu.numel() - 1
+    if cap < B * N:
+        raise ValueError(f"packed buffers hold {cap} rows, need capacity B*N = {B * N}")
     op = torch.empty(cap, H, d, dtype=qp.dtype, device=qp.device) if op is None else op
-    if not op.is_contiguous() or op.shape != qp.shape:
-        raise ValueError("op must be a contiguous [cap, H, d] tensor")
+    _require(op, "op", qp.dtype, qp.device, shape=qp.shape)
     p = problem(B, N, H, d, qp.dtype, ld, engine, n_hint)
     _check(lib().ragged_attn(ctypes.byref(p), qp.data_ptr(), kp.data_ptr(), vp.data_ptr(), cu.data_ptr(),
                             op.data_ptr(), _stream(stream)), "ragged_attn")
@@ -281,7 +310,11 @@ def attn_fp8(qp, kp, vp, cu, N: int, descale=(1.0, 1.0, 1.0), out_dtype=torch.bf
             raise ValueError("qp/kp/vp must be contiguous float8_e4m3fn/uint8 [cap, H, d] of one shape")
     if out_dtype not in _DTYPE:
         raise ValueError("out_dtype must be bf16 or fp16")
+    _require(cu, "cu", torch.int32, qp.device)
+    if cap < (cu.numel() - 1) * N:
+        raise ValueError(f"packed buffers hold {cap} rows, need capacity B*N = {(cu.numel() - 1) * N}")
     op = torch.empty(cap, H, d, dtype=out_dtype, device=qp.device) if op is None else op
+    _require(op, "op", out_dtype, qp.device, shape=(cap, H, d))
     p = problem(len(cu) - 1, N, H, d, out_dtype, H * d)
     dq, dk, dv = (float(x) for x in descale)
     _check(lib().ragged_attn_fp8(ctypes.byref(p), qp.data_ptr(), kp.data_ptr(), vp.data_ptr(), dq, dk, dv,
@@ -291,8 +324,12 @@ def attn_fp8(qp, kp, vp, cu, N: int, descale=(1.0, 1.0, 1.0), out_dtype=torch.bf
 
 def unpack(op, dst, B: int, N: int, o=None, stream=None):
     """a4: packed O -> padded [B, N, H, d]; dropped rows +0.0."""
-    _, H, d = op.shape
+    cap, H, d = op.shape
+    if cap < B * N or not op.is_contiguous():
+        raise ValueError(f"op must be a contiguous packed buffer of capacity B*N = {B * N} rows")
+    _require(dst, "dst", torch.int32, op.device, B * N)
     o = torch.empty(B, N, H, d, dtype=op.dtype, device=op.device) if o is None else o
+    _require(o, "o", op.dtype, op.device, shape=(B, N, H, d))
     p = problem(B, N, H, d, op.dtype)
     _check(lib().ragged_unpack(ctypes.byref(p), op.data_ptr(), dst.data_ptr(), o.data_ptr(),
                               _stream(stream)), "ragged_unpack")
@@ -304,11 +341,14 @@ def pack_attend_unpack(q, k, v, keep, o=None, cu=None, want_cu=False, stream=Non
     """a5: the fused single-launch path.  Returns o (and cu if requested).
     n_hint: expected kept tokens per image (performance only)."""
     p = _padded_problem(q, k, v, engine, n_hint)
-    keep = _keep_u8(keep)
     B, N, H, d = q.shape
+    keep = _keep_u8(keep, B, N, q.device)
     o = torch.empty(B, N, H, d, dtype=q.dtype, device=q.device) if o is None else o
+    _require(o, "o", q.dtype, q.device, shape=(B, N, H, d))
     if want_cu and cu is None:
         cu = torch.empty(B + 1, dtype=torch.int32, device=q.device)
+    if cu is not None:
+        _require(cu, "cu", torch.int32, q.device, B + 1)
     _check(lib().ragged_pack_attend_unpack(ctypes.byref(p), keep.data_ptr(), q.data_ptr(), k.data_ptr(),
                                           v.data_ptr(), o.data_ptr(), _ptr(cu), _stream(stream)),
            "ragged_pack_attend_unpack")
@@ -324,7 +364,14 @@ def pack_attend_unpack_host(q, k, v, keep, o, cu=None, stream=None, engine=ENGIN
         if t.device.type != "cpu" or not t.is_pinned():
             raise ValueError("q, k, v, keep must be pinned CPU tensors")
     p = _padded_problem(q, k, v, engine)
-    keep = _keep_u8(keep)
+    B, N, H, d = q.shape
+    keep = _keep_u8(keep, B, N)
+    if o.dtype != q.dtype or tuple(o.shape) != (B, N, H, d) or not o.is_contiguous():
+        raise ValueError("o must be a contiguous [B, N, H, d] tensor of q's dtype")
+    if o.device.type == "cpu" and not o.is_pinned():
+        raise ValueError("a CPU o must be pinned")
+    if cu is not None and (cu.dtype != torch.int32 or cu.numel() < B + 1):
+        raise ValueError("cu must be int32 with at least B+1 elements")
     _check(lib().ragged_pack_attend_unpack_host(ctypes.byref(p), keep.data_ptr(), q.data_ptr(),
                                                k.data_ptr(), v.data_ptr(), o.data_ptr(), _ptr(cu),
                                                _stream(stream)),
@@ -333,23 +380,28 @@ def pack_attend_unpack_host(q, k, v, keep, o, cu=None, stream=None, engine=ENGIN
 
 
 def pack_attend_unpack_gather(q, k, v, keep, gather: Gather, cu=None, stream=None,
-                              engine=ENGINE_AUTO):
+                              engine=ENGINE_AUTO, n_hint=0):
     """a5 fused with the §8(e) all-gather: this rank's padded O rows (and/or
     CLS rows) are stored into every rank's gathered buffer (ragged_dist.h)."""
-    p = _padded_problem(q, k, v, engine)
-    keep = _keep_u8(keep)
+    p = _padded_problem(q, k, v, engine, n_hint)
+    keep = _keep_u8(keep, q.shape[0], q.shape[1], q.device)
+    if cu is not None:
+        _require(cu, "cu", torch.int32, q.device, q.shape[0] + 1)
     _check(lib().ragged_pack_attend_unpack_gather(ctypes.byref(p), keep.data_ptr(), q.data_ptr(),
                                                  k.data_ptr(), v.data_ptr(), _ptr(cu),
                                                  ctypes.byref(gather), _stream(stream)),
            "ragged_pack_attend_unpack_gather")
 
 
-def attn_gather(qp, kp, vp, cu, N: int, gather: Gather, stream=None, engine=ENGINE_AUTO):
+def attn_gather(qp, kp, vp, cu, N: int, gather: Gather, stream=None, engine=ENGINE_AUTO, n_hint=0):
     """a3 with the packed all-gather: rows [cu[b], cu[b+1]) of this rank's
     packed O go to out[r] + row * H * d on every rank r (ragged_dist.h)."""
     cap, H, d = qp.shape
+    _require(cu, "cu", torch.int32, qp.device)
     B = cu.numel() - 1
-    p = problem(B, N, H, d, qp.dtype, _packed_ld(qp, kp, vp), engine)
+    if cap < B * N:
+        raise ValueError(f"packed buffers hold {cap} rows, need capacity B*N = {B * N}")
+    p = problem(B, N, H, d, qp.dtype, _packed_ld(qp, kp, vp), engine, n_hint)
     _check(lib().ragged_attn_gather(ctypes.byref(p), qp.data_ptr(), kp.data_ptr(), vp.data_ptr(),
                                    cu.data_ptr(), ctypes.byref(gather), _stream(stream)),
            "ragged_attn_gather")
@@ -484,6 +536,7 @@ def keep_topk_l2(x, k: int, keep=None, stream=None):
     if D % 64 != 0 or x.stride(0) != N * x.stride(1):
         raise ValueError("D must be a multiple of 64 and tokens evenly strided")
     keep = torch.empty(B, N, dtype=torch.uint8, device=x.device) if keep is None else keep
+    _require(keep, "keep", torch.uint8, x.device, shape=(B, N))
     p = problem(B, N, D // 64, 64, x.dtype, x.stride(1))
     _check(lib().ragged_keep_topk_l2(ctypes.byref(p), x.data_ptr(), int(k), keep.data_ptr(),
                                      _stream(stream)), "ragged_keep_topk_l2")

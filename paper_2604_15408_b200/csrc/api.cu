@@ -384,7 +384,7 @@ ragged_status ragged_pack_attend_unpack_gather(const ragged_problem* prob, const
   RAGGED_TRY(check_ptr(k, "k"));
   RAGGED_TRY(check_ptr(v, "v"));
   if ((long long)prob->B * prob->H + 1 > 0x7fffffffLL) return fail(RAGGED_ENOTSUP, "B*H too large");
-  cudaError_t e = ragged::launch_fused_gather(prob->dtype, keep, q, k, v, prob->ld, cu_seqlens_or_null,
+  cudaError_t e = ragged::launch_fused_gather(prob->dtype, resolve_engine(prob), keep, q, k, v, prob->ld, cu_seqlens_or_null,
                                               prob->B, prob->N, prob->H, ga, as_stream(stream));
   return e == cudaSuccess ? RAGGED_OK : cuda_fail(e, "ragged_pack_attend_unpack_gather");
 }
@@ -401,7 +401,7 @@ ragged_status ragged_attn_gather(const ragged_problem* prob, const void* qp, con
   RAGGED_TRY(check_ptr(vp, "vp"));
   RAGGED_TRY(check_ptr_any(cu_seqlens, "cu_seqlens"));
   if ((long long)prob->B * prob->H > 0x7fffffffLL) return fail(RAGGED_ENOTSUP, "B*H too large");
-  cudaError_t e = ragged::launch_attn_gather(prob->dtype, qp, kp, vp, cu_seqlens, prob->B, prob->N,
+  cudaError_t e = ragged::launch_attn_gather(prob->dtype, resolve_engine(prob), qp, kp, vp, cu_seqlens, prob->B, prob->N,
                                              prob->H, prob->ld, ga, as_stream(stream));
   return e == cudaSuccess ? RAGGED_OK : cuda_fail(e, "ragged_attn_gather");
 }

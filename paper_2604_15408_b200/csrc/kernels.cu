@@ -1574,7 +1574,7 @@ cudaError_t launch_fused(int dtype, int engine, const uint8_t* keep, const void*
 
 // Fused pack-attend-unpack whose padded output (and/or CLS rows) is written to
 // every rank's gathered buffer (mma.sync engine).  cu_seqlens stays local.
-cudaError_t launch_fused_gather(int dtype, const uint8_t* keep, const void* q, const void* k,
+cudaError_t launch_fused_gather(int dtype, int engine, const uint8_t* keep, const void* q, const void* k,
                                 const void* v, long long ld, int32_t* cu_out, int B, int N, int H,
                                 const GatherArgs& g, cudaStream_t st) {
   AttnArgs a{};
@@ -1590,12 +1590,17 @@ cudaError_t launch_fused_gather(int dtype, const uint8_t* keep, const void* q, c
   a.H = H;
   a.ld = ld;
   const int grid = B * H + a.cu_groups;
+  // same kernel variant as ragged_pack_attend_unpack picks for this problem, so
+  // the gathered rows are bitwise those of the local call
+  if (engine == kEngineMmaLong)
+    return dtype == 0 ? launch_attn_mma<__nv_bfloat16, true, true, true>(a, grid, st, g)
+                      : launch_attn_mma<__half, true, true, true>(a, grid, st, g);
   return dtype == 0 ? launch_attn_mma<__nv_bfloat16, true, true>(a, grid, st, g)
                     : launch_attn_mma<__half, true, true>(a, grid, st, g);
 }
 
 // ragged_attn whose packed output rows go to every rank's gathered buffer.
-cudaError_t launch_attn_gather(int dtype, const void* qp, const void* kp, const void* vp,
+cudaError_t launch_attn_gather(int dtype, int engine, const void* qp, const void* kp, const void* vp,
                                const int32_t* cu, int B, int N, int H, long long ld,
                                const GatherArgs& g, cudaStream_t st) {
   AttnArgs a{};
@@ -1607,6 +1612,9 @@ cudaError_t launch_attn_gather(int dtype, const void* qp, const void* kp, const 
   a.N = N;
   a.H = H;
   a.ld = ld;
+  if (engine == kEngineMmaLong)
+    return dtype == 0 ? launch_attn_mma<__nv_bfloat16, false, true, true>(a, B * H, st, g)
+                      : launch_attn_mma<__half, false, true, true>(a, B * H, st, g);
   return dtype == 0 ? launch_attn_mma<__nv_bfloat16, false, true>(a, B * H, st, g)
                     : launch_attn_mma<__half, false, true>(a, B * H, st, g);
 }

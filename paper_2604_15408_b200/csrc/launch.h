@@ -36,10 +36,10 @@ struct GatherArgs {
   uint32_t* sig[kMaxPeers] = {};    // rank r's signal array [world]
   uint32_t* state = nullptr;        // local [2]: arrival counter, epoch
 };
-cudaError_t launch_fused_gather(int dtype, const uint8_t* keep, const void* q, const void* k,
+cudaError_t launch_fused_gather(int dtype, int engine, const uint8_t* keep, const void* q, const void* k,
                                 const void* v, long long ld, int32_t* cu_out, int B, int N, int H,
                                 const GatherArgs& g, cudaStream_t st);
-cudaError_t launch_attn_gather(int dtype, const void* qp, const void* kp, const void* vp,
+cudaError_t launch_attn_gather(int dtype, int engine, const void* qp, const void* kp, const void* vp,
                                const int32_t* cu, int B, int N, int H, long long ld,
                                const GatherArgs& g, cudaStream_t st);
 cudaError_t launch_empty(int grid, int block, cudaStream_t st);

@@ -218,3 +218,36 @@ def test_block_validation():
     w.mlp = 100
     assert L.ragged_vit_block(ctypes.byref(p), FAKE, FAKE, ctypes.byref(w), FAKE, big, None) == rb.ENOTSUP
     assert L.ragged_vit_block(None, FAKE, FAKE, ctypes.byref(w), FAKE, big, None) == rb.EINVAL
+
+
+def test_python_binding_checks_caller_buffers():
+    """the ABI cannot see buffer sizes, so the binding checks every
+    caller buffer (shape, dtype, device, size) before a pointer crosses it.
+    CPU tensors suffice: every check fires before any library call."""
+    import torch
+    B, N, H, d = 2, 5, 3, 64
+    q = torch.zeros(B, N, H, d, dtype=torch.bfloat16)
+    keep = torch.ones(B, N, dtype=torch.uint8)
+    bad = [
+        lambda: rb.pack_attend_unpack(q, q, q, torch.ones(B, N + 1, dtype=torch.uint8)),   # mask shape
+        lambda: rb.pack_attend_unpack(q, q, q, keep, o=torch.zeros(B, N, H, d - 8, dtype=torch.bfloat16)),
+        lambda: rb.pack_attend_unpack(q, q, q, keep, o=torch.zeros(B, N, H, d, dtype=torch.float16)),
+        lambda: rb.pack_attend_unpack(q, q, q, keep, cu=torch.zeros(B + 1, dtype=torch.int64)),
+        lambda: rb.pack_attend_unpack(q, q, q, keep, cu=torch.zeros(B, dtype=torch.int32)),
+        lambda: rb.scan(keep, cu=torch.zeros(B, dtype=torch.int32)),
+        lambda: rb.scan(keep, dst=torch.zeros(B * N - 1, dtype=torch.int32)),
+        lambda: rb.pack(q, q, q, keep, out=(torch.zeros(B * N - 1, H, d, dtype=torch.bfloat16),) * 3
+                        + (torch.zeros(B + 1, dtype=torch.int32), torch.zeros(B * N, dtype=torch.int32),
+                           torch.zeros(B * N, dtype=torch.int32))),
+        lambda: rb.attn(*(torch.zeros(B * N - 1, H, d, dtype=torch.bfloat16),) * 3, torch.zeros(B + 1, dtype=torch.int32), N),
+        lambda: rb.attn(*(torch.zeros(B * N, H, d, dtype=torch.bfloat16),) * 3, torch.zeros(B + 1, dtype=torch.int64), N),
+        lambda: rb.attn(*(torch.zeros(B * N, H, d, dtype=torch.bfloat16),) * 3, torch.zeros(B + 1, dtype=torch.int32), N,
+                        op=torch.zeros(B * N - 1, H, d, dtype=torch.bfloat16)),
+        lambda: rb.unpack(torch.zeros(B * N, H, d, dtype=torch.bfloat16), torch.zeros(B * N - 1, dtype=torch.int32), B, N),
+        lambda: rb.unpack(torch.zeros(B * N, H, d, dtype=torch.bfloat16), torch.zeros(B * N, dtype=torch.int32), B, N,
+                          o=torch.zeros(B, N, H, d // 2, dtype=torch.bfloat16)),
+        lambda: rb.keep_topk_l2(torch.zeros(B, N, 128, dtype=torch.bfloat16), 3, keep=torch.zeros(B, N - 1, dtype=torch.uint8)),
+    ]
+    for i, f in enumerate(bad):
+        with pytest.raises(ValueError):
+            f()

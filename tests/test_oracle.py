@@ -369,3 +369,194 @@ def test_attention_fp8_is_attention_of_dequantised_inputs():
     assert np.array_equal(a, b)
     c = oracle.attention_fp8(q8, k8, v8, (0.5, 0.25, 4.0), cu)
     assert np.array_equal(c, 2.0 * a)
+
+
+# ------------------------------------ round-2 pins for the helper functions ----
+
+def _sdpa64(q, k, v, mask=None):
+    """torch SDPA in fp64 on [n, d] (library routine; default scale 1/sqrt(d))."""
+    t = [torch.as_tensor(np.asarray(x, np.float64))[None, None] for x in (q, k, v)]
+    return torch.nn.functional.scaled_dot_product_attention(*t, attn_mask=mask)[0, 0].numpy()
+
+
+def test_attention_image_head_equals_masked_sdpa_for_every_image_and_head():
+    """attention_image_head(b, h) -- the C5 sampled checker -- against torch
+    SDPA in fp64 on the padded (b, h) slice with a key-padding mask (P:40-42:
+    padded attention with masks computes the same kept rows), for every (b, h)
+    of a ragged batch that includes an empty image and a CLS-only image; and
+    against the whole-path oracle on the same rows."""
+    B, N, H = 5, 23, 3
+    q, k, v, keep = synth.make_inputs(B, N, H, 0.6, "random", "bf16", seed=21, dist="peaked")
+    keep = keep.numpy().copy()
+    keep[1] = 0                       # empty image
+    keep[3] = 0
+    keep[3, 0] = 1                    # CLS only
+    o, _ = oracle.pack_attend_unpack(q, k, v, keep)
+    for b in range(B):
+        kb = keep[b].astype(bool)
+        for h in range(H):
+            pos, rows = oracle.attention_image_head(q, k, v, keep, b, h)
+            assert pos.tolist() == np.flatnonzero(kb).tolist()
+            assert rows.shape == (kb.sum(), 64)
+            if kb.sum() == 0:
+                continue
+            mask = torch.as_tensor(kb)[None, None, None, :]
+            ref = _sdpa64(q[b, :, h].double(), k[b, :, h].double(), v[b, :, h].double(), mask)[kb]
+            np.testing.assert_allclose(rows, ref, rtol=0, atol=1e-12)
+            np.testing.assert_array_equal(rows, o[b, pos, h])
+    # a wrong head or image selection must not pass: neighbouring heads differ
+    _, r0 = oracle.attention_image_head(q, k, v, keep, 0, 0)
+    _, r1 = oracle.attention_image_head(q, k, v, keep, 0, 1)
+    assert np.abs(r0 - r1).max() > 1e-3
+
+
+@pytest.mark.parametrize("d", [64, 32, 80])
+def test_softmax_weights_equals_torch_softmax_and_reproduces_attention(d):
+    """softmax_weights(q, k) == torch.softmax(q k^T / sqrt(d)) in fp64 (library
+    routine; a wrong 1/sqrt(d) fails, which rows-sum-to-one alone would not
+    catch), and softmax_weights(q, k) @ v == SDPA(q, k, v)."""
+    rng = np.random.default_rng(22 + d)
+    q, k, v = rng.standard_normal((3, 29, d)) * np.array([3.0, 1.0, 1.0])[:, None, None]
+    P = oracle.softmax_weights(q, k)
+    ref = torch.softmax(torch.as_tensor(q) @ torch.as_tensor(k).T / math.sqrt(d), dim=1).numpy()
+    np.testing.assert_allclose(P, ref, rtol=0, atol=1e-14)
+    np.testing.assert_allclose(P @ v, _sdpa64(q, k, v), rtol=0, atol=1e-12)
+    np.testing.assert_allclose(oracle.attention_one(q, k, v), _sdpa64(q, k, v), rtol=0, atol=1e-12)
+
+
+def test_attention_fp8_equals_torch_float8_dequant_sdpa():
+    """attention_fp8 by an independent route: the bytes viewed as
+    torch.float8_e4m3fn (library decode), widened to fp64, multiplied by the
+    descales in torch, then torch SDPA in fp64 per image (P:286-326 applied to
+    the dequantised values, R23).  Includes subnormal and max-magnitude bytes."""
+    rng = np.random.default_rng(23)
+    T, H, d = 13, 2, 32
+    q8, k8, v8 = (rng.integers(0, 256, size=(T, H, d), dtype=np.uint8) for _ in range(3))
+    for t in (q8, k8, v8):          # no NaN bytes (0x7f / 0xff): parity is on finite inputs
+        t[(t & 0x7F) == 0x7F] = 0x7E
+    q8[0, 0, :4] = [0x01, 0x81, 0x07, 0x7E]         # subnormals and 448
+    cu = np.array([0, 1, 1, 6, 13])                   # n = 1, an empty image, 5, 7
+    desc = (0.03125, 0.0625, 1.5)
+    got = oracle.attention_fp8(q8, k8, v8, desc, cu)
+
+    def deq(b, s):
+        return torch.from_numpy(b).view(torch.float8_e4m3fn).to(torch.float64) * s
+
+    tq, tk, tv = deq(q8, desc[0]), deq(k8, desc[1]), deq(v8, desc[2])
+    for i in range(len(cu) - 1):
+        s, e = int(cu[i]), int(cu[i + 1])
+        for h in range(H):
+            if e == s:
+                continue
+            ref = torch.nn.functional.scaled_dot_product_attention(
+                tq[s:e, h][None, None], tk[s:e, h][None, None], tv[s:e, h][None, None])[0, 0].numpy()
+            np.testing.assert_allclose(got[s:e, h], ref, rtol=0, atol=1e-9 * max(1.0, np.abs(ref).max()))
+
+
+def test_keep_topk_l2_rejects_k_below_one_and_ranks_nan_last():
+    """CLS always survives (R6): k < 1 is an error; a NaN score ranks below every
+    finite one, so at most k tokens are kept (R20)."""
+    x = np.ones((1, 5, 4))
+    x[0, 2] = np.nan
+    with pytest.raises(ValueError):
+        oracle.keep_topk_l2(x, 0)
+    assert oracle.keep_topk_l2(x, 4)[0].tolist() == [1, 1, 0, 1, 1]
+    assert oracle.keep_topk_l2(x, 5)[0].tolist() == [1, 1, 1, 1, 1]
+
+
+# ------------------------------------------- N2: EViT keep mask (R17) ----
+
+def _evit_logits_loops(q, k):
+    """Independent triple loop in plain Python floats (not the oracle's matmuls)."""
+    B, N, H, d = k.shape
+    out = [[0.0] * N for _ in range(B)]
+    for b in range(B):
+        for n in range(N):
+            acc = 0.0
+            for h in range(H):
+                acc += sum(float(q[b, 0, h, c]) * float(k[b, n, h, c]) for c in range(d)) / math.sqrt(d)
+            out[b][n] = acc / H
+    return np.array(out)
+
+
+def test_evit_logits_equal_loops_and_cls_attention_of_sdpa():
+    """evit_logits against (i) plain loops and (ii) the CLS row of torch's fp64
+    attention logits q k^T / sqrt(d) (SDPA's own scale), head-averaged."""
+    q, k, v, _ = synth.make_inputs(2, 9, 3, 0.0, "all", "bf16", seed=31, d=16)
+    got = oracle.evit_logits(q, k)
+    np.testing.assert_allclose(got, _evit_logits_loops(q.double().numpy(), k.double().numpy()), rtol=0, atol=1e-12)
+    qt, kt = q.double().transpose(1, 2), k.double().transpose(1, 2)          # [B, H, N, d]
+    S = (qt @ kt.transpose(-1, -2)) / math.sqrt(16)                            # SDPA's logits
+    np.testing.assert_allclose(got, S[:, :, 0, :].mean(1).numpy(), rtol=0, atol=1e-12)
+
+
+def test_keep_evit_brute_force():
+    """Tiny inputs, every k: the kept non-CLS, non-fused set is the lexicographic
+    best (logit desc, index asc) subset of size k-2 over all subsets of 1..N-1
+    (brute force on loop logits); the fused token sits in the first dropped
+    position and equals the softmax(logit)-weighted mean of ALL dropped rows,
+    computed here row by row."""
+    rng = np.random.default_rng(32)
+    for trial in range(25):
+        N, H, d = int(rng.integers(3, 8)), int(rng.integers(1, 3)), 4
+        q = np.round(rng.standard_normal((1, N, H, d)) * 2) / 2       # ties happen
+        k = np.round(rng.standard_normal((1, N, H, d)) * 2) / 2
+        v = rng.standard_normal((1, N, H, d))
+        kk = int(rng.integers(1, N + 1))
+        keep, f, fused = oracle.keep_evit(q, k, v, kk)
+        lg = _evit_logits_loops(q, k)[0]
+        if kk >= N:
+            assert keep[0].tolist() == [1] * N and f[0] == -1
+            continue
+        best = None
+        for subset in itertools.combinations(range(1, N), max(kk - 2, 0)):
+            key = sorted((-lg[n], n) for n in subset)
+            if best is None or key < best[0]:
+                best = (key, subset)
+        chosen = {0, *best[1]}
+        dropped = [n for n in range(N) if n not in chosen]
+        want = np.zeros(N, np.uint8)
+        want[list(chosen)] = 1
+        if kk >= 2:
+            want[dropped[0]] = 1
+            assert f[0] == dropped[0]
+            w = [math.exp(lg[j] - max(lg[i] for i in dropped)) for j in dropped]
+            z = sum(w)
+            for t, x in enumerate((q, k, v)):
+                ref = sum(wj / z * x[0, j] for wj, j in zip(w, dropped))
+                np.testing.assert_allclose(fused[0, t], ref, rtol=0, atol=1e-12)
+        else:
+            assert f[0] == -1
+        assert keep[0].tolist() == want.tolist(), (kk, lg)
+        assert keep[0].sum() == min(kk, N)
+
+
+def test_keep_evit_closed_forms_and_generator_agreement():
+    """Equal logits -> the lowest positions kept and the fused token is the plain
+    mean of the dropped rows; identical dropped rows -> the fused token equals
+    that row exactly (weights sum to 1); and agreement with the independent
+    host generator synth.mask_evit (same reading R17, separate code)."""
+    B, N, H, d = 1, 10, 2, 8
+    q = np.zeros((B, N, H, d))                       # CLS query 0 -> every logit 0
+    rng = np.random.default_rng(33)
+    k, v = rng.standard_normal((2, B, N, H, d))
+    keep, f, fused = oracle.keep_evit(q, k, v, 5)
+    assert keep[0].tolist() == [1, 1, 1, 1, 1, 0, 0, 0, 0, 0] and f[0] == 4
+    np.testing.assert_allclose(fused[0, 2], v[0, 4:].mean(0), rtol=0, atol=1e-14)
+    q2, k2 = rng.standard_normal((2, B, N, H, d))
+    v2 = v.copy()
+    v2[0, 1:] = v2[0, 9]                              # every non-CLS row identical
+    keep2, f2, fused2 = oracle.keep_evit(q2, k2, v2, 4)
+    assert f2[0] > 0 and keep2[0].sum() == 4
+    assert np.abs(fused2[0, 2] - v2[0, 9]).max() < 1e-14
+    # the host generator (bf16 inputs, fused rows rounded to bf16)
+    q, k, v, _ = synth.make_inputs(3, 40, 3, 0.0, "all", "bf16", seed=34)
+    for kk in (2, 9, 21, 39):
+        mask, qs, ks, vs = synth.mask_evit(q, k, v, kk)
+        keep, f, fused = oracle.keep_evit(q, k, v, kk)
+        assert np.array_equal(mask, keep), kk
+        for b in range(3):
+            if f[b] >= 0:
+                for t, x in enumerate((qs, ks, vs)):
+                    ref = torch.from_numpy(fused[b, t]).to(torch.bfloat16).double().numpy()
+                    np.testing.assert_array_equal(x[b, f[b]].double().numpy(), ref)
