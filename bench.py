@@ -744,6 +744,13 @@ def _eager_time(torch, fns, reps):
     return 1e3 * s.elapsed_time(e) / reps
 
 
+def _hbm_peak():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]
+    except Exception:
+        return 6650.0
+
+
 def _graph_time(torch, fns, reps):
     """Device µs per call: `reps` calls (rotating over fns) in one CUDA graph."""
     for f in fns:                   # eager first call: one-time attributes outside capture
@@ -757,6 +764,7 @@ def _graph_time(torch, fns, reps):
     g.replay()
     torch.cuda.synchronize()
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda._sleep(GATE_CYCLES // 4)   # host submission off the device clock
     s.record()
     g.replay()
     e.record()
@@ -828,7 +836,7 @@ def extras(args, rb, torch, dev, sets, c, B, N, H, dt, T):
           "unpack_us": 4 * B * N + T * HDe + B * N * HDe}
     out["separate_kernels_roofline"] = {
         k: {"alg_bytes": v, "achieved_GBps": v / (out[k] * 1e-6) / 1e9,
-            "frac_of_measured_hbm": v / (out[k] * 1e-6) / 1e9 / 6560.6} for k, v in kb.items()}
+            "frac_of_measured_hbm": v / (out[k] * 1e-6) / 1e9 / _hbm_peak()} for k, v in kb.items()}
 
     # padded SDPA baseline on the same box (R15)
     F = torch.nn.functional
@@ -913,7 +921,7 @@ def extras(args, rb, torch, dev, sets, c, B, N, H, dt, T):
         sd = statistics.median(sdpa_t[p]) if sdpa_t[p] else None
         ab = algorithmic_bytes(B, N, H, B * kk)
         sweep.append({"p": p, "tok": kk, "fused_us_median": f_med, "fused_us_reps": fused_t[p],
-                      "padded_sdpa_us": sd, "fused_hbm_frac": ab / (f_med * 1e-6) / 1e9 / 6560.6,
+                      "padded_sdpa_us": sd, "fused_hbm_frac": ab / (f_med * 1e-6) / 1e9 / _hbm_peak(),
                       "alg_bytes": ab})
     out["prune_sweep"] = sweep
     meds = [c_["fused_us_median"] for c_ in sweep]
@@ -929,18 +937,43 @@ def extras(args, rb, torch, dev, sets, c, B, N, H, dt, T):
     # NEXT row N2: on-device Threshold-l2 keep mask from hidden states (x is
     # B x N x H*64, the tensor the paper prunes at layer 4), alone and
     # ahead of the fused path (two launches, PDL-overlapped)
-    xs = [synth.hidden_states(B, N, H * 64, args.dtype, seed=40 + i).to(dev) for i in range(4)]
+    # 17 hidden-state batches over the 16 buffer sets: consecutive uses of one
+    # keep buffer see different masks, so the fused kernel's speculative pre-wait
+    # read of the keep row (stale, from the previous use) never hits by accident.
+    NX = N_SETS + 1
+    xs = [synth.hidden_states(B, N, H * 64, args.dtype, seed=40 + i).to(dev) for i in range(NX)]
     kk = synth.kept_tokens(N, c["p"])
     keeps = [torch.empty(B, N, dtype=torch.uint8, device=dev) for _ in range(N_SETS)]
-    out["prune_l2_mask_us"] = _graph_time(torch, [(lambda i=i: rb.keep_topk_l2(xs[i % 4], kk, keep=keeps[i]))
-                                                  for i in range(N_SETS)], reps)
-    out["prune_l2_mask_alg_bytes"] = B * N * H * 64 * 2 + B * N
+    L = N_SETS * NX
+    out["prune_l2_mask_us"] = _graph_time(torch, [(lambda j=j: rb.keep_topk_l2(xs[j % NX], kk, keep=keeps[j % N_SETS]))
+                                                  for j in range(L)], reps)
+    l2b = B * N * H * 64 * 2 + B * N
+    out["prune_l2_mask_alg_bytes"] = l2b
+    out["prune_l2_mask_hbm_frac"] = l2b / (out["prune_l2_mask_us"] * 1e-6) / 1e9 / _hbm_peak()
 
-    def prune_fused(i):
-        s = sets[i]
-        rb.keep_topk_l2(xs[i % 4], kk, keep=keeps[i])
-        rb.pack_attend_unpack(s["q"], s["k"], s["v"], keeps[i], o=s["o"], cu=s["cu"])
-    out["prune_then_fused_us"] = _graph_time(torch, [(lambda i=i: prune_fused(i)) for i in range(N_SETS)], reps)
+    def prune_fused(j):
+        s = sets[j % N_SETS]
+        rb.keep_topk_l2(xs[j % NX], kk, keep=keeps[j % N_SETS])
+        rb.pack_attend_unpack(s["q"], s["k"], s["v"], keeps[j % N_SETS], o=s["o"], cu=s["cu"], n_hint=kk)
+    out["prune_then_fused_us"] = _graph_time(torch, [(lambda j=j: prune_fused(j)) for j in range(L)], reps)
+    # EViT (R17) on the device: mask + fused token written into q/k/v, alone and
+    # ahead of the fused path, at this config's shape and ratio.  It rewrites one
+    # row of q/k/v per image in place, so each set is a private copy.
+    ev = [dict(q=s["q"].clone(), k=s["k"].clone(), v=s["v"].clone(), keep=torch.empty_like(s["keep"]))
+          for s in sets]
+    out["prune_evit_mask_us"] = _graph_time(torch, [(lambda e=e: rb.keep_evit(e["q"], e["k"], e["v"], kk,
+                                                                                keep=e["keep"])) for e in ev], reps)
+    # algorithmic bytes: all K rows + the dropped Q and V rows + the fused row (3 tensors) + mask
+    evb = B * N * H * 128 + 2 * B * (N - kk + 1) * H * 128 + 3 * B * H * 128 + B * N
+    out["prune_evit_mask_alg_bytes"] = evb
+    out["prune_evit_mask_hbm_frac"] = evb / (out["prune_evit_mask_us"] * 1e-6) / 1e9 / _hbm_peak()
+
+    def evit_fused(i):
+        e, s = ev[i], sets[i]
+        rb.keep_evit(e["q"], e["k"], e["v"], kk, keep=e["keep"])
+        rb.pack_attend_unpack(e["q"], e["k"], e["v"], e["keep"], o=s["o"], cu=s["cu"], n_hint=kk)
+    out["prune_evit_then_fused_us"] = _graph_time(torch, [(lambda i=i: evit_fused(i)) for i in range(N_SETS)], reps)
+    del ev
     # the paper's dispatch study through the C ABI with no Python in the loop
     # (SURVEY §8(d) timing modes M1/M2/M3): tools/ragged_bench, if built
     try:
@@ -1162,7 +1195,7 @@ def config_extras(rb, torch, dev, dt):
     T5 = int(keep.sum().item())
     ab = algorithmic_bytes(B5, 197, 12, T5)
     res["C5"] = {"fused_us": us, "images_per_s": B5 / (us * 1e-6), "alg_bytes": ab,
-                 "hbm_frac": ab / (us * 1e-6) / 1e9 / 6560.6}
+                 "hbm_frac": ab / (us * 1e-6) / 1e9 / _hbm_peak()}
     del q, k, v, o, s5
     torch.cuda.empty_cache()
     return res

@@ -195,10 +195,33 @@ RAGGED_API void ragged_graph_destroy(ragged_graph* graph);
  * hidden states x [B, N, D] (D = H*d, token stride ld elements, bf16/fp16 by
  * prob->dtype) write keep[b, n] = 1 for CLS (n = 0) and the k - 1 other tokens
  * with the largest ||x[b, n, :]||_2 (ties to the lower position; scores in
- * fp32), 0 otherwise (R20).  k < 0 -> RAGGED_EINVAL; k >= N keeps all.
- * One launch, one CTA per image.  Feeds ragged_pack / ragged_pack_attend_unpack. */
+ * fp32; a NaN score ranks below every finite one, so at most k tokens are
+ * kept), 0 otherwise (R20).  k < 1 -> RAGGED_EINVAL (CLS always
+ * survives); k >= N keeps all; H > 56 at N = 256 -> RAGGED_ENOTSUP (rows
+ * staged in shared memory).  One launch: a cluster of 8 CTAs per image, each
+ * reading 1/8 of the image's rows, scores exchanged through distributed shared
+ * memory.  Feeds ragged_pack / ragged_pack_attend_unpack (PDL-chained). */
 RAGGED_API ragged_status ragged_keep_topk_l2(const ragged_problem* prob, const void* x, int32_t k,
                                              uint8_t* keep, void* stream);
+
+/* NEXT row N2 -- on-device EViT keep mask with a fused token (EViT
+ * "ranks tokens by CLS-attention scores and fuses pruned tokens into a single
+ * representative"; R17).  q, k, v are the padded [B, N, H, d] tensors
+ * of ragged_pack_attend_unpack (token stride prob->ld, so a fused qkv buffer
+ * works), read AND written:
+ *   score[b, n] = (1/H) sum_h q[b,0,h] . k[b,n,h] / sqrt(d)   (fp32)
+ *   keep CLS + the k_keep - 2 highest-scoring other tokens (ties to the lower
+ *   position; NaN ranks last); if k_keep >= 2 the fused token
+ *   sum_{j dropped} w_j row_j, w = softmax(score[dropped]), is computed in fp32
+ *   for each of q, k, v (all heads), rounded once to the dtype and written into
+ *   the first dropped position f of q, k and v, and keep[b, f] = 1.
+ * So k_keep tokens per image are kept (k_keep >= N keeps all, no fused token).
+ * k_keep < 1 -> RAGGED_EINVAL; H > 25 at N = 256 (row buffers beyond shared
+ * memory) -> RAGGED_ENOTSUP.  One launch, a cluster
+ * of 8 CTAs per image (row split, DSMEM exchange of scores and of the fused
+ * token's partial sums, reduced in a fixed order: deterministic). */
+RAGGED_API ragged_status ragged_keep_evit(const ragged_problem* prob, void* q, void* k, void* v,
+                                          int32_t k_keep, uint8_t* keep, void* stream);
 
 /* Launch-floor probe: an empty kernel launched with `grid` x
  * `block` threads; its latency is the dispatch floor of this library. */

@@ -107,6 +107,7 @@ def _load() -> ctypes.CDLL:
         "ragged_graph_launch": [V, V],
         "ragged_empty_launch": [I32, I32, V],
         "ragged_keep_topk_l2": [P, V, I32, V, V],
+        "ragged_keep_evit": [P, V, V, V, I32, V, V],
         "ragged_validate_cu_seqlens": [ctypes.POINTER(I32), I32, I64],
         "ragged_pack_attend_unpack_gather": [P, V, V, V, V, V, ctypes.POINTER(Gather), V],
         "ragged_attn_gather": [P, V, V, V, V, ctypes.POINTER(Gather), V],
@@ -138,7 +139,7 @@ EXPORTS = ("ragged_scan", "ragged_pack", "ragged_attn", "ragged_unpack", "ragged
            "ragged_pack_attend_unpack_host", "ragged_attn_fp8",
            "ragged_graph_create", "ragged_graph_launch", "ragged_graph_destroy", "ragged_empty_launch",
            "ragged_validate_cu_seqlens", "ragged_status_str", "ragged_last_error", "ragged_build_info",
-           "ragged_keep_topk_l2", "ragged_pack_attend_unpack_gather", "ragged_attn_gather",
+           "ragged_keep_topk_l2", "ragged_keep_evit", "ragged_pack_attend_unpack_gather", "ragged_attn_gather",
            "ragged_layer_norm", "ragged_linear", "ragged_vit_block_workspace", "ragged_vit_block",
            "ragged_vit_pipeline_graph_create")
 
@@ -540,6 +541,19 @@ def keep_topk_l2(x, k: int, keep=None, stream=None):
     p = problem(B, N, D // 64, 64, x.dtype, x.stride(1))
     _check(lib().ragged_keep_topk_l2(ctypes.byref(p), x.data_ptr(), int(k), keep.data_ptr(),
                                      _stream(stream)), "ragged_keep_topk_l2")
+    return keep
+
+
+def keep_evit(q, k, v, k_keep: int, keep=None, stream=None, n_hint=0):
+    """N2 (R17): EViT keep mask from padded q, k, v [B, N, H, d]
+    (head-averaged CLS logits, CLS + top-(k_keep-2) + one fused token written
+    IN PLACE into the first dropped position of q, k and v) -> uint8 keep [B, N]."""
+    p = _padded_problem(q, k, v, ENGINE_AUTO, n_hint)
+    B, N = q.shape[0], q.shape[1]
+    keep = torch.empty(B, N, dtype=torch.uint8, device=q.device) if keep is None else keep
+    _require(keep, "keep", torch.uint8, q.device, shape=(B, N))
+    _check(lib().ragged_keep_evit(ctypes.byref(p), q.data_ptr(), k.data_ptr(), v.data_ptr(), int(k_keep),
+                                  keep.data_ptr(), _stream(stream)), "ragged_keep_evit")
     return keep
 
 

@@ -16,7 +16,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libragged.so")
-SOURCES = ["kernels.cu", "block.cu", "attn_general.cu", "api.cu"]
+SOURCES = ["kernels.cu", "prune.cu", "block.cu", "attn_general.cu", "api.cu"]
 HEADERS = ["device.cuh", "launch.h", "tcgen05.cuh", "attn_tc.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr", "-Xcompiler", "-fPIC",

@@ -319,13 +319,33 @@ void ragged_graph_destroy(ragged_graph* graph) {
 ragged_status ragged_keep_topk_l2(const ragged_problem* prob, const void* x, int32_t k,
                                   uint8_t* keep, void* stream) {
   RAGGED_TRY(check_problem(prob));
-  if (k < 0) return fail(RAGGED_EINVAL, "k < 0");
+  if (k < 1) return fail(RAGGED_EINVAL, "k < 1 (CLS always survives)");
+  if (ragged::l2_smem_bytes(prob->N, prob->H * prob->d) > 227 * 1024)
+    return fail(RAGGED_ENOTSUP, "ceil(N/8) rows of x exceed shared memory (H too large)");
+  if ((long long)prob->B * 8 > 0x7fffffffLL) return fail(RAGGED_ENOTSUP, "B * 8 CTAs exceed the grid");
   if (prob->B == 0) return RAGGED_OK;
   RAGGED_TRY(check_ptr(x, "x"));
   RAGGED_TRY(check_ptr_any(keep, "keep"));
   cudaError_t e = ragged::launch_keep_topk_l2(prob->dtype, x, prob->ld, prob->B, prob->N,
                                               prob->H * prob->d, k, keep, as_stream(stream));
   return e == cudaSuccess ? RAGGED_OK : cuda_fail(e, "ragged_keep_topk_l2");
+}
+
+ragged_status ragged_keep_evit(const ragged_problem* prob, void* q, void* k, void* v, int32_t k_keep,
+                               uint8_t* keep, void* stream) {
+  RAGGED_TRY(check_problem(prob));
+  if (k_keep < 1) return fail(RAGGED_EINVAL, "k_keep < 1 (CLS always survives)");
+  if (ragged::evit_smem_bytes(prob->N, prob->H) > 227 * 1024)
+    return fail(RAGGED_ENOTSUP, "EViT row buffers exceed shared memory (H too large)");
+  if ((long long)prob->B * 8 > 0x7fffffffLL) return fail(RAGGED_ENOTSUP, "B * 8 CTAs exceed the grid");
+  if (prob->B == 0) return RAGGED_OK;
+  RAGGED_TRY(check_ptr(q, "q"));
+  RAGGED_TRY(check_ptr(k, "k"));
+  RAGGED_TRY(check_ptr(v, "v"));
+  RAGGED_TRY(check_ptr_any(keep, "keep"));
+  cudaError_t e = ragged::launch_keep_evit(prob->dtype, q, k, v, prob->ld, prob->B, prob->N, prob->H, k_keep,
+                                           keep, as_stream(stream));
+  return e == cudaSuccess ? RAGGED_OK : cuda_fail(e, "ragged_keep_evit");
 }
 
 ragged_status ragged_empty_launch(int32_t grid, int32_t block, void* stream) {
@@ -609,6 +629,9 @@ int32_t ragged_debug_pairs_timeline(void* host, int32_t max_ctas) {
 }
 int32_t ragged_debug_gemm_timeline(void* host, int32_t max_ctas) {
   return ragged::gemm_timeline_copy(host, max_ctas);
+}
+int32_t ragged_debug_prune_timeline(void* host, int32_t max_ctas) {
+  return ragged::prune_timeline_copy(host, max_ctas);
 }
 #endif
 

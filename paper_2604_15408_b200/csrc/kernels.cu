@@ -1326,74 +1326,6 @@ __global__ void __launch_bounds__(kAttnThreads, 3) attn_kernel(const AttnArgs a,
 
 namespace ragged {
 
-// ------------------------------------------------------ N2: prune (l2) ----
-// Threshold-l2 keep mask (R20): one CTA per
-// image.  Score = ||x_n||^2 in fp32 (monotone in the l2 norm), CLS forced first;
-// keep[n] = (rank_n < k) where rank_n = #{m : s_m > s_n or (s_m == s_n and m < n)}
-// -- an exact, deterministic top-k by counting (N <= 256 -> <= 65536 compares).
-constexpr int kPruneThreads = 1024;
-
-template <typename T>
-__global__ void __launch_bounds__(kPruneThreads, 1)
-    keep_topk_l2_kernel(const T* __restrict__ x, long long ld, int N, int D, int k,
-                        uint8_t* __restrict__ keep) {
-  __shared__ float s_score[kMaxN];
-  pdl_launch_dependents();
-#ifndef RAGGED_NO_KEEP_PREFETCH
-  {  // the image's hidden rows into L2 before the grid-dependency wait (prefetch
-     // only: every value is read after the wait; L2 is the point of coherence)
-    const char* ib = reinterpret_cast<const char*>(x + (long long)blockIdx.x * N * ld);
-    const int lpr = D >> 6;  // 128-byte lines per row (D % 64 == 0)
-    for (int i = threadIdx.x; i < N * lpr; i += kPruneThreads) {
-      const int rn = i / lpr, l = i - rn * lpr;
-      prefetch_l2(ib + (long long)rn * ld * 2 + l * 128);
-    }
-  }
-#endif
-  pdl_wait_prerequisites();
-  const int b = blockIdx.x, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int cpr = D >> 3;  // 16-byte chunks per row
-  const T* img = x + (long long)b * N * ld;
-  constexpr int kRows = 8;  // rows per warp in flight (32 warps x 8 = 256 >= N)
-  float acc[kRows];
-#pragma unroll
-  for (int i = 0; i < kRows; ++i) acc[i] = 0.f;
-  for (int c0 = lane; c0 < cpr; c0 += 32) {
-    uint4 v[kRows];
-#pragma unroll
-    for (int i = 0; i < kRows; ++i) {
-      const int n = warp + 32 * i;
-      v[i] = n < N ? ld_global_nc_16(img + (long long)n * ld + 8 * c0) : make_uint4(0u, 0u, 0u, 0u);
-    }
-#pragma unroll
-    for (int i = 0; i < kRows; ++i) {
-      const T* e = reinterpret_cast<const T*>(&v[i]);
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const float f = static_cast<float>(e[j]);
-        acc[i] = fmaf(f, f, acc[i]);
-      }
-    }
-  }
-#pragma unroll
-  for (int i = 0; i < kRows; ++i) {
-    float a = acc[i];
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
-    const int n = warp + 32 * i;
-    if (lane == 0 && n < N) s_score[n] = n == 0 ? INFINITY : a;
-  }
-  __syncthreads();
-  if (tid < N) {
-    const float sn = s_score[tid];
-    int rank = 0;
-    for (int m = 0; m < N; ++m) {
-      const float sm = s_score[m];
-      rank += (sm > sn || (sm == sn && m < tid)) ? 1 : 0;
-    }
-    keep[(long long)b * N + tid] = rank < k ? 1 : 0;
-  }
-}
 
 __global__ void empty_kernel() {}
 
@@ -1619,14 +1551,6 @@ cudaError_t launch_attn_gather(int dtype, int engine, const void* qp, const void
                     : launch_attn_mma<__half, false, true>(a, B * H, st, g);
 }
 
-cudaError_t launch_keep_topk_l2(int dtype, const void* x, long long ld, int B, int N, int D, int k,
-                                uint8_t* keep, cudaStream_t st) {
-  if (dtype == 0)
-    return launch_pdl(keep_topk_l2_kernel<__nv_bfloat16>, dim3(B), dim3(kPruneThreads), 0, st,
-                      static_cast<const __nv_bfloat16*>(x), ld, N, D, k, keep);
-  return launch_pdl(keep_topk_l2_kernel<__half>, dim3(B), dim3(kPruneThreads), 0, st,
-                    static_cast<const __half*>(x), ld, N, D, k, keep);
-}
 
 cudaError_t launch_empty(int grid, int block, cudaStream_t st) {
   empty_kernel<<<grid, block, 0, st>>>();

@@ -71,12 +71,18 @@ cudaError_t launch_layer_norm(int dtype, const void* x, long long ldx, const voi
                               cudaStream_t st);
 cudaError_t launch_keep_topk_l2(int dtype, const void* x, long long ld, int B, int N, int D, int k,
                                 uint8_t* keep, cudaStream_t st);
+// NEXT row N2 (prune.cu): EViT keep mask + fused token written into q/k/v
+cudaError_t launch_keep_evit(int dtype, void* q, void* k, void* v, long long ld, int B, int N, int H, int kk,
+                             uint8_t* keep, cudaStream_t st);
+int l2_smem_bytes(int N, int D);      // must be <= 227 KB (checked in api.cu)
+int evit_smem_bytes(int N, int H);
 int fused_smem_bytes(int N);
 #ifdef RAGGED_TIMELINE
 int timeline_copy(void* host, int max_ctas);
 int pairs_timeline_copy(void* host, int max_ctas);
 int gemm_timeline_copy(void* host, int max_ctas);
 int timeline_clear();
+int prune_timeline_copy(void* host, int max_ctas);
 #endif
 
 }  // namespace ragged

@@ -330,7 +330,8 @@ def test_keep_topk_l2_matches_oracle(dtype, B, N, D, p):
 
 
 def test_keep_topk_l2_ties_and_k_edges():
-    """Exact ties resolve to the lower position; k = 0 keeps nothing, k >= N all."""
+    """Exact ties resolve to the lower position; k < 1 is rejected (CLS always
+    survives), k >= N keeps all; a NaN score ranks last (at most k kept)."""
     x = torch.zeros(2, 9, 64, dtype=torch.bfloat16)
     x[:, 1:, 0] = 1.0                       # all non-CLS scores equal
     x[1, 5, 0] = 2.0
@@ -338,8 +339,15 @@ def test_keep_topk_l2_ties_and_k_edges():
     got = rb.keep_topk_l2(xd, 4).cpu().numpy()
     assert got[0].tolist() == [1, 1, 1, 1, 0, 0, 0, 0, 0]
     assert got[1].tolist() == [1, 1, 1, 0, 0, 1, 0, 0, 0]
-    assert rb.keep_topk_l2(xd, 0).cpu().numpy().sum() == 0
+    with pytest.raises(rb.RaggedError):
+        rb.keep_topk_l2(xd, 0)
+    assert rb.keep_topk_l2(xd, 1).cpu().numpy().tolist() == [[1] + [0] * 8] * 2
     assert rb.keep_topk_l2(xd, 50).cpu().numpy().sum() == 18
+    xn = x.clone()
+    xn[0, 2, 3] = float("nan")
+    got = rb.keep_topk_l2(xn.to(DEV), 4).cpu().numpy()
+    assert got[0].tolist() == [1, 1, 0, 1, 1, 0, 0, 0, 0]
+    assert got.sum(1).tolist() == [4, 4]
 
 
 def test_prune_then_fused_path():

@@ -1,0 +1,111 @@
+"""GPU parity for NEXT row N2's EViT keep mask (ragged_keep_evit, R17) against
+the fp64 oracle: the kept set is exact wherever the decision is unique (the
+score gap at the threshold is well above fp32 rounding), otherwise it must be a
+valid top-k; the fused token (written in place into q/k/v at the first dropped
+position) is within one output ulp + fp32 accumulation error of the oracle;
+every other q/k/v byte is untouched; the result drives the fused path."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+from helpers import bits, check_attention, to_np
+
+rb = pytest.importorskip("paper_2604_15408_b200")
+pytestmark = pytest.mark.gpu
+DEV = "cuda"
+DT = {"bf16": torch.bfloat16, "fp16": torch.float16}
+
+
+def _check_evit(q, k, v, kk, keep_gpu, q2, k2, v2):
+    """q, k, v: host inputs; q2/k2/v2: device results (in place)."""
+    want, f, fused = oracle.keep_evit(q, k, v, kk)
+    s = oracle.evit_logits(q, k)
+    B, N = want.shape
+    qkv_in = (q, k, v)
+    qkv_out = [t.cpu() for t in (q2, k2, v2)]
+    exact = 0
+    for b in range(B):
+        got = keep_gpu[b]
+        assert got.sum() == min(kk, N) and got[0] == 1, b
+        if np.array_equal(got, want[b]):
+            exact += 1
+            if f[b] >= 0:
+                for t in range(3):
+                    g = qkv_out[t][b, f[b]].double().numpy()
+                    ref = fused[b, t]
+                    scale = np.abs(qkv_in[t][b].double().numpy()).max()
+                    ulp = np.abs(ref) * 2.0 ** (-7 if qkv_in[t].dtype == torch.bfloat16 else -10)
+                    assert np.all(np.abs(g - ref) <= ulp + 2.0 ** -16 * scale), (b, t)
+            # every other row untouched (bitwise)
+            for t in range(3):
+                rows = [n for n in range(N) if n != f[b]]
+                assert np.array_equal(bits(qkv_out[t][b, rows]), bits(qkv_in[t][b, rows])), (b, t)
+            continue
+        others = np.sort(s[b, 1:])[::-1]
+        j = kk - 2
+        gap = abs(others[j - 1] - others[j]) if 0 < j < others.size else np.inf
+        assert gap < 1e-5 * max(1.0, np.abs(others).max()), f"image {b}: masks differ, gap {gap:.2e}"
+    return exact
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "fp16"])
+@pytest.mark.parametrize("B,N,H,p", [(64, 197, 12, 0.7), (4, 197, 3, 0.5), (7, 33, 2, 0.3), (3, 256, 6, 0.9),
+                                     (2, 5, 1, 0.5), (5, 197, 12, 0.99)])
+def test_keep_evit_matches_oracle(dtype, B, N, H, p):
+    q, k, v = synth.activations(B, N, H, 64, dtype, seed=41)
+    kk = max(1, synth.kept_tokens(N, p))
+    qd, kd, vd = (t.to(DEV) for t in (q, k, v))
+    keep = rb.keep_evit(qd, kd, vd, kk)
+    torch.cuda.synchronize()
+    assert _check_evit(q, k, v, kk, keep.cpu().numpy(), qd, kd, vd) >= B - 1
+
+
+@pytest.mark.parametrize("kk", [1, 2, 3, 196, 197, 300])
+def test_keep_evit_k_edges(kk):
+    """k = 1: CLS only, no fused token; k = 2: CLS + fused token; k = N - 1: two
+    dropped tokens fused into one; k >= N: all kept, q/k/v untouched."""
+    B, N, H = 3, 197, 4
+    q, k, v = synth.activations(B, N, H, 64, "bf16", seed=42)
+    qd, kd, vd = (t.to(DEV) for t in (q, k, v))
+    keep = rb.keep_evit(qd, kd, vd, kk).cpu().numpy()
+    torch.cuda.synchronize()
+    _check_evit(q, k, v, kk, keep, qd, kd, vd)
+    if kk >= N:
+        assert keep.sum() == B * N
+        for a, b in ((q, qd), (k, kd), (v, vd)):
+            assert np.array_equal(bits(a), bits(b.cpu()))
+
+
+def test_keep_evit_rejects_bad_k_and_is_deterministic():
+    B, N, H = 6, 197, 12
+    q, k, v = synth.activations(B, N, H, 64, "bf16", seed=43)
+    with pytest.raises(rb.RaggedError):
+        rb.keep_evit(*(t.to(DEV) for t in (q, k, v)), 0)
+    outs = []
+    for _ in range(3):
+        qd, kd, vd = (t.to(DEV) for t in (q, k, v))
+        keep = rb.keep_evit(qd, kd, vd, 59)
+        torch.cuda.synchronize()
+        outs.append((keep.cpu().numpy(), bits(qd.cpu()), bits(kd.cpu()), bits(vd.cpu())))
+    for o in outs[1:]:
+        assert all(np.array_equal(a, b) for a, b in zip(o, outs[0]))
+
+
+def test_keep_evit_fused_qkv_layout_then_fused_path():
+    """EViT on one fused [B, N, 3, H, d] qkv buffer (ld = 3*H*d), then the fused
+    pack-attend-unpack on the mask and the modified rows, PDL-chained with no
+    host sync: equals the oracle end to end (keep_evit -> pack_attend_unpack)."""
+    B, N, H = 8, 197, 12
+    kk = synth.kept_tokens(N, 0.7)
+    q, k, v = synth.activations(B, N, H, 64, "bf16", seed=44)
+    qkv = torch.stack([q, k, v], dim=2).to(DEV)                    # [B, N, 3, H, d]
+    qd, kd, vd = qkv[:, :, 0], qkv[:, :, 1], qkv[:, :, 2]
+    keep = rb.keep_evit(qd, kd, vd, kk)
+    o = rb.pack_attend_unpack(qd, kd, vd, keep, n_hint=kk)
+    torch.cuda.synchronize()
+    km = keep.cpu().numpy()
+    _check_evit(q, k, v, kk, km, qd, kd, vd)
+    ref, _ = oracle.pack_attend_unpack(qd.cpu(), kd.cpu(), vd.cpu(), km)
+    check_attention(to_np(o), ref, torch.bfloat16)
