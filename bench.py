@@ -956,6 +956,14 @@ def extras(args, rb, torch, dev, sets, c, B, N, H, dt, T):
         rb.keep_topk_l2(xs[j % NX], kk, keep=keeps[j % N_SETS])
         rb.pack_attend_unpack(s["q"], s["k"], s["v"], keeps[j % N_SETS], o=s["o"], cu=s["cu"], n_hint=kk)
     out["prune_then_fused_us"] = _graph_time(torch, [(lambda j=j: prune_fused(j)) for j in range(L)], reps)
+    # the mask computed inside the fused launch (one cluster of H CTAs per image)
+    def prune_in_fused(j):
+        s = sets[j % N_SETS]
+        rb.prune_l2_pack_attend_unpack(xs[j % NX], s["q"], s["k"], s["v"], kk, o=s["o"], cu=s["cu"])
+    try:
+        out["prune_l2_in_fused_us"] = _graph_time(torch, [(lambda j=j: prune_in_fused(j)) for j in range(L)], reps)
+    except Exception as ex:
+        out["prune_l2_in_fused_us"] = repr(ex)[:200]
     # EViT (R17) on the device: mask + fused token written into q/k/v, alone and
     # ahead of the fused path, at this config's shape and ratio.  It rewrites one
     # row of q/k/v per image in place, so each set is a private copy.

@@ -204,6 +204,26 @@ RAGGED_API void ragged_graph_destroy(ragged_graph* graph);
 RAGGED_API ragged_status ragged_keep_topk_l2(const ragged_problem* prob, const void* x, int32_t k,
                                              uint8_t* keep, void* stream);
 
+/* NEXT row N2 fused ahead of the scan -- Threshold-l2 pruning + a1-a4 in ONE
+ * launch (the prune step produces the keep mask, then the ragged
+ * path runs on the survivors).  The keep row of every image is computed inside
+ * the fused kernel from hidden states x [B, N, H*d] (token stride ldx elements,
+ * prob->dtype): keep = CLS + the k - 1 other tokens with the largest ||x||_2,
+ * exactly as ragged_keep_topk_l2 defines it (fp32 scores; ties to the lower
+ * position; NaN last), then O = ragged_pack_attend_unpack(q, k, v, keep).
+ * The image's H CTAs form one thread-block cluster (H <= 16, else
+ * RAGGED_ENOTSUP) that exchanges per-head partial squared norms through
+ * distributed shared memory; no mask round trip through HBM, no second launch.
+ * keep_or_null receives the mask [B, N] if non-NULL; cu_seqlens_or_null
+ * receives b * min(k, N) (every image keeps min(k, N) tokens).  k < 1 ->
+ * RAGGED_EINVAL; RAGGED_ENGINE_TCGEN05 -> RAGGED_ENOTSUP (mma.sync engine;
+ * the variant for min(k, N) > 64 is picked automatically). */
+RAGGED_API ragged_status ragged_prune_l2_pack_attend_unpack(const ragged_problem* prob, const void* x,
+                                                            int64_t ldx, int32_t k, const void* q,
+                                                            const void* kt, const void* v, void* o,
+                                                            uint8_t* keep_or_null,
+                                                            int32_t* cu_seqlens_or_null, void* stream);
+
 /* NEXT row N2 -- on-device EViT keep mask with a fused token (EViT
  * "ranks tokens by CLS-attention scores and fuses pruned tokens into a single
  * representative"; R17).  q, k, v are the padded [B, N, H, d] tensors

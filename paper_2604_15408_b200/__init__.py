@@ -108,6 +108,7 @@ def _load() -> ctypes.CDLL:
         "ragged_empty_launch": [I32, I32, V],
         "ragged_keep_topk_l2": [P, V, I32, V, V],
         "ragged_keep_evit": [P, V, V, V, I32, V, V],
+        "ragged_prune_l2_pack_attend_unpack": [P, V, I64, I32, V, V, V, V, V, V, V],
         "ragged_validate_cu_seqlens": [ctypes.POINTER(I32), I32, I64],
         "ragged_pack_attend_unpack_gather": [P, V, V, V, V, V, ctypes.POINTER(Gather), V],
         "ragged_attn_gather": [P, V, V, V, V, ctypes.POINTER(Gather), V],
@@ -139,7 +140,7 @@ EXPORTS = ("ragged_scan", "ragged_pack", "ragged_attn", "ragged_unpack", "ragged
            "ragged_pack_attend_unpack_host", "ragged_attn_fp8",
            "ragged_graph_create", "ragged_graph_launch", "ragged_graph_destroy", "ragged_empty_launch",
            "ragged_validate_cu_seqlens", "ragged_status_str", "ragged_last_error", "ragged_build_info",
-           "ragged_keep_topk_l2", "ragged_keep_evit", "ragged_pack_attend_unpack_gather", "ragged_attn_gather",
+           "ragged_keep_topk_l2", "ragged_keep_evit", "ragged_prune_l2_pack_attend_unpack", "ragged_pack_attend_unpack_gather", "ragged_attn_gather",
            "ragged_layer_norm", "ragged_linear", "ragged_vit_block_workspace", "ragged_vit_block",
            "ragged_vit_pipeline_graph_create")
 
@@ -542,6 +543,29 @@ def keep_topk_l2(x, k: int, keep=None, stream=None):
     _check(lib().ragged_keep_topk_l2(ctypes.byref(p), x.data_ptr(), int(k), keep.data_ptr(),
                                      _stream(stream)), "ragged_keep_topk_l2")
     return keep
+
+
+def prune_l2_pack_attend_unpack(x, q, k, v, k_keep: int, o=None, keep=None, cu=None, stream=None,
+                                engine=ENGINE_AUTO):
+    """N2 fused ahead of the scan: Threshold-l2 keep mask from hidden states
+    x [B, N, H*64] computed inside the fused pack-attend-unpack launch.
+    Returns o (padded [B, N, H, d]); keep [B, N] / cu [B+1] filled if given."""
+    p = _padded_problem(q, k, v, engine)
+    B, N, H, d = q.shape
+    if x.dim() != 3 or tuple(x.shape) != (B, N, H * d) or x.dtype != q.dtype or x.stride(2) != 1 \
+            or x.stride(0) != N * x.stride(1) or x.device != q.device:
+        raise ValueError("x must be [B, N, H*d] of q's dtype and device, unit feature stride")
+    o = torch.empty(B, N, H, d, dtype=q.dtype, device=q.device) if o is None else o
+    _require(o, "o", q.dtype, q.device, shape=(B, N, H, d))
+    if keep is not None:
+        _require(keep, "keep", torch.uint8, q.device, shape=(B, N))
+    if cu is not None:
+        _require(cu, "cu", torch.int32, q.device, B + 1)
+    _check(lib().ragged_prune_l2_pack_attend_unpack(ctypes.byref(p), x.data_ptr(), x.stride(1), int(k_keep),
+                                                    q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr(),
+                                                    _ptr(keep), _ptr(cu), _stream(stream)),
+           "ragged_prune_l2_pack_attend_unpack")
+    return o
 
 
 def keep_evit(q, k, v, k_keep: int, keep=None, stream=None, n_hint=0):

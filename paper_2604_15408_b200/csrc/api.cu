@@ -215,6 +215,33 @@ ragged_status ragged_pack_attend_unpack(const ragged_problem* prob, const uint8_
   return e == cudaSuccess ? RAGGED_OK : cuda_fail(e, "ragged_pack_attend_unpack");
 }
 
+ragged_status ragged_prune_l2_pack_attend_unpack(const ragged_problem* prob, const void* x, int64_t ldx,
+                                                int32_t k, const void* q, const void* kt, const void* v, void* o,
+                                                uint8_t* keep_or_null, int32_t* cu_seqlens_or_null,
+                                                void* stream) {
+  RAGGED_TRY(check_problem(prob));
+  if (k < 1) return fail(RAGGED_EINVAL, "k < 1 (CLS always survives)");
+  if (prob->H > 16) return fail(RAGGED_ENOTSUP, "H > 16 (one thread-block cluster per image)");
+  if (ldx < (int64_t)prob->H * prob->d) return fail(RAGGED_EINVAL, "ldx < H*d");
+  if (ldx % 8 != 0) return fail(RAGGED_EALIGN, "ldx % 8 != 0 (rows must be 16-byte aligned)");
+  if (ldx > (1LL << 22)) return fail(RAGGED_ENOTSUP, "ldx > 2^22 elements");
+  if (prob->B == 0) return RAGGED_OK;
+  RAGGED_TRY(check_ptr(x, "x"));
+  RAGGED_TRY(check_ptr(q, "q"));
+  RAGGED_TRY(check_ptr(kt, "k"));
+  RAGGED_TRY(check_ptr(v, "v"));
+  RAGGED_TRY(check_ptr(o, "o"));
+  if ((long long)prob->B * prob->H > 0x7fffffffLL) return fail(RAGGED_ENOTSUP, "B*H too large");
+  int engine = resolve_engine(prob);
+  if (engine == RAGGED_ENGINE_TCGEN05) return fail(RAGGED_ENOTSUP, "the fused prune runs on the mma.sync engine");
+  // every image keeps exactly min(k, N) tokens: the long-sequence variant is
+  // chosen from that count whatever n_hint says
+  engine = (k < prob->N ? k : prob->N) > 64 ? ragged::kEngineMmaLong : RAGGED_ENGINE_MMA_SYNC;
+  cudaError_t e = ragged::launch_prune_l2_fused(prob->dtype, engine, x, ldx, k, q, kt, v, prob->ld, o, keep_or_null,
+                                                cu_seqlens_or_null, prob->B, prob->N, prob->H, as_stream(stream));
+  return e == cudaSuccess ? RAGGED_OK : cuda_fail(e, "ragged_prune_l2_pack_attend_unpack");
+}
+
 namespace {
 // A pointer the device can dereference: device memory as is, page-locked host
 // memory through its device mapping; pageable host memory is rejected.

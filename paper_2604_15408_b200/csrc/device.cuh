@@ -151,6 +151,33 @@ __device__ __forceinline__ void split2<__half>(float a, float b, uint32_t& hi, u
   lo = *reinterpret_cast<uint32_t*>(&l);
 }
 
+// ---- per-image top-k selection (N2 keep masks) ------------------------------
+// Rank of token n among tokens [first, N) of the scores s (shared memory) --
+// #{m : s_m > s_n, or s_m == s_n and m < n} (descending, ties to the lower
+// position) -- computed by a group of g consecutive lanes (g a power of two
+// <= 32; `part` = lane index in the group): each lane compares a strided 1/g of
+// the tokens, four independent counters, then the group sums.  Every lane of
+// the warp must call it (the sum is a shuffle); the result is in every lane.
+__device__ __forceinline__ int group_rank(const float* s, int n, int first, int N, int g, int part) {
+  const float sn = s[n];
+  int c0 = 0, c1 = 0, c2 = 0, c3 = 0;
+  int m = first + part;
+  for (; m + 3 * g < N; m += 4 * g) {
+    const float x0 = s[m], x1 = s[m + g], x2 = s[m + 2 * g], x3 = s[m + 3 * g];
+    c0 += (x0 > sn || (x0 == sn && m < n)) ? 1 : 0;
+    c1 += (x1 > sn || (x1 == sn && m + g < n)) ? 1 : 0;
+    c2 += (x2 > sn || (x2 == sn && m + 2 * g < n)) ? 1 : 0;
+    c3 += (x3 > sn || (x3 == sn && m + 3 * g < n)) ? 1 : 0;
+  }
+  for (; m < N; m += g) {
+    const float x = s[m];
+    c0 += (x > sn || (x == sn && m < n)) ? 1 : 0;
+  }
+  int r = c0 + c1 + c2 + c3;
+  for (int o = 1; o < g; o <<= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
+  return r;
+}
+
 // Byte offset of 16-byte chunk c of row r in a 128-byte-row tile with the
 // XOR-8 swizzle (chunk c of row r lives at chunk c ^ (r & 7)): conflict-free
 // ldmatrix over 8 consecutive rows, identical to the TMA 128B swizzle pattern.

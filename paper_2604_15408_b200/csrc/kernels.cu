@@ -380,6 +380,14 @@ struct AttnArgs {
   int B, N, H;
   long long ld;            // input token stride in elements
   int cu_groups;           // cu_mode 1: scan items (mma engine: one per 128 images; tcgen05: 1)
+  // kPrune (N2 fused ahead of the scan): the keep row is computed in the kernel
+  // from hidden states x [B, N, H*64] (token stride ldx): CLS + top-(kkeep-1) by
+  // ||x||_2 (R20), the image's H CTAs forming one cluster that exchanges the
+  // per-head partial squared norms through distributed shared memory.
+  const void* x;
+  long long ldx;
+  int kkeep;
+  uint8_t* keep_out;       // optional [B, N] copy of the computed mask
 };
 
 // Zero (+0.0) the 128-byte head slices of dropped rows sDrop[first], [first +
@@ -728,10 +736,11 @@ struct NoMid {
 template <bool kFused, typename Sync, typename Mid = NoMid>
 __device__ __forceinline__ void image_rows(const AttnArgs& a, int b, int16_t* sPos, int16_t* sDrop,
                                            uint32_t* sWords, int& n, long long& row_base, int tid,
-                                           Sync sync, Mid mid = Mid()) {
+                                           Sync sync, Mid mid = Mid(), const uint8_t* keep_row = nullptr) {
   const int warp = tid >> 5, lane = tid & 31;
   if constexpr (kFused) {
-    const uint8_t* km = a.keep + (long long)b * a.N;
+    // keep_row: the mask row already computed in shared memory (kPrune)
+    const uint8_t* km = keep_row != nullptr ? keep_row : a.keep + (long long)b * a.N;
     const int p0 = tid, p1 = tid + kAttnThreads;
     const uint8_t m0 = p0 < a.N ? km[p0] : (uint8_t)0;
     const uint8_t m1 = p1 < a.N ? km[p1] : (uint8_t)0;
@@ -926,7 +935,111 @@ __device__ __forceinline__ void attn_chunk(const uint8_t* sK, const uint8_t* sV,
 // kLargeN: the chunk loop with exact tile counts (attn_chunk), chosen on the host
 // from the caller's expected kept tokens per image (ragged_problem.n_hint > 64):
 // a separate kernel so the short-sequence kernel keeps its register allocation.
-template <typename T, bool kFused, bool kGather, bool kLargeN = false>
+__device__ __forceinline__ void cluster_arrive_relaxed() {
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.wait.aligned;" ::: "memory"); }
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void st_peer_u8(const void* p, uint32_t rank, uint8_t v) {
+  uint32_t a;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(a) : "r"(smem_u32(p)), "r"(rank));
+  asm volatile("st.shared::cluster.u8 [%0], %1;" ::"r"(a), "h"((unsigned short)v) : "memory");
+}
+__device__ __forceinline__ void st_peer_f32(const void* p, uint32_t rank, float v) {
+  uint32_t a;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(a) : "r"(smem_u32(p)), "r"(rank));
+  asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(a), "f"(v) : "memory");
+}
+
+// N2 fused ahead of the scan (Threshold-l2; R20): the
+// keep row of image b computed inside the attention kernel.  The image's H
+// CTAs (one per head, head fastest) form one thread-block cluster.  CTA h
+// stages its head's 64-column slice of x for every token (the same 128-byte
+// slices the kernel already works with) with cp.async, squares and sums them in
+// fp32, and stores the N partial sums into every CTA of the cluster (DSMEM);
+// after one cluster barrier each CTA adds the H partials in head order
+// (identical bits in every CTA); CTA h ranks tokens h, h + H, ... (CLS = +inf,
+// NaN last, ties to the lower position) and pushes their keep flags to every
+// CTA; a second cluster barrier publishes them.  Layout: x
+// slices in the K area, partials / keys / keep row in the V + Q areas; the
+// gather overwrites them only after image_rows' barrier (every read done).
+// Returns the keep row in shared memory.
+template <typename T>
+__device__ __forceinline__ const uint8_t* prune_l2_row(const AttnArgs& a, int b, int h, uint8_t* smem, int tid) {
+  const int rows_cap = attn_rows_cap(a.N);
+  uint8_t* s_x = smem;                                                      // [N][128 B]
+  float* s_part = reinterpret_cast<float*>(smem + rows_cap * kRowBytes);   // [H][N]
+  uint32_t* s_key = reinterpret_cast<uint32_t*>(s_part + a.H * a.N);       // [N]
+  uint8_t* s_keep = reinterpret_cast<uint8_t*>(s_key + kMaxN);              // [N]
+  const char* xb = static_cast<const char*>(a.x) + (long long)b * a.N * a.ldx * 2 + h * kRowBytes;
+  {  // 8 threads per 128-byte row slice; every copy in flight at once
+    const int c = tid & 7;
+    for (int p = tid >> 3; p < a.N; p += kAttnThreads / 8)
+      cp_async_16(smem_u32(s_x + p * kRowBytes + c * 16), xb + p * a.ldx * 2 + c * 16, 16);
+    cp_async_commit();
+    cp_async_wait_all();
+  }
+  __syncthreads();
+  TL(7);
+  float sq[2] = {0.f, 0.f};
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const int p = min(tid + i * kAttnThreads, a.N - 1);
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const uint4 raw = *reinterpret_cast<const uint4*>(s_x + p * kRowBytes + ((c + tid) & 7) * 16);
+      const T* e = reinterpret_cast<const T*>(&raw);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const float f = static_cast<float>(e[j]);
+        sq[i] = fmaf(f, f, sq[i]);
+      }
+    }
+  }
+  cluster_wait();  // every CTA of the cluster has started: DSMEM is live
+  TL(8);
+  for (int r = 0; r < a.H; ++r) {
+    if (tid < a.N) st_peer_f32(s_part + h * a.N + tid, r, sq[0]);
+    if (tid + kAttnThreads < a.N) st_peer_f32(s_part + h * a.N + tid + kAttnThreads, r, sq[1]);
+  }
+  TL(9);
+  cluster_sync_all();  // all H partials of every token delivered
+  TL(10);
+  float* s_score = reinterpret_cast<float*>(s_key);
+  for (int p = tid; p < a.N; p += kAttnThreads) {
+    float t = 0.f;
+    for (int r = 0; r < a.H; ++r) t += s_part[r * a.N + p];
+    s_score[p] = p == 0 ? INFINITY : (t != t ? -INFINITY : t);
+  }
+  __syncthreads();
+  TL(11);
+  // this CTA ranks tokens p = h, h + H, ... (g lanes per token) and stores the
+  // flags into every CTA of the cluster: the O(N^2) comparisons are split H ways
+  {
+    const int cnt = (a.N - h + a.H - 1) / a.H;             // tokens of this CTA
+    int g = 32;
+    while (g > 1 && g * cnt > kAttnThreads) g >>= 1;
+    const int per = kAttnThreads / g;                       // tokens per round
+    for (int base = 0; base < cnt; base += per) {          // uniform trip count
+      const int slot = base + tid / g;
+      const int p = h + a.H * min(slot, cnt - 1);
+      const int r = group_rank(s_score, p, 0, a.N, g, tid & (g - 1));
+      if ((tid & (g - 1)) == 0 && slot < cnt) {
+        const uint8_t kp = r < a.kkeep ? 1 : 0;
+        for (int d = 0; d < a.H; ++d) st_peer_u8(s_keep + p, d, kp);
+        if (a.keep_out != nullptr) a.keep_out[(long long)b * a.N + p] = kp;
+      }
+    }
+  }
+  cluster_sync_all();  // all N flags in every CTA
+  TL(12);
+  return s_keep;
+}
+
+// kPrune: N2 fused ahead of the scan -- see prune_l2_row above and AttnArgs::x.
+template <typename T, bool kFused, bool kGather, bool kLargeN = false, bool kPrune = false>
 __global__ void __launch_bounds__(kAttnThreads, 3) attn_kernel(const AttnArgs a, const GatherArgs ga) {
   extern __shared__ __align__(1024) uint8_t smem[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -939,9 +1052,15 @@ __global__ void __launch_bounds__(kAttnThreads, 3) attn_kernel(const AttnArgs a,
   uint32_t* sWords = reinterpret_cast<uint32_t*>(sDrop + kMaxN);
 
   TL(0);
+  if constexpr (kPrune) cluster_arrive_relaxed();  // paired with the wait before the first DSMEM store
   pdl_launch_dependents();
 #ifndef RAGGED_NO_KEEP_PREFETCH
-  if constexpr (kFused) {
+  if constexpr (kPrune) {
+    // the image's hidden rows (this head's 128-byte slice) into L2 before the wait
+    const int pb = (int)blockIdx.x / a.H, ph = (int)blockIdx.x - pb * a.H;
+    const char* xb = static_cast<const char*>(a.x) + (long long)pb * a.N * a.ldx * 2 + ph * kRowBytes;
+    for (int p = tid; p < a.N; p += kAttnThreads) prefetch_l2(xb + p * a.ldx * 2);
+  } else if constexpr (kFused) {
     // Before the grid-dependency wait (PDL: this CTA may be resident while the
     // previous kernel in the stream still runs): read this image's keep row
     // through L2 (.cg: nothing is left in L1) and prefetch the kept rows' q/k/v
@@ -1031,7 +1150,9 @@ __global__ void __launch_bounds__(kAttnThreads, 3) attn_kernel(const AttnArgs a,
   //  (Measured and rejected: zeroing all of the head's padded rows here, kept
   //  rows overwritten later -- C3 6.8 -> 7.5 us: the 25 KB of stores per CTA
   //  queue ahead of the gathers; the dropped rows are zeroed during the compute.)
-  const bool cu_here = kFused && a.cu_mode == 2 && h == 0;
+  const bool cu_here = kFused && !kPrune && a.cu_mode == 2 && h == 0;
+  const uint8_t* keep_row = nullptr;
+  if constexpr (kPrune) keep_row = prune_l2_row<T>(a, b, h, smem, tid);
   PrefixLoads pl;
   int n;
   long long row_base;
@@ -1043,7 +1164,15 @@ __global__ void __launch_bounds__(kAttnThreads, 3) attn_kernel(const AttnArgs a,
       for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
       if (lane == 0) sWords[8 + warp] = (uint32_t)c;
     }
-  });
+  }, keep_row);
+  if constexpr (kPrune) {
+    // every image keeps exactly min(kkeep, N) tokens: cu_seqlens is b * that
+    if (a.cu_out != nullptr && h == 0 && tid == 0) {
+      const int kc = min(a.kkeep, a.N);
+      a.cu_out[b] = b * kc;
+      if (b == a.B - 1) a.cu_out[a.B] = a.B * kc;
+    }
+  }
   const char* img_q = reinterpret_cast<const char*>(gq) + row_base * ldb + h * kRowBytes;
   const char* img_k = reinterpret_cast<const char*>(gk) + row_base * ldb + h * kRowBytes;
   const char* img_v = reinterpret_cast<const char*>(gv) + row_base * ldb + h * kRowBytes;
@@ -1437,6 +1566,58 @@ static cudaError_t launch_attn_mma(const AttnArgs& a, int grid, cudaStream_t st,
   if (e != cudaSuccess) return e;
   return launch_pdl(attn_kernel<T, kFused, kGather, kLargeN>, dim3(grid), dim3(kAttnThreads),
                     attn_smem_bytes(a.N), st, a, g);
+}
+
+// N2 fused ahead of the scan: one cluster of H CTAs per image (H <= 16).
+template <typename T, bool kLargeN>
+static cudaError_t launch_attn_prune(const AttnArgs& a, cudaStream_t st) {
+  static bool done[64] = {false};
+  auto kern = attn_kernel<T, true, false, kLargeN, true>;
+  cudaError_t e = smem_attr_once(kern, attn_smem_bytes(kMaxN), done);
+  if (e != cudaSuccess) return e;
+  if (a.H > 8) {
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e != cudaSuccess) return e;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(a.B * a.H);
+  cfg.blockDim = dim3(kAttnThreads);
+  cfg.dynamicSmemBytes = attn_smem_bytes(a.N);
+  cfg.stream = st;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  attr[1].id = cudaLaunchAttributeClusterDimension;
+  attr[1].val.clusterDim.x = a.H;
+  attr[1].val.clusterDim.y = 1;
+  attr[1].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 2;
+  return cudaLaunchKernelEx(&cfg, kern, a, GatherArgs{});
+}
+
+cudaError_t launch_prune_l2_fused(int dtype, int engine, const void* x, long long ldx, int kkeep, const void* q,
+                                  const void* k, const void* v, long long ld, void* o, uint8_t* keep_out,
+                                  int32_t* cu_out, int B, int N, int H, cudaStream_t st) {
+  AttnArgs a{};
+  a.q = q;
+  a.k = k;
+  a.v = v;
+  a.o = o;
+  a.cu_out = cu_out;
+  a.cu_mode = 0;
+  a.B = B;
+  a.N = N;
+  a.H = H;
+  a.ld = ld;
+  a.x = x;
+  a.ldx = ldx;
+  a.kkeep = kkeep;
+  a.keep_out = keep_out;
+  const bool large = engine == kEngineMmaLong;
+  if (dtype == 0)
+    return large ? launch_attn_prune<__nv_bfloat16, true>(a, st) : launch_attn_prune<__nv_bfloat16, false>(a, st);
+  return large ? launch_attn_prune<__half, true>(a, st) : launch_attn_prune<__half, false>(a, st);
 }
 
 // tcgen05 engine: persistent grid of min(#SMs, work items) CTAs x nslots slots.

@@ -43,6 +43,11 @@ cudaError_t launch_attn_gather(int dtype, int engine, const void* qp, const void
                                const int32_t* cu, int B, int N, int H, long long ld,
                                const GatherArgs& g, cudaStream_t st);
 cudaError_t launch_empty(int grid, int block, cudaStream_t st);
+// N2 fused ahead of the scan: Threshold-l2 keep row computed inside the fused
+// pack-attend-unpack kernel (one cluster of H CTAs per image, H <= 16)
+cudaError_t launch_prune_l2_fused(int dtype, int engine, const void* x, long long ldx, int kkeep, const void* q,
+                                  const void* k, const void* v, long long ld, void* o, uint8_t* keep_out,
+                                  int32_t* cu_out, int B, int N, int H, cudaStream_t st);
 
 // ---- NEXT row N4 (attn_general.cu): d in {32, 64, 80, 128}, any N ----
 // NEXT row N4, fp8 (e4m3) inputs for ragged_attn (out_dtype 0 = bf16, 1 = fp16)

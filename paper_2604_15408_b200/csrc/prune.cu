@@ -80,6 +80,9 @@ __device__ __forceinline__ uint32_t peer_addr(const void* p, uint32_t rank) {
 __device__ __forceinline__ void st_peer_f32(uint32_t a, float v) {
   asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(a), "f"(v) : "memory");
 }
+__device__ __forceinline__ void st_peer_u8(uint32_t a, uint8_t v) {
+  asm volatile("st.shared::cluster.u8 [%0], %1;" ::"r"(a), "h"((unsigned short)v) : "memory");
+}
 __device__ __forceinline__ void st_peer_v4(uint32_t a, float x, float y, float z, float w) {
   asm volatile("st.shared::cluster.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(a), "f"(x), "f"(y), "f"(z), "f"(w)
                : "memory");
@@ -112,28 +115,6 @@ __device__ __forceinline__ void copy_rows(uint8_t* dst, const char* src, long lo
 
 // NaN scores rank below every finite score (R20), so at most k tokens survive.
 __device__ __forceinline__ float nan_low(float s) { return s != s ? -INFINITY : s; }
-
-// rank of token n among tokens [first, N) by score, descending, ties to the
-// lower position.  Four independent counters, loop unrolled: the shared-memory
-// loads (broadcasts) pipeline instead of forming one dependent chain.
-__device__ __forceinline__ int rank_of(const float* s, int n, int first, int N) {
-  const float sn = s[n];
-  int r[4] = {0, 0, 0, 0};
-  int m = first;
-#pragma unroll 2
-  for (; m + 4 <= N; m += 4) {
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const float sm = s[m + i];
-      r[i] += (sm > sn || (sm == sn && m + i < n)) ? 1 : 0;
-    }
-  }
-  for (; m < N; ++m) {
-    const float sm = s[m];
-    r[0] += (sm > sn || (sm == sn && m < n)) ? 1 : 0;
-  }
-  return r[0] + r[1] + r[2] + r[3];
-}
 
 // Per warp, rows warp + 8i (i < 4) of a [nrows][cpr x 16 B] SMEM row buffer:
 // acc[i] = sum over the row's 16-byte chunks cc of f(chunk, cc), reduced over
@@ -240,21 +221,11 @@ __global__ void __launch_bounds__(kPThr) keep_l2_cluster_kernel(const T* __restr
   PTL(4);
   cluster_sync_all();  // every CTA now holds all N scores of the image
   PTL(5);
-  // rank own rows: 8 threads per row, each comparing a strided eighth of the N
-  // scores, counts summed over the 8 lanes
+  // rank own rows: 8 lanes per row (R <= 32 rows on 256 threads)
   {
-    const int rr = tid >> 3, part = tid & 7, n = r0 + rr;
-    const float sn = n < r1 ? s_score[n] : 0.f;
-    int r = 0;
-#pragma unroll 8
-    for (int m = part; m < N; m += 8) {
-      const float sm = s_score[m];
-      r += (sm > sn || (sm == sn && m < n)) ? 1 : 0;
-    }
-    r += __shfl_xor_sync(0xffffffffu, r, 1);
-    r += __shfl_xor_sync(0xffffffffu, r, 2);
-    r += __shfl_xor_sync(0xffffffffu, r, 4);
-    if (part == 0 && n < r1) keep[(long long)b * N + n] = r < k ? 1 : 0;
+    const int rr = tid >> 3, n = min(r0 + rr, N - 1);
+    const int r = group_rank(s_score, n, 0, N, 8, tid & 7);
+    if ((tid & 7) == 0 && r0 + rr < r1) keep[(long long)b * N + r0 + rr] = r < k ? 1 : 0;
   }
   PTL(6);
 }
@@ -396,11 +367,20 @@ __global__ void __launch_bounds__(kPThr) keep_evit_cluster_kernel(T* __restrict_
   cluster_sync_all();  // all N logits in every CTA
   PTL(4);
   // 2. ranking (every CTA, all tokens: identical in every CTA): CLS + top-(kk-2)
-  if (tid < N) {
-    const bool kept = tid == 0 || (kk >= 2 && rank_of(s_logit, tid, 1, N) < kk - 2);
-    s_keep[tid] = kept ? 1 : 0;
-    if (!kept) atomicMin(&s_f, tid);
+  // rank own rows among the other tokens [1, N) (8 lanes per row): kept if
+  // CLS or rank < kk - 2; the flags go to every CTA of the cluster
+  {
+    const int rr = tid >> 3, n = min(max(r0 + rr, 1), N - 1);
+    const int r = group_rank(s_logit, n, 1, N, 8, tid & 7);
+    const int nn = r0 + rr;
+    if ((tid & 7) == 0 && nn < r1) {
+      const uint8_t kp = (nn == 0 || r < kk - 2) ? 1 : 0;
+#pragma unroll
+      for (int d = 0; d < kPC; ++d) st_peer_u8(peer_addr(&s_keep[nn], d), kp);
+    }
   }
+  cluster_sync_all();  // every CTA holds all N keep flags
+  if (tid > 0 && tid < N && !s_keep[tid]) atomicMin(&s_f, tid);
   __syncthreads();
   const int f = s_f;
   const bool fuse = kk >= 2 && f < N;  // uniform

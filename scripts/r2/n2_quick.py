@@ -33,3 +33,11 @@ def ef(i):
 res["evit_then_fused_us"] = bench._graph_time(torch, [(lambda i=i: ef(i)) for i in range(16)], 500)
 res["l2_hbm_frac"] = (B * N * H * 128 + B * N) / (res["l2_us"] * 1e-6) / 1e9 / bench._hbm_peak()
 print(json.dumps(res, indent=1))
+pr = []
+for j in range(L):
+    pass
+def fp(j):
+    s = sets[j % 16]
+    rb.prune_l2_pack_attend_unpack(xs[j % NX], s["q"], s["k"], s["v"], kk, o=s["o"], cu=s["cu"])
+res["prune_l2_fused_us"] = bench._graph_time(torch, [(lambda j=j: fp(j)) for j in range(L)], 500)
+print(json.dumps({"prune_l2_fused_us": res["prune_l2_fused_us"]}))

@@ -109,3 +109,79 @@ def test_keep_evit_fused_qkv_layout_then_fused_path():
     _check_evit(q, k, v, kk, km, qd, kd, vd)
     ref, _ = oracle.pack_attend_unpack(qd.cpu(), kd.cpu(), vd.cpu(), km)
     check_attention(to_np(o), ref, torch.bfloat16)
+
+
+# ------------------------- N2 fused ahead of the scan (Threshold-l2) ----
+
+def _l2_mask_ok(x, k, got):
+    """Exact where the threshold gap exceeds fp32 rounding; else a valid top-k."""
+    want = oracle.keep_topk_l2(x, k)
+    s = oracle.l2_scores(x)
+    for b in range(want.shape[0]):
+        if np.array_equal(got[b], want[b]):
+            continue
+        srt = np.sort(s[b])[::-1]
+        kk = min(k, s.shape[1])
+        gap = (srt[kk - 1] - srt[kk]) / srt[kk] if kk < s.shape[1] else np.inf
+        assert gap < 1e-5, f"image {b}: masks differ although the threshold gap is {gap:.2e}"
+        assert got[b].sum() == want[b].sum() and got[b][0] == 1
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "fp16"])
+@pytest.mark.parametrize("B,N,H,p", [(32, 197, 12, 0.8), (4, 197, 3, 0.5), (7, 33, 6, 0.3), (3, 256, 16, 0.9),
+                                     (5, 197, 12, 0.0), (2, 1, 4, 0.0), (6, 100, 12, 0.5)])
+def test_prune_l2_fused_matches_oracle(dtype, B, N, H, p):
+    """Mask computed inside the fused launch == ragged_keep_topk_l2's definition
+    (oracle), output == oracle pack-attend-unpack on that mask, cu = b*min(k,N);
+    and bit-identical to the two-launch path (mask kernel -> fused kernel) on the
+    same mask (same attention kernel variant)."""
+    kk = max(1, synth.kept_tokens(N, p))
+    x = synth.hidden_states(B, N, H * 64, dtype, seed=51)
+    q, k, v = synth.activations(B, N, H, 64, dtype, seed=52)
+    xd, qd, kd, vd = (t.to(DEV) for t in (x, q, k, v))
+    keep = torch.empty(B, N, dtype=torch.uint8, device=DEV)
+    cu = torch.empty(B + 1, dtype=torch.int32, device=DEV)
+    o = rb.prune_l2_pack_attend_unpack(xd, qd, kd, vd, kk, keep=keep, cu=cu)
+    torch.cuda.synchronize()
+    km = keep.cpu().numpy()
+    _l2_mask_ok(x, kk, km)
+    assert cu.cpu().tolist() == [b * min(kk, N) for b in range(B + 1)]
+    ref, _ = oracle.pack_attend_unpack(q, k, v, km)
+    check_attention(to_np(o), ref, DT[dtype])
+    o2 = rb.pack_attend_unpack(qd, kd, vd, keep, n_hint=min(kk, N))
+    torch.cuda.synchronize()
+    assert np.array_equal(bits(o), bits(o2))
+
+
+def test_prune_l2_fused_pipelined_masks_change():
+    """40 PDL-chained fused-prune calls on one stream alternating two hidden-state
+    batches (different masks) into ONE output buffer set: every call equals the
+    synchronised result bit for bit (nothing read before the grid-dependency
+    wait reaches a result)."""
+    B, N, H = 16, 197, 12
+    kk = synth.kept_tokens(N, 0.7)
+    xs = [synth.hidden_states(B, N, H * 64, "bf16", seed=s).to(DEV) for s in (61, 62)]
+    q, k, v = (t.to(DEV) for t in synth.activations(B, N, H, 64, "bf16", seed=63))
+    ref = []
+    for x in xs:
+        ref.append(rb.prune_l2_pack_attend_unpack(x, q, k, v, kk))
+        torch.cuda.synchronize()
+    assert not torch.equal(ref[0], ref[1])
+    outs = [torch.empty_like(ref[0]) for _ in range(40)]
+    keep = torch.empty(B, N, dtype=torch.uint8, device=DEV)
+    for i, o in enumerate(outs):
+        rb.prune_l2_pack_attend_unpack(xs[i % 2], q, k, v, kk, o=o, keep=keep)
+    torch.cuda.synchronize()
+    for i, o in enumerate(outs):
+        assert np.array_equal(bits(o), bits(ref[i % 2])), f"call {i}"
+
+
+def test_prune_l2_fused_validation():
+    q = torch.zeros(2, 9, 17, 64, dtype=torch.bfloat16, device=DEV)
+    x = torch.zeros(2, 9, 17 * 64, dtype=torch.bfloat16, device=DEV)
+    with pytest.raises(rb.RaggedError):
+        rb.prune_l2_pack_attend_unpack(x, q, q, q, 3)          # H = 17 > 16
+    q = q[:, :, :4].contiguous()
+    x = x[:, :, :256].contiguous()
+    with pytest.raises(rb.RaggedError):
+        rb.prune_l2_pack_attend_unpack(x, q, q, q, 0)          # k < 1
