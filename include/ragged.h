@@ -66,7 +66,10 @@ typedef enum {
 typedef enum {
   RAGGED_ENGINE_AUTO = 0,
   RAGGED_ENGINE_MMA_SYNC = 1,   /* mma.sync.m16n8k16, fp32 accumulate in registers */
-  RAGGED_ENGINE_TCGEN05 = 2     /* tcgen05.mma, fp32 accumulate in TMEM            */
+  RAGGED_ENGINE_TCGEN05 = 2,    /* tcgen05.mma, fp32 accumulate in TMEM            */
+  RAGGED_ENGINE_TCGEN05_WS = 3  /* warp-specialised tcgen05 (M = 128 query tiles in
+                                   ping-pong, TMEM-resident S/P/O): ragged_attn with
+                                   d = 64, any N -- the long-sequence engine */
 } ragged_engine;
 
 /* The problem statement of the paper: B images, N padded tokens per image
@@ -120,10 +123,14 @@ RAGGED_API ragged_status ragged_pack(const ragged_problem* prob, const uint8_t* 
  * bidirectional, no dropout, no KV cache.  One CTA per (image,
  * head) pair, head fastest (pid -> h = pid mod H, i = pid / H).
  * Shapes: the DeiT path takes d = 64, N <= 256 (one-stage K/V in shared
- * memory).  Other shapes (NEXT row N4) run a streaming kernel: d in {32, 64,
- * 80, 128} and N up to 2^20, K/V in 64-key chunks with Alg. 1's online
- * softmax; rows are prob->ld elements apart as below, op rows
- * H*d apart.  Other d -> RAGGED_ENOTSUP.
+ * memory).  Other shapes (NEXT row N4) run streaming kernels (Alg. 1's outer
+ * loops): at d = 64 and N > 256 (or with RAGGED_ENGINE_TCGEN05_WS at
+ * any N) the warp-specialised tcgen05 engine (128-row query tiles, 128-key
+ * K/V blocks by TMA, S/P/O in TMEM) -- it requires qp/kp/vp to hold the
+ * B*N-row capacity (rows past cu[B] are read, never used); d in {32, 80,
+ * 128} the mma.sync streaming kernel (N up to 2^20, 64-key chunks).  Rows
+ * are prob->ld elements apart as below, op rows H*d apart.  Other d ->
+ * RAGGED_ENOTSUP.
  * Input rows of qp/kp/vp are prob->ld elements apart (H*d for three packed
  * [cap, H, d] buffers; 3*H*d for one packed qkv buffer [cap, 3, H, d] with
  * kp = qp + H*d, vp = qp + 2*H*d -- the N1 block's qkv GEMM output); op rows

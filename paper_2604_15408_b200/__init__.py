@@ -22,7 +22,7 @@ _PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("RAGGED_LIB") or os.path.join(_PKG, "libragged.so")
 
 BF16, FP16 = 0, 1
-ENGINE_AUTO, ENGINE_MMA_SYNC, ENGINE_TCGEN05 = 0, 1, 2
+ENGINE_AUTO, ENGINE_MMA_SYNC, ENGINE_TCGEN05, ENGINE_TCGEN05_WS = 0, 1, 2, 3
 OK, EINVAL, ENOTSUP, EALIGN, ECUDA = 0, 1, 2, 3, 4
 _DTYPE = {torch.bfloat16: BF16, torch.float16: FP16}
 

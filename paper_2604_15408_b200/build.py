@@ -16,7 +16,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libragged.so")
-SOURCES = ["kernels.cu", "prune.cu", "block.cu", "attn_general.cu", "api.cu"]
+SOURCES = ["kernels.cu", "prune.cu", "block.cu", "attn_general.cu", "attn_fa.cu", "api.cu"]
 HEADERS = ["device.cuh", "launch.h", "tcgen05.cuh", "attn_tc.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr", "-Xcompiler", "-fPIC",
@@ -42,7 +42,10 @@ VARIANTS = {"": [], "tl": ["-DRAGGED_TIMELINE"],
             # A/B of the fused kernel's pre-wait prefetch: none / keep row only (default: keep row
             # read + kept q/k/v rows prefetched)
             "nopf": ["-DRAGGED_NO_KEEP_PREFETCH"],
-            "keeppf": ["-DRAGGED_KEEP_PREFETCH_ONLY"]}
+            "keeppf": ["-DRAGGED_KEEP_PREFETCH_ONLY"],
+            # ablations of the warp-specialised engine (timing experiments only)
+            "fansm": ["-DRAGGED_FA_ABLATE_SOFTMAX"], "fanpv": ["-DRAGGED_FA_ABLATE_PV"],
+            "fanone": ["-DRAGGED_FA_ABLATE_SOFTMAX", "-DRAGGED_FA_ABLATE_PV"]}
 
 
 def lib_path(variant: str = "") -> str:

@@ -52,7 +52,7 @@ ragged_status check_problem(const ragged_problem* p, bool general = false) {
   if (p->dtype != RAGGED_BF16 && p->dtype != RAGGED_FP16)
     return fail(RAGGED_ENOTSUP, "dtype must be RAGGED_BF16 or RAGGED_FP16");
   if (p->engine != RAGGED_ENGINE_AUTO && p->engine != RAGGED_ENGINE_MMA_SYNC &&
-      p->engine != RAGGED_ENGINE_TCGEN05)
+      p->engine != RAGGED_ENGINE_TCGEN05 && p->engine != RAGGED_ENGINE_TCGEN05_WS)
     return fail(RAGGED_ENOTSUP, "unknown engine");
   if ((long long)p->B * p->N > 0x7fffffffLL) return fail(RAGGED_ENOTSUP, "B*N exceeds int32 indices");
   if ((long long)p->H * p->d > (1LL << 22)) return fail(RAGGED_ENOTSUP, "H*d > 2^22");
@@ -127,6 +127,8 @@ ragged_status ragged_pack(const ragged_problem* prob, const uint8_t* keep, const
                           const void* k, const void* v, int32_t* cu_seqlens, int32_t* dst_index,
                           int32_t* src_index, void* qp, void* kp, void* vp, void* stream) {
   RAGGED_TRY(check_problem(prob));
+  if (prob->engine == RAGGED_ENGINE_TCGEN05_WS)
+    return fail(RAGGED_ENOTSUP, "RAGGED_ENGINE_TCGEN05_WS runs ragged_attn only");
   if (prob->B == 0) return RAGGED_OK;
   RAGGED_TRY(check_ptr_any(keep, "keep"));
   RAGGED_TRY(check_ptr(q, "q"));
@@ -154,6 +156,19 @@ ragged_status ragged_attn(const ragged_problem* prob, const void* qp, const void
   RAGGED_TRY(check_ptr_any(cu_seqlens, "cu_seqlens"));
   RAGGED_TRY(check_ptr(op, "op"));
   if ((long long)prob->B * prob->H > 0x7fffffffLL) return fail(RAGGED_ENOTSUP, "B*H too large");
+  // AUTO at head_dim 64 past the one-stage cap (N > 256): the warp-specialised
+  // tcgen05 engine (measured 1.9x the streaming mma.sync kernel at ViT-L/16@384,
+  // 1.6x at N = 1024; at N <= 256 the one-CTA-per-(image, head) kernels win or tie)
+  const bool ws = prob->engine == RAGGED_ENGINE_TCGEN05_WS ||
+                  (prob->engine == RAGGED_ENGINE_AUTO && prob->d == 64 && prob->N > 256);
+  if (ws) {  // warp-specialised tcgen05 engine (attn_fa.cu)
+    if (prob->d != 64) return fail(RAGGED_ENOTSUP, "the warp-specialised engine takes head_dim 64");
+    if ((long long)prob->B * prob->H * ((prob->N + 255) / 256) > 0x7fffffffLL)
+      return fail(RAGGED_ENOTSUP, "too many query tiles");
+    cudaError_t e = ragged::launch_attn_fa(prob->dtype, qp, kp, vp, cu_seqlens, op, prob->B, prob->N, prob->H,
+                                           prob->ld, as_stream(stream));
+    return e == cudaSuccess ? RAGGED_OK : cuda_fail(e, "ragged_attn/ws");
+  }
   if (prob->N > 256 || prob->d != 64) {  // NEXT row N4: the streaming kernel (attn_general.cu)
     if ((long long)prob->B * prob->H * ((prob->N + 63) / 64) > 0x7fffffffLL)
       return fail(RAGGED_ENOTSUP, "too many query blocks");
@@ -203,6 +218,8 @@ ragged_status ragged_pack_attend_unpack(const ragged_problem* prob, const uint8_
                                         const void* q, const void* k, const void* v, void* o,
                                         int32_t* cu_seqlens_or_null, void* stream) {
   RAGGED_TRY(check_problem(prob));
+  if (prob->engine == RAGGED_ENGINE_TCGEN05_WS)
+    return fail(RAGGED_ENOTSUP, "RAGGED_ENGINE_TCGEN05_WS runs ragged_attn only");
   if (prob->B == 0) return RAGGED_OK;
   RAGGED_TRY(check_ptr_any(keep, "keep"));
   RAGGED_TRY(check_ptr(q, "q"));
@@ -220,6 +237,8 @@ ragged_status ragged_prune_l2_pack_attend_unpack(const ragged_problem* prob, con
                                                 uint8_t* keep_or_null, int32_t* cu_seqlens_or_null,
                                                 void* stream) {
   RAGGED_TRY(check_problem(prob));
+  if (prob->engine == RAGGED_ENGINE_TCGEN05_WS)
+    return fail(RAGGED_ENOTSUP, "RAGGED_ENGINE_TCGEN05_WS runs ragged_attn only");
   if (k < 1) return fail(RAGGED_EINVAL, "k < 1 (CLS always survives)");
   if (prob->H > 16) return fail(RAGGED_ENOTSUP, "H > 16 (one thread-block cluster per image)");
   if (ldx < (int64_t)prob->H * prob->d) return fail(RAGGED_EINVAL, "ldx < H*d");
@@ -274,6 +293,8 @@ ragged_status ragged_pack_attend_unpack_host(const ragged_problem* prob, const u
                                              const void* q, const void* k, const void* v, void* o,
                                              int32_t* cu_seqlens_or_null, void* stream) {
   RAGGED_TRY(check_problem(prob));
+  if (prob->engine == RAGGED_ENGINE_TCGEN05_WS)
+    return fail(RAGGED_ENOTSUP, "RAGGED_ENGINE_TCGEN05_WS runs ragged_attn only");
   if (prob->B == 0) return RAGGED_OK;
   RAGGED_TRY(check_ptr_any(keep, "keep"));
   RAGGED_TRY(check_ptr(q, "q"));
@@ -298,6 +319,8 @@ ragged_status ragged_graph_create(const ragged_problem* prob, const uint8_t* kee
   if (out == nullptr) return fail(RAGGED_EINVAL, "out is NULL");
   *out = nullptr;
   RAGGED_TRY(check_problem(prob));
+  if (prob->engine == RAGGED_ENGINE_TCGEN05_WS)
+    return fail(RAGGED_ENOTSUP, "RAGGED_ENGINE_TCGEN05_WS runs ragged_attn only");
   cudaStream_t st = nullptr;
   cudaError_t e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
   if (e != cudaSuccess) return cuda_fail(e, "ragged_graph_create/stream");
@@ -423,6 +446,8 @@ ragged_status ragged_pack_attend_unpack_gather(const ragged_problem* prob, const
                                                int32_t* cu_seqlens_or_null, const ragged_gather* g,
                                                void* stream) {
   RAGGED_TRY(check_problem(prob));
+  if (prob->engine == RAGGED_ENGINE_TCGEN05_WS)
+    return fail(RAGGED_ENOTSUP, "RAGGED_ENGINE_TCGEN05_WS runs ragged_attn only");
   ragged::GatherArgs ga;
   RAGGED_TRY(to_gather_args(prob, g, true, ga));
   if (prob->B == 0) return RAGGED_OK;
@@ -440,6 +465,8 @@ ragged_status ragged_attn_gather(const ragged_problem* prob, const void* qp, con
                                  const void* vp, const int32_t* cu_seqlens, const ragged_gather* g,
                                  void* stream) {
   RAGGED_TRY(check_problem(prob));
+  if (prob->engine == RAGGED_ENGINE_TCGEN05_WS)
+    return fail(RAGGED_ENOTSUP, "RAGGED_ENGINE_TCGEN05_WS runs ragged_attn only");
   ragged::GatherArgs ga;
   RAGGED_TRY(to_gather_args(prob, g, false, ga));
   if (prob->B == 0) return RAGGED_OK;
@@ -659,6 +686,9 @@ int32_t ragged_debug_gemm_timeline(void* host, int32_t max_ctas) {
 }
 int32_t ragged_debug_prune_timeline(void* host, int32_t max_ctas) {
   return ragged::prune_timeline_copy(host, max_ctas);
+}
+int32_t ragged_debug_fa_timeline(void* host, int32_t max_ctas) {
+  return ragged::fa_timeline_copy(host, max_ctas);
 }
 #endif
 

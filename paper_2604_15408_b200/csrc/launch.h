@@ -16,7 +16,7 @@ cudaError_t launch_scan_pack(const uint8_t* keep, const void* q, const void* k, 
                              int32_t* src, void* qp, void* kp, void* vp, cudaStream_t st);
 // engine: 1 = mma.sync, 2 = tcgen05 (api.cu resolves RAGGED_ENGINE_AUTO),
 // kEngineMmaLong = mma.sync with the long-sequence chunk loop (n_hint > 64)
-constexpr int kEngineMmaLong = 3;
+constexpr int kEngineMmaLong = 16;
 cudaError_t launch_attn(int dtype, int engine, const void* qp, const void* kp, const void* vp, const int32_t* cu,
                         void* op, int B, int N, int H, long long ld, cudaStream_t st);
 cudaError_t launch_unpack(const void* op, const int32_t* dst, void* o, int B, int N, int H,
@@ -55,6 +55,9 @@ cudaError_t launch_attn_general_f8(int out_dtype, int d, const void* qp, const v
                                    float dq, float dk, float dv, const int32_t* cu, void* op, int B, int N, int H,
                                    long long ld, cudaStream_t st);
 bool attn_general_supports(int d);
+// warp-specialised tcgen05 engine (attn_fa.cu): packed q/k/v, d = 64, any N
+cudaError_t launch_attn_fa(int dtype, const void* qp, const void* kp, const void* vp, const int32_t* cu, void* op,
+                           int B, int N, int H, long long ld, cudaStream_t st);
 cudaError_t launch_attn_general(int dtype, int d, const void* qp, const void* kp, const void* vp, const int32_t* cu,
                                 void* op, int B, int N, int H, long long ld, cudaStream_t st);
 
@@ -88,6 +91,7 @@ int pairs_timeline_copy(void* host, int max_ctas);
 int gemm_timeline_copy(void* host, int max_ctas);
 int timeline_clear();
 int prune_timeline_copy(void* host, int max_ctas);
+int fa_timeline_copy(void* host, int max_ctas);
 #endif
 
 }  // namespace ragged

@@ -210,6 +210,12 @@ __device__ __forceinline__ void st_x16(uint32_t taddr, const uint32_t (&r)[16]) 
       "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
       : "memory");
 }
+__device__ __forceinline__ void st_x8(uint32_t taddr, const uint32_t (&r)[8]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr), "r"(r[0]), "r"(r[1]),
+      "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
+      : "memory");
+}
 // 16 lanes x 256 bits, x8 along columns (64 columns): thread t gets, for each
 // 8-column group j, regs [4j, 4j+3] = (lane t/4: cols 8j+2(t%4), +1),
 // (lane t/4 + 8: same cols) -- the mma.sync accumulator fragment shape.

@@ -31,6 +31,28 @@ def _packed_case(lengths, H, d, dt, seed, dist="standard"):
     return qp, kp, vp, cu, N, T
 
 
+def _cap(t, rows):
+    """Pad a packed [T, H, d] tensor to `rows` (the binding requires the B*N-row
+    capacity that ragged_pack produces)."""
+    if t.shape[0] >= rows:
+        return t
+    pad = torch.zeros((rows - t.shape[0],) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
+    return torch.cat([t, pad])
+
+
+def attn_cap(qp, kp, vp, cu, N, **kw):
+    rows = (cu.numel() - 1) * N
+    T = qp.shape[0]
+    return rb.attn(_cap(qp, rows), _cap(kp, rows), _cap(vp, rows), cu, N, **kw)[:T]
+
+
+def attn_fp8_cap(qp, kp, vp, cu, N, *a, **kw):
+    rows = (cu.numel() - 1) * N
+    T = qp.shape[0]
+    pad = lambda t: _cap(t.view(torch.uint8), rows).view(t.dtype)  # noqa: E731
+    return rb.attn_fp8(pad(qp), pad(kp), pad(vp), cu, N, *a, **kw)[:T]
+
+
 @pytest.mark.parametrize("d", [32, 64, 80, 128])
 @pytest.mark.parametrize("dt", ["bf16", "fp16"])
 def test_general_head_dims(d, dt):
@@ -38,7 +60,7 @@ def test_general_head_dims(d, dt):
     H = 3
     qp, kp, vp, cu, N, T = _packed_case(lengths, H, d, dt, seed=d)
     cud = torch.from_numpy(cu.astype(np.int32)).to(DEV)
-    got = rb.attn(qp.to(DEV), kp.to(DEV), vp.to(DEV), cud, N)
+    got = attn_cap(qp.to(DEV), kp.to(DEV), vp.to(DEV), cud, N)
     torch.cuda.synchronize()
     ref = oracle.attention(qp, kp, vp, cu)
     check_attention(to_np(got[:T]), ref, DT[dt])
@@ -50,7 +72,7 @@ def test_general_long_sequences(dt):
     ragged mix)."""
     lengths = [577, 1000, 300, 257, 5]
     qp, kp, vp, cu, N, T = _packed_case(lengths, 2, 64, dt, seed=7)
-    got = rb.attn(qp.to(DEV), kp.to(DEV), vp.to(DEV), torch.from_numpy(cu.astype(np.int32)).to(DEV), N)
+    got = attn_cap(qp.to(DEV), kp.to(DEV), vp.to(DEV), torch.from_numpy(cu.astype(np.int32)).to(DEV), N)
     torch.cuda.synchronize()
     check_attention(to_np(got[:T]), oracle.attention(qp, kp, vp, cu), DT[dt])
 
@@ -59,7 +81,7 @@ def test_general_long_sequences(dt):
 def test_general_distributions(dist):
     lengths = [400, 77, 129]
     qp, kp, vp, cu, N, T = _packed_case(lengths, 2, 128, "bf16", seed=9, dist=dist)
-    got = rb.attn(qp.to(DEV), kp.to(DEV), vp.to(DEV), torch.from_numpy(cu.astype(np.int32)).to(DEV), N)
+    got = attn_cap(qp.to(DEV), kp.to(DEV), vp.to(DEV), torch.from_numpy(cu.astype(np.int32)).to(DEV), N)
     torch.cuda.synchronize()
     vmax = float(vp.abs().max()) if dist == "heavy" else None
     check_attention(to_np(got[:T]), oracle.attention(qp, kp, vp, cu), torch.bfloat16, vmax=vmax, dist=dist)
@@ -71,7 +93,7 @@ def test_general_strided_qkv_and_untouched_rows():
     lengths = [300, 45, 0, 260]
     H, d = 2, 80
     qp, kp, vp, cu, N, T = _packed_case(lengths, H, d, "bf16", seed=11)
-    cap = T + 37
+    cap = max(T + 37, len(lengths) * N)
     qkv = torch.zeros(cap, 3, H, d, dtype=torch.bfloat16)
     qkv[:T, 0], qkv[:T, 1], qkv[:T, 2] = qp, kp, vp
     qkv = qkv.to(DEV)
@@ -86,11 +108,11 @@ def test_general_deterministic_and_isolated():
     lengths = [333, 90]
     qp, kp, vp, cu, N, T = _packed_case(lengths, 2, 128, "bf16", seed=13)
     cud = torch.from_numpy(cu.astype(np.int32)).to(DEV)
-    a = rb.attn(qp.to(DEV), kp.to(DEV), vp.to(DEV), cud, N)
-    b = rb.attn(qp.to(DEV), kp.to(DEV), vp.to(DEV), cud, N)
+    a = attn_cap(qp.to(DEV), kp.to(DEV), vp.to(DEV), cud, N)
+    b = attn_cap(qp.to(DEV), kp.to(DEV), vp.to(DEV), cud, N)
     kp2 = kp.clone()
     kp2[333:] += 1.0                       # perturb image 1 only
-    c = rb.attn(qp.to(DEV), kp2.to(DEV), vp.to(DEV), cud, N)
+    c = attn_cap(qp.to(DEV), kp2.to(DEV), vp.to(DEV), cud, N)
     torch.cuda.synchronize()
     assert torch.equal(a.view(torch.int16), b.view(torch.int16))
     assert torch.equal(a[:333].view(torch.int16), c[:333].view(torch.int16))
@@ -114,7 +136,7 @@ def test_general_fp8_inputs(d, out):
     qp, kp, vp, cu, N, T = _packed_case(lengths, H, d, "fp16", seed=100 + d)
     (q8, sq), (k8, sk), (v8, sv) = (_quant_e4m3(t) for t in (qp, kp, vp))
     cud = torch.from_numpy(cu.astype(np.int32)).to(DEV)
-    got = rb.attn_fp8(q8.to(DEV), k8.to(DEV), v8.to(DEV), cud, N, (sq, sk, sv), out_dtype=DT[out])
+    got = attn_fp8_cap(q8.to(DEV), k8.to(DEV), v8.to(DEV), cud, N, (sq, sk, sv), out_dtype=DT[out])
     torch.cuda.synchronize()
     u8 = lambda t: t.view(torch.uint8).numpy()  # noqa: E731
     ref = oracle.attention_fp8(u8(q8), u8(k8), u8(v8), (sq, sk, sv), cu)
@@ -127,7 +149,7 @@ def test_general_fp8_deit_shape_and_peaked():
     lengths = [39] * 32
     qp, kp, vp, cu, N, T = _packed_case(lengths, 12, 64, "bf16", seed=5, dist="peaked")
     (q8, sq), (k8, sk), (v8, sv) = (_quant_e4m3(t) for t in (qp, kp, vp))
-    got = rb.attn_fp8(q8.to(DEV), k8.to(DEV), v8.to(DEV), torch.from_numpy(cu.astype(np.int32)).to(DEV), 197,
+    got = attn_fp8_cap(q8.to(DEV), k8.to(DEV), v8.to(DEV), torch.from_numpy(cu.astype(np.int32)).to(DEV), 197,
                       (sq, sk, sv))
     torch.cuda.synchronize()
     u8 = lambda t: t.view(torch.uint8).numpy()  # noqa: E731
