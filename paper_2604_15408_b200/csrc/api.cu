@@ -177,7 +177,7 @@ ragged_status ragged_attn(const ragged_problem* prob, const void* qp, const void
     return e == cudaSuccess ? RAGGED_OK : cuda_fail(e, "ragged_attn/general");
   }
   cudaError_t e = ragged::launch_attn(prob->dtype, resolve_engine(prob), qp, kp, vp, cu_seqlens, op, prob->B, prob->N,
-                                      prob->H, prob->ld, as_stream(stream));
+                                      prob->H, prob->ld, as_stream(stream), prob->n_hint);
   return e == cudaSuccess ? RAGGED_OK : cuda_fail(e, "ragged_attn");
 }
 
@@ -228,7 +228,7 @@ ragged_status ragged_pack_attend_unpack(const ragged_problem* prob, const uint8_
   RAGGED_TRY(check_ptr(o, "o"));
   if ((long long)prob->B * prob->H + 1 > 0x7fffffffLL) return fail(RAGGED_ENOTSUP, "B*H too large");
   cudaError_t e = ragged::launch_fused(prob->dtype, resolve_engine(prob), keep, q, k, v, prob->ld, o, cu_seqlens_or_null,
-                                       prob->B, prob->N, prob->H, as_stream(stream));
+                                       prob->B, prob->N, prob->H, as_stream(stream), prob->n_hint);
   return e == cudaSuccess ? RAGGED_OK : cuda_fail(e, "ragged_pack_attend_unpack");
 }
 
@@ -609,7 +609,7 @@ ragged_status ragged_vit_block(const ragged_problem* prob, void* x, const int32_
   const int32_t rh = p.n_hint > 0 ? (int32_t)std::min<long long>((long long)p.B * p.n_hint, rows) : 0;
   RAGGED_TRY(linear_impl((ragged_dtype)p.dtype, rows, 3 * D, D, y, D, w->w_qkv, w->b_qkv, 0, nullptr, 0, qkv, 3 * D, live, st, rh));
   e = ragged::launch_attn(p.dtype, resolve_engine(&p), qkvb, qkvb + D * 2, qkvb + 2 * D * 2, cu_seqlens, a,
-                          p.B, p.N, p.H, 3LL * D, st);
+                          p.B, p.N, p.H, 3LL * D, st, p.n_hint);
   if (e != cudaSuccess) return cuda_fail(e, "ragged_vit_block/attn");
   RAGGED_TRY(linear_impl((ragged_dtype)p.dtype, rows, D, D, a, D, w->w_proj, w->b_proj, 2, x, D, x, D, live, st, rh));
   e = ragged::launch_layer_norm(p.dtype, x, D, w->ln2_w, w->ln2_b, 1e-6f, y, D, rows, live, D, st);

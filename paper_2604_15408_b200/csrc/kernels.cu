@@ -1117,9 +1117,14 @@ __global__ void __launch_bounds__(kAttnThreads, 3) attn_kernel(const AttnArgs a,
 #endif
   pdl_wait_prerequisites();
   int bid = blockIdx.x;
+  // Query split (small batches): gridDim.y CTAs share one (image, head); CTA
+  // qy owns the 16-row query slices 4 (qy + qs k) + warp.  Each stages the whole
+  // K/V of its problem; only qy == 0 writes the +0.0 rows and cu_seqlens.
+  const int qy = (int)blockIdx.y, qs = (int)gridDim.y;
   if constexpr (kFused) {
     if (a.cu_mode == 1) {
       if (bid < a.cu_groups) {  // scan CTAs: cu_seqlens only, concurrent with the rest
+        if (qy != 0) return;
         scan_group_cu(a, bid, sK, tid, [] { __syncthreads(); });
         if constexpr (kGather) {
           if (ga.state != nullptr) {
@@ -1150,7 +1155,7 @@ __global__ void __launch_bounds__(kAttnThreads, 3) attn_kernel(const AttnArgs a,
   //  (Measured and rejected: zeroing all of the head's padded rows here, kept
   //  rows overwritten later -- C3 6.8 -> 7.5 us: the 25 KB of stores per CTA
   //  queue ahead of the gathers; the dropped rows are zeroed during the compute.)
-  const bool cu_here = kFused && !kPrune && a.cu_mode == 2 && h == 0;
+  const bool cu_here = kFused && !kPrune && a.cu_mode == 2 && h == 0 && qy == 0;
   const uint8_t* keep_row = nullptr;
   if constexpr (kPrune) keep_row = prune_l2_row<T>(a, b, h, smem, tid);
   PrefixLoads pl;
@@ -1167,12 +1172,13 @@ __global__ void __launch_bounds__(kAttnThreads, 3) attn_kernel(const AttnArgs a,
   }, keep_row);
   if constexpr (kPrune) {
     // every image keeps exactly min(kkeep, N) tokens: cu_seqlens is b * that
-    if (a.cu_out != nullptr && h == 0 && tid == 0) {
+    if (a.cu_out != nullptr && h == 0 && qy == 0 && tid == 0) {
       const int kc = min(a.kkeep, a.N);
       a.cu_out[b] = b * kc;
       if (b == a.B - 1) a.cu_out[a.B] = a.B * kc;
     }
   }
+  if (qy > 0 && qy * 64 >= n) return;  // this split CTA owns no query slice (image_rows ended with a barrier)
   const char* img_q = reinterpret_cast<const char*>(gq) + row_base * ldb + h * kRowBytes;
   const char* img_k = reinterpret_cast<const char*>(gk) + row_base * ldb + h * kRowBytes;
   const char* img_v = reinterpret_cast<const char*>(gv) + row_base * ldb + h * kRowBytes;
@@ -1181,7 +1187,7 @@ __global__ void __launch_bounds__(kAttnThreads, 3) attn_kernel(const AttnArgs a,
   const long long o_off = kGather ? row_base * HDb + h * kRowBytes + (tid & 7) * 16 : 0;
   const long long cls_off = kGather ? (long long)b * HDb + h * kRowBytes + (tid & 7) * 16 : 0;
   if constexpr (kGather && kFused) {  // a dropped CLS token still owns a (+0) CLS row
-    if (tid < 8 && n < a.N && sDrop[0] == 0) {
+    if (qy == 0 && tid < 8 && n < a.N && sDrop[0] == 0) {
 #pragma unroll
       for (int d = 0; d < kMaxPeers; ++d)
         if (d < ga.world && ga.cls[d] != nullptr) st_global_16(ga.cls[d] + cls_off, make_uint4(0, 0, 0, 0));
@@ -1217,7 +1223,7 @@ __global__ void __launch_bounds__(kAttnThreads, 3) attn_kernel(const AttnArgs a,
                   valid ? 16 : 0);
     }
   };
-  if (warp * 16 < n) load_q(qwarp, warp);
+  if ((4 * qy + warp) * 16 < n) load_q(qwarp, 4 * qy + warp);
   cp_async_commit();
 
   TL(2);
@@ -1236,27 +1242,27 @@ __global__ void __launch_bounds__(kAttnThreads, 3) attn_kernel(const AttnArgs a,
   // others' compute; if every warp has a slice, after the compute.  Keeping
   // these stores out of the gather phase leaves the SM->L2 path to the gathers.
   const int nsl = (n + 15) >> 4;
-  const int busy = nsl < 4 ? nsl : 4;  // warps [0, busy) own slices
+  const int busy = min(4, max(0, nsl - 4 * qy));  // warps [0, busy) own slices (first group)
   auto zero_dropped = [&](int t, int nthr) {
 #ifndef RAGGED_ABLATE_ZERO
     if constexpr (kFused && kGather) gather_zero_rows(ga, o_off, sDrop, t >> 3, a.N - n, nthr >> 3, HDb);
     else if constexpr (kFused) zero_rows(img_o, sDrop, t >> 3, a.N - n, nthr >> 3, HDb);
 #endif
   };
-  if (busy < 4 && warp >= busy) zero_dropped(tid - busy * 32, (4 - busy) * 32);
+  if (qy == 0 && busy < 4 && warp >= busy) zero_dropped(tid - busy * 32, (4 - busy) * 32);
 
   // ---- per-warp query slices: S = Q K^T, online softmax (Alg. 1), O += P V
   const int g = lane >> 2, t4 = lane & 3;
   constexpr float kScaleLog2 = 0.18033688011112042f;  // log2(e) / sqrt(64)
   int buf = 0;
-  for (int slice = warp; slice * 16 < n; slice += 4) {
+  for (int slice = 4 * qy + warp; slice * 16 < n; slice += 4 * qs) {
     uint8_t* qcur = qwarp + buf * kQBufBytes;
     uint32_t qf[4][4];
 #pragma unroll
     for (int kk = 0; kk < 4; ++kk)
       ldmatrix_x4(smem_u32(qcur + swz(lane & 15, 2 * kk + (lane >> 4))), qf[kk][0], qf[kk][1],
                   qf[kk][2], qf[kk][3]);
-    if ((slice + 4) * 16 < n) load_q(qwarp + (buf ^ 1) * kQBufBytes, slice + 4);
+    if ((slice + 4 * qs) * 16 < n) load_q(qwarp + (buf ^ 1) * kQBufBytes, slice + 4 * qs);
     cp_async_commit();
 
     float o[8][4];
@@ -1436,7 +1442,7 @@ __global__ void __launch_bounds__(kAttnThreads, 3) attn_kernel(const AttnArgs a,
     __syncwarp();
     buf ^= 1;
   }
-  if (busy == 4) zero_dropped(tid, kAttnThreads);
+  if (qy == 0 && busy == 4) zero_dropped(tid, kAttnThreads);
   if constexpr (kGather) {
     if (ga.state != nullptr) {
       __syncthreads();
@@ -1560,12 +1566,32 @@ static cudaError_t smem_attr_once(Kern kern, int max_bytes, bool (&done)[64]) {
 
 template <typename T, bool kFused, bool kGather = false, bool kLargeN = false>
 static cudaError_t launch_attn_mma(const AttnArgs& a, int grid, cudaStream_t st,
-                                   const GatherArgs& g = GatherArgs{}) {
+                                   const GatherArgs& g = GatherArgs{}, int qsplit = 1) {
   static bool done[64] = {false};
   cudaError_t e = smem_attr_once(attn_kernel<T, kFused, kGather, kLargeN>, attn_smem_bytes(kMaxN), done);
   if (e != cudaSuccess) return e;
-  return launch_pdl(attn_kernel<T, kFused, kGather, kLargeN>, dim3(grid), dim3(kAttnThreads),
+  return launch_pdl(attn_kernel<T, kFused, kGather, kLargeN>, dim3(grid, qsplit), dim3(kAttnThreads),
                     attn_smem_bytes(a.N), st, a, g);
+}
+
+// Query split for small batches (the mma.sync engine): when the B*H problems
+// fill less than two CTAs per SM, split each problem's query slices over up to
+// ceil(rows / 64) CTAs (64 = 4 warps x 16 rows), rows = the expected kept
+// tokens (n_hint, else N).  Measured need: at BS = 4 / 16, p = 0 one CTA per
+// (image, head) ran 13 slices on 4 warps while 100+ SMs idled (N3 grid).
+static int attn_qsplit(int problems, int N, int n_hint) {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  static int cached[64] = {0};
+  if (dev >= 0 && dev < 64) {
+    if (cached[dev] == 0) cudaDeviceGetAttribute(&cached[dev], cudaDevAttrMultiProcessorCount, dev);
+    sms = cached[dev];
+  }
+  const int rows = n_hint > 0 ? (n_hint < N ? n_hint : N) : N;
+  const int want = (2 * sms + problems - 1) / (problems > 0 ? problems : 1);
+  const int maxs = (rows + 63) / 64;
+  int qs = want < maxs ? want : maxs;
+  return qs < 1 ? 1 : qs;
 }
 
 // N2 fused ahead of the scan: one cluster of H CTAs per image (H <= 16).
@@ -1635,19 +1661,21 @@ static cudaError_t launch_attn_tc(const AttnArgs& a, int nwork, cudaStream_t st)
 }
 
 template <bool kFused>
-static cudaError_t dispatch_attn(int dtype, int engine, const AttnArgs& a, int nwork, cudaStream_t st) {
+static cudaError_t dispatch_attn(int dtype, int engine, const AttnArgs& a, int nwork, cudaStream_t st,
+                                 int qsplit = 1) {
   if (engine == 2)
     return dtype == 0 ? launch_attn_tc<__nv_bfloat16, kFused>(a, nwork, st)
                       : launch_attn_tc<__half, kFused>(a, nwork, st);
   if (engine == kEngineMmaLong)
-    return dtype == 0 ? launch_attn_mma<__nv_bfloat16, kFused, false, true>(a, nwork, st)
-                      : launch_attn_mma<__half, kFused, false, true>(a, nwork, st);
-  return dtype == 0 ? launch_attn_mma<__nv_bfloat16, kFused>(a, nwork, st)
-                    : launch_attn_mma<__half, kFused>(a, nwork, st);
+    return dtype == 0 ? launch_attn_mma<__nv_bfloat16, kFused, false, true>(a, nwork, st, GatherArgs{}, qsplit)
+                      : launch_attn_mma<__half, kFused, false, true>(a, nwork, st, GatherArgs{}, qsplit);
+  return dtype == 0 ? launch_attn_mma<__nv_bfloat16, kFused>(a, nwork, st, GatherArgs{}, qsplit)
+                    : launch_attn_mma<__half, kFused>(a, nwork, st, GatherArgs{}, qsplit);
 }
 
 cudaError_t launch_attn(int dtype, int engine, const void* qp, const void* kp, const void* vp,
-                        const int32_t* cu, void* op, int B, int N, int H, long long ld, cudaStream_t st) {
+                        const int32_t* cu, void* op, int B, int N, int H, long long ld, cudaStream_t st,
+                        int n_hint) {
   AttnArgs a{};
   a.q = qp;
   a.k = kp;
@@ -1658,12 +1686,12 @@ cudaError_t launch_attn(int dtype, int engine, const void* qp, const void* kp, c
   a.N = N;
   a.H = H;
   a.ld = ld;
-  return dispatch_attn<false>(dtype, engine, a, B * H, st);
+  return dispatch_attn<false>(dtype, engine, a, B * H, st, engine == 2 ? 1 : attn_qsplit(B * H, N, n_hint));
 }
 
 cudaError_t launch_fused(int dtype, int engine, const uint8_t* keep, const void* q, const void* k,
                          const void* v, long long ld, void* o, int32_t* cu_out, int B, int N, int H,
-                         cudaStream_t st) {
+                         cudaStream_t st, int n_hint) {
   AttnArgs a{};
   a.keep = keep;
   a.q = q;
@@ -1682,7 +1710,8 @@ cudaError_t launch_fused(int dtype, int engine, const uint8_t* keep, const void*
   a.N = N;
   a.H = H;
   a.ld = ld;
-  return dispatch_attn<true>(dtype, engine, a, B * H + a.cu_groups, st);
+  return dispatch_attn<true>(dtype, engine, a, B * H + a.cu_groups, st,
+                            engine == 2 ? 1 : attn_qsplit(B * H, N, n_hint));
 }
 
 // Fused pack-attend-unpack whose padded output (and/or CLS rows) is written to

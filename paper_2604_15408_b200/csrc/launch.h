@@ -18,12 +18,12 @@ cudaError_t launch_scan_pack(const uint8_t* keep, const void* q, const void* k, 
 // kEngineMmaLong = mma.sync with the long-sequence chunk loop (n_hint > 64)
 constexpr int kEngineMmaLong = 16;
 cudaError_t launch_attn(int dtype, int engine, const void* qp, const void* kp, const void* vp, const int32_t* cu,
-                        void* op, int B, int N, int H, long long ld, cudaStream_t st);
+                        void* op, int B, int N, int H, long long ld, cudaStream_t st, int n_hint = 0);
 cudaError_t launch_unpack(const void* op, const int32_t* dst, void* o, int B, int N, int H,
                           cudaStream_t st);
 cudaError_t launch_fused(int dtype, int engine, const uint8_t* keep, const void* q, const void* k,
                          const void* v, long long ld, void* o, int32_t* cu_out, int B, int N, int H,
-                         cudaStream_t st);
+                         cudaStream_t st, int n_hint = 0);
 // Fused compute + all-gather over peer memory: every output
 // row goes to up to kMaxPeers destinations (device pointers, peer-mapped for
 // other ranks), then the last CTA of the grid signals every rank and waits

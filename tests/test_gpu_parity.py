@@ -514,3 +514,32 @@ def test_mask_rewritten_by_previous_kernel(n_hint):
     torch.cuda.synchronize()
     for i, o in enumerate(outs):
         assert np.array_equal(bits(o), bits(ref[i % 2])), f"call {i}"
+
+
+@pytest.mark.parametrize("n_hint", [0, 39, 197])
+def test_query_split_small_batch_bitwise_equals_unsplit(n_hint):
+    """Small batches split each (image, head) problem's query slices over
+    several CTAs (mma.sync engine, attn_qsplit): the output must be bitwise the
+    one computed with one CTA per problem (the same images inside a batch large
+    enough not to split), for the fused path and ragged_attn, with cu_seqlens."""
+    B, N, H = 2, 197, 3
+    q, k, v, keep = synth.make_inputs(B, N, H, 0.0, "random", "bf16", seed=77)
+    keep = keep.clone()
+    keep[1, 150:] = 0                              # ragged: 197 and 150 tokens
+    big = 120                                      # B * H = 360 >= 2 * #SMs: no split
+    rep = lambda t: torch.cat([t] * (big // B)).contiguous()  # noqa: E731
+    qd, kd, vd, kp = _dev(q, k, v, keep)
+    Qd, Kd, Vd, Kp = _dev(rep(q), rep(k), rep(v), rep(keep))
+    o_small, cu_small = rb.pack_attend_unpack(qd, kd, vd, kp, want_cu=True, n_hint=n_hint)
+    o_big = rb.pack_attend_unpack(Qd, Kd, Vd, Kp, n_hint=n_hint)
+    torch.cuda.synchronize()
+    assert np.array_equal(bits(o_small), bits(o_big[:B]))
+    assert cu_small.cpu().tolist() == [0, 197, 347]
+    ref, _ = oracle.pack_attend_unpack(q, k, v, keep.numpy())
+    check_attention(to_np(o_small), ref, torch.bfloat16)
+    qp, kpk, vp, cu, _, _ = rb.pack(qd, kd, vd, kp)
+    Qp, Kpk, Vp, CU, _, _ = rb.pack(Qd, Kd, Vd, Kp)
+    a_small = rb.attn(qp, kpk, vp, cu, N, n_hint=n_hint)
+    a_big = rb.attn(Qp, Kpk, Vp, CU, N, n_hint=n_hint)
+    torch.cuda.synchronize()
+    assert np.array_equal(bits(a_small[:347]), bits(a_big[:347]))
