@@ -97,6 +97,22 @@ RAGGED_API ragged_status ragged_vit_pipeline_graph_create(const ragged_problem* 
                                                           void* workspace, int64_t ws_bytes,
                                                           ragged_graph** out);
 
+/* The prune point of the pipeline: pack the hidden
+ * state x [B, N, D] (D = prob->H * 64, token stride prob->ld elements, dtype
+ * prob->dtype) ONCE into packed rows xp [B*N capacity, D] (row stride D) by
+ * the keep mask, writing cu_seqlens [B+1], dst_index [B*N] and src_index
+ * [B*N] exactly as ragged_scan.  One launch for B*N <= 65536 (one CTA per
+ * (image, 64-column slice)); else two.  Errors as ragged_pack. */
+RAGGED_API ragged_status ragged_pack_rows(const ragged_problem* prob, const uint8_t* keep, const void* x,
+                                          int32_t* cu_seqlens, int32_t* dst_index, int32_t* src_index,
+                                          void* xp, void* stream);
+
+/* CLS readout from packed rows ("CLS token read from packed buffer at
+ * cu_seqlens[b]"): out[b, :] = xp[cu[b], :] (D = prob->H * 64 columns, row
+ * stride D) if image b has a kept row, else +0.0.  One launch. */
+RAGGED_API ragged_status ragged_cls_rows(const ragged_problem* prob, const void* xp, const int32_t* cu_seqlens,
+                                         void* out, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

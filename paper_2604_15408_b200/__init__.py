@@ -115,6 +115,8 @@ def _load() -> ctypes.CDLL:
         "ragged_layer_norm": [I32, I32, I32, V, I64, V, V, ctypes.c_float, V, I64, V, V],
         "ragged_linear": [I32, I32, I32, I32, V, I64, V, V, I32, V, I64, V, I64, V, V],
         "ragged_vit_block": [P, V, V, ctypes.POINTER(VitWeights), V, I64, V],
+        "ragged_pack_rows": [P, V, V, V, V, V, V, V],
+        "ragged_cls_rows": [P, V, V, V, V],
         "ragged_vit_pipeline_graph_create": [P, V, V, ctypes.POINTER(VitWeights), I32, V, I64, ctypes.POINTER(V)],
     }
     for name, args in sigs.items():
@@ -142,6 +144,7 @@ EXPORTS = ("ragged_scan", "ragged_pack", "ragged_attn", "ragged_unpack", "ragged
            "ragged_validate_cu_seqlens", "ragged_status_str", "ragged_last_error", "ragged_build_info",
            "ragged_keep_topk_l2", "ragged_keep_evit", "ragged_prune_l2_pack_attend_unpack", "ragged_pack_attend_unpack_gather", "ragged_attn_gather",
            "ragged_layer_norm", "ragged_linear", "ragged_vit_block_workspace", "ragged_vit_block",
+           "ragged_pack_rows", "ragged_cls_rows",
            "ragged_vit_pipeline_graph_create")
 
 
@@ -468,6 +471,90 @@ class VitBlock:
         _check(lib().ragged_vit_block(ctypes.byref(self.p), x.data_ptr(), cu.data_ptr(), ctypes.byref(self.w),
                                      self.ws.data_ptr(), self.ws.numel(), _stream(stream)), "ragged_vit_block")
         return x
+
+
+def pack_rows(x, keep, xp=None, cu=None, dst=None, src=None, stream=None):
+    """N1 prune point: hidden state x [B, N, D] (D = H*64, unit
+    feature stride) -> packed rows xp [B*N, D] + cu [B+1], dst, src."""
+    if x.dim() != 3 or x.stride(2) != 1 or x.dtype not in _DTYPE or x.shape[2] % 64 != 0:
+        raise ValueError("x must be [B, N, D] bf16/fp16 with D % 64 == 0 and unit feature stride")
+    B, N, D = x.shape
+    if x.stride(0) != N * x.stride(1):
+        raise ValueError("x tokens must be evenly strided")
+    keep = _keep_u8(keep, B, N, x.device)
+    xp = torch.empty(B * N, D, dtype=x.dtype, device=x.device) if xp is None else xp
+    _require(xp, "xp", x.dtype, x.device, numel=B * N * D)
+    cu = torch.empty(B + 1, dtype=torch.int32, device=x.device) if cu is None else cu
+    dst = torch.empty(B * N, dtype=torch.int32, device=x.device) if dst is None else dst
+    src = torch.empty(B * N, dtype=torch.int32, device=x.device) if src is None else src
+    for t, nm, n in ((cu, "cu", B + 1), (dst, "dst", B * N), (src, "src", B * N)):
+        _require(t, nm, torch.int32, x.device, n)
+    p = problem(B, N, D // 64, 64, x.dtype, x.stride(1))
+    _check(lib().ragged_pack_rows(ctypes.byref(p), keep.data_ptr(), x.data_ptr(), cu.data_ptr(), dst.data_ptr(),
+                                  src.data_ptr(), xp.data_ptr(), _stream(stream)), "ragged_pack_rows")
+    return xp, cu, dst, src
+
+
+def cls_rows(xp, cu, N: int, out=None, stream=None):
+    """CLS readout: out[b] = xp[cu[b]] (+0.0 for an empty image)."""
+    if xp.dim() != 2 or not xp.is_contiguous() or xp.dtype not in _DTYPE or xp.shape[1] % 64 != 0:
+        raise ValueError("xp must be a contiguous [rows, D] bf16/fp16 tensor, D % 64 == 0")
+    _require(cu, "cu", torch.int32, xp.device)
+    B, D = cu.numel() - 1, xp.shape[1]
+    if xp.shape[0] < B * N:
+        raise ValueError("xp must hold the B*N-row capacity")
+    out = torch.empty(B, D, dtype=xp.dtype, device=xp.device) if out is None else out
+    _require(out, "out", xp.dtype, xp.device, shape=(B, D))
+    p = problem(B, N, D // 64, 64, xp.dtype)
+    _check(lib().ragged_cls_rows(ctypes.byref(p), xp.data_ptr(), cu.data_ptr(), out.data_ptr(), _stream(stream)),
+           "ragged_cls_rows")
+    return out
+
+
+class VitPrunedForward:
+    """The paper's pruned DeiT forward (§4.4 steps 1-5) as a sequence
+    of library calls (plumbing only: every step is a libragged kernel, all
+    PDL-chained on one stream, capturable in one CUDA graph):
+      1. layers [0, prune_at): dense blocks on all B*N rows (ragged_vit_block with
+         the all-kept cu_seqlens b*N -- packed == padded);
+      2. Threshold-l2 keep mask of the hidden state (ragged_keep_topk_l2, k kept);
+      3. pack the hidden state once (ragged_pack_rows);
+      4. layers [prune_at, L): packed blocks (ragged_vit_block on cu);
+      5. CLS rows from the packed buffer (ragged_cls_rows).
+    Buffers are allocated once; __call__(x) copies the input [B, N, D] into the
+    padded buffer and returns the CLS rows [B, D]."""
+
+    def __init__(self, layer_params, B: int, N: int, H: int, k_keep: int, prune_at: int = 4,
+                 dtype=torch.bfloat16):
+        dev = layer_params[0]["w_qkv"].device
+        D = H * 64
+        self.B, self.N, self.H, self.D, self.k, self.prune_at = B, N, H, D, int(k_keep), prune_at
+        self.dense = [VitBlock(p, B, N, H, dtype, n_hint=N) for p in layer_params[:prune_at]]
+        self.packed = [VitBlock(p, B, N, H, dtype, n_hint=min(k_keep, N)) for p in layer_params[prune_at:]]
+        self.x = torch.empty(B * N, D, dtype=dtype, device=dev)
+        self.xp = torch.empty(B * N, D, dtype=dtype, device=dev)
+        self.cu_all = (torch.arange(B + 1, dtype=torch.int32, device=dev) * N).contiguous()
+        self.keep = torch.empty(B, N, dtype=torch.uint8, device=dev)
+        self.cu = torch.empty(B + 1, dtype=torch.int32, device=dev)
+        self.dst = torch.empty(B * N, dtype=torch.int32, device=dev)
+        self.src = torch.empty(B * N, dtype=torch.int32, device=dev)
+        self.cls = torch.empty(B, D, dtype=dtype, device=dev)
+
+    def run(self, stream=None):
+        """Steps 1-5 on the resident input self.x (no host sync)."""
+        for blk in self.dense:
+            blk(self.x, self.cu_all, stream)
+        x3 = self.x.view(self.B, self.N, self.D)
+        keep_topk_l2(x3, self.k, keep=self.keep, stream=stream)
+        pack_rows(x3, self.keep, xp=self.xp, cu=self.cu, dst=self.dst, src=self.src, stream=stream)
+        for blk in self.packed:
+            blk(self.xp, self.cu, stream)
+        cls_rows(self.xp, self.cu, self.N, out=self.cls, stream=stream)
+        return self.cls
+
+    def __call__(self, x, stream=None):
+        self.x.view(self.B, self.N, self.D).copy_(x, non_blocking=True)
+        return self.run(stream)
 
 
 class VitPipelineGraph:

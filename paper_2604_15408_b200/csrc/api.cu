@@ -572,6 +572,32 @@ int64_t ragged_vit_block_workspace(const ragged_problem* prob, int32_t mlp) {
   return rows * (5 * D + mlp) * 2;
 }
 
+ragged_status ragged_pack_rows(const ragged_problem* prob, const uint8_t* keep, const void* x, int32_t* cu_seqlens,
+                               int32_t* dst_index, int32_t* src_index, void* xp, void* stream) {
+  RAGGED_TRY(check_problem(prob));
+  if (prob->B == 0) return RAGGED_OK;
+  RAGGED_TRY(check_ptr_any(keep, "keep"));
+  RAGGED_TRY(check_ptr(x, "x"));
+  RAGGED_TRY(check_ptr_any(cu_seqlens, "cu_seqlens"));
+  RAGGED_TRY(check_ptr_any(dst_index, "dst_index"));
+  RAGGED_TRY(check_ptr_any(src_index, "src_index"));
+  RAGGED_TRY(check_ptr(xp, "xp"));
+  cudaError_t e = ragged::launch_pack_rows(keep, x, prob->ld, prob->B, prob->N, prob->H, cu_seqlens, dst_index,
+                                           src_index, xp, as_stream(stream));
+  return e == cudaSuccess ? RAGGED_OK : cuda_fail(e, "ragged_pack_rows");
+}
+
+ragged_status ragged_cls_rows(const ragged_problem* prob, const void* xp, const int32_t* cu_seqlens, void* out,
+                              void* stream) {
+  RAGGED_TRY(check_problem(prob));
+  if (prob->B == 0) return RAGGED_OK;
+  RAGGED_TRY(check_ptr(xp, "xp"));
+  RAGGED_TRY(check_ptr_any(cu_seqlens, "cu_seqlens"));
+  RAGGED_TRY(check_ptr(out, "out"));
+  cudaError_t e = ragged::launch_cls_rows(xp, cu_seqlens, prob->B, prob->H * prob->d, out, as_stream(stream));
+  return e == cudaSuccess ? RAGGED_OK : cuda_fail(e, "ragged_cls_rows");
+}
+
 ragged_status ragged_vit_block(const ragged_problem* prob, void* x, const int32_t* cu_seqlens,
                                const ragged_vit_weights* w, void* workspace, int64_t ws_bytes, void* stream) {
   if (prob == nullptr) return fail(RAGGED_EINVAL, "problem is NULL");

@@ -602,7 +602,9 @@ __device__ __forceinline__ void scan_group_cu(const AttnArgs& a, int g, uint8_t*
 // would grow with B).
 constexpr int kImgThreads = 128;
 
-template <bool kPack>
+// kOne: pack a single tensor (q -> qp; k, v, kp, vp unused) -- the hidden
+// state x at the prune point (pack [B, S, D] once).
+template <bool kPack, bool kOne = false>
 __global__ void __launch_bounds__(kImgThreads)
     image_scan_kernel(const uint8_t* __restrict__ keep, int B, int N, int H, int32_t* __restrict__ cu,
                       int32_t* __restrict__ dst, int32_t* __restrict__ src, const uint8_t* __restrict__ q,
@@ -625,13 +627,13 @@ __global__ void __launch_bounds__(kImgThreads)
       const long long o1 = ((long long)sb * N + s1) * ld_bytes + sh * kRowBytes;
       if (m0 != 0) {
         prefetch_l2(q + o0);
-        prefetch_l2(k + o0);
-        prefetch_l2(v + o0);
+        if (!kOne) prefetch_l2(k + o0);
+        if (!kOne) prefetch_l2(v + o0);
       }
       if (m1 != 0) {
         prefetch_l2(q + o1);
-        prefetch_l2(k + o1);
-        prefetch_l2(v + o1);
+        if (!kOne) prefetch_l2(k + o1);
+        if (!kOne) prefetch_l2(v + o1);
       }
     } else if (threadIdx.x * 128 < N) {
       prefetch_l2(skm + threadIdx.x * 128);
@@ -703,8 +705,8 @@ __global__ void __launch_bounds__(kImgThreads)
         if (ru < n) {
           const long long so = soff + sPos[ru] * ld_bytes;
           vq[u] = ld_global_nc_16(q + so);
-          vk[u] = ld_global_nc_16(k + so);
-          vv[u] = ld_global_nc_16(v + so);
+          if (!kOne) vk[u] = ld_global_nc_16(k + so);
+          if (!kOne) vv[u] = ld_global_nc_16(v + so);
         }
       }
 #pragma unroll
@@ -713,8 +715,8 @@ __global__ void __launch_bounds__(kImgThreads)
         if (ru < n) {
           const long long d = doff + ru * row_bytes;
           st_global_16(qp + d, vq[u]);
-          st_global_16(kp + d, vk[u]);
-          st_global_16(vp + d, vv[u]);
+          if (!kOne) st_global_16(kp + d, vk[u]);
+          if (!kOne) st_global_16(vp + d, vv[u]);
         }
       }
     }
@@ -1761,6 +1763,40 @@ cudaError_t launch_attn_gather(int dtype, int engine, const void* qp, const void
                     : launch_attn_mma<__half, false, true>(a, B * H, st, g);
 }
 
+
+// One tensor x [B, N, H*64] (token stride ld) -> packed rows xp [B*N cap, H*64]
+// + cu / dst / src (a1 + a2 for the hidden state).
+cudaError_t launch_pack_rows(const uint8_t* keep, const void* x, long long ld_elems, int B, int N, int H,
+                             int32_t* cu, int32_t* dst, int32_t* src, void* xp, cudaStream_t st) {
+  if ((long long)B * N <= kImageScanMaxBN && (long long)B * H <= 0x7fffffffLL)
+    return launch_pdl(image_scan_kernel<true, true>, dim3(B * H), dim3(kImgThreads), 0, st, keep, B, N, H, cu, dst,
+                      src, static_cast<const uint8_t*>(x), (const uint8_t*)nullptr, (const uint8_t*)nullptr,
+                      ld_elems * 2, static_cast<uint8_t*>(xp), (uint8_t*)nullptr, (uint8_t*)nullptr);
+  // large batches: the three-tensor path with the same source / destination
+  return launch_scan_pack(keep, x, x, x, ld_elems, B, N, H, cu, dst, src, xp, xp, xp, st);
+}
+
+// CLS readout from packed rows: out[b] = xp[cu[b]] if image b kept any
+// token (its CLS token when CLS is kept, R6), else +0.0.  One warp per image,
+// 16-byte copies.
+__global__ void cls_rows_kernel(const uint8_t* __restrict__ xp, const int32_t* __restrict__ cu, int B,
+                                int row_bytes, uint8_t* __restrict__ out) {
+  pdl_launch_dependents();
+  pdl_wait_prerequisites();
+  const int b = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (b >= B) return;
+  const int s = cu[b], e = cu[b + 1];
+  for (int c = lane * 16; c < row_bytes; c += 32 * 16) {
+    const uint4 v = e > s ? ld_global_nc_16(xp + (long long)s * row_bytes + c) : make_uint4(0, 0, 0, 0);
+    st_global_16(out + (long long)b * row_bytes + c, v);
+  }
+}
+
+cudaError_t launch_cls_rows(const void* xp, const int32_t* cu, int B, int D, void* out, cudaStream_t st) {
+  const int wpb = 8;
+  return launch_pdl(cls_rows_kernel, dim3((B + wpb - 1) / wpb), dim3(32 * wpb), 0, st,
+                    static_cast<const uint8_t*>(xp), cu, B, D * 2, static_cast<uint8_t*>(out));
+}
 
 cudaError_t launch_empty(int grid, int block, cudaStream_t st) {
   empty_kernel<<<grid, block, 0, st>>>();

@@ -43,6 +43,10 @@ cudaError_t launch_attn_gather(int dtype, int engine, const void* qp, const void
                                const int32_t* cu, int B, int N, int H, long long ld,
                                const GatherArgs& g, cudaStream_t st);
 cudaError_t launch_empty(int grid, int block, cudaStream_t st);
+// N1 pipeline pieces: pack the hidden state (one tensor) and read CLS rows from packed rows
+cudaError_t launch_pack_rows(const uint8_t* keep, const void* x, long long ld_elems, int B, int N, int H,
+                             int32_t* cu, int32_t* dst, int32_t* src, void* xp, cudaStream_t st);
+cudaError_t launch_cls_rows(const void* xp, const int32_t* cu, int B, int D, void* out, cudaStream_t st);
 // N2 fused ahead of the scan: Threshold-l2 keep row computed inside the fused
 // pack-attend-unpack kernel (one cluster of H CTAs per image, H <= 16)
 cudaError_t launch_prune_l2_fused(int dtype, int engine, const void* x, long long ldx, int kkeep, const void* q,
