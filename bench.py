@@ -330,8 +330,9 @@ def main():
 
     # the four exchange variants, after the headline (never part of it)
     gv = None
-    impls = {"auto": ["nccl"] if ws > 1 else ["peer"], "none": [], "nccl": ["nccl"] if ws > 1 else [],
-             "all": (["nccl", "peer"] if ws > 1 else ["peer"])}[args.gather_variants]
+    impls = {"auto": ["nccl", "lib_nccl"] if ws > 1 else ["peer", "lib_nccl"], "none": [],
+             "nccl": ["nccl", "lib_nccl"] if ws > 1 else ["lib_nccl"],
+             "all": (["nccl", "lib_nccl", "peer"] if ws > 1 else ["peer", "lib_nccl"])}[args.gather_variants]
     if impls:
         try:
             gv = gather_variants(rb, torch, dev, sets, ws, rank, B, N, H, T, impls)
@@ -690,6 +691,30 @@ def gather_variants(rb, torch, dev, sets, ws, rank, B, N, H, T, impls, reps=200)
         res["padded_us"] = timed([lambda s=s: padded_step(s) for s in sets], graph=False)
         res["timing"] = "eager launches, CUDA events, max over ranks"
         out["nccl"] = res
+
+    if "lib_nccl" in impls:
+        # the library's own NCCL exchange (ragged_dist.h): the shard computed into
+        # its slot, then one in-place ncclAllGather -- both captured in the graph
+        res = {}
+        try:
+            from paper_2604_15408_b200.shard import broadcast_bytes
+            uid = rb.nccl_unique_id() if rank == 0 else None
+            if ws > 1:
+                uid = broadcast_bytes(uid, device=dev)
+            comm = rb.NcclComm(uid, ws, rank)
+            o_all = torch.empty(Bg, N, H, 64, dtype=dt, device=dev)
+            cls_all = torch.empty(Bg, HD, dtype=dt, device=dev)
+            rb.pack_attend_unpack_allgather(sets[0]["q"], sets[0]["k"], sets[0]["v"], sets[0]["keep"], comm, o_all)
+            torch.cuda.synchronize()
+            res["padded_us"] = timed([lambda s=s: rb.pack_attend_unpack_allgather(
+                s["q"], s["k"], s["v"], s["keep"], comm, o_all) for s in sets])
+            res["cls_us"] = timed([lambda s=s: rb.cls_allgather(s["q"], s["k"], s["v"], s["keep"], comm, cls_all)
+                                   for s in sets])
+            res["timing"] = "CUDA graph of K steps (kernel + ncclAllGather each), max over ranks"
+            comm.close()
+        except Exception as ex:
+            res["error"] = repr(ex)[:300]
+        out["lib_nccl"] = res
 
     if "peer" in impls:
         res = {}

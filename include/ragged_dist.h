@@ -84,6 +84,44 @@ RAGGED_API ragged_status ragged_attn_gather(const ragged_problem* prob, const vo
                                             const int32_t* cu_seqlens, const ragged_gather* g,
                                             void* stream);
 
+/* ---- NCCL exchange (the baseline of the fused peer-memory gather above) ----
+ * BASELINE.json north_star: "NCCL used only to all-gather outputs"; SURVEY
+ * §8(e).  The library loads NCCL at run time (dlopen libnccl.so.2: the copy
+ * already in the process, e.g. torch's, else the system one), so nothing here
+ * is a link-time dependency; without NCCL every call returns RAGGED_ENOTSUP.
+ * One communicator per rank (one process per GPU, ncclCommInitRank from an id
+ * the caller distributes) or per device of one process (ncclCommInitAll). */
+typedef struct ragged_nccl ragged_nccl;
+
+/* RAGGED_OK if NCCL can be loaded, else RAGGED_ENOTSUP. */
+RAGGED_API ragged_status ragged_dist_nccl_available(void);
+/* ncclGetUniqueId into id128 (128 bytes), to be shared with every rank. */
+RAGGED_API ragged_status ragged_dist_nccl_unique_id(uint8_t* id128);
+/* ncclCommInitRank on the current device.  Collective over the world ranks. */
+RAGGED_API ragged_status ragged_dist_nccl_init(const uint8_t* id128, int32_t world, int32_t rank,
+                                               ragged_nccl** out);
+/* ncclCommInitAll: one communicator per listed device (ndev <= 8), out[ndev]. */
+RAGGED_API ragged_status ragged_dist_nccl_init_all(int32_t ndev, const int32_t* devices, ragged_nccl** out);
+RAGGED_API void ragged_dist_nccl_destroy(ragged_nccl* comm);
+
+/* This rank's shard (prob->B images) of the fused pack-attend-unpack written
+ * straight into its slot of the gathered padded output o_all [world*B, N, H, d]
+ * (slot = rank*B images), then ONE in-place ncclAllGather of o_all (and, if
+ * cls_all != NULL, of the CLS rows cls_all [world*B, H*d], row b = O[b, 0]).
+ * Two stream-ordered operations, graph-capturable.  Every rank calls with the
+ * same B (equal counts).  Rows bitwise those of ragged_pack_attend_unpack. */
+RAGGED_API ragged_status ragged_dist_pack_attend_unpack_allgather(const ragged_problem* prob, const uint8_t* keep,
+                                                                  const void* q, const void* k, const void* v,
+                                                                  void* o_all, void* cls_all,
+                                                                  int32_t* cu_seqlens_or_null, ragged_nccl* comm,
+                                                                  void* stream);
+/* CLS-only exchange (the classifier input): the shard's padded O into
+ * o_local [B, N, H, d] (or NULL: not stored), its CLS rows into its slot of
+ * cls_all [world*B, H*d], then one in-place ncclAllGather of cls_all. */
+RAGGED_API ragged_status ragged_dist_cls_allgather(const ragged_problem* prob, const uint8_t* keep, const void* q,
+                                                   const void* k, const void* v, void* o_local, void* cls_all,
+                                                   int32_t* cu_seqlens_or_null, ragged_nccl* comm, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -116,6 +116,12 @@ def _load() -> ctypes.CDLL:
         "ragged_linear": [I32, I32, I32, I32, V, I64, V, V, I32, V, I64, V, I64, V, V],
         "ragged_vit_block": [P, V, V, ctypes.POINTER(VitWeights), V, I64, V],
         "ragged_pack_rows": [P, V, V, V, V, V, V, V],
+        "ragged_dist_nccl_available": [],
+        "ragged_dist_nccl_unique_id": [V],
+        "ragged_dist_nccl_init": [V, I32, I32, ctypes.POINTER(V)],
+        "ragged_dist_nccl_init_all": [I32, V, V],
+        "ragged_dist_pack_attend_unpack_allgather": [P, V, V, V, V, V, V, V, V, V],
+        "ragged_dist_cls_allgather": [P, V, V, V, V, V, V, V, V, V],
         "ragged_cls_rows": [P, V, V, V, V],
         "ragged_vit_pipeline_graph_create": [P, V, V, ctypes.POINTER(VitWeights), I32, V, I64, ctypes.POINTER(V)],
     }
@@ -127,6 +133,8 @@ def _load() -> ctypes.CDLL:
     lib.ragged_vit_block_workspace.restype = ctypes.c_int64
     lib.ragged_graph_destroy.argtypes = [V]
     lib.ragged_graph_destroy.restype = None
+    lib.ragged_dist_nccl_destroy.argtypes = [V]
+    lib.ragged_dist_nccl_destroy.restype = None
     lib.ragged_status_str.argtypes = [ctypes.c_int32]
     lib.ragged_status_str.restype = ctypes.c_char_p
     lib.ragged_last_error.argtypes = []
@@ -144,7 +152,9 @@ EXPORTS = ("ragged_scan", "ragged_pack", "ragged_attn", "ragged_unpack", "ragged
            "ragged_validate_cu_seqlens", "ragged_status_str", "ragged_last_error", "ragged_build_info",
            "ragged_keep_topk_l2", "ragged_keep_evit", "ragged_prune_l2_pack_attend_unpack", "ragged_pack_attend_unpack_gather", "ragged_attn_gather",
            "ragged_layer_norm", "ragged_linear", "ragged_vit_block_workspace", "ragged_vit_block",
-           "ragged_pack_rows", "ragged_cls_rows",
+           "ragged_pack_rows", "ragged_cls_rows", "ragged_dist_nccl_available", "ragged_dist_nccl_unique_id",
+           "ragged_dist_nccl_init", "ragged_dist_nccl_init_all", "ragged_dist_nccl_destroy",
+           "ragged_dist_pack_attend_unpack_allgather", "ragged_dist_cls_allgather",
            "ragged_vit_pipeline_graph_create")
 
 
@@ -410,6 +420,76 @@ def attn_gather(qp, kp, vp, cu, N: int, gather: Gather, stream=None, engine=ENGI
     _check(lib().ragged_attn_gather(ctypes.byref(p), qp.data_ptr(), kp.data_ptr(), vp.data_ptr(),
                                    cu.data_ptr(), ctypes.byref(gather), _stream(stream)),
            "ragged_attn_gather")
+
+
+# ---- §8(e) NCCL exchange inside the library (include/ragged_dist.h) ---------
+
+def nccl_available() -> bool:
+    return lib().ragged_dist_nccl_available() == OK
+
+
+def nccl_unique_id() -> bytes:
+    buf = (ctypes.c_uint8 * 128)()
+    _check(lib().ragged_dist_nccl_unique_id(buf), "ragged_dist_nccl_unique_id")
+    return bytes(buf)
+
+
+class NcclComm:
+    """One rank's ragged_nccl communicator (ncclCommInitRank on the current
+    device) from a 128-byte id shared by the caller (e.g. a torch.distributed
+    broadcast of nccl_unique_id() from rank 0)."""
+
+    def __init__(self, uid: bytes, world: int, rank: int):
+        if len(uid) != 128:
+            raise ValueError("unique id must be 128 bytes")
+        buf = (ctypes.c_uint8 * 128).from_buffer_copy(uid)
+        h = ctypes.c_void_p()
+        _check(lib().ragged_dist_nccl_init(buf, int(world), int(rank), ctypes.byref(h)), "ragged_dist_nccl_init")
+        self._h, self.world, self.rank = h, world, rank
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().ragged_dist_nccl_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def pack_attend_unpack_allgather(q, k, v, keep, comm: NcclComm, o_all, cls_all=None, cu=None, stream=None,
+                                 engine=ENGINE_AUTO, n_hint=0):
+    """This rank's shard -> its slot of o_all [world*B, N, H, d], then the
+    library's in-place ncclAllGather (and of cls_all [world*B, H*d] if given)."""
+    p = _padded_problem(q, k, v, engine, n_hint)
+    B, N, H, d = q.shape
+    keep = _keep_u8(keep, B, N, q.device)
+    _require(o_all, "o_all", q.dtype, q.device, shape=(comm.world * B, N, H, d))
+    if cls_all is not None:
+        _require(cls_all, "cls_all", q.dtype, q.device, shape=(comm.world * B, H * d))
+    if cu is not None:
+        _require(cu, "cu", torch.int32, q.device, B + 1)
+    _check(lib().ragged_dist_pack_attend_unpack_allgather(ctypes.byref(p), keep.data_ptr(), q.data_ptr(), k.data_ptr(),
+                                                          v.data_ptr(), o_all.data_ptr(), _ptr(cls_all), _ptr(cu),
+                                                          comm._h, _stream(stream)),
+           "ragged_dist_pack_attend_unpack_allgather")
+    return o_all
+
+
+def cls_allgather(q, k, v, keep, comm: NcclComm, cls_all, o_local=None, cu=None, stream=None, engine=ENGINE_AUTO,
+                  n_hint=0):
+    p = _padded_problem(q, k, v, engine, n_hint)
+    B, N, H, d = q.shape
+    keep = _keep_u8(keep, B, N, q.device)
+    _require(cls_all, "cls_all", q.dtype, q.device, shape=(comm.world * B, H * d))
+    if o_local is not None:
+        _require(o_local, "o_local", q.dtype, q.device, shape=(B, N, H, d))
+    _check(lib().ragged_dist_cls_allgather(ctypes.byref(p), keep.data_ptr(), q.data_ptr(), k.data_ptr(),
+                                           v.data_ptr(), _ptr(o_local), cls_all.data_ptr(), _ptr(cu), comm._h,
+                                           _stream(stream)), "ragged_dist_cls_allgather")
+    return cls_all
 
 
 # ---- NEXT row N1: packed ViT block (include/ragged_block.h) -----------------

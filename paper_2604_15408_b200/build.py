@@ -16,7 +16,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libragged.so")
-SOURCES = ["kernels.cu", "prune.cu", "block.cu", "attn_general.cu", "attn_fa.cu", "api.cu"]
+SOURCES = ["kernels.cu", "prune.cu", "block.cu", "attn_general.cu", "attn_fa.cu", "dist_nccl.cu", "api.cu"]
 HEADERS = ["device.cuh", "launch.h", "tcgen05.cuh", "attn_tc.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr", "-Xcompiler", "-fPIC",
@@ -86,7 +86,7 @@ def build(force: bool = False, verbose: bool = False, variant: str = "") -> str:
         if p.returncode != 0:
             raise RuntimeError("nvcc failed: " + " ".join(cmd))
     tmp = lib + ".tmp"
-    cmd = [nvcc(), *ARCH, "-shared", "-Xcompiler", "-fPIC", "-o", tmp, *objs]
+    cmd = [nvcc(), *ARCH, "-shared", "-Xcompiler", "-fPIC", "-o", tmp, *objs, "-ldl"]
     r = subprocess.run(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT)
     if r.returncode != 0:
         sys.stderr.write(r.stdout.decode(errors="replace"))

@@ -103,6 +103,12 @@ int resolve_engine(const ragged_problem* p) {
 
 }  // namespace
 
+namespace ragged {  // status plumbing for dist_nccl.cu
+ragged_status dist_fail(ragged_status s, const char* what) { return fail(s, what); }
+ragged_status dist_cuda_fail(cudaError_t e, const char* what) { return cuda_fail(e, what); }
+ragged_status dist_check_problem(const ragged_problem* p) { return check_problem(p); }
+}  // namespace ragged
+
 struct ragged_graph {
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t exec = nullptr;

@@ -46,3 +46,28 @@ def all_gather_images(local: torch.Tensor, B_global: int) -> torch.Tensor:
         off, cnt = shard(B_global, world, r)
         parts.append(out[r * per: r * per + cnt])
     return torch.cat(parts, 0)
+
+
+def weak_shard(B_per_rank: int, world: int, rank: int) -> tuple[int, int]:
+    """Weak scaling (bench.py): the global batch is world * B_per_rank images;
+    this rank's (first image, count) -- every rank holds B_per_rank images, so
+    the equal-count all-gathers of ragged_dist.h apply."""
+    return shard(world * B_per_rank, world, rank)
+
+
+def packed_capacity(T_local: int, device=None) -> int:
+    """Rows per rank slot of a packed all-gather: the largest rank's live row
+    count (ranks' T differ under data-dependent masks)."""
+    return int(max_over_ranks(float(T_local), device))
+
+
+def broadcast_bytes(data: bytes | None, nbytes: int = 128, src: int = 0, device=None) -> bytes:
+    """Broadcast an opaque byte string (e.g. the library's NCCL unique id,
+    ragged_dist_nccl_unique_id) from rank `src` to every rank."""
+    t = torch.zeros(nbytes, dtype=torch.uint8, device=device)
+    if dist.get_rank() == src:
+        if data is None or len(data) != nbytes:
+            raise ValueError("source rank must provide nbytes of data")
+        t.copy_(torch.frombuffer(bytearray(data), dtype=torch.uint8))
+    dist.broadcast(t, src)
+    return bytes(t.cpu().tolist())

@@ -251,3 +251,21 @@ def test_python_binding_checks_caller_buffers():
     for i, f in enumerate(bad):
         with pytest.raises(ValueError):
             f()
+
+
+def test_dist_nccl_entry_validation():
+    """NCCL entry points: NULL / range checks return synchronously; NCCL itself
+    is loaded at run time (available or RAGGED_ENOTSUP, never a crash)."""
+    import ctypes
+    lib = rb.lib()
+    assert lib.ragged_dist_nccl_available() in (rb.OK, rb.ENOTSUP)
+    assert lib.ragged_dist_nccl_unique_id(None) == rb.EINVAL
+    h = ctypes.c_void_p()
+    uid = (ctypes.c_uint8 * 128)()
+    assert lib.ragged_dist_nccl_init(None, 1, 0, ctypes.byref(h)) == rb.EINVAL
+    assert lib.ragged_dist_nccl_init(uid, 2, 2, ctypes.byref(h)) == rb.EINVAL
+    assert lib.ragged_dist_nccl_init_all(0, None, None) == rb.EINVAL
+    p = rb.problem(2, 197, 12)
+    assert lib.ragged_dist_pack_attend_unpack_allgather(ctypes.byref(p), None, None, None, None, None, None, None,
+                                                        None, None) == rb.EINVAL
+    lib.ragged_dist_nccl_destroy(None)

@@ -12,7 +12,8 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_2604_15408_b200.shard import all_gather_images, max_over_ranks, shard
+from paper_2604_15408_b200.shard import (all_gather_images, broadcast_bytes, max_over_ranks, packed_capacity, shard,
+                                        weak_shard)
 
 
 def test_shard_partition():
@@ -80,3 +81,67 @@ def test_two_rank_gather_equals_single_process(B):
     for rank, g, t in res:
         assert np.array_equal(g, ref)        # bitwise: same inputs, same arithmetic
         assert t == 2.0                      # max over ranks
+
+
+def _ragged(keep, off):
+    """Per-image token counts that differ across ranks: image g drops its last
+    g % 5 kept tokens (deterministic in the global image index)."""
+    keep = keep.clone()
+    for i in range(keep.shape[0]):
+        idx = torch.nonzero(keep[i]).flatten()
+        drop = (off + i) % 5
+        if drop:
+            keep[i, idx[-drop:]] = 0
+    return keep
+
+
+def _bench_entry(rank, world, port, Bper, out_q):
+    """bench.py's N > 1 bookkeeping on gloo: weak-scaling shards of the global
+    batch, per-rank inputs equal to the global slice, the packed all-gather
+    capacity (max T over ranks), the NCCL unique-id broadcast, max-over-ranks
+    timing and the all-gathered outputs of the per-rank compute."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import oracle
+    import synth
+    off, cnt = weak_shard(Bper, world, rank)
+    q, k, v, keep = synth.make_inputs(cnt, 33, 2, 0.5, "l2", "bf16", seed=5, image_offset=off)
+    keep = _ragged(keep, off)
+    T = int(keep.numpy().astype(bool).sum())
+    tcap = packed_capacity(T)
+    uid = broadcast_bytes(bytes(range(128)) if rank == 0 else None)
+    o, _ = oracle.pack_attend_unpack(q, k, v, keep.numpy())
+    g = all_gather_images(torch.from_numpy(o), world * Bper)
+    t = max_over_ranks(0.5 * (rank + 1))
+    dist.barrier()
+    dist.destroy_process_group()
+    out_q.put((rank, off, cnt, T, tcap, uid, g.numpy(), t))
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_bench_sharding_bookkeeping(world):
+    import oracle
+    import synth
+    Bper = 3
+    q, k, v, keep = synth.make_inputs(world * Bper, 33, 2, 0.5, "l2", "bf16", seed=5)
+    keep = _ragged(keep, 0)
+    ref, _ = oracle.pack_attend_unpack(q, k, v, keep.numpy())
+    ctx = mp.get_context("spawn")
+    out_q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_bench_entry, args=(r, world, port, Bper, out_q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(out_q.get(timeout=180) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    Ts = [r[3] for r in res]
+    kn = keep.numpy().astype(bool)
+    for rank, off, cnt, T, tcap, uid, g, t in res:
+        assert (off, cnt) == (rank * Bper, Bper)                      # weak scaling: equal shards
+        assert T == int(kn[off:off + cnt].sum())                      # data-dependent per-rank T
+        assert tcap == max(Ts)
+        assert uid == bytes(range(128))
+        assert np.array_equal(g, ref)
+        assert t == 0.5 * world

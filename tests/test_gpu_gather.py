@@ -196,3 +196,31 @@ def test_tcgen05_engine_rejected():
         rb.pack_attend_unpack_gather(q, k, v, keep, rb.gather_desc(1, 0, out=[o]),
                                      engine=rb.ENGINE_TCGEN05)
     assert e.value.status == rb.ENOTSUP
+
+
+def test_library_nccl_allgather_world1_bitwise():
+    """The library's NCCL exchange (ragged_dist.h, NCCL dlopen'ed at run time)
+    with a world-1 communicator: the shard's rows land in o_all / cls_all
+    bitwise equal to ragged_pack_attend_unpack's, and the call graph-captures."""
+    if not rb.nccl_available():
+        pytest.skip("NCCL not loadable")
+    B, N, H = 6, 197, 12
+    q, k, v, keep = _inputs(B, N, H, 0.7, seed=21)
+    keep[2, 0] = 0
+    ref = rb.pack_attend_unpack(q, k, v, keep)
+    comm = rb.NcclComm(rb.nccl_unique_id(), 1, 0)
+    o_all = _sentinel((B, N, H, 64), q.dtype)
+    cls_all = _sentinel((B, H * 64), q.dtype)
+    cu = torch.empty(B + 1, dtype=torch.int32, device=DEV)
+    rb.pack_attend_unpack_allgather(q, k, v, keep, comm, o_all, cls_all=cls_all, cu=cu)
+    torch.cuda.synchronize()
+    assert (bits(o_all) == bits(ref)).all()
+    assert (bits(cls_all) == bits(ref[:, 0].reshape(B, H * 64))).all()
+    cls2 = _sentinel((B, H * 64), q.dtype)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        rb.cls_allgather(q, k, v, keep, comm, cls2)
+    g.replay()
+    torch.cuda.synchronize()
+    assert (bits(cls2) == bits(cls_all)).all()
+    comm.close()
