@@ -418,10 +418,12 @@ def single_call_latency(torch, step, stream, reps=N_SETS):
 
 
 def traffic_from_profile():
-    """DRAM bytes (read + write) per launch of the fused kernel from the
-    committed ncu --set full summary (profiles/r01_ncu_fused_traffic.json,
-    written by scripts/ncu_traffic.py), or None."""
-    p = os.path.join(ROOT, "profiles", "r01", "r01_ncu_fused_traffic.json")
+    """DRAM bytes (read + write) per launch of the fused kernel, measured by ncu
+    over a WINDOW of 64 back-to-back launches with 16 rotating sets so the
+    padded-O write-back is counted (profiles/r02/r02_ncu_window_traffic.json,
+    scripts/r2/gpu_final.sh; a single-launch ncu --set full capture sees ~0
+    written bytes because the 9.7 MB of O stay in L2 until later launches)."""
+    p = os.path.join(ROOT, "profiles", "r02", "r02_ncu_window_traffic.json")
     try:
         return json.load(open(p))["dram_bytes_per_launch"]
     except Exception:
@@ -1066,12 +1068,20 @@ def n4_general_extras(rb, torch, dev, dt):
         lens = keep.sum(1).astype(np.int64)
         cu = torch.from_numpy(np.concatenate([[0], np.cumsum(lens)]).astype(np.int32)).to(dev)
         T = int(lens.sum())
-        qp, kp, vp = (t.reshape(B * N, H, d)[idx].contiguous().to(dev) for t in (q, k, v))
-        op = torch.empty_like(qp)
-        us = _graph_time(torch, [lambda: rb.attn(qp, kp, vp, cu, N, op=op)], 100)
+        def cap(t):   # packed rows in the B*N-row capacity the ABI takes (ragged_pack's layout)
+            out = torch.zeros(B * N, H, d, dtype=t.dtype)
+            out[:T] = t.reshape(B * N, H, d)[idx]
+            return out.to(dev)
+        qc, kc, vc = cap(q), cap(k), cap(v)
+        qp, kp, vp = qc[:T], kc[:T], vc[:T]
+        opc = torch.empty_like(qc)
+        kk = int(lens.max())
+        us = _graph_time(torch, [lambda: rb.attn(qc, kc, vc, cu, N, op=opc, n_hint=kk)], 100)
         flops = 4.0 * float((lens.astype(np.float64) ** 2).sum()) * d * H
         hbm = 4.0 * T * H * d * 2
-        r = {"T": T, "us": us, "tflops": flops / us / 1e6, "hbm_GBps": hbm / us / 1e3}
+        r = {"T": T, "us": us, "tflops": flops / us / 1e6, "hbm_GBps": hbm / us / 1e3,
+             "engine": "tcgen05 warp-specialised (AUTO, d = 64, N > 256)" if (d == 64 and N > 256) else
+             ("mma.sync one-stage (d = 64, N <= 256)" if d == 64 else "mma.sync streaming")}
         try:
             from flash_attn import flash_attn_varlen_func
             nmax = int(lens.max())
@@ -1081,8 +1091,8 @@ def n4_general_extras(rb, torch, dev, dt):
             r["fa2_varlen_error"] = repr(ex)[:120]
         # fp8 (E4M3) inputs, per-tensor scales (ragged_attn_fp8): half the input bytes
         try:
-            q8, k8, v8 = ((t.float() / (float(t.abs().max()) / 448.0)).to(torch.float8_e4m3fn) for t in (qp, kp, vp))
-            o8 = torch.empty_like(qp)
+            q8, k8, v8 = ((t.float() / (float(t.abs().max()) / 448.0)).to(torch.float8_e4m3fn) for t in (qc, kc, vc))
+            o8 = torch.empty_like(qc)
             r["fp8_us"] = _graph_time(torch, [lambda: rb.attn_fp8(q8, k8, v8, cu, N, (1.0, 1.0, 1.0),
                                                                   out_dtype=dt, op=o8)], 100)
             r["fp8_hbm_GBps"] = (3.0 * T * H * d + T * H * d * 2) / r["fp8_us"] / 1e3
