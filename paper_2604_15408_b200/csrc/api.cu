@@ -542,8 +542,10 @@ static ragged_status linear_impl(ragged_dtype dtype, int32_t rows, int32_t N, in
   g.m_dev = live;
   // tile width from the expected live rows when the caller knows them (performance only;
   // the grid still covers the capacity and the kernel reads the live count on the device)
-  const int bn = ragged::gemm_pick_bn(rows_hint > 0 && rows_hint < rows ? rows_hint : rows, N, device_sms());
-  cudaError_t e = ragged::launch_gemm(dtype, a, lda, w, g, epi, bn, st);
+  const int m_hint = rows_hint > 0 && rows_hint < rows ? rows_hint : rows;
+  int bn = ragged::gemm_pick_bn(m_hint, N, device_sms());
+  const int split = ragged::gemm_pick_split(m_hint, N, K, device_sms(), &bn);
+  cudaError_t e = ragged::launch_gemm(dtype, a, lda, w, g, epi, bn, st, split);
   return e == cudaSuccess ? RAGGED_OK : cuda_fail(e, "ragged_linear");
 }
 

@@ -173,16 +173,65 @@ __host__ __device__ constexpr int epi_stage_bytes() {  // per warp: 32 rows x 32
   return epi_warps<kEpi>() * 32 * kEpiRowBytes;
 }
 
-template <int BN, int kEpi>
+// Cluster split-K (kSplit > 1): the partial accumulator of a non-leader CTA
+// goes through its shared memory as fp32 rows of BN + 4 floats (the +4 keeps
+// the 16-byte row segments of 8 consecutive lanes on distinct banks).
+template <int BN, int kSplit>
+__host__ __device__ constexpr int red_bytes() {
+  return kSplit > 1 ? kGemmBM * (BN + 4) * 4 : 0;
+}
+template <int BN, int kEpi, int kSplit = 1>
 __host__ __device__ constexpr int gemm_stages() {
-  return (226 * 1024 - epi_stage_bytes<kEpi>() - 1280) / ((kGemmBM + BN) * kGemmBK * 2) < 8
-             ? (226 * 1024 - epi_stage_bytes<kEpi>() - 1280) / ((kGemmBM + BN) * kGemmBK * 2)
+  return (226 * 1024 - epi_stage_bytes<kEpi>() - red_bytes<BN, kSplit>() - 1280) / ((kGemmBM + BN) * kGemmBK * 2) < 8
+             ? (226 * 1024 - epi_stage_bytes<kEpi>() - red_bytes<BN, kSplit>() - 1280) / ((kGemmBM + BN) * kGemmBK * 2)
              : 8;
 }
-template <int BN, int kEpi>
+template <int BN, int kEpi, int kSplit = 1>
 __host__ __device__ constexpr int gemm_smem_bytes() {
-  return gemm_stages<BN, kEpi>() * (kGemmBM + BN) * kGemmBK * 2 + epi_stage_bytes<kEpi>() + 1024 /*align*/ +
-         256 /*barriers*/;
+  return gemm_stages<BN, kEpi, kSplit>() * (kGemmBM + BN) * kGemmBK * 2 + epi_stage_bytes<kEpi>() +
+         red_bytes<BN, kSplit>() + 1024 /*align*/ + 256 /*barriers*/;
+}
+
+__device__ __forceinline__ uint32_t gemm_cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void gemm_cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t gemm_mapa(uint32_t addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+// arrive on an mbarrier of CTA `rank` of the cluster, releasing this thread's
+// prior shared-memory writes at cluster scope
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t bar, uint32_t rank) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(gemm_mapa(bar, rank)) : "memory");
+}
+// wait with cluster-scope acquire (pairs with mbar_arrive_remote)
+__device__ __forceinline__ void mbar_wait_cluster(uint32_t bar, uint32_t parity) {
+  uint32_t done = 0;
+  for (uint32_t spins = 0;; ++spins) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}\n"
+        : "=r"(done)
+        : "r"(bar), "r"(parity)
+        : "memory");
+    if (done) return;
+    if (spins > (1u << 26)) __trap();
+  }
+}
+__device__ __forceinline__ float4 ld_peer_f4(uint32_t addr) {
+  float4 v;
+  asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "r"(addr)
+               : "memory");
+  return v;
 }
 
 // TMEM columns for two BN-wide accumulators, rounded up to a power of two (allocation unit)
@@ -196,11 +245,20 @@ __host__ __device__ constexpr uint32_t tmem_cols() {
 // blocks in L2 and every CTA streams the L2-resident weights).  Two TMEM
 // accumulators (2 x BN columns): the epilogue of tile i overlaps the
 // mainloop of tile i + 1.
-template <typename T, int BN, int kEpi>
+// kSplit > 1: a cluster of kSplit CTAs per output tile, CTA r accumulating the
+// k-blocks [r nk / kSplit, (r+1) nk / kSplit) in its own TMEM; the non-leader
+// CTAs write their fp32 partial tile into their shared memory and signal the
+// leader's mbarrier (release, cluster scope); the leader's epilogue adds the
+// partials read through distributed shared memory in CTA order (deterministic)
+// to its own accumulator before the usual epilogue, then frees the peers'
+// buffers for the next tile.  For small live row counts, where a tile grid of
+// one 128-row round leaves most SMs idle and each CTA walks all K.
+template <typename T, int BN, int kEpi, int kSplit>
 __global__ void __launch_bounds__(gemm_threads<kEpi>(), 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const GemmArgs g) {
-  constexpr int kStages = gemm_stages<BN, kEpi>();
+  constexpr int kStages = gemm_stages<BN, kEpi, kSplit>();
+  constexpr int kRedStride = BN + 4;  // floats per partial-tile row
   constexpr int kEpiWarps = epi_warps<kEpi>();
   constexpr int kEpiStageBytes = epi_stage_bytes<kEpi>();
   constexpr uint32_t kABytes = kGemmBM * kGemmBK * 2, kBBytes = BN * kGemmBK * 2;
@@ -209,12 +267,15 @@ __global__ void __launch_bounds__(gemm_threads<kEpi>(), 1)
   const uint32_t raw = smem_u32(smem_raw);
   const uint32_t base = (raw + 1023u) & ~1023u;  // SWIZZLE_128B atoms need 1024-B alignment
   const uint32_t stage_epi = base + kStages * kStageBytes;
-  const uint32_t bars = stage_epi + kEpiStageBytes;
+  const uint32_t red = stage_epi + kEpiStageBytes;                 // split-K partial tile (kSplit > 1)
+  const uint32_t bars = red + red_bytes<BN, kSplit>();
   auto full = [&](int s) { return bars + 8u * (uint32_t)s; };
   auto empty = [&](int s) { return bars + 8u * (uint32_t)(kStages + s); };
   auto tfull = [&](int a) { return bars + 8u * (uint32_t)(2 * kStages + a); };
   auto tempty = [&](int a) { return bars + 8u * (uint32_t)(2 * kStages + 2 + a); };
-  const uint32_t tslot = bars + 8u * (uint32_t)(2 * kStages + 4);
+  const uint32_t part_full = bars + 8u * (uint32_t)(2 * kStages + 4);  // leader: peers' partials landed
+  const uint32_t part_free = part_full + 8u;                           // peer: leader consumed the partial
+  const uint32_t tslot = bars + 8u * (uint32_t)(2 * kStages + 6);
   uint32_t* tslot_ptr = reinterpret_cast<uint32_t*>(smem_raw + (tslot - raw));
 
   // Setup (barriers, TMEM, descriptor prefetch) runs before the PDL wait,
@@ -231,6 +292,10 @@ __global__ void __launch_bounds__(gemm_threads<kEpi>(), 1)
       tc::mbar_init(tfull(a), 1);
       tc::mbar_init(tempty(a), kEpiWarps);  // one arrival per epilogue warp
     }
+    if (kSplit > 1) {
+      tc::mbar_init(part_full, (kSplit - 1) * kEpiWarps * 32);  // every epilogue thread of every peer
+      tc::mbar_init(part_free, kEpiWarps * 32);                 // every epilogue thread of the leader
+    }
     tc::fence_mbar_init();
     prefetch_tmap(&tmA);
     prefetch_tmap(&tmB);
@@ -238,9 +303,15 @@ __global__ void __launch_bounds__(gemm_threads<kEpi>(), 1)
   if (warp == 1) tc::alloc(tslot, tmem_cols<BN>());
   tc::fence_before();
   __syncthreads();
+  if (kSplit > 1) gemm_cluster_sync();  // every CTA's barriers initialised before any remote arrival
   tc::fence_after();
+  const int crank = kSplit > 1 ? (int)gemm_cluster_rank() : 0;
+  const int cid = kSplit > 1 ? (int)blockIdx.x / kSplit : (int)blockIdx.x;
+  const int ncl = kSplit > 1 ? (int)gridDim.x / kSplit : (int)gridDim.x;
   const uint32_t tmem = *tslot_ptr;
-  const int nk = g.K / kGemmBK;
+  const int nk_all = g.K / kGemmBK;
+  const int kb0 = kSplit > 1 ? crank * nk_all / kSplit : 0;      // this CTA's k-block range
+  const int kb1 = kSplit > 1 ? (crank + 1) * nk_all / kSplit : nk_all;
   if (threadIdx.x == 0) GT(1);
   pdl_wait_prerequisites();
   if (threadIdx.x == 0) GT(2);
@@ -251,9 +322,9 @@ __global__ void __launch_bounds__(gemm_threads<kEpi>(), 1)
   if (warp == 0) {
     if (lane == 0) {  // TMA producer
       int it = 0;
-      for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+      for (int t = cid; t < tiles; t += ncl) {
         const int m0 = (t / n_tiles) * kGemmBM, n0 = (t % n_tiles) * BN;
-        for (int kb = 0; kb < nk; ++kb, ++it) {
+        for (int kb = kb0; kb < kb1; ++kb, ++it) {
           const int s = it % kStages, r = it / kStages;
           if (r > 0) tc::mbar_wait(empty(s), (uint32_t)((r - 1) & 1));
           const uint32_t sa = base + (uint32_t)s * kStageBytes;
@@ -268,19 +339,19 @@ __global__ void __launch_bounds__(gemm_threads<kEpi>(), 1)
       const uint32_t idesc = tc::idesc_f16(std::is_same<T, __half>::value ? 0u : 1u, kGemmBM, BN, 0u);
       const uint64_t adesc0 = tc::sw128_desc(base), bdesc0 = tc::sw128_desc(base + kABytes);
       int it = 0, i = 0;
-      for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++i) {
+      for (int t = cid; t < tiles; t += ncl, ++i) {
         const int acc = i & 1, use = i >> 1;
         if (use > 0) tc::mbar_wait(tempty(acc), (uint32_t)((use - 1) & 1));
         tc::fence_after();
         const uint32_t d = tmem + (uint32_t)(acc * BN);
-        for (int kb = 0; kb < nk; ++kb, ++it) {
+        for (int kb = kb0; kb < kb1; ++kb, ++it) {
           const int s = it % kStages, r = it / kStages;
           tc::mbar_wait(full(s), (uint32_t)(r & 1));
           tc::fence_after();
           if (it == 0) GT(3);
           // one burst of 4 UMMAs with precomputed descriptors (stage offset >> 4)
           const uint64_t soff = (uint64_t)((s * kStageBytes) >> 4);
-          tc::mma_ss_k64_acc(d, adesc0 + soff, bdesc0 + soff, idesc, kb != 0 ? 1u : 0u);
+          tc::mma_ss_k64_acc(d, adesc0 + soff, bdesc0 + soff, idesc, kb != kb0 ? 1u : 0u);
           tc::commit(empty(s));  // frees the stage when these MMAs complete
         }
         tc::commit(tfull(acc));
@@ -298,9 +369,42 @@ __global__ void __launch_bounds__(gemm_threads<kEpi>(), 1)
     uint8_t* stg = smem_raw + (stage_epi - raw) + (warp - 2) * 32 * kEpiRowBytes;
     const T* bias = static_cast<const T*>(g.bias);
     int i = 0;
-    for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++i) {
+    for (int t = cid; t < tiles; t += ncl, ++i) {
       const int acc = i & 1;
       const int m0 = (t / n_tiles) * kGemmBM, n0 = (t % n_tiles) * BN;
+      const int row_local = 32 * quad + lane;
+      if (kSplit > 1 && crank > 0) {
+        // split-K peer: the partial tile to shared memory, then signal the leader
+        tc::mbar_wait_sleep(tfull(acc), (uint32_t)((i >> 1) & 1), 256);
+        tc::fence_after();
+        if (i > 0) mbar_wait_cluster(part_free, (uint32_t)((i - 1) & 1));  // previous partial consumed
+        const uint32_t tb = tmem + ((uint32_t)(32 * quad) << 16) + (uint32_t)(acc * BN);
+        if (32 * half < BN) {
+#pragma unroll
+          for (int ci = 0; ci < (BN / 32 + kEp - 1) / kEp; ++ci) {
+            const int c = 32 * half + 32 * kEp * ci;
+            if (c >= BN) break;
+            uint32_t r[32];
+            tc::ld_x32(tb + (uint32_t)c, r);
+            tc::wait_ld();
+            if (c + 32 * kEp >= BN) {  // last chunk of this warp: the accumulator goes back to the MMA warp
+              tc::fence_before();
+              __syncwarp();
+              if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tempty(acc)) : "memory");
+            }
+            const uint32_t dst = red + (uint32_t)((row_local * kRedStride + c) * 4);
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+              asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(dst + 16 * q), "r"(r[4 * q]),
+                           "r"(r[4 * q + 1]), "r"(r[4 * q + 2]), "r"(r[4 * q + 3])
+                           : "memory");
+          }
+        } else if (lane == 0) {
+          asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tempty(acc)) : "memory");
+        }
+        mbar_arrive_remote(part_full, 0);  // each thread releases its own partial rows
+        continue;
+      }
       const long long my_row = (long long)m0 + 32 * quad + lane;
       const bool live = my_row < M;
       // residual segments are independent of the accumulator: the first is
@@ -327,9 +431,12 @@ __global__ void __launch_bounds__(gemm_threads<kEpi>(), 1)
       }
       tc::mbar_wait_sleep(tfull(acc), (uint32_t)((i >> 1) & 1), 256);  // don't steal issue slots from TMA / MMA
       tc::fence_after();
+      if (kSplit > 1) mbar_wait_cluster(part_full, (uint32_t)(i & 1));  // the peers' partials landed
       if (i == 0 && warp == 2 && lane == 0) GT(5);
       if (32 * half >= BN) {  // no chunk for this warp at this tile width: just count in
         if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tempty(acc)) : "memory");
+        if (kSplit > 1)
+          for (int pr = 1; pr < kSplit; ++pr) mbar_arrive_remote(part_free, (uint32_t)pr);
         continue;
       }
       const uint32_t tbase = tmem + ((uint32_t)(32 * quad) << 16) + (uint32_t)(acc * BN);
@@ -353,6 +460,21 @@ __global__ void __launch_bounds__(gemm_threads<kEpi>(), 1)
         float v[32];
 #pragma unroll
         for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+        if constexpr (kSplit > 1) {  // + the peers' partials, in CTA order (deterministic)
+          const uint32_t src = red + (uint32_t)((row_local * kRedStride + c) * 4);
+#pragma unroll
+          for (int pr = 1; pr < kSplit; ++pr) {
+            const uint32_t ps = gemm_mapa(src, (uint32_t)pr);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              const float4 f = ld_peer_f4(ps + 16 * q);
+              v[4 * q] += f.x;
+              v[4 * q + 1] += f.y;
+              v[4 * q + 2] += f.z;
+              v[4 * q + 3] += f.w;
+            }
+          }
+        }
         if (bias != nullptr) {
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
@@ -399,11 +521,14 @@ __global__ void __launch_bounds__(gemm_threads<kEpi>(), 1)
         }
         __syncwarp();  // staging is rewritten by the next chunk
       }
+      if (kSplit > 1)  // every partial of this thread's rows read: the peers may refill
+        for (int pr = 1; pr < kSplit; ++pr) mbar_arrive_remote(part_free, (uint32_t)pr);
       if (i == 0 && warp == 2 && lane == 0) GT(6);
     }
   }
   tc::fence_before();
   __syncthreads();
+  if (kSplit > 1) gemm_cluster_sync();  // no CTA leaves while a peer may still read its shared memory
   if (warp == 1) {
     tc::fence_after();
     tc::dealloc(tmem, tmem_cols<BN>());
@@ -486,15 +611,16 @@ static bool make_tmap(CUtensorMap* m, int dtype, const void* ptr, long long rows
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <typename T, int BN, int kEpi>
+template <typename T, int BN, int kEpi, int kSplit>
 static cudaError_t launch_gemm_t(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& g,
                                  cudaStream_t st) {
   static bool done[64] = {false};
   int dev = 0;
   cudaGetDevice(&dev);
   if (dev >= 0 && dev < 64 && !done[dev]) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_tc_kernel<T, BN, kEpi>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         gemm_smem_bytes<BN, kEpi>());
+    cudaError_t e = cudaFuncSetAttribute(gemm_tc_kernel<T, BN, kEpi, kSplit>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         gemm_smem_bytes<BN, kEpi, kSplit>());
     if (e != cudaSuccess) return e;
     done[dev] = true;
   }
@@ -508,18 +634,45 @@ static cudaError_t launch_gemm_t(const CUtensorMap& ta, const CUtensorMap& tb, c
     return e ? atoi(e) : 0;
   }();
   const int cap = grid_cap > 0 && grid_cap < nsm ? grid_cap : nsm;
-  const dim3 grid((unsigned)(tiles < cap ? tiles : cap));
-  return launch_pdl_b(gemm_tc_kernel<T, BN, kEpi>, grid, dim3(gemm_threads<kEpi>()), gemm_smem_bytes<BN, kEpi>(), st,
-                      ta, tb,
-                      g);
+  if (kSplit == 1) {
+    const dim3 grid((unsigned)(tiles < cap ? tiles : cap));
+    return launch_pdl_b(gemm_tc_kernel<T, BN, kEpi, 1>, grid, dim3(gemm_threads<kEpi>()),
+                        gemm_smem_bytes<BN, kEpi, 1>(), st, ta, tb, g);
+  }
+  // split-K: clusters of kSplit CTAs, persistent over tiles
+  const long long clusters = tiles < cap / kSplit ? tiles : cap / kSplit;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(clusters * kSplit));
+  cfg.blockDim = dim3(gemm_threads<kEpi>());
+  cfg.dynamicSmemBytes = gemm_smem_bytes<BN, kEpi, kSplit>();
+  cfg.stream = st;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  attr[1].id = cudaLaunchAttributeClusterDimension;
+  attr[1].val.clusterDim.x = kSplit;
+  attr[1].val.clusterDim.y = 1;
+  attr[1].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 2;
+  return cudaLaunchKernelEx(&cfg, gemm_tc_kernel<T, BN, kEpi, kSplit>, ta, tb, g);
 }
 
+template <typename T, int BN, int kSplit>
+static cudaError_t launch_gemm_s(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& g, int epi,
+                                 cudaStream_t st) {
+  if (epi == 1) return launch_gemm_t<T, BN, 1, kSplit>(ta, tb, g, st);
+  if (epi == 2) return launch_gemm_t<T, BN, 2, kSplit>(ta, tb, g, st);
+  return launch_gemm_t<T, BN, 0, kSplit>(ta, tb, g, st);
+}
 template <typename T, int BN>
 static cudaError_t launch_gemm_bn(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& g, int epi,
-                                  cudaStream_t st) {
-  if (epi == 1) return launch_gemm_t<T, BN, 1>(ta, tb, g, st);
-  if (epi == 2) return launch_gemm_t<T, BN, 2>(ta, tb, g, st);
-  return launch_gemm_t<T, BN, 0>(ta, tb, g, st);
+                                  cudaStream_t st, int split) {
+  if constexpr (BN <= 128) {  // split-K variants only where the partial tile leaves room for >= 3 stages
+    if (split == 4) return launch_gemm_s<T, BN, 4>(ta, tb, g, epi, st);
+    if (split == 2) return launch_gemm_s<T, BN, 2>(ta, tb, g, epi, st);
+  }
+  return launch_gemm_s<T, BN, 1>(ta, tb, g, epi, st);
 }
 
 // Tile width from {256, 128, 64} (dividing N) minimising the estimated time
@@ -548,21 +701,51 @@ int gemm_pick_bn(int M_cap, int N, int sms) {
   return best;
 }
 
+// Split-K for small live row counts: when the chosen tile grid fits in one
+// round and leaves room, a 128- (or 64-) wide tile grid with clusters of 2 / 4
+// CTAs splitting K, if that cuts the k-blocks each CTA walks (a k-block costs
+// ~0.29 us per CTA whatever BN at small T -- the per-CTA pipeline constant --
+// so fewer k-blocks per CTA is what shortens a one-round GEMM).
+int gemm_pick_split(int M_hint, int N, int K, int sms, int* bn) {
+  static const int forced = [] {
+    const char* e = getenv("RAGGED_GEMM_SPLIT");  // tuning experiments only
+    return e ? atoi(e) : -1;
+  }();
+  const long long mt = (M_hint + kGemmBM - 1) / kGemmBM;
+  const int nk = K / kGemmBK;
+  if (forced == 1) return 1;
+  // measured (scripts/r2/gemm_split_probe.py, T = 1248): fc2 (K = 3072) 17.6 -> 16.2 us with 2 CTAs,
+  // proj (K = 768) 6.7 -> 10.5 us: the DSMEM partial exchange costs more than a short K saves
+  if (mt * (N / *bn) > sms || nk < 32) return 1;
+  for (int bn2 : {128, 64}) {
+    if (N % bn2 != 0) continue;
+    const long long t2 = mt * (N / bn2);
+    for (int sp : {4, 2}) {
+      if (forced > 1 && sp != forced) continue;
+      if (t2 * sp <= sms && nk / sp >= 4 && nk / sp + 2 < nk) {
+        *bn = bn2;
+        return sp;
+      }
+    }
+  }
+  return 1;
+}
+
 cudaError_t launch_gemm(int dtype, const void* a, long long lda, const void* w, const GemmArgs& g, int epi,
-                        int bn, cudaStream_t st) {
+                        int bn, cudaStream_t st, int split) {
   CUtensorMap ta, tb;
   if (!make_tmap(&ta, dtype, a, g.M_cap, g.K, lda, kGemmBM)) return cudaErrorInvalidValue;
   if (!make_tmap(&tb, dtype, w, g.N, g.K, g.K, bn)) return cudaErrorInvalidValue;
   if (dtype == 0) {
-    if (bn == 256) return launch_gemm_bn<__nv_bfloat16, 256>(ta, tb, g, epi, st);
-    if (bn == 192) return launch_gemm_bn<__nv_bfloat16, 192>(ta, tb, g, epi, st);
-    if (bn == 128) return launch_gemm_bn<__nv_bfloat16, 128>(ta, tb, g, epi, st);
-    return launch_gemm_bn<__nv_bfloat16, 64>(ta, tb, g, epi, st);
+    if (bn == 256) return launch_gemm_bn<__nv_bfloat16, 256>(ta, tb, g, epi, st, split);
+    if (bn == 192) return launch_gemm_bn<__nv_bfloat16, 192>(ta, tb, g, epi, st, split);
+    if (bn == 128) return launch_gemm_bn<__nv_bfloat16, 128>(ta, tb, g, epi, st, split);
+    return launch_gemm_bn<__nv_bfloat16, 64>(ta, tb, g, epi, st, split);
   }
-  if (bn == 256) return launch_gemm_bn<__half, 256>(ta, tb, g, epi, st);
-  if (bn == 192) return launch_gemm_bn<__half, 192>(ta, tb, g, epi, st);
-  if (bn == 128) return launch_gemm_bn<__half, 128>(ta, tb, g, epi, st);
-  return launch_gemm_bn<__half, 64>(ta, tb, g, epi, st);
+  if (bn == 256) return launch_gemm_bn<__half, 256>(ta, tb, g, epi, st, split);
+  if (bn == 192) return launch_gemm_bn<__half, 192>(ta, tb, g, epi, st, split);
+  if (bn == 128) return launch_gemm_bn<__half, 128>(ta, tb, g, epi, st, split);
+  return launch_gemm_bn<__half, 64>(ta, tb, g, epi, st, split);
 }
 
 }  // namespace ragged

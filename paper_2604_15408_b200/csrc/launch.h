@@ -76,8 +76,10 @@ struct GemmArgs {
 };
 // epi: 0 none, 1 exact GELU, 2 residual add.  bn in {64, 128, 256}, N % bn == 0, K % 64 == 0.
 cudaError_t launch_gemm(int dtype, const void* a, long long lda, const void* w, const GemmArgs& g, int epi,
-                        int bn, cudaStream_t st);
+                        int bn, cudaStream_t st, int split = 1);
 int gemm_pick_bn(int M_cap, int N, int sms);
+// split-K cluster size (1, 2 or 4) for a small live row count; may change *bn to 128 / 64
+int gemm_pick_split(int M_hint, int N, int K, int sms, int* bn);
 cudaError_t launch_layer_norm(int dtype, const void* x, long long ldx, const void* w, const void* b,
                               float eps, void* y, long long ldy, int M_cap, const int32_t* m_dev, int D,
                               cudaStream_t st);
