@@ -269,3 +269,35 @@ def test_dist_nccl_entry_validation():
     assert lib.ragged_dist_pack_attend_unpack_allgather(ctypes.byref(p), None, None, None, None, None, None, None,
                                                         None, None) == rb.EINVAL
     lib.ragged_dist_nccl_destroy(None)
+
+
+def test_round2_entry_validation():
+    """Round-2 entry points (N2 EViT / fused prune, N1 pack_rows / cls_rows, the
+    WS engine): host-checkable errors return synchronously, before any CUDA
+    call (FAKE pointers are never dereferenced)."""
+    lib = rb.lib()
+    p = rb.problem(4, 197, 12)
+    # ragged_keep_evit: k < 1, NULL q, H too large for its row buffers at N = 256
+    assert lib.ragged_keep_evit(ctypes.byref(p), FAKE, FAKE, FAKE, 0, FAKE, None) == rb.EINVAL
+    assert lib.ragged_keep_evit(ctypes.byref(p), None, FAKE, FAKE, 5, FAKE, None) == rb.EINVAL
+    big = rb.problem(4, 256, 40)
+    assert lib.ragged_keep_evit(ctypes.byref(big), FAKE, FAKE, FAKE, 5, FAKE, None) == rb.ENOTSUP
+    assert lib.ragged_keep_evit(ctypes.byref(rb.problem(0, 197, 12)), None, None, None, 5, None, None) == rb.OK
+    # ragged_keep_topk_l2: k < 1
+    assert lib.ragged_keep_topk_l2(ctypes.byref(p), FAKE, 0, FAKE, None) == rb.EINVAL
+    # ragged_prune_l2_pack_attend_unpack: k < 1, H > 16, ldx < H*d, ldx alignment, the WS engine
+    f = lib.ragged_prune_l2_pack_attend_unpack
+    assert f(ctypes.byref(p), FAKE, 768, 0, FAKE, FAKE, FAKE, FAKE, None, None, None) == rb.EINVAL
+    assert f(ctypes.byref(rb.problem(4, 197, 17)), FAKE, 17 * 64, 5, FAKE, FAKE, FAKE, FAKE, None, None,
+             None) == rb.ENOTSUP
+    assert f(ctypes.byref(p), FAKE, 512, 5, FAKE, FAKE, FAKE, FAKE, None, None, None) == rb.EINVAL
+    assert f(ctypes.byref(p), FAKE, 772, 5, FAKE, FAKE, FAKE, FAKE, None, None, None) == rb.EALIGN
+    ws = rb.problem(4, 197, 12, engine=rb.ENGINE_TCGEN05_WS)
+    assert f(ctypes.byref(ws), FAKE, 768, 5, FAKE, FAKE, FAKE, FAKE, None, None, None) == rb.ENOTSUP
+    # the WS engine runs ragged_attn only; head_dim 64 only
+    assert lib.ragged_pack_attend_unpack(ctypes.byref(ws), FAKE, FAKE, FAKE, FAKE, FAKE, None, None) == rb.ENOTSUP
+    ws80 = rb.problem(4, 300, 12, d=80, engine=rb.ENGINE_TCGEN05_WS)
+    assert lib.ragged_attn(ctypes.byref(ws80), FAKE, FAKE, FAKE, FAKE, FAKE, None) == rb.ENOTSUP
+    # N1 pieces: NULL pointers
+    assert lib.ragged_pack_rows(ctypes.byref(p), FAKE, None, FAKE, FAKE, FAKE, FAKE, None) == rb.EINVAL
+    assert lib.ragged_cls_rows(ctypes.byref(p), FAKE, FAKE, None, None) == rb.EINVAL
