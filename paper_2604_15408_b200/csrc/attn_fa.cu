@@ -421,7 +421,7 @@ __global__ void __launch_bounds__(kFaThreads, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   FaBars& bars = *reinterpret_cast<FaBars*>(smem + kOffBar);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int warp = tc::warp_uniform_idx(), lane = threadIdx.x & 31;
   constexpr uint32_t kFmt = std::is_same<T, __nv_bfloat16>::value ? 1u : 0u;
 
   if (threadIdx.x == 0) FTL(48);
@@ -481,8 +481,8 @@ __global__ void __launch_bounds__(kFaThreads, 1)
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
     // The whole warp runs the schedule (descriptor arithmetic stays warp-
-    // uniform, in uniform registers); lane 0 alone issues the tcgen05 ops.
-    const bool issuer = lane == 0;
+    // uniform, in uniform registers); one elect.sync-chosen lane issues the
+    // tcgen05 ops (tc::elect_one: no per-UMMA R2UR waterfall).
     {
       uint32_t kv = 0, ph_p[2] = {0u, 0u};
       int nitem = 0;
@@ -507,11 +507,12 @@ __global__ void __launch_bounds__(kFaThreads, 1)
           const int nv = min(kFaRows, I.n);
           idesc_s0 = tc::idesc_f16(kFmt, kFaRows, (uint32_t)((nv + 15) & ~15), 0);
           kd0 = tc::sw128_desc(smem_u32(smem + kOffKV + s * 2 * kFaTileBytes));
-          if (issuer) {
+          if (tc::elect_one()) {
             tc::mma_ss_k64(tmem, qd[0], kd0, idesc_s0);
             tc::commit(smem_u32(&bars.s[0]));
             if (nitem == 0) FTL(49);
           }
+          __syncwarp();
         }
         for (int j = 0; j < I.nb; ++j, ++kv) {
           const int s = kv % kFaStages;
@@ -529,31 +530,40 @@ __global__ void __launch_bounds__(kFaThreads, 1)
             tc::mbar_wait(smem_u32(&bars.p[x]), ph_p[x]);
             ph_p[x] ^= 1u;
             tc::fence_after();
-            if (issuer && nitem == 0 && x == 0 && j < 8) FTL(32 + 2 * j);
-            if (issuer && x == 0 && j == 0 && I.ntile == 2) {  // the deferred S_B(0)
-              tc::mma_ss_k64(tmem + 256u, qd[1], kd0, idesc_s0);
-              tc::commit(smem_u32(&bars.s[1]));
+            if (lane == 0 && nitem == 0 && x == 0 && j < 8) FTL(32 + 2 * j);
+            if (x == 0 && j == 0 && I.ntile == 2) {  // the deferred S_B(0)
+              if (tc::elect_one()) {
+                tc::mma_ss_k64(tmem + 256u, qd[1], kd0, idesc_s0);
+                tc::commit(smem_u32(&bars.s[1]));
+              }
+              __syncwarp();
             }
 #ifndef RAGGED_FA_ABLATE_PV
-            if (issuer) fa_pv(tmem + 256u * x + 128u, tmem + 256u * x, vd, idesc_o, (nv + 15) >> 4, j > 0 ? 1u : 0u);
+            if (tc::elect_one())
+              fa_pv(tmem + 256u * x + 128u, tmem + 256u * x, vd, idesc_o, (nv + 15) >> 4, j > 0 ? 1u : 0u);
+            __syncwarp();
 #endif
             if (more) {
               if (x == 0) {
                 tc::mbar_wait(smem_u32(&bars.full[s1]), ((kv + 1) / kFaStages) & 1);
                 tc::fence_after();
               }
-              if (issuer)
+              if (tc::elect_one())
                 tc::mma_ss_k64(tmem + 256u * x, qd[x], kd1,
                                tc::idesc_f16(kFmt, kFaRows, (uint32_t)((nv1 + 15) & ~15), 0));
+              __syncwarp();
             }
-            if (issuer) {
+            if (tc::elect_one()) {
               tc::commit(smem_u32(&bars.s[x]));  // S(j+1) ready / final O ready
               if (nitem == 0 && x == 0 && j < 8) FTL(33 + 2 * j);
             }
+            __syncwarp();
           }
-          if (issuer) tc::commit(smem_u32(&bars.empty[s]));  // stage s free once these UMMAs complete
+          if (tc::elect_one()) tc::commit(smem_u32(&bars.empty[s]));  // stage s free once these UMMAs complete
+          __syncwarp();
         }
-        if (issuer) tc::commit(smem_u32(&bars.q_free[qb]));
+        if (tc::elect_one()) tc::commit(smem_u32(&bars.q_free[qb]));
+        __syncwarp();
         ++nitem;
       }
     }

@@ -66,8 +66,10 @@ __global__ void __launch_bounds__(3 * kTcSlotThreads, 1) attn_tc_kernel(const At
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   const int nslots = blockDim.x / kTcSlotThreads;
-  const int slot = threadIdx.x / kTcSlotThreads, tid = threadIdx.x % kTcSlotThreads;
-  const int warp = tid >> 5;  // == CTA warp index % 4: this warp's TMEM lane quarter
+  // warp-uniform slot / warp indices (UMMA operands then stay in uniform registers)
+  const int wu = tc::warp_uniform_idx();
+  const int slot = wu / (kTcSlotThreads / 32), tid = threadIdx.x % kTcSlotThreads;
+  const int warp = wu % (kTcSlotThreads / 32);  // == CTA warp index % 4: this warp's TMEM lane quarter
   const TcSmem L = tc_smem(a.N);
   uint8_t* base = smem + slot * L.slot_bytes;
   uint8_t* sQ = base + L.off_q;
@@ -224,11 +226,14 @@ __global__ void __launch_bounds__(3 * kTcSlotThreads, 1) attn_tc_kernel(const At
           tc::mma_ss_k64(tS + ((uint32_t)(16 * X) << 16), qd0 + 512ull * (uint64_t)X, kd0 + 512ull * (uint64_t)jj,
                          tc::idesc_f16(kFmt, kTcTile, kc, 0));
         };
-        if (tid == 0) {
-          for (int X = 0; X < ntl; ++X) {
-            issue_s(X, 0);
-            tc::commit(bar_x + 8u * (uint32_t)X);
+        if (warp == 0) {
+          if (tc::elect_one()) {
+            for (int X = 0; X < ntl; ++X) {
+              issue_s(X, 0);
+              tc::commit(bar_x + 8u * (uint32_t)X);
+            }
           }
+          __syncwarp();
         }
         for (int j = 0; j < nchunks; ++j) {
           for (int X = 0; X < ntl; ++X) {
@@ -326,14 +331,17 @@ __global__ void __launch_bounds__(3 * kTcSlotThreads, 1) attn_tc_kernel(const At
                            : "memory");
             }
             prev = __shfl_sync(0xffffffffu, prev, 0);
-            if ((prev & 3u) == 3u && (tid & 31) == 0) {  // P_j V_j for tile X, then S_{j+1} behind it
+            if ((prev & 3u) == 3u) {  // P_j V_j for tile X, then S_{j+1} behind it
               tc::fence_after();
               const int nk = (min(kTcChunk, n - j * kTcChunk) + 15) >> 4;
-              tc::mma_ts_pv(tO + ((uint32_t)(16 * X) << 16), tS + ((uint32_t)(16 * X) << 16),
-                            vd0 + 512ull * (uint64_t)j, idesc_o, nk, j > 0 ? 1u : 0u);
-              if (j + 1 < nchunks) issue_s(X, j + 1);
-              tc::commit(bar_x + 8u * (uint32_t)X);
-              if (pr == 0 && slot == 0 && j < 4) PT(3 + 6 * j + 3 * X);
+              if (tc::elect_one()) {
+                tc::mma_ts_pv(tO + ((uint32_t)(16 * X) << 16), tS + ((uint32_t)(16 * X) << 16),
+                              vd0 + 512ull * (uint64_t)j, idesc_o, nk, j > 0 ? 1u : 0u);
+                if (j + 1 < nchunks) issue_s(X, j + 1);
+                tc::commit(bar_x + 8u * (uint32_t)X);
+                if (pr == 0 && slot == 0 && j < 4) PT(3 + 6 * j + 3 * X);
+              }
+              __syncwarp();
             }
           }
         }
@@ -408,11 +416,14 @@ __global__ void __launch_bounds__(3 * kTcSlotThreads, 1) attn_tc_kernel(const At
       for (int j = 0; warp_live && j < nchunks; ++j) {
         const int kc = min(kTcChunk, n16 - j * kTcChunk);     // keys in chunk (multiple of 16)
         // ---- S_j = Q K_j^T: 4 UMMA of K = 16 (+32 B along the SW128 rows each)
-        if (tid == 0) {
+        if (warp == 0) {
           tc::fence_after();
-          tc::mma_ss_k64(tS, tc::sw128_desc(smem_u32(sQ)), tc::sw128_desc(smem_u32(sK)) + 512ull * (uint64_t)j,
-                         tc::idesc_f16(kFmt, kTcTile, kc, 0));
-          tc::commit(bar_s);
+          if (tc::elect_one()) {
+            tc::mma_ss_k64(tS, tc::sw128_desc(smem_u32(sQ)), tc::sw128_desc(smem_u32(sK)) + 512ull * (uint64_t)j,
+                           tc::idesc_f16(kFmt, kTcTile, kc, 0));
+            tc::commit(bar_s);
+          }
+          __syncwarp();
         }
         tc::mbar_wait(bar_s, ph_s);
         ph_s ^= 1u;
@@ -495,12 +506,15 @@ __global__ void __launch_bounds__(3 * kTcSlotThreads, 1) attn_tc_kernel(const At
         sync_live();
         TL(8);
         // ---- O += P_hi V_j + P_lo V_j (K = 16 keys per UMMA) --------------------
-        if (tid == 0) {
+        if (warp == 0) {
           tc::fence_after();
           const int nk = (min(kTcChunk, n - j * kTcChunk) + 15) >> 4;
-          tc::mma_ts_pv(tO, tS, tc::sw128_desc(smem_u32(sV)) + 512ull * (uint64_t)j, idesc_o, nk,
-                        j > 0 ? 1u : 0u);
-          tc::commit(bar_o);
+          if (tc::elect_one()) {
+            tc::mma_ts_pv(tO, tS, tc::sw128_desc(smem_u32(sV)) + 512ull * (uint64_t)j, idesc_o, nk,
+                          j > 0 ? 1u : 0u);
+            tc::commit(bar_o);
+          }
+          __syncwarp();
         }
         tc::mbar_wait(bar_o, ph_o);  // before S_{j+1} overwrites P_j, and before the epilogue
         ph_o ^= 1u;

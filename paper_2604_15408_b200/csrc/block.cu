@@ -165,7 +165,57 @@ __device__ __forceinline__ void prefetch_tmap(const CUtensorMap* m) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(m)) : "memory");
 }
 
-__device__ __forceinline__ float gelu_erf(float x) { return 0.5f * x * (1.f + erff(x * 0.70710678118654752f)); }
+// Exact GELU, 0.5 x (1 + erf(x / sqrt 2)) = 0.5 x (x < 0 ? E : 2 - E) with
+// E = erfc(u), u = |x| / sqrt 2, evaluated on pairs with packed fp32x2 FMAs
+// and one MUFU.EX2 per element: E = 2^(Q(u) - x^2 log2(e) / 2), Q(u) =
+// log2(erfc(u) e^(u^2)) a degree-11 polynomial on u in [0, 4.5] (u clamped
+// there: past it E < 2e-10 and only the x^2 term matters).  Max relative
+// error of E 3.9e-6 (fit and check: scripts/r2/fit_gelu.py), i.e. ~1000x
+// below a bf16 ulp of the output.  erff costs ~42 instructions + 2 MUFU per
+// element, which made the GELU epilogue issue-bound (5.4 us per 128 x 256
+// tile; DESIGN.md §7 N1).
+__device__ __forceinline__ uint64_t g_pack(float a, float b) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ void g_unpack(uint64_t v, float& a, float& b) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+}
+__device__ __forceinline__ uint64_t g_fma2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ uint64_t g_mul2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ float g_ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ void gelu_pair(float& a, float& b) {
+  constexpr float kC[12] = {1.156962810e-07f,  -1.627914429e+00f, 5.243244767e-01f,  -1.485833526e-01f,
+                            2.823024057e-02f,  -3.963231866e-04f, -2.060696948e-03f, 8.438329096e-04f,
+                            -1.895271998e-04f, 2.609425610e-05f,  -2.062811973e-06f, 7.190923412e-08f};
+  const uint64_t u = g_pack(fminf(fabsf(a) * 0.70710678118654752f, 4.5f), fminf(fabsf(b) * 0.70710678118654752f, 4.5f));
+  uint64_t q = g_fma2(g_pack(kC[11], kC[11]), u, g_pack(kC[10], kC[10]));
+#pragma unroll
+  for (int i = 9; i >= 0; --i) q = g_fma2(q, u, g_pack(kC[i], kC[i]));
+  const uint64_t x = g_pack(a, b);
+  const float kH = -0.72134752044448170f;  // -log2(e) / 2
+  float e0, e1;
+  g_unpack(g_fma2(g_mul2(x, x), g_pack(kH, kH), q), e0, e1);
+  e0 = g_ex2(e0);
+  e1 = g_ex2(e1);
+  float h0, h1;
+  g_unpack(g_mul2(x, g_pack(0.5f, 0.5f)), h0, h1);
+  const uint64_t r = g_mul2(g_pack(h0, h1), g_pack(a < 0.f ? e0 : 2.f - e0, b < 0.f ? e1 : 2.f - e1));
+  g_unpack(r, a, b);
+}
 
 constexpr int kEpiRowBytes = 80;                               // 64 B of bf16 + 16 B pad
 template <int kEpi>
@@ -281,7 +331,7 @@ __global__ void __launch_bounds__(gemm_threads<kEpi>(), 1)
   // Setup (barriers, TMEM, descriptor prefetch) runs before the PDL wait,
   // overlapping the previous kernel's tail; the live row count is read after.
   pdl_launch_dependents();
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int warp = tc::warp_uniform_idx(), lane = threadIdx.x & 31;
   if (threadIdx.x == 0) GT(0);
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
@@ -335,28 +385,32 @@ __global__ void __launch_bounds__(gemm_threads<kEpi>(), 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {  // MMA issuer
-      const uint32_t idesc = tc::idesc_f16(std::is_same<T, __half>::value ? 0u : 1u, kGemmBM, BN, 0u);
-      const uint64_t adesc0 = tc::sw128_desc(base), bdesc0 = tc::sw128_desc(base + kABytes);
-      int it = 0, i = 0;
-      for (int t = cid; t < tiles; t += ncl, ++i) {
-        const int acc = i & 1, use = i >> 1;
-        if (use > 0) tc::mbar_wait(tempty(acc), (uint32_t)((use - 1) & 1));
+    // MMA issuer: the whole warp runs the schedule (warp-uniform operands in
+    // uniform registers), the elected lane issues the UMMAs and commits
+    const uint32_t idesc = tc::idesc_f16(std::is_same<T, __half>::value ? 0u : 1u, kGemmBM, BN, 0u);
+    const uint64_t adesc0 = tc::sw128_desc(base), bdesc0 = tc::sw128_desc(base + kABytes);
+    int it = 0, i = 0;
+    for (int t = cid; t < tiles; t += ncl, ++i) {
+      const int acc = i & 1, use = i >> 1;
+      if (use > 0) tc::mbar_wait(tempty(acc), (uint32_t)((use - 1) & 1));
+      tc::fence_after();
+      const uint32_t d = tmem + (uint32_t)(acc * BN);
+      for (int kb = kb0; kb < kb1; ++kb, ++it) {
+        const int s = it % kStages, r = it / kStages;
+        tc::mbar_wait(full(s), (uint32_t)(r & 1));
         tc::fence_after();
-        const uint32_t d = tmem + (uint32_t)(acc * BN);
-        for (int kb = kb0; kb < kb1; ++kb, ++it) {
-          const int s = it % kStages, r = it / kStages;
-          tc::mbar_wait(full(s), (uint32_t)(r & 1));
-          tc::fence_after();
-          if (it == 0) GT(3);
-          // one burst of 4 UMMAs with precomputed descriptors (stage offset >> 4)
-          const uint64_t soff = (uint64_t)((s * kStageBytes) >> 4);
+        if (it == 0 && lane == 0) GT(3);
+        // one burst of 4 UMMAs with precomputed descriptors (stage offset >> 4)
+        const uint64_t soff = (uint64_t)((s * kStageBytes) >> 4);
+        if (tc::elect_one()) {
           tc::mma_ss_k64_acc(d, adesc0 + soff, bdesc0 + soff, idesc, kb != kb0 ? 1u : 0u);
           tc::commit(empty(s));  // frees the stage when these MMAs complete
         }
-        tc::commit(tfull(acc));
-        if (i == 0) GT(4);
+        __syncwarp();
       }
+      if (tc::elect_one()) tc::commit(tfull(acc));
+      __syncwarp();
+      if (i == 0 && lane == 0) GT(4);
     }
   } else {
     // Epilogue: warp w reads TMEM lanes 32*(w % 4) .. +31 (one row per
@@ -490,7 +544,7 @@ __global__ void __launch_bounds__(gemm_threads<kEpi>(), 1)
         }
         if constexpr (kEpi == 1) {
 #pragma unroll
-          for (int j = 0; j < 32; ++j) v[j] = gelu_erf(v[j]);
+          for (int j = 0; j < 32; j += 2) gelu_pair(v[j], v[j + 1]);
         }
         if constexpr (kEpi == 2) {
 #pragma unroll

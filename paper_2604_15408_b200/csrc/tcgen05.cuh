@@ -146,6 +146,21 @@ __device__ __forceinline__ void mma_ts_pv(uint32_t o, uint32_t pa, uint64_t vd, 
 }
 
 // Arrive on an mbarrier when all previously issued tcgen05 ops of this thread complete.
+// One lane of a converged warp (elect.sync): UMMA issue sites run the whole
+// warp through the schedule so the operands stay warp-uniform (uniform
+// registers) and only the elected lane issues -- under `if (lane == 0)` ptxas
+// wraps every tcgen05.mma in an ELECT / R2UR.BROADCAST / BRA.U.ANY loop that
+// costs ~200 cycles per UMMA (profiles/r02: umma_tput, GEMM k-block probe).
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\telect.sync _|p, 0xffffffff;\n\tselp.u32 %0, 1, 0, p;\n\t}\n"
+      : "=r"(pred));
+  return pred != 0;
+}
+// warp index as a value ptxas treats as warp-uniform
+__device__ __forceinline__ int warp_uniform_idx() { return __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0); }
+
 __device__ __forceinline__ void commit(uint32_t bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                    bar)

@@ -30,7 +30,7 @@ for name, B, N, H, p in cases:
         sets.append((qp, pk(k), pk(v), cu.to(dev), torch.empty_like(qp)))
     torch.cuda.synchronize()
     r = {"T": int(sets[0][3][-1].item())}
-    for eng, nm in ((3, "ws"), (1, "mma"), (0, "auto")):
+    for eng, nm in ((3, "ws"), (2, "tc"), (1, "mma"), (0, "auto")):
         try:
             r[nm + "_us"] = bench._graph_time(torch, [(lambda s=s, e=eng: rb.attn(s[0], s[1], s[2], s[3], N, op=s[4], engine=e, n_hint=kk)) for s in sets], 200)
         except Exception as ex:
@@ -49,3 +49,19 @@ for name, B, N, H, p in cases:
     res[name] = r
     print(name, r, flush=True)
 print(json.dumps(res))
+
+# the fused path per engine (C3 shapes, padded inputs)
+for p in (0.0, 0.5, 0.8):
+    B, N, H = 32, 197, 12
+    kk = synth.kept_tokens(N, p)
+    sets = []
+    for i in range(8):
+        q, k, v, keep = synth.make_inputs(B, N, H, p, "random", "bf16", seed=i)
+        sets.append((q.to(dev), k.to(dev), v.to(dev), keep.to(dev), torch.empty(B, N, H, 64, dtype=torch.bfloat16, device=dev)))
+    r = {}
+    for eng, nm in ((2, "tc"), (1, "mma"), (0, "auto")):
+        try:
+            r[nm + "_us"] = bench._graph_time(torch, [(lambda s=s, e=eng: rb.pack_attend_unpack(s[0], s[1], s[2], s[3], o=s[4], engine=e, n_hint=kk)) for s in sets], 200)
+        except Exception as ex:
+            r[nm + "_us"] = repr(ex)[:100]
+    print(f"fused_C3_p{p}", r, flush=True)

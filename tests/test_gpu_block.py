@@ -116,6 +116,28 @@ def test_linear_epilogues(M, N, K, epi):
     _gemm_case(M, N, K, epi, seed=M + N + K + epi)
 
 
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float16])
+def test_linear_gelu_wide_range(dtype):
+    """The GELU epilogue's erfc polynomial (u clamped at 4.5) and both signs'
+    branches, over pre-activations spanning about +-40: every output within a
+    storage ulp (+ the accumulation term) of the fp64 exact GELU."""
+    M, N, K = 384, 256, 64
+    g = torch.Generator().manual_seed(21)
+    a = torch.randn(M, K, generator=g).to(dtype)
+    w = (torch.rand(N, K, generator=g) * 2.0 - 1.0).mul(torch.linspace(0.02, 2.5, N)[:, None]).to(dtype)
+    bias = torch.zeros(N).to(dtype)
+    out = _sentinel((M, N), dtype)
+    rb.linear(a.to(DEV), w.to(DEV), bias.to(DEV), rb.EPI_GELU, None, out=out)
+    torch.cuda.synchronize()
+    pre = oracle.linear(a, w, bias)
+    assert pre.min() < -30 and pre.max() > 30 and (np.abs(pre) < 0.5).any()
+    ref = oracle.gelu(pre)
+    mag = np.abs(oracle.as_f64(a)) @ np.abs(oracle.as_f64(w)).T
+    bound = ulp(ref, dtype) + K * 2.0 ** -23 * mag
+    err = np.abs(to_np(out) - ref)
+    assert (err <= bound).all(), f"worst ratio {(err / bound).max():.3f}"
+
+
 def test_linear_fp16_and_live_rows():
     _gemm_case(333, 384, 192, rb.EPI_GELU, dtype=torch.float16, seed=5)
     _gemm_case(640, 512, 256, rb.EPI_RESIDUAL, live=517, seed=6)     # partial last live tile
