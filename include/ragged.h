@@ -89,7 +89,10 @@ typedef struct {
                       built for long sequences (exact per-chunk tile counts);
                       both variants meet the same tolerance (R2) and are
                       deterministic, but their bits may differ (different
-                      multiply-add contraction).  >= 0. */
+                      multiply-add contraction).  ragged_attn with
+                      RAGGED_ENGINE_AUTO at d = 64 takes the warp-specialised
+                      tcgen05 engine when n_hint > 148 (measured crossover at
+                      DeiT-B).  >= 0. */
 } ragged_problem;
 
 /* a1 -- scan.  Per-image cumulative sums produce cu_seqlens and per-token
@@ -124,8 +127,8 @@ RAGGED_API ragged_status ragged_pack(const ragged_problem* prob, const uint8_t* 
  * head) pair, head fastest (pid -> h = pid mod H, i = pid / H).
  * Shapes: the DeiT path takes d = 64, N <= 256 (one-stage K/V in shared
  * memory).  Other shapes (NEXT row N4) run streaming kernels (Alg. 1's outer
- * loops): at d = 64 and N > 256 (or with RAGGED_ENGINE_TCGEN05_WS at
- * any N) the warp-specialised tcgen05 engine (128-row query tiles, 128-key
+ * loops): at d = 64 and N > 256 (or N <= 256 with n_hint > 148, or
+ * RAGGED_ENGINE_TCGEN05_WS at any N) the warp-specialised tcgen05 engine (128-row query tiles, 128-key
  * K/V blocks by TMA, S/P/O in TMEM) -- it requires qp/kp/vp to hold the
  * B*N-row capacity (rows past cu[B] are read, never used); d in {32, 80,
  * 128} the mma.sync streaming kernel (N up to 2^20, 64-key chunks).  Rows

@@ -96,6 +96,11 @@ cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
 // RAGGED_ENGINE_AUTO -> the engine measured fastest; the
 // mma.sync engine's long-sequence variant when the caller expects > 64 kept
 // tokens per image (ragged_problem.n_hint).
+// ragged_attn / ragged_vit_block AUTO: the warp-specialised tcgen05 engine at
+// d = 64 when the caller expects more than this many kept tokens per image
+// (measured crossover at DeiT-B, scripts/r2/ws_cross.py).
+constexpr int kWsMinHint = 148;
+
 int resolve_engine(const ragged_problem* p) {
   const int e = p->engine == RAGGED_ENGINE_AUTO ? RAGGED_ENGINE_MMA_SYNC : p->engine;
   return (e == RAGGED_ENGINE_MMA_SYNC && p->n_hint > 64) ? ragged::kEngineMmaLong : e;
@@ -162,11 +167,15 @@ ragged_status ragged_attn(const ragged_problem* prob, const void* qp, const void
   RAGGED_TRY(check_ptr_any(cu_seqlens, "cu_seqlens"));
   RAGGED_TRY(check_ptr(op, "op"));
   if ((long long)prob->B * prob->H > 0x7fffffffLL) return fail(RAGGED_ENOTSUP, "B*H too large");
-  // AUTO at head_dim 64 past the one-stage cap (N > 256): the warp-specialised
-  // tcgen05 engine (measured 1.9x the streaming mma.sync kernel at ViT-L/16@384,
-  // 1.6x at N = 1024; at N <= 256 the one-CTA-per-(image, head) kernels win or tie)
+  // AUTO at head_dim 64: the warp-specialised tcgen05 engine past the one-stage
+  // cap (N > 256; measured 2.5x the streaming mma.sync kernel at ViT-L/16@384,
+  // 2.2x at N = 1024) and, at N <= 256, when the caller expects long sequences
+  // (n_hint > kWsMinHint): measured at DeiT-B B = 32 (scripts/r2/ws_cross.py),
+  // n = 197: 22.8 vs 28.4 us, n = 158: 18.3 vs 19.0, n = 138: 17.8 vs 16.5 (the
+  // mma.sync kernels win below ~150 kept tokens per image).
   const bool ws = prob->engine == RAGGED_ENGINE_TCGEN05_WS ||
-                  (prob->engine == RAGGED_ENGINE_AUTO && prob->d == 64 && prob->N > 256);
+                  (prob->engine == RAGGED_ENGINE_AUTO && prob->d == 64 &&
+                   (prob->N > 256 || prob->n_hint > kWsMinHint));
   if (ws) {  // warp-specialised tcgen05 engine (attn_fa.cu)
     if (prob->d != 64) return fail(RAGGED_ENOTSUP, "the warp-specialised engine takes head_dim 64");
     if ((long long)prob->B * prob->H * ((prob->N + 255) / 256) > 0x7fffffffLL)
@@ -642,8 +651,13 @@ ragged_status ragged_vit_block(const ragged_problem* prob, void* x, const int32_
   // for ~B*n_hint live rows, and the long-sequence attention kernel above 64
   const int32_t rh = p.n_hint > 0 ? (int32_t)std::min<long long>((long long)p.B * p.n_hint, rows) : 0;
   RAGGED_TRY(linear_impl((ragged_dtype)p.dtype, rows, 3 * D, D, y, D, w->w_qkv, w->b_qkv, 0, nullptr, 0, qkv, 3 * D, live, st, rh));
-  e = ragged::launch_attn(p.dtype, resolve_engine(&p), qkvb, qkvb + D * 2, qkvb + 2 * D * 2, cu_seqlens, a,
-                          p.B, p.N, p.H, 3LL * D, st, p.n_hint);
+  // attention over the packed qkv rows (row stride 3D): the warp-specialised
+  // tcgen05 engine for long expected sequences (as ragged_attn's AUTO), else mma.sync
+  if (p.d == 64 && p.n_hint > kWsMinHint)
+    e = ragged::launch_attn_fa(p.dtype, qkvb, qkvb + D * 2, qkvb + 2 * D * 2, cu_seqlens, a, p.B, p.N, p.H, 3LL * D, st);
+  else
+    e = ragged::launch_attn(p.dtype, resolve_engine(&p), qkvb, qkvb + D * 2, qkvb + 2 * D * 2, cu_seqlens, a,
+                            p.B, p.N, p.H, 3LL * D, st, p.n_hint);
   if (e != cudaSuccess) return cuda_fail(e, "ragged_vit_block/attn");
   RAGGED_TRY(linear_impl((ragged_dtype)p.dtype, rows, D, D, a, D, w->w_proj, w->b_proj, 2, x, D, x, D, live, st, rh));
   e = ragged::launch_layer_norm(p.dtype, x, D, w->ln2_w, w->ln2_b, 1e-6f, y, D, rows, live, D, st);

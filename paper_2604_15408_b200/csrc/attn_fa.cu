@@ -58,21 +58,24 @@
 namespace ragged {
 
 #ifdef RAGGED_TIMELINE
-// clock64 stamps of CTA-local events (debug build only): per CTA 64 slots --
-// [0, 16) softmax tile A warp 4 lane 0: (S ready, P stored) per block of the
-// first item; [16, 32) tile B warp 8 lane 0 likewise; [32, 48) MMA thread:
-// (P_A seen, PV_A + S_A issued) per block; [48] kernel entry; [49] first S_A
-// issue; [50] first epilogue done (tile A); [51] CTA end; [52] items done.
+// clock64 stamps of CTA-local events (debug build only): per CTA 64 slots,
+// items it < 4 of the CTA, key blocks j < 2 -- [16 x + 4 it + 2 j (+1)] softmax
+// of tile x, warp 4 / 8 lane 0: S ready (P stored); [32 + 4 it] MMA: P_A(0)
+// seen, [+1] PV_A(0) (+ S_A(1)) issued, [+3] S_A(0) issued; [48] kernel entry;
+// [49] first S_A issue; [50 + 4 x + it] epilogue of tile x done; [58] CTA end;
+// [59 + it] producer issues the item's Q tiles; [64 + k] (k < 5) softmax of the
+// first block of tile A, warp 4 lane 0: pass-1 loads landed, row max done,
+// pass-2 chunks 0 / 3 / 7 done.
 constexpr int kFaTlMax = 1024;
-__device__ unsigned long long g_fa_tl[kFaTlMax * 64];
+__device__ unsigned long long g_fa_tl[kFaTlMax * 128];
 #define FTL(slot)                                                        \
   do {                                                                   \
-    if (blockIdx.x < kFaTlMax && (slot) >= 0 && (slot) < 64)             \
-      g_fa_tl[blockIdx.x * 64 + (slot)] = clock64();                     \
+    if (blockIdx.x < kFaTlMax && (slot) >= 0 && (slot) < 128)            \
+      g_fa_tl[blockIdx.x * 128 + (slot)] = clock64();                    \
   } while (0)
 int fa_timeline_copy(void* host, int max_ctas) {
   const int n = max_ctas < kFaTlMax ? max_ctas : kFaTlMax;
-  return cudaMemcpyFromSymbol(host, g_fa_tl, (size_t)n * 64 * 8) == cudaSuccess ? n : -1;
+  return cudaMemcpyFromSymbol(host, g_fa_tl, (size_t)n * 128 * 8) == cudaSuccess ? n : -1;
 }
 #else
 #define FTL(slot) \
@@ -133,6 +136,35 @@ __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
 struct FaItem {
   int b, h, pair, s0, n, rows0, ntile, nb;   // rows0 = first query row of tile A; ntile in {1, 2}; nb = key blocks
 };
+// cu_seqlens of an item's image, loaded one item ahead of its use by the MMA
+// and softmax roles (measured: the L2 round trip of these two loads sat between
+// consecutive items on the critical path, ~0.4-1 us per item at DeiT lengths).
+struct FaCu {
+  int c0, c1;
+};
+__device__ __forceinline__ FaCu fa_cu_load(const FaArgs& a, int it) {
+  FaCu c{0, 0};
+  if (it < a.nitems) {
+    const int b = (it % (a.B * a.H)) / a.H;
+    c.c0 = a.cu[b];
+    c.c1 = a.cu[b + 1];
+  }
+  return c;
+}
+__device__ __forceinline__ bool fa_item_cu(const FaArgs& a, int it, FaCu c, FaItem& I) {
+  const int P = a.B * a.H;
+  I.pair = it / P;
+  const int w = it - I.pair * P;
+  I.b = w / a.H;
+  I.h = w - I.b * a.H;
+  I.s0 = c.c0;
+  I.n = min(max(c.c1 - c.c0, 0), a.N);
+  I.rows0 = I.pair * 2 * kFaRows;
+  if (I.rows0 >= I.n) return false;
+  I.ntile = I.n - I.rows0 > kFaRows ? 2 : 1;
+  I.nb = (I.n + kFaRows - 1) / kFaRows;
+  return true;
+}
 __device__ __forceinline__ bool fa_item(const FaArgs& a, int it, FaItem& I) {
   // pair-major: every problem's first tile pair, then every second pair, ...
   // (empty pairs of short sequences collect at the end of the item range, so
@@ -332,7 +364,10 @@ __device__ __forceinline__ void split_pair<__half>(uint64_t p, uint32_t& hi, uin
 // kFull: all 128 keys valid (no masking).
 template <typename T, bool kFull>
 __device__ __forceinline__ void fa_softmax_block(uint32_t tS, uint32_t tO, int nv, bool first, float& m_ref,
-                                                 float& l) {
+                                                 float& l, bool tl = false) {
+#ifndef RAGGED_TIMELINE
+  (void)tl;
+#endif
   constexpr float kScaleLog2 = 0.18033688011112042f;  // log2(e) / sqrt(64)
   // Partial blocks: only the UMMA's N16 = ceil(nv / 16) * 16 columns exist (and
   // only they feed PV); chunks past them are skipped, masking applies inside.
@@ -346,6 +381,7 @@ __device__ __forceinline__ void fa_softmax_block(uint32_t tS, uint32_t tO, int n
     tc::ld_x32(tS + 64 * hf, *reinterpret_cast<uint32_t(*)[32]>(sr));
     tc::ld_x32(tS + 64 * hf + 32, *reinterpret_cast<uint32_t(*)[32]>(sr + 32));
     tc::wait_ld();
+    if (tl && hf == 0) FTL(64);
 #pragma unroll
     for (int c = 0; c < 64; c += 2) {
       const float a = (kFull || 64 * hf + c < nv) ? __uint_as_float(sr[c]) : -INFINITY;      // keys past n (R4)
@@ -355,6 +391,7 @@ __device__ __forceinline__ void fa_softmax_block(uint32_t tS, uint32_t tO, int n
     }
   }
   const float ms = fmaxf(mx0, mx1) * kScaleLog2;
+  if (tl) FTL(65);
   if (first) {
     m_ref = ms;
   } else {
@@ -408,6 +445,7 @@ __device__ __forceinline__ void fa_softmax_block(uint32_t tS, uint32_t tO, int n
     }
     tc::st_x8(tS + 8 * q, hi);
     tc::st_x8(tS + kFaLoCol + 8 * q, lo);
+    if (tl && (q == 0 || q == 3 || q == 7)) FTL(q == 0 ? 66 : q == 3 ? 67 : 68);
   }
   float s0, s1;
   f2unpack(acc, s0, s1);
@@ -462,6 +500,7 @@ __global__ void __launch_bounds__(kFaThreads, 1)
         const int qb = nitem & 1;
         if (nitem >= 2) tc::mbar_wait(smem_u32(&bars.q_free[qb]), ((nitem >> 1) - 1) & 1);
         const uint32_t qbar = smem_u32(&bars.q_full[qb]);
+        if (nitem < 4) FTL(59 + nitem);
         expect_tx(qbar, I.ntile * kFaTileBytes);
         for (int x = 0; x < I.ntile; ++x)
           tma_2d(smem_u32(smem + kOffQ + (2 * qb + x) * kFaTileBytes), &tq, qbar, I.h * kHeadDim,
@@ -487,9 +526,12 @@ __global__ void __launch_bounds__(kFaThreads, 1)
       uint32_t kv = 0, ph_p[2] = {0u, 0u};
       int nitem = 0;
       const uint32_t idesc_o = tc::idesc_f16(kFmt, kFaRows, kHeadDim, 1);
+      FaCu cn = fa_cu_load(a, blockIdx.x);
       for (int it = blockIdx.x; it < a.nitems; it += gridDim.x) {
+        const FaCu cc = cn;
+        cn = fa_cu_load(a, it + gridDim.x);  // the next item's cu, off the critical path
         FaItem I;
-        if (!fa_item(a, it, I)) continue;
+        if (!fa_item_cu(a, it, cc, I)) continue;
         const int qb = nitem & 1;
         tc::mbar_wait(smem_u32(&bars.q_full[qb]), (nitem >> 1) & 1);
         tc::fence_after();
@@ -511,6 +553,7 @@ __global__ void __launch_bounds__(kFaThreads, 1)
             tc::mma_ss_k64(tmem, qd[0], kd0, idesc_s0);
             tc::commit(smem_u32(&bars.s[0]));
             if (nitem == 0) FTL(49);
+            if (nitem < 4) FTL(32 + 4 * nitem + 3);
           }
           __syncwarp();
         }
@@ -530,7 +573,7 @@ __global__ void __launch_bounds__(kFaThreads, 1)
             tc::mbar_wait(smem_u32(&bars.p[x]), ph_p[x]);
             ph_p[x] ^= 1u;
             tc::fence_after();
-            if (lane == 0 && nitem == 0 && x == 0 && j < 8) FTL(32 + 2 * j);
+            if (lane == 0 && nitem < 4 && x == 0 && j < 1) FTL(32 + 4 * nitem + 2 * j);
             if (x == 0 && j == 0 && I.ntile == 2) {  // the deferred S_B(0)
               if (tc::elect_one()) {
                 tc::mma_ss_k64(tmem + 256u, qd[1], kd0, idesc_s0);
@@ -555,7 +598,7 @@ __global__ void __launch_bounds__(kFaThreads, 1)
             }
             if (tc::elect_one()) {
               tc::commit(smem_u32(&bars.s[x]));  // S(j+1) ready / final O ready
-              if (nitem == 0 && x == 0 && j < 8) FTL(33 + 2 * j);
+              if (nitem < 4 && x == 0 && j < 1) FTL(33 + 4 * nitem + 2 * j);
             }
             __syncwarp();
           }
@@ -575,20 +618,24 @@ __global__ void __launch_bounds__(kFaThreads, 1)
     const uint32_t tS = tmem + 256u * x + lane_off, tO = tS + 128u;
     uint32_t ph_s = 0;
     int nit = 0;
+    FaCu cn = fa_cu_load(a, blockIdx.x);
     for (int it = blockIdx.x; it < a.nitems; it += gridDim.x) {
+      const FaCu cc = cn;
+      cn = fa_cu_load(a, it + gridDim.x);  // the next item's cu, off the critical path
       FaItem I;
-      if (!fa_item(a, it, I)) continue;
+      if (!fa_item_cu(a, it, cc, I)) continue;
       if (x >= I.ntile) continue;
       float m_ref = -INFINITY, l = 0.f;
       for (int j = 0; j < I.nb; ++j) {
         tc::mbar_wait(smem_u32(&bars.s[x]), ph_s);
         ph_s ^= 1u;
         tc::fence_after();
-        if (nit == 0 && q4 == 0 && lane == 0 && j < 8) FTL(16 * x + 2 * j);
+        if (nit < 4 && q4 == 0 && lane == 0 && j < 2) FTL(16 * x + 4 * nit + 2 * j);
         const int nv = min(kFaRows, I.n - j * kFaRows);
 #ifndef RAGGED_FA_ABLATE_SOFTMAX
-        if (nv == kFaRows) fa_softmax_block<T, true>(tS, tO, nv, j == 0, m_ref, l);
-        else fa_softmax_block<T, false>(tS, tO, nv, j == 0, m_ref, l);
+        const bool tl = nit == 0 && j == 0 && x == 0 && q4 == 0 && lane == 0;
+        if (nv == kFaRows) fa_softmax_block<T, true>(tS, tO, nv, j == 0, m_ref, l, tl);
+        else fa_softmax_block<T, false>(tS, tO, nv, j == 0, m_ref, l, tl);
 #else
         l = 1.f;
 #endif
@@ -596,7 +643,7 @@ __global__ void __launch_bounds__(kFaThreads, 1)
         tc::fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(smem_u32(&bars.p[x]));
-        if (nit == 0 && q4 == 0 && lane == 0 && j < 8) FTL(16 * x + 2 * j + 1);
+        if (nit < 4 && q4 == 0 && lane == 0 && j < 2) FTL(16 * x + 4 * nit + 2 * j + 1);
       }
       // final O ready
       tc::mbar_wait(smem_u32(&bars.s[x]), ph_s);
@@ -619,12 +666,12 @@ __global__ void __launch_bounds__(kFaThreads, 1)
         for (int c = 0; c < 8; ++c) st_global_16(dst + c * 16, out[c]);
       }
       tc::fence_before();  // the TMEM reads above precede the next item's UMMAs (ordered by bars.p / bars.s)
-      if (nit == 0 && x == 0 && q4 == 0 && lane == 0) FTL(50);
+      if (nit < 4 && q4 == 0 && lane == 0) FTL(50 + 4 * x + nit);
       ++nit;
     }
   }
   __syncthreads();
-  if (threadIdx.x == 0) FTL(51);
+  if (threadIdx.x == 0) FTL(58);
   tc::fence_after();
   if (warp == 0) tc::dealloc(tmem, 512);
 }

@@ -9,7 +9,7 @@ ap.add_argument("--case", default="vitl")
 ap.add_argument("--engine", type=int, default=3)
 ap.add_argument("--iters", type=int, default=6)
 a = ap.parse_args()
-B, N, H, p = {"vitl": (8, 577, 16, 0.0), "c3p0": (32, 197, 12, 0.0), "n1024": (8, 1024, 12, 0.5)}[a.case]
+B, N, H, p = {"vitl": (8, 577, 16, 0.0), "c3p0": (32, 197, 12, 0.0), "c3p05": (32, 197, 12, 0.5), "c3p08": (32, 197, 12, 0.8), "n1024": (8, 1024, 12, 0.5)}[a.case]
 dev = torch.device("cuda")
 q, k, v, keep = synth.make_inputs(B, N, H, p, "random", "bf16", seed=0)
 kb = keep.bool()

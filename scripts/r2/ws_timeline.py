@@ -11,7 +11,7 @@ sys.argv = [sys.argv[0], "--case", os.environ.get("CASE", "vitl"), "--iters", "3
 exec(open(os.path.join(ROOT, "scripts", "r2", "ws_one.py")).read().replace('print("ok")', ''))
 lib = rb.lib()
 lib.ragged_debug_fa_timeline.argtypes = [ctypes.c_void_p, ctypes.c_int32]
-buf = np.zeros((148, 64), np.uint64)
+buf = np.zeros((148, 128), np.uint64)
 lib.ragged_debug_fa_timeline(buf.ctypes.data, 148)
 t = buf.astype(np.int64)
 res = {}

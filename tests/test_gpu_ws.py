@@ -99,3 +99,17 @@ def test_ws_isolation_and_untouched_rows():
     assert (op[T:] == 7.0).all()
     assert torch.equal(op[:300].view(torch.int16), op2[:300].view(torch.int16))
     assert torch.equal(op[390:T].view(torch.int16), op2[390:T].view(torch.int16))
+
+
+@pytest.mark.parametrize("n_hint,engine", [(197, WS), (158, WS), (138, 1), (39, 1), (0, 1)])
+def test_auto_engine_choice_by_n_hint(n_hint, engine):
+    """AUTO at N <= 256: the warp-specialised engine when the caller expects more
+    than 148 kept tokens per image (measured crossover), the mma.sync kernels
+    otherwise -- the AUTO result is bitwise the chosen engine's (same n_hint)."""
+    pk, cap, cu, N, T = _case([197, 150, 60, 197], 4, "bf16", seed=n_hint)
+    cud = torch.from_numpy(cu.astype(np.int32)).to(DEV)
+    auto = rb.attn(*cap, cud, N, engine=rb.ENGINE_AUTO, n_hint=n_hint)
+    ref = rb.attn(*cap, cud, N, engine=engine, n_hint=n_hint)
+    torch.cuda.synchronize()
+    assert torch.equal(auto[:T].view(torch.int16), ref[:T].view(torch.int16))
+    check_attention(to_np(auto[:T]), oracle.attention(*pk, cu), torch.bfloat16)
