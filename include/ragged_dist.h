@@ -78,7 +78,10 @@ RAGGED_API ragged_status ragged_pack_attend_unpack_gather(const ragged_problem* 
 
 /* ragged_attn (ragged.h) whose packed output rows [cu[b], cu[b+1]) go to
  * out[r] + row * H * d for every rank r (packed all-gather, capacity slots).
- * Bitwise identical rows to ragged_attn on the same inputs and prob. */
+ * Runs the mma.sync engine: bitwise identical rows to ragged_attn on the same
+ * inputs and prob with RAGGED_ENGINE_MMA_SYNC (ragged_attn's AUTO takes the
+ * warp-specialised tcgen05 engine at n_hint > 148, whose rows agree within the
+ * R2 tolerance, not bitwise). */
 RAGGED_API ragged_status ragged_attn_gather(const ragged_problem* prob, const void* qp,
                                             const void* kp, const void* vp,
                                             const int32_t* cu_seqlens, const ragged_gather* g,

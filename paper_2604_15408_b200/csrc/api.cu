@@ -645,11 +645,12 @@ ragged_status ragged_vit_block(const ragged_problem* prob, void* x, const int32_
   void* a = ws + (int64_t)rows * 4 * D * 2;             // [rows, D]   attention output
   void* f = ws + (int64_t)rows * 5 * D * 2;             // [rows, MLP]
   const char* qkvb = static_cast<const char*>(qkv);
-  cudaError_t e = ragged::launch_layer_norm(p.dtype, x, D, w->ln1_w, w->ln1_b, 1e-6f, y, D, rows, live, D, st);
-  if (e != cudaSuccess) return cuda_fail(e, "ragged_vit_block/ln1");
-  // n_hint (expected kept tokens per image, performance only): GEMM tile widths
-  // for ~B*n_hint live rows, and the long-sequence attention kernel above 64
+
+  // n_hint (expected kept tokens per image, performance only): LayerNorm grid and
+  // GEMM tile widths for ~B*n_hint live rows, the attention engine for the length
   const int32_t rh = p.n_hint > 0 ? (int32_t)std::min<long long>((long long)p.B * p.n_hint, rows) : 0;
+  cudaError_t e = ragged::launch_layer_norm(p.dtype, x, D, w->ln1_w, w->ln1_b, 1e-6f, y, D, rows, live, D, st, rh);
+  if (e != cudaSuccess) return cuda_fail(e, "ragged_vit_block/ln1");
   RAGGED_TRY(linear_impl((ragged_dtype)p.dtype, rows, 3 * D, D, y, D, w->w_qkv, w->b_qkv, 0, nullptr, 0, qkv, 3 * D, live, st, rh));
   // attention over the packed qkv rows (row stride 3D): the warp-specialised
   // tcgen05 engine for long expected sequences (as ragged_attn's AUTO), else mma.sync
@@ -660,7 +661,7 @@ ragged_status ragged_vit_block(const ragged_problem* prob, void* x, const int32_
                             p.B, p.N, p.H, 3LL * D, st, p.n_hint);
   if (e != cudaSuccess) return cuda_fail(e, "ragged_vit_block/attn");
   RAGGED_TRY(linear_impl((ragged_dtype)p.dtype, rows, D, D, a, D, w->w_proj, w->b_proj, 2, x, D, x, D, live, st, rh));
-  e = ragged::launch_layer_norm(p.dtype, x, D, w->ln2_w, w->ln2_b, 1e-6f, y, D, rows, live, D, st);
+  e = ragged::launch_layer_norm(p.dtype, x, D, w->ln2_w, w->ln2_b, 1e-6f, y, D, rows, live, D, st, rh);
   if (e != cudaSuccess) return cuda_fail(e, "ragged_vit_block/ln2");
   RAGGED_TRY(linear_impl((ragged_dtype)p.dtype, rows, mlp, D, y, D, w->w_fc1, w->b_fc1, 1, nullptr, 0, f, mlp, live, st, rh));
   RAGGED_TRY(linear_impl((ragged_dtype)p.dtype, rows, D, mlp, f, mlp, w->w_fc2, w->b_fc2, 2, x, D, x, D, live, st, rh));

@@ -32,33 +32,18 @@ namespace ragged {
 // ------------------------------------------------------------ LayerNorm ----
 constexpr int kLnThreads = 256;  // 8 rows (warps) per CTA
 
-template <typename T, int kCPL>  // kCPL: 16-byte chunks per lane (D <= 256 * kCPL)
-__global__ void __launch_bounds__(kLnThreads) layer_norm_kernel(const T* __restrict__ x, long long ldx,
-                                                                 const T* __restrict__ w,
-                                                                 const T* __restrict__ bvec, float eps,
-                                                                 T* __restrict__ y, long long ldy, int M_cap,
-                                                                 const int32_t* __restrict__ m_dev, int D) {
-  pdl_launch_dependents();
-  pdl_wait_prerequisites();
+// One warp per row.  The grid covers the rows the caller expects to be live
+// (rows_hint, performance only) and warps loop over any further live rows, so
+// at a high pruning ratio the dead capacity rows are never read (round 1
+// launched over the whole capacity and every CTA read its rows before seeing
+// the live count: 5.3 us vs 4.4 for torch at T = 1248 of 6304).  The first
+// row's data, gamma and beta are loaded together with the live count: one
+// memory round trip when the hint holds.
+// y row = LN(x row): two-pass fp32 statistics from registers (one warp per row).
+template <typename T, int kCPL>
+__device__ __forceinline__ void ln_row(const uint4 (&raw)[kCPL], const uint4 (&wraw)[kCPL], const uint4 (&braw)[kCPL],
+                                       int nch, int D, float eps, T* __restrict__ yr) {
   const int lane = threadIdx.x & 31;
-  const long long row = (long long)blockIdx.x * (kLnThreads / 32) + (threadIdx.x >> 5);
-  if (row >= M_cap) return;
-  // The row (inside the capacity, so always addressable), gamma and beta are
-  // loaded together with the live count: one memory round trip, not two.
-  const int nch = D >> 3;  // 16-byte chunks per row
-  const T* xr = x + row * ldx;
-  uint4 raw[kCPL], wraw[kCPL], braw[kCPL];
-#pragma unroll
-  for (int i = 0; i < kCPL; ++i) {
-    const int c = lane + 32 * i;
-    if (c < nch) {
-      raw[i] = *reinterpret_cast<const uint4*>(xr + c * 8);
-      wraw[i] = ld_global_nc_16(w + c * 8);
-      braw[i] = ld_global_nc_16(bvec + c * 8);
-    }
-  }
-  const int M = m_dev ? min(*m_dev, M_cap) : M_cap;
-  if (row >= M) return;
   float v[kCPL][8];
   float s = 0.f;
 #pragma unroll
@@ -96,7 +81,6 @@ __global__ void __launch_bounds__(kLnThreads) layer_norm_kernel(const T* __restr
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) q += __shfl_xor_sync(0xffffffffu, q, o);
   const float rstd = rsqrtf(q / (float)D + eps);
-  T* yr = y + row * ldy;
 #pragma unroll
   for (int i = 0; i < kCPL; ++i) {
     const int c = lane + 32 * i;
@@ -107,11 +91,53 @@ __global__ void __launch_bounds__(kLnThreads) layer_norm_kernel(const T* __restr
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         const float2 gw = unpack2<T>(ww[j]), gb = unpack2<T>(bw[j]);
-        o[j] = pack2<T>((v[i][2 * j] - mean) * rstd * gw.x + gb.x,
-                        (v[i][2 * j + 1] - mean) * rstd * gw.y + gb.y);
+        o[j] = pack2<T>((v[i][2 * j] - mean) * rstd * gw.x + gb.x, (v[i][2 * j + 1] - mean) * rstd * gw.y + gb.y);
       }
       st_global_16(yr + c * 8, make_uint4(o[0], o[1], o[2], o[3]));
     }
+  }
+}
+
+// One warp per row.  The grid covers the rows the caller expects to be live
+// (rows_hint, performance only) and warps loop over any further live rows, so
+// at a high pruning ratio the dead capacity rows are never read (round 1
+// launched over the whole capacity and every CTA read its rows before seeing
+// the live count).  The first row's data, gamma and beta are loaded together
+// with the live count: one memory round trip when the hint holds.
+template <typename T, int kCPL>  // kCPL: 16-byte chunks per lane (D <= 256 * kCPL)
+__global__ void __launch_bounds__(kLnThreads) layer_norm_kernel(const T* __restrict__ x, long long ldx,
+                                                                 const T* __restrict__ w,
+                                                                 const T* __restrict__ bvec, float eps,
+                                                                 T* __restrict__ y, long long ldy, int M_cap,
+                                                                 const int32_t* __restrict__ m_dev, int D) {
+  pdl_launch_dependents();
+  pdl_wait_prerequisites();
+  const int lane = threadIdx.x & 31;
+  long long row = (long long)blockIdx.x * (kLnThreads / 32) + (threadIdx.x >> 5);
+  if (row >= M_cap) return;
+  const int nch = D >> 3;  // 16-byte chunks per row
+  uint4 raw[kCPL], wraw[kCPL], braw[kCPL];
+#pragma unroll
+  for (int i = 0; i < kCPL; ++i) {
+    const int c = lane + 32 * i;
+    if (c < nch) {
+      raw[i] = *reinterpret_cast<const uint4*>(x + row * ldx + c * 8);  // inside the capacity: addressable
+      wraw[i] = ld_global_nc_16(w + c * 8);
+      braw[i] = ld_global_nc_16(bvec + c * 8);
+    }
+  }
+  const int M = m_dev ? min(*m_dev, M_cap) : M_cap;
+  if (row >= M) return;
+  ln_row<T, kCPL>(raw, wraw, braw, nch, D, eps, y + row * ldy);
+  // rows past the grid's first pass (the live count exceeded the hint)
+  const long long stride = (long long)gridDim.x * (kLnThreads / 32);
+  for (row += stride; row < M; row += stride) {
+#pragma unroll
+    for (int i = 0; i < kCPL; ++i) {
+      const int c = lane + 32 * i;
+      if (c < nch) raw[i] = *reinterpret_cast<const uint4*>(x + row * ldx + c * 8);
+    }
+    ln_row<T, kCPL>(raw, wraw, braw, nch, D, eps, y + row * ldy);
   }
 }
 
@@ -609,9 +635,11 @@ static cudaError_t launch_pdl_b(void (*kern)(KArgs...), dim3 grid, dim3 block, s
 
 cudaError_t launch_layer_norm(int dtype, const void* x, long long ldx, const void* w, const void* b,
                               float eps, void* y, long long ldy, int M_cap, const int32_t* m_dev, int D,
-                              cudaStream_t st) {
+                              cudaStream_t st, int rows_hint) {
   const int rows_per = kLnThreads / 32;
-  const dim3 grid((M_cap + rows_per - 1) / rows_per);
+  // grid for the expected live rows (+1/8 margin), never more than the capacity
+  const int cover = (m_dev != nullptr && rows_hint > 0) ? std::min(M_cap, rows_hint + rows_hint / 8 + rows_per) : M_cap;
+  const dim3 grid((cover + rows_per - 1) / rows_per);
   const int cpl = (D / 8 + 31) / 32;
 #define RAGGED_LN(TT, C)                                                                             \
   return launch_pdl_b(layer_norm_kernel<TT, C>, grid, dim3(kLnThreads), 0, st, (const TT*)x, ldx,  \

@@ -82,7 +82,7 @@ int gemm_pick_bn(int M_cap, int N, int sms);
 int gemm_pick_split(int M_hint, int N, int K, int sms, int* bn);
 cudaError_t launch_layer_norm(int dtype, const void* x, long long ldx, const void* w, const void* b,
                               float eps, void* y, long long ldy, int M_cap, const int32_t* m_dev, int D,
-                              cudaStream_t st);
+                              cudaStream_t st, int rows_hint = 0);  // rows_hint: expected live rows (performance only)
 cudaError_t launch_keep_topk_l2(int dtype, const void* x, long long ld, int B, int N, int D, int k,
                                 uint8_t* keep, cudaStream_t st);
 // NEXT row N2 (prune.cu): EViT keep mask + fused token written into q/k/v

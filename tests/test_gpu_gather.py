@@ -230,15 +230,17 @@ def test_library_nccl_allgather_world1_bitwise():
 def test_gather_kernel_variant_follows_n_hint(n_hint):
     """the gather entry points pick the same kernel variant as the
     local call for the same prob (the long-sequence variant for n_hint > 64),
-    so the gathered rows are bitwise those of ragged_pack_attend_unpack and
-    ragged_attn with that n_hint."""
+    so the gathered rows are bitwise those of ragged_pack_attend_unpack and of
+    ragged_attn on the mma.sync engine with that n_hint."""
     B, N, H = 6, 197, 12
     q, k, v, keep = _inputs(B, N, H, 0.0 if n_hint == 197 else 0.8, seed=31)
     ref = rb.pack_attend_unpack(q, k, v, keep, n_hint=n_hint)
     o = _sentinel((B, N, H, 64), q.dtype)
     rb.pack_attend_unpack_gather(q, k, v, keep, rb.gather_desc(1, 0, out=[o]), n_hint=n_hint)
     qp, kp, vp, cu, _, _ = rb.pack(q, k, v, keep)
-    refp = rb.attn(qp, kp, vp, cu, N, n_hint=n_hint)
+    # the gather kernels run the mma.sync engine: compare with ragged_attn on that
+    # engine (AUTO takes the warp-specialised engine at n_hint > 148)
+    refp = rb.attn(qp, kp, vp, cu, N, n_hint=n_hint, engine=rb.ENGINE_MMA_SYNC)
     op = _sentinel((B * N, H, 64), q.dtype)
     rb.attn_gather(qp, kp, vp, cu, N, rb.gather_desc(1, 0, out=[op]), n_hint=n_hint)
     torch.cuda.synchronize()
