@@ -421,7 +421,7 @@ def traffic_from_profile():
     """DRAM bytes (read + write) per launch of the fused kernel, measured by ncu
     over a WINDOW of 64 back-to-back launches with 16 rotating sets so the
     padded-O write-back is counted (profiles/r02/r02_ncu_window_traffic.json,
-    scripts/r2/gpu_final.sh; a single-launch ncu --set full capture sees ~0
+    re-measured identically by scripts/gpu_validate.sh in session 3; a single-launch ncu --set full capture sees ~0
     written bytes because the 9.7 MB of O stay in L2 until later launches)."""
     p = os.path.join(ROOT, "profiles", "r02", "r02_ncu_window_traffic.json")
     try:
@@ -993,6 +993,18 @@ def extras(args, rb, torch, dev, sets, c, B, N, H, dt, T):
         rb.keep_topk_l2(xs[j % NX], kk, keep=keeps[j % N_SETS])
         rb.pack_attend_unpack(s["q"], s["k"], s["v"], keeps[j % N_SETS], o=s["o"], cu=s["cu"], n_hint=kk)
     out["prune_then_fused_us"] = _graph_time(torch, [(lambda j=j: prune_fused(j)) for j in range(L)], reps)
+    # the row-parallel mask kernel (ragged_keep_topk_l2_ws: no cluster, scores in a
+    # caller workspace, each image ranked by the CTA that completes it), alone and ahead
+    l2ws = rb.l2_workspace(B, N, dev)
+    out["prune_l2_mask_ws_us"] = _graph_time(torch, [(lambda j=j: rb.keep_topk_l2(
+        xs[j % NX], kk, keep=keeps[j % N_SETS], workspace=l2ws)) for j in range(L)], reps)
+    out["prune_l2_mask_ws_hbm_frac"] = l2b / (out["prune_l2_mask_ws_us"] * 1e-6) / 1e9 / _hbm_peak()
+
+    def prune_ws_fused(j):
+        s = sets[j % N_SETS]
+        rb.keep_topk_l2(xs[j % NX], kk, keep=keeps[j % N_SETS], workspace=l2ws)
+        rb.pack_attend_unpack(s["q"], s["k"], s["v"], keeps[j % N_SETS], o=s["o"], cu=s["cu"], n_hint=kk)
+    out["prune_ws_then_fused_us"] = _graph_time(torch, [(lambda j=j: prune_ws_fused(j)) for j in range(L)], reps)
     # the mask computed inside the fused launch (one cluster of H CTAs per image)
     def prune_in_fused(j):
         s = sets[j % N_SETS]
