@@ -993,18 +993,6 @@ def extras(args, rb, torch, dev, sets, c, B, N, H, dt, T):
         rb.keep_topk_l2(xs[j % NX], kk, keep=keeps[j % N_SETS])
         rb.pack_attend_unpack(s["q"], s["k"], s["v"], keeps[j % N_SETS], o=s["o"], cu=s["cu"], n_hint=kk)
     out["prune_then_fused_us"] = _graph_time(torch, [(lambda j=j: prune_fused(j)) for j in range(L)], reps)
-    # the row-parallel mask kernel (ragged_keep_topk_l2_ws: no cluster, scores in a
-    # caller workspace, each image ranked by the CTA that completes it), alone and ahead
-    l2ws = rb.l2_workspace(B, N, dev)
-    out["prune_l2_mask_ws_us"] = _graph_time(torch, [(lambda j=j: rb.keep_topk_l2(
-        xs[j % NX], kk, keep=keeps[j % N_SETS], workspace=l2ws)) for j in range(L)], reps)
-    out["prune_l2_mask_ws_hbm_frac"] = l2b / (out["prune_l2_mask_ws_us"] * 1e-6) / 1e9 / _hbm_peak()
-
-    def prune_ws_fused(j):
-        s = sets[j % N_SETS]
-        rb.keep_topk_l2(xs[j % NX], kk, keep=keeps[j % N_SETS], workspace=l2ws)
-        rb.pack_attend_unpack(s["q"], s["k"], s["v"], keeps[j % N_SETS], o=s["o"], cu=s["cu"], n_hint=kk)
-    out["prune_ws_then_fused_us"] = _graph_time(torch, [(lambda j=j: prune_ws_fused(j)) for j in range(L)], reps)
     # the mask computed inside the fused launch (one cluster of H CTAs per image)
     def prune_in_fused(j):
         s = sets[j % N_SETS]

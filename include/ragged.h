@@ -214,22 +214,6 @@ RAGGED_API void ragged_graph_destroy(ragged_graph* graph);
 RAGGED_API ragged_status ragged_keep_topk_l2(const ragged_problem* prob, const void* x, int32_t k,
                                              uint8_t* keep, void* stream);
 
-/* The same Threshold-l2 mask as ragged_keep_topk_l2 (identical definition and
- * ties; bitwise the same keep rows), row-parallel without a thread-block
- * cluster: 16 token rows per CTA over the whole batch, the scores (fp32
- * ||x||^2, CLS = +inf, NaN last) written to the caller's workspace, and the CTA
- * that completes an image (per-image arrival counter) ranks its N scores and
- * writes the keep row.  workspace: ragged_keep_topk_l2_workspace(prob) bytes
- * (B*N floats + B uint32 counters), 4-byte aligned, caller-owned; the counters
- * must be zero before the first call (e.g. cudaMemset once) and every call
- * leaves them zero, so one workspace serves any number of stream-ordered calls
- * (not concurrent calls on different streams).  D = H*d <= 2048 (else
- * RAGGED_ENOTSUP); k < 1 -> RAGGED_EINVAL; ws_bytes too small -> RAGGED_EINVAL. */
-RAGGED_API int64_t ragged_keep_topk_l2_workspace(const ragged_problem* prob);
-RAGGED_API ragged_status ragged_keep_topk_l2_ws(const ragged_problem* prob, const void* x, int32_t k,
-                                                uint8_t* keep, void* workspace, int64_t ws_bytes,
-                                                void* stream);
-
 /* NEXT row N2 fused ahead of the scan -- Threshold-l2 pruning + a1-a4 in ONE
  * launch (the prune step produces the keep mask, then the ragged
  * path runs on the survivors).  The keep row of every image is computed inside

@@ -107,7 +107,6 @@ def _load() -> ctypes.CDLL:
         "ragged_graph_launch": [V, V],
         "ragged_empty_launch": [I32, I32, V],
         "ragged_keep_topk_l2": [P, V, I32, V, V],
-        "ragged_keep_topk_l2_ws": [P, V, I32, V, V, I64, V],
         "ragged_keep_evit": [P, V, V, V, I32, V, V],
         "ragged_prune_l2_pack_attend_unpack": [P, V, I64, I32, V, V, V, V, V, V, V],
         "ragged_validate_cu_seqlens": [ctypes.POINTER(I32), I32, I64],
@@ -132,8 +131,6 @@ def _load() -> ctypes.CDLL:
         f.restype = ctypes.c_int32
     lib.ragged_vit_block_workspace.argtypes = [P, I32]
     lib.ragged_vit_block_workspace.restype = ctypes.c_int64
-    lib.ragged_keep_topk_l2_workspace.argtypes = [P]
-    lib.ragged_keep_topk_l2_workspace.restype = ctypes.c_int64
     lib.ragged_graph_destroy.argtypes = [V]
     lib.ragged_graph_destroy.restype = None
     lib.ragged_dist_nccl_destroy.argtypes = [V]
@@ -153,7 +150,7 @@ EXPORTS = ("ragged_scan", "ragged_pack", "ragged_attn", "ragged_unpack", "ragged
            "ragged_pack_attend_unpack_host", "ragged_attn_fp8",
            "ragged_graph_create", "ragged_graph_launch", "ragged_graph_destroy", "ragged_empty_launch",
            "ragged_validate_cu_seqlens", "ragged_status_str", "ragged_last_error", "ragged_build_info",
-           "ragged_keep_topk_l2", "ragged_keep_topk_l2_ws", "ragged_keep_topk_l2_workspace", "ragged_keep_evit", "ragged_prune_l2_pack_attend_unpack", "ragged_pack_attend_unpack_gather", "ragged_attn_gather",
+           "ragged_keep_topk_l2", "ragged_keep_evit", "ragged_prune_l2_pack_attend_unpack", "ragged_pack_attend_unpack_gather", "ragged_attn_gather",
            "ragged_layer_norm", "ragged_linear", "ragged_vit_block_workspace", "ragged_vit_block",
            "ragged_pack_rows", "ragged_cls_rows", "ragged_dist_nccl_available", "ragged_dist_nccl_unique_id",
            "ragged_dist_nccl_init", "ragged_dist_nccl_init_all", "ragged_dist_nccl_destroy",
@@ -600,8 +597,7 @@ class VitPrunedForward:
     PDL-chained on one stream, capturable in one CUDA graph):
       1. layers [0, prune_at): dense blocks on all B*N rows (ragged_vit_block with
          the all-kept cu_seqlens b*N -- packed == padded);
-      2. Threshold-l2 keep mask of the hidden state (ragged_keep_topk_l2_ws, the
-         row-parallel kernel with a workspace allocated here; k kept);
+      2. Threshold-l2 keep mask of the hidden state (ragged_keep_topk_l2, k kept);
       3. pack the hidden state once (ragged_pack_rows);
       4. layers [prune_at, L): packed blocks (ragged_vit_block on cu);
       5. CLS rows from the packed buffer (ragged_cls_rows).
@@ -623,14 +619,13 @@ class VitPrunedForward:
         self.dst = torch.empty(B * N, dtype=torch.int32, device=dev)
         self.src = torch.empty(B * N, dtype=torch.int32, device=dev)
         self.cls = torch.empty(B, D, dtype=dtype, device=dev)
-        self.l2ws = l2_workspace(B, N, dev)
 
     def run(self, stream=None):
         """Steps 1-5 on the resident input self.x (no host sync)."""
         for blk in self.dense:
             blk(self.x, self.cu_all, stream)
         x3 = self.x.view(self.B, self.N, self.D)
-        keep_topk_l2(x3, self.k, keep=self.keep, stream=stream, workspace=self.l2ws)
+        keep_topk_l2(x3, self.k, keep=self.keep, stream=stream)
         pack_rows(x3, self.keep, xp=self.xp, cu=self.cu, dst=self.dst, src=self.src, stream=stream)
         for blk in self.packed:
             blk(self.xp, self.cu, stream)
@@ -701,21 +696,9 @@ class Graph:
             pass
 
 
-def l2_workspace(B: int, N: int, device) -> torch.Tensor:
-    """Zeroed workspace for keep_topk_l2(..., workspace=): B*N fp32 scores + B
-    arrival counters (every call leaves the counters zero)."""
-    p = problem(B, N, 1, 64)
-    nbytes = lib().ragged_keep_topk_l2_workspace(ctypes.byref(p))
-    if nbytes < 0:
-        raise ValueError("invalid B, N")
-    return torch.zeros(max(nbytes, 16), dtype=torch.uint8, device=device)
-
-
-def keep_topk_l2(x, k: int, keep=None, stream=None, workspace=None):
+def keep_topk_l2(x, k: int, keep=None, stream=None):
     """N2: Threshold-l2 keep mask from hidden states
-    x [B, N, D] (token stride x.stride(1)) -> uint8 keep [B, N].  With a
-    workspace (l2_workspace(B, N, device)) the row-parallel kernel runs
-    (ragged_keep_topk_l2_ws: no cluster; the same mask), else the cluster kernel."""
+    x [B, N, D] (token stride x.stride(1)) -> uint8 keep [B, N]."""
     if x.dim() != 3 or x.stride(2) != 1 or x.dtype not in _DTYPE:
         raise ValueError("x must be [B, N, D] bf16/fp16 with unit feature stride")
     B, N, D = x.shape
@@ -724,13 +707,6 @@ def keep_topk_l2(x, k: int, keep=None, stream=None, workspace=None):
     keep = torch.empty(B, N, dtype=torch.uint8, device=x.device) if keep is None else keep
     _require(keep, "keep", torch.uint8, x.device, shape=(B, N))
     p = problem(B, N, D // 64, 64, x.dtype, x.stride(1))
-    if workspace is not None:
-        need = lib().ragged_keep_topk_l2_workspace(ctypes.byref(p))
-        _require(workspace, "workspace", torch.uint8, x.device, numel=need)
-        _check(lib().ragged_keep_topk_l2_ws(ctypes.byref(p), x.data_ptr(), int(k), keep.data_ptr(),
-                                            workspace.data_ptr(), workspace.numel(), _stream(stream)),
-               "ragged_keep_topk_l2_ws")
-        return keep
     _check(lib().ragged_keep_topk_l2(ctypes.byref(p), x.data_ptr(), int(k), keep.data_ptr(),
                                      _stream(stream)), "ragged_keep_topk_l2")
     return keep

@@ -396,28 +396,6 @@ ragged_status ragged_keep_topk_l2(const ragged_problem* prob, const void* x, int
   return e == cudaSuccess ? RAGGED_OK : cuda_fail(e, "ragged_keep_topk_l2");
 }
 
-int64_t ragged_keep_topk_l2_workspace(const ragged_problem* prob) {
-  if (prob == nullptr || prob->B < 0 || prob->N < 1) return -1;
-  return ragged::l2_rows_workspace_bytes(prob->B, prob->N);
-}
-
-ragged_status ragged_keep_topk_l2_ws(const ragged_problem* prob, const void* x, int32_t k, uint8_t* keep,
-                                     void* workspace, int64_t ws_bytes, void* stream) {
-  RAGGED_TRY(check_problem(prob));
-  if (k < 1) return fail(RAGGED_EINVAL, "k < 1 (CLS always survives)");
-  if ((long long)prob->H * prob->d > 2048) return fail(RAGGED_ENOTSUP, "D = H*d > 2048");
-  if ((long long)prob->B * prob->N > (1LL << 31) - 16) return fail(RAGGED_ENOTSUP, "B*N too large");
-  if (ws_bytes < ragged::l2_rows_workspace_bytes(prob->B, prob->N)) return fail(RAGGED_EINVAL, "workspace too small");
-  if (prob->B == 0) return RAGGED_OK;
-  RAGGED_TRY(check_ptr(x, "x"));
-  RAGGED_TRY(check_ptr_any(keep, "keep"));
-  RAGGED_TRY(check_ptr_any(workspace, "workspace"));
-  if (reinterpret_cast<uintptr_t>(workspace) % 4 != 0) return fail(RAGGED_EALIGN, "workspace must be 4-byte aligned");
-  cudaError_t e = ragged::launch_keep_topk_l2_rows(prob->dtype, x, prob->ld, prob->B, prob->N, prob->H * prob->d, k,
-                                                   workspace, keep, as_stream(stream));
-  return e == cudaSuccess ? RAGGED_OK : cuda_fail(e, "ragged_keep_topk_l2_ws");
-}
-
 ragged_status ragged_keep_evit(const ragged_problem* prob, void* q, void* k, void* v, int32_t k_keep,
                                uint8_t* keep, void* stream) {
   RAGGED_TRY(check_problem(prob));

@@ -86,10 +86,6 @@ cudaError_t launch_layer_norm(int dtype, const void* x, long long ldx, const voi
 cudaError_t launch_keep_topk_l2(int dtype, const void* x, long long ld, int B, int N, int D, int k,
                                 uint8_t* keep, cudaStream_t st);
 // NEXT row N2 (prune.cu): EViT keep mask + fused token written into q/k/v
-// Threshold-l2 mask without a cluster (workspace: B*N fp32 scores + B zeroed u32 counters)
-long long l2_rows_workspace_bytes(int B, int N);
-cudaError_t launch_keep_topk_l2_rows(int dtype, const void* x, long long ld, int B, int N, int D, int k,
-                                     void* workspace, uint8_t* keep, cudaStream_t st);
 cudaError_t launch_keep_evit(int dtype, void* q, void* k, void* v, long long ld, int B, int N, int H, int kk,
                              uint8_t* keep, cudaStream_t st);
 int l2_smem_bytes(int N, int D);      // must be <= 227 KB (checked in api.cu)

@@ -230,106 +230,6 @@ __global__ void __launch_bounds__(kPThr) keep_l2_cluster_kernel(const T* __restr
   PTL(6);
 }
 
-// ------------------------------------------------- l2, row-parallel --------
-// The same mask (R20) without a cluster: CTA c scores the flattened token rows
-// [16 c, 16 c + 16) of the batch (2 rows per warp, each lane 16-byte chunks
-// lane, lane + 32, ...), writes them to the caller's workspace, and counts
-// them into the image's arrival counter; the CTA whose count completes an
-// image ranks its N scores (one thread per token) and writes the keep row,
-// then zeroes the counter for the next launch.  No cluster co-scheduling and
-// no DSMEM barrier: the rows are read at full-grid parallelism (the cluster
-// kernel's 1-us row staging and 0.8-us cluster barrier are what bound it).
-constexpr int kRwRowsPerWarp = 2;
-constexpr int kRwRows = (kPThr / 32) * kRwRowsPerWarp;  // 16 rows per CTA
-constexpr int kRwMaxChunks = 8;                        // 16-byte chunks per lane: D <= 2048
-
-template <typename T>
-__global__ void __launch_bounds__(kPThr) keep_l2_rows_kernel(const T* __restrict__ x, long long ld, int B, int N,
-                                                              int D, int k, float* __restrict__ scores,
-                                                              unsigned* __restrict__ counts,
-                                                              uint8_t* __restrict__ keep) {
-  __shared__ float s_sc[kMaxN];
-  __shared__ int s_img[kRwRows + 1], s_nimg;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const long long total = (long long)B * N;
-  const long long r0 = (long long)blockIdx.x * kRwRows;
-  const long long r1 = r0 + kRwRows < total ? r0 + kRwRows : total;
-  const int cpr = D >> 3;  // 16-byte chunks per row
-  pdl_launch_dependents();
-#ifndef RAGGED_NO_KEEP_PREFETCH
-  // own rows into L2 before the grid-dependency wait (prefetch only; values are read after it)
-  for (int i = tid; i < kRwRows * (cpr >> 3); i += kPThr) {
-    const long long r = r0 + i / (cpr >> 3);
-    if (r < r1) prefetch_l2(reinterpret_cast<const char*>(x + (r / N) * N * ld + (r % N) * ld) + (i % (cpr >> 3)) * 128);
-  }
-#endif
-  pdl_wait_prerequisites();
-  if (tid == 0) s_nimg = 0;
-  {
-    uint4 raw[kRwRowsPerWarp][kRwMaxChunks];
-#pragma unroll
-    for (int i = 0; i < kRwRowsPerWarp; ++i) {
-      const long long r = r0 + warp + (kPThr / 32) * i;
-      const long long rr = r < r1 ? r : r1 - 1;  // clamped: always addressable, result discarded
-      const T* row = x + (rr / N) * N * ld + (rr % N) * ld;
-#pragma unroll
-      for (int j = 0; j < kRwMaxChunks; ++j) {
-        const int c = lane + 32 * j;
-        if (c < cpr) raw[i][j] = ld_global_nc_16(row + c * 8);
-      }
-    }
-#pragma unroll
-    for (int i = 0; i < kRwRowsPerWarp; ++i) {
-      // the cluster kernel's order exactly (per-chunk fma chain, chunks added in
-      // lane + 32 j order, then the xor tree): the same fp32 scores, so the same
-      // keep rows bit for bit
-      float a = 0.f;
-#pragma unroll
-      for (int j = 0; j < kRwMaxChunks; ++j) {
-        if (lane + 32 * j < cpr) {
-          const T* e = reinterpret_cast<const T*>(&raw[i][j]);
-          float c = 0.f;
-#pragma unroll
-          for (int t = 0; t < 8; ++t) {
-            const float f = static_cast<float>(e[t]);
-            c = fmaf(f, f, c);
-          }
-          a += c;
-        }
-      }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
-      const long long r = r0 + warp + (kPThr / 32) * i;
-      // ||x||^2 ranks like ||x|| (R20); CLS is +inf so it always survives (R6); NaN last (R25)
-      if (lane == 0 && r < r1) {
-        scores[r] = (r % N) == 0 ? INFINITY : nan_low(a);
-        __threadfence();  // the score is visible device-wide before this CTA's count
-      }
-    }
-  }
-  __syncthreads();
-  if (tid == 0) {
-    // count this CTA's rows into every image they belong to; remember the
-    // images this CTA completes (each image is completed by exactly one CTA)
-    for (long long b = r0 / N; b * N < r1; ++b) {
-      const long long lo = b * N > r0 ? b * N : r0, hi = (b + 1) * N < r1 ? (b + 1) * N : r1;
-      const unsigned cnt = (unsigned)(hi - lo);
-      if (atomicAdd(&counts[b], cnt) + cnt == (unsigned)N) s_img[s_nimg++] = (int)b;
-    }
-    __threadfence();  // acquire side: the other CTAs' scores are read after this
-  }
-  __syncthreads();
-  const int nimg = s_nimg;
-  for (int m = 0; m < nimg; ++m) {
-    const int b = s_img[m];
-    for (int n = tid; n < N; n += kPThr) s_sc[n] = __ldcg(scores + (long long)b * N + n);
-    __syncthreads();
-    for (int n = tid; n < N; n += kPThr) keep[(long long)b * N + n] = group_rank(s_sc, n, 0, N, 1, 0) < k ? 1 : 0;
-    if (tid == 0) counts[b] = 0u;  // ready for the next launch (stream-ordered)
-    __syncthreads();
-  }
-}
-
 // -------------------------------------------------------------- EViT --------
 // Dynamic shared memory: s_qc [D] floats (the CLS query) | s_red [kPC][3H][8]
 // floats (partial fused-token sums pushed by every CTA to the owner of each
@@ -589,29 +489,6 @@ cudaError_t launch_keep_topk_l2(int dtype, const void* x, long long ld, int B, i
   if (e != cudaSuccess) return e;
   return launch_cluster_pdl(keep_l2_cluster_kernel<__half>, B * kPC, smem, st, static_cast<const __half*>(x), ld,
                             N, D, k, keep);
-}
-
-long long l2_rows_workspace_bytes(int B, int N) { return 4LL * B * N + 4LL * B; }
-
-cudaError_t launch_keep_topk_l2_rows(int dtype, const void* x, long long ld, int B, int N, int D, int k,
-                                     void* workspace, uint8_t* keep, cudaStream_t st) {
-  float* scores = static_cast<float*>(workspace);
-  unsigned* counts = reinterpret_cast<unsigned*>(scores + (long long)B * N);
-  const long long grid = ((long long)B * N + kRwRows - 1) / kRwRows;
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)grid);
-  cfg.blockDim = dim3(kPThr);
-  cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  if (dtype == 0)
-    return cudaLaunchKernelEx(&cfg, keep_l2_rows_kernel<__nv_bfloat16>, static_cast<const __nv_bfloat16*>(x), ld,
-                              B, N, D, k, scores, counts, keep);
-  return cudaLaunchKernelEx(&cfg, keep_l2_rows_kernel<__half>, static_cast<const __half*>(x), ld, B, N, D, k, scores,
-                            counts, keep);
 }
 
 cudaError_t launch_keep_evit(int dtype, void* q, void* k, void* v, long long ld, int B, int N, int H, int kk,

@@ -285,15 +285,6 @@ def test_round2_entry_validation():
     assert lib.ragged_keep_evit(ctypes.byref(rb.problem(0, 197, 12)), None, None, None, 5, None, None) == rb.OK
     # ragged_keep_topk_l2: k < 1
     assert lib.ragged_keep_topk_l2(ctypes.byref(p), FAKE, 0, FAKE, None) == rb.EINVAL
-    # ragged_keep_topk_l2_ws: k < 1, workspace too small, misaligned, D > 2048; size query
-    need = lib.ragged_keep_topk_l2_workspace(ctypes.byref(p))
-    assert need == 4 * p.B * p.N + 4 * p.B
-    fw = lib.ragged_keep_topk_l2_ws
-    assert fw(ctypes.byref(p), FAKE, 0, FAKE, FAKE, need, None) == rb.EINVAL
-    assert fw(ctypes.byref(p), FAKE, 5, FAKE, FAKE, need - 1, None) == rb.EINVAL
-    assert fw(ctypes.byref(p), FAKE, 5, FAKE, FAKE + 2, need, None) == rb.EALIGN
-    assert fw(ctypes.byref(rb.problem(4, 197, 33)), FAKE, 5, FAKE, FAKE, 1 << 20, None) == rb.ENOTSUP
-    assert fw(ctypes.byref(rb.problem(0, 197, 12)), None, 5, None, None, 0, None) == rb.OK
     # ragged_prune_l2_pack_attend_unpack: k < 1, H > 16, ldx < H*d, ldx alignment, the WS engine
     f = lib.ragged_prune_l2_pack_attend_unpack
     assert f(ctypes.byref(p), FAKE, 768, 0, FAKE, FAKE, FAKE, FAKE, None, None, None) == rb.EINVAL

@@ -350,44 +350,6 @@ def test_keep_topk_l2_ties_and_k_edges():
     assert got.sum(1).tolist() == [4, 4]
 
 
-@pytest.mark.parametrize("dtype", ["bf16", "fp16"])
-@pytest.mark.parametrize("B,N,D,p", [(32, 197, 768, 0.8), (4, 197, 192, 0.5), (7, 33, 64, 0.3),
-                                     (3, 256, 1024, 0.9), (2, 1, 64, 0.0), (300, 197, 768, 0.7), (5, 17, 2048, 0.5)])
-def test_keep_topk_l2_workspace_kernel(dtype, B, N, D, p):
-    """ragged_keep_topk_l2_ws (row-parallel, per-image last-CTA ranking) writes
-    the cluster kernel's mask bit for bit (same fp32 score order, same ranks),
-    within the oracle's definition; it leaves the arrival counters zero, so the
-    workspace is reusable across back-to-back calls on one stream."""
-    k = synth.kept_tokens(N, p)
-    ws = rb.l2_workspace(B, N, DEV)
-    for seed in (5, 6, 7):
-        x = synth.hidden_states(B, N, D, dtype, seed=seed)
-        xd = x.to(DEV)
-        a = rb.keep_topk_l2(xd, k)
-        b = rb.keep_topk_l2(xd, k, workspace=ws)
-        torch.cuda.synchronize()
-        assert torch.equal(a, b)
-        _check_l2_mask(x, k, b.cpu().numpy())
-    counts = ws[4 * B * N:4 * B * N + 4 * B]
-    assert int(counts.sum()) == 0
-
-
-def test_keep_topk_l2_workspace_ties_nan_and_validation():
-    x = torch.zeros(2, 9, 64, dtype=torch.bfloat16)
-    x[:, 1:, 0] = 1.0
-    x[1, 5, 0] = 2.0
-    x[0, 2, 3] = float("nan")
-    ws = rb.l2_workspace(2, 9, DEV)
-    got = rb.keep_topk_l2(x.to(DEV), 4, workspace=ws).cpu().numpy()
-    assert got[0].tolist() == [1, 1, 0, 1, 1, 0, 0, 0, 0]        # NaN ranks last, ties to the lower position
-    assert got[1].tolist() == [1, 1, 1, 0, 0, 1, 0, 0, 0]
-    assert rb.keep_topk_l2(x.to(DEV), 50, workspace=ws).cpu().numpy().sum() == 18
-    with pytest.raises(rb.RaggedError):
-        rb.keep_topk_l2(x.to(DEV), 0, workspace=ws)
-    with pytest.raises(ValueError):
-        rb.keep_topk_l2(x.to(DEV), 3, workspace=ws[:8])
-
-
 def test_prune_then_fused_path():
     """N2 -> a5: the on-device mask drives the fused path; equals the oracle end to end."""
     B, N, H = 8, 197, 12
