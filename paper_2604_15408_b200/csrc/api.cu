@@ -742,7 +742,7 @@ int32_t ragged_debug_fa_timeline(void* host, int32_t max_ctas) {
 #endif
 
 const char* ragged_build_info(void) {
-  return "libragged 0.3 sm_100a engines=mma_sync,tcgen05 gather=peer";
+  return "libragged 0.4 sm_100a engines=mma_sync,tcgen05,tcgen05_ws gather=peer,nccl";
 }
 
 }  // extern "C"
