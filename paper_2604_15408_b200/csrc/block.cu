@@ -795,9 +795,11 @@ int gemm_pick_split(int M_hint, int N, int K, int sms, int* bn) {
   }();
   const long long mt = (M_hint + kGemmBM - 1) / kGemmBM;
   const int nk = K / kGemmBK;
-  if (forced == 1) return 1;
-  // measured (scripts/r2/gemm_split_probe.py, T = 1248): fc2 (K = 3072) 17.6 -> 16.2 us with 2 CTAs,
-  // proj (K = 768) 6.7 -> 10.5 us: the DSMEM partial exchange costs more than a short K saves
+  if (forced <= 1) return 1;
+  // Off unless forced (RAGGED_GEMM_SPLIT=2|4, experiments and tests): measured at the block's
+  // T = 1248 (scripts/r2/gemm_split_probe.py) before the UMMA issue fix, fc2 (K = 3072) 17.6 -> 16.2 us
+  // with 2 CTAs and proj (K = 768) 6.7 -> 10.5; after it (round 2, session 3) fc2 13.4 (one CTA) vs
+  // 14.1 (split 2) and the block at p = 0.8 49.5 vs 50.4 us -- the DSMEM partial exchange no longer pays.
   if (mt * (N / *bn) > sms || nk < 32) return 1;
   for (int bn2 : {128, 64}) {
     if (N % bn2 != 0) continue;
