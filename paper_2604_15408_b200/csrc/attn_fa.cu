@@ -527,19 +527,13 @@ __global__ void __launch_bounds__(kFaThreads, 1)
       int nitem = 0;
       const uint32_t idesc_o = tc::idesc_f16(kFmt, kFaRows, kHeadDim, 1);
       FaCu cn = fa_cu_load(a, blockIdx.x);
-      // early: S_A(0) of this item was issued at the end of the previous item,
-      // right after its last PV_A (tile A then starts the item while tile B
-      // still finishes the previous one; measured per-item gap ~1 us at C3 p = 0)
-      bool early = false;
       for (int it = blockIdx.x; it < a.nitems; it += gridDim.x) {
         const FaCu cc = cn;
         cn = fa_cu_load(a, it + gridDim.x);  // the next item's cu, off the critical path
         FaItem I;
         if (!fa_item_cu(a, it, cc, I)) continue;
-        FaItem In;                            // the next item (early S_A(0) only if it is real)
-        const bool next_ok = it + (int)gridDim.x < a.nitems && fa_item_cu(a, it + gridDim.x, cn, In);
         const int qb = nitem & 1;
-        if (!early) tc::mbar_wait(smem_u32(&bars.q_full[qb]), (nitem >> 1) & 1);
+        tc::mbar_wait(smem_u32(&bars.q_full[qb]), (nitem >> 1) & 1);
         tc::fence_after();
         uint64_t qd[2];
         for (int x = 0; x < 2; ++x) qd[x] = tc::sw128_desc(smem_u32(smem + kOffQ + (2 * qb + x) * kFaTileBytes));
@@ -550,21 +544,18 @@ __global__ void __launch_bounds__(kFaThreads, 1)
         uint32_t idesc_s0;
         {
           const int s = kv % kFaStages;
-          if (!early) tc::mbar_wait(smem_u32(&bars.full[s]), (kv / kFaStages) & 1);
+          tc::mbar_wait(smem_u32(&bars.full[s]), (kv / kFaStages) & 1);
           tc::fence_after();
           const int nv = min(kFaRows, I.n);
           idesc_s0 = tc::idesc_f16(kFmt, kFaRows, (uint32_t)((nv + 15) & ~15), 0);
           kd0 = tc::sw128_desc(smem_u32(smem + kOffKV + s * 2 * kFaTileBytes));
-          if (!early) {
-            if (tc::elect_one()) {
-              tc::mma_ss_k64(tmem, qd[0], kd0, idesc_s0);
-              tc::commit(smem_u32(&bars.s[0]));
-              if (nitem == 0) FTL(49);
-              if (nitem < 4) FTL(32 + 4 * nitem + 3);
-            }
-            __syncwarp();
+          if (tc::elect_one()) {
+            tc::mma_ss_k64(tmem, qd[0], kd0, idesc_s0);
+            tc::commit(smem_u32(&bars.s[0]));
+            if (nitem == 0) FTL(49);
+            if (nitem < 4) FTL(32 + 4 * nitem + 3);
           }
-          early = false;
+          __syncwarp();
         }
         for (int j = 0; j < I.nb; ++j, ++kv) {
           const int s = kv % kFaStages;
@@ -610,29 +601,6 @@ __global__ void __launch_bounds__(kFaThreads, 1)
               if (nitem < 4 && x == 0 && j < 1) FTL(33 + 4 * nitem + 2 * j);
             }
             __syncwarp();
-            if (x == 0 && !more && next_ok) {
-              // the next item's S_A(0) right behind this item's last PV_A (in-order
-              // pipe: it overwrites tile A's S/P columns only after PV_A read them;
-              // O is untouched), if its Q tiles and first K block have landed
-              const int qbn = (nitem + 1) & 1, sn = (kv + 1) % kFaStages;
-              const bool ready =
-                  __shfl_sync(0xffffffffu, (int)(tc::mbar_test(smem_u32(&bars.q_full[qbn]), ((nitem + 1) >> 1) & 1) &&
-                                                 tc::mbar_test(smem_u32(&bars.full[sn]), ((kv + 1) / kFaStages) & 1)),
-                              0) != 0;
-              if (ready) {
-                tc::fence_after();
-                const uint64_t qdn = tc::sw128_desc(smem_u32(smem + kOffQ + (2 * qbn) * kFaTileBytes));
-                const uint64_t kdn = tc::sw128_desc(smem_u32(smem + kOffKV + sn * 2 * kFaTileBytes));
-                const uint32_t idn = tc::idesc_f16(kFmt, kFaRows, (uint32_t)((min(kFaRows, In.n) + 15) & ~15), 0);
-                if (tc::elect_one()) {
-                  tc::mma_ss_k64(tmem, qdn, kdn, idn);
-                  tc::commit(smem_u32(&bars.s[0]));
-                  if (nitem + 1 < 4) FTL(32 + 4 * (nitem + 1) + 3);
-                }
-                __syncwarp();
-                early = true;
-              }
-            }
           }
           if (tc::elect_one()) tc::commit(smem_u32(&bars.empty[s]));  // stage s free once these UMMAs complete
           __syncwarp();
