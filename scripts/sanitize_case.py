@@ -53,5 +53,22 @@ c0 = torch.empty(8, 3 * 64, device="cuda", dtype=dt)
 off = 4 * 197 * 3 * 64 * 2
 rb.pack_attend_unpack_gather(q, k, v, keep, rb.gather_desc(2, 1, out=[d0.data_ptr() + off, d1.data_ptr() + off],
                                                            cls=[c0.data_ptr() + 4 * 3 * 64 * 2, None]))
+# round 2: the warp-specialised engine (capacity buffers from ragged_pack; N <= 256 via n_hint and
+# N > 256), the block with n_hint (LayerNorm grid loop at hint 1, WS attention at hint 197), the
+# EViT mask and the mask fused ahead of the scan
+for (B, N, H, p) in [(3, 197, 2, 0.0), (2, 577, 2, 0.3)]:
+    q, k, v, keep = (t.cuda() for t in synth.make_inputs(B, N, H, p, "random", "bf16", seed=5))
+    qp, kp, vp, cu2, dst, src = rb.pack(q, k, v, keep)
+    rb.attn(qp, kp, vp, cu2, N, engine=rb.ENGINE_TCGEN05_WS)
+    rb.attn(qp, kp, vp, cu2, N, n_hint=N)
+cud3 = torch.from_numpy(cu3.astype(np.int32)).cuda()
+for hint in (1, 197):
+    blk2 = rb.VitBlock({k2: v2.cuda() for k2, v2 in synth.vit_weights(pr["D"], pr["MLP"], dt, 1).items()}, 3, 197,
+                       pr["H"], dt, n_hint=hint)
+    blk2(xb, cud3)
+q, k, v, keep = (t.cuda() for t in synth.make_inputs(3, 197, 4, 0.5, "l2", "bf16", seed=6))
+rb.keep_evit(q, k, v, 60)
+xh = synth.hidden_states(3, 197, 4 * 64, "bf16", seed=7).cuda()
+rb.prune_l2_pack_attend_unpack(xh, q, k, v, 60)
 torch.cuda.synchronize()
 print("sanitize case done")
