@@ -104,7 +104,12 @@ __device__ __forceinline__ void ln_row(const uint4 (&raw)[kCPL], const uint4 (&w
 // launched over the whole capacity and every CTA read its rows before seeing
 // the live count).  The first row's data, gamma and beta are loaded together
 // with the live count: one memory round trip when the hint holds.
-template <typename T, int kCPL>  // kCPL: 16-byte chunks per lane (D <= 256 * kCPL)
+// kLoop: the grid covers only the caller's expected live rows and warps stride
+// over any further ones -- a separate instantiation because the loop raises the
+// register count (64 -> 124 at D = 768, halving the occupancy: ~1 us per launch
+// over the whole capacity), which the capacity-sized grid of the plain ABI path
+// must not pay.
+template <typename T, int kCPL, bool kLoop>  // kCPL: 16-byte chunks per lane (D <= 256 * kCPL)
 __global__ void __launch_bounds__(kLnThreads) layer_norm_kernel(const T* __restrict__ x, long long ldx,
                                                                  const T* __restrict__ w,
                                                                  const T* __restrict__ bvec, float eps,
@@ -129,15 +134,17 @@ __global__ void __launch_bounds__(kLnThreads) layer_norm_kernel(const T* __restr
   const int M = m_dev ? min(*m_dev, M_cap) : M_cap;
   if (row >= M) return;
   ln_row<T, kCPL>(raw, wraw, braw, nch, D, eps, y + row * ldy);
-  // rows past the grid's first pass (the live count exceeded the hint)
-  const long long stride = (long long)gridDim.x * (kLnThreads / 32);
-  for (row += stride; row < M; row += stride) {
+  if constexpr (kLoop) {
+    const long long stride = (long long)gridDim.x * (kLnThreads / 32);
+#pragma unroll 1
+    for (row += stride; row < M; row += stride) {
 #pragma unroll
-    for (int i = 0; i < kCPL; ++i) {
-      const int c = lane + 32 * i;
-      if (c < nch) raw[i] = *reinterpret_cast<const uint4*>(x + row * ldx + c * 8);
+      for (int i = 0; i < kCPL; ++i) {
+        const int c = lane + 32 * i;
+        if (c < nch) raw[i] = *reinterpret_cast<const uint4*>(x + row * ldx + c * 8);
+      }
+      ln_row<T, kCPL>(raw, wraw, braw, nch, D, eps, y + row * ldy);
     }
-    ln_row<T, kCPL>(raw, wraw, braw, nch, D, eps, y + row * ldy);
   }
 }
 
@@ -642,8 +649,12 @@ cudaError_t launch_layer_norm(int dtype, const void* x, long long ldx, const voi
   const dim3 grid((cover + rows_per - 1) / rows_per);
   const int cpl = (D / 8 + 31) / 32;
 #define RAGGED_LN(TT, C)                                                                             \
-  return launch_pdl_b(layer_norm_kernel<TT, C>, grid, dim3(kLnThreads), 0, st, (const TT*)x, ldx,  \
-                      (const TT*)w, (const TT*)b, eps, (TT*)y, ldy, M_cap, m_dev, D)
+  return cover < M_cap ? launch_pdl_b(layer_norm_kernel<TT, C, true>, grid, dim3(kLnThreads), 0, st,     \
+                                      (const TT*)x, ldx, (const TT*)w, (const TT*)b, eps, (TT*)y, ldy,    \
+                                      M_cap, m_dev, D)                                                     \
+                       : launch_pdl_b(layer_norm_kernel<TT, C, false>, grid, dim3(kLnThreads), 0, st,    \
+                                      (const TT*)x, ldx, (const TT*)w, (const TT*)b, eps, (TT*)y, ldy,    \
+                                      M_cap, m_dev, D)
   if (dtype == 0) {
     switch (cpl) {
       case 1: RAGGED_LN(__nv_bfloat16, 1);
