@@ -1372,13 +1372,28 @@ def config_extras(rb, torch, dev, dt):
             for L, s in enumerate(layers):
                 rb.pack_attend_unpack(s["q"], s["k"], s["v"], s["keep"], o=s["o"], n_hint=197 if L < 4 else kp)
         us = _graph_time(torch, [step], 50)
+        # the dense layers as plain attention: all tokens kept means padded == packed, so
+        # ragged_attn runs on the padded buffers with cu = b * N (n_hint 197: the warp-
+        # specialised engine); the pruned layers keep the fused path
+        cu_all = (torch.arange(33, dtype=torch.int32, device=dev) * 197).contiguous()
+
+        def step_dense_attn(layers=layers, kp=synth.kept_tokens(197, p)):
+            for L, s in enumerate(layers):
+                if L < 4:
+                    rb.attn(s["q"].view(32 * 197, 6, 64), s["k"].view(32 * 197, 6, 64), s["v"].view(32 * 197, 6, 64),
+                            cu_all, 197, op=s["o"].view(32 * 197, 6, 64), n_hint=197)
+                else:
+                    rb.pack_attend_unpack(s["q"], s["k"], s["v"], s["keep"], o=s["o"], n_hint=kp)
+        us_da = _graph_time(torch, [step_dense_attn], 50)
 
         def step_sdpa(layers=layers):
             for s in layers:
                 sdpa_fn(s)()
         us_sd = _graph_time(torch, [step_sdpa], 10)
         c2.append({"p": p, "tok": synth.kept_tokens(197, p), "us_12_layers": us,
-                   "images_per_s": 32 / (us * 1e-6), "padded_sdpa_us_12_layers": us_sd,
+                   "images_per_s": 32 / (us * 1e-6),
+                   "us_12_layers_dense_attn": us_da, "images_per_s_dense_attn": 32 / (us_da * 1e-6),
+                   "padded_sdpa_us_12_layers": us_sd,
                    "padded_sdpa_images_per_s": 32 / (us_sd * 1e-6)})
     res["C2"] = c2
     # C4: DeiT-B, B = 64, four generators x {50, 70, 90} %
