@@ -22,9 +22,9 @@ __attribute__((visibility("default"))) int32_t ragged_debug_timeline_clear(void)
 __attribute__((visibility("default"))) int32_t ragged_debug_pairs_timeline(void* host, int32_t max_ctas);
 /* %globaltimer stamps of the tcgen05 GEMM (8 x uint64 per CTA, block.cu GT slots). */
 __attribute__((visibility("default"))) int32_t ragged_debug_gemm_timeline(void* host, int32_t max_ctas);
-/* %globaltimer stamps of the N2 mask kernels (8 x uint64 per CTA, prune.cu PTL slots). */
+/* %globaltimer stamps of the N2 mask kernels (16 x uint64 per CTA, prune.cu PTL slots). */
 __attribute__((visibility("default"))) int32_t ragged_debug_prune_timeline(void* host, int32_t max_ctas);
-/* clock64 stamps of the warp-specialised tcgen05 engine (64 x uint64 per CTA, attn_fa.cu FTL slots). */
+/* clock64 stamps of the warp-specialised tcgen05 engine (128 x uint64 per CTA, attn_fa.cu FTL slots). */
 __attribute__((visibility("default"))) int32_t ragged_debug_fa_timeline(void* host, int32_t max_ctas);
 #endif
 #ifdef __cplusplus

@@ -38,18 +38,18 @@ namespace ragged {
 // 0 entry, 1 after the PDL wait, 2 rows landed, 3 scores pushed, 4 after the
 // cluster barrier, 5 end (EViT: 5 partials pushed, 6 end).
 constexpr int kPtlMax = 1 << 14;
-__device__ unsigned long long g_prune_tl[kPtlMax * 8];
+__device__ unsigned long long g_prune_tl[kPtlMax * 16];
 #define PTL(i)                                                                \
   do {                                                                        \
     if (threadIdx.x == 0 && blockIdx.x < kPtlMax) {                           \
       unsigned long long t_;                                                  \
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                  \
-      g_prune_tl[blockIdx.x * 8 + (i)] = t_;                                  \
+      g_prune_tl[blockIdx.x * 16 + (i)] = t_;                                 \
     }                                                                         \
   } while (0)
 int prune_timeline_copy(void* host, int max_ctas) {
   const int n = max_ctas < kPtlMax ? max_ctas : kPtlMax;
-  return cudaMemcpyFromSymbol(host, g_prune_tl, (size_t)n * 64) == cudaSuccess ? n : -1;
+  return cudaMemcpyFromSymbol(host, g_prune_tl, (size_t)n * 128) == cudaSuccess ? n : -1;
 }
 #else
 #define PTL(i) \
@@ -175,7 +175,7 @@ __global__ void __launch_bounds__(kPThr) keep_l2_cluster_kernel(const T* __restr
   if (tid == 0 && blockIdx.x < kPtlMax) {
     uint32_t smid;
     asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-    g_prune_tl[blockIdx.x * 8 + 7] = smid;
+    g_prune_tl[blockIdx.x * 16 + 15] = smid;
   }
 #endif
   pdl_launch_dependents();
@@ -233,38 +233,90 @@ __global__ void __launch_bounds__(kPThr) keep_l2_cluster_kernel(const T* __restr
 // -------------------------------------------------------------- EViT --------
 // Dynamic shared memory: s_qc [D] floats (the CLS query) | s_red [kPC][3H][8]
 // floats (partial fused-token sums pushed by every CTA to the owner of each
-// 16-byte column chunk of [q | k | v]) | two row buffers [R][D] (K, then V; Q).
+// 16-byte column chunk of [q | k | v]) | two row buffers [R][D] (K, then V; Q) |
+// s_scr [G][D/8][8] floats (row-group partials, G = kPThr / (D/8) >= 2).
+__host__ __device__ constexpr int evit_groups(int H) { return (H * 8) <= kPThr / 2 ? kPThr / (H * 8) : 1; }
 __host__ __device__ constexpr int evit_smem(int N, int H) {
-  return H * kHeadDim * 4 + 3 * H * 8 * kPC * 4 + 2 * ((N + kPC - 1) / kPC) * H * kHeadDim * 2;
+  return H * kHeadDim * 4 + 3 * H * 8 * kPC * 4 + 2 * ((N + kPC - 1) / kPC) * H * kHeadDim * 2 +
+         (evit_groups(H) >= 2 ? evit_groups(H) * H * 8 * 8 * 4 : 0);
 }
 
-// Own dropped rows' contribution to one tensor's fused row: thread -> 16-byte
-// column chunk, weighted sum over the rows in `buf` (slot n - r0), pushed to
-// the CTA that owns the chunk.
+// Own dropped rows' contribution to one tensor's fused row (rows s_drow[0, nd)
+// of this CTA, in `buf` at slot n - r0), pushed to the CTA that owns each
+// 16-byte column chunk.  With G = kPThr / cpr >= 2 the rows are split over G
+// thread groups (thread -> (group, chunk)); the groups' partials meet in shared
+// memory and are added in group order (deterministic).  One thread per chunk
+// walking every row (round 2's first version) took ~2.5 us per tensor at C3:
+// 96 of 256 threads busy, 25 rows in a dependent chain.
 template <typename T>
-__device__ __forceinline__ void fuse_partial(const uint8_t* buf, int t, int cpr, int H, int r0, int r1, int rowb,
-                                             const uint8_t* s_keep, const float* s_w, float* s_red, int c) {
+__device__ __forceinline__ void fuse_partial(const uint8_t* buf, int t, int cpr, int H, int r0, int rowb,
+                                             const int16_t* s_drow, int nd, const float* s_w, float* s_red,
+                                             float* s_scr, int c) {
   const int per = 3 * H;
-  for (int cc = threadIdx.x; cc < cpr; cc += kPThr) {
-    float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-    for (int n = r0; n < r1; n += 4) {  // four rows' loads in flight; kept rows' slots
-      uint4 raw[4];                      // hold stale bytes and are selected out
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-        raw[i] = *reinterpret_cast<const uint4*>(buf + (min(n + i, r1 - 1) - r0) * rowb + cc * 16);
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const bool use = n + i < r1 && !s_keep[n + i];
-        const float w = use ? s_w[n + i] : 0.f;
-        const T* e = reinterpret_cast<const T*>(&raw[i]);
-#pragma unroll
-        for (int j = 0; j < 8; ++j) acc[j] = fmaf(w, use ? static_cast<float>(e[j]) : 0.f, acc[j]);
-      }
-    }
+  const int G = evit_groups(H);
+  const int tid = threadIdx.x;
+  auto push = [&](int cc, const float (&acc)[8]) {
     const int ch = t * cpr + cc, owner = ch / per, li = ch - owner * per;
     const uint32_t dst = peer_addr(s_red + (c * per + li) * 8, owner);
     st_peer_v4(dst, acc[0], acc[1], acc[2], acc[3]);
     st_peer_v4(dst + 16, acc[4], acc[5], acc[6], acc[7]);
+  };
+  if (G >= 2) {
+    const int g = tid / cpr, cc = tid - g * cpr;
+    if (g < G) {
+      float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+      for (int i = g; i < nd; i += 4 * G) {  // four rows' loads in flight
+        uint4 raw[4];
+        float w[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int ii = i + u * G;
+          const int n = s_drow[ii < nd ? ii : nd - 1];
+          raw[u] = *reinterpret_cast<const uint4*>(buf + (n - r0) * rowb + cc * 16);
+          w[u] = ii < nd ? s_w[n] : 0.f;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const bool use = i + u * G < nd;
+          const T* e = reinterpret_cast<const T*>(&raw[u]);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) acc[j] = fmaf(w[u], use ? static_cast<float>(e[j]) : 0.f, acc[j]);
+        }
+      }
+      float4* o = reinterpret_cast<float4*>(s_scr + (g * cpr + cc) * 8);
+      o[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
+      o[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
+    }
+    __syncthreads();
+    for (int cc2 = tid; cc2 < cpr; cc2 += kPThr) {
+      float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+      for (int gg = 0; gg < G; ++gg) {
+        const float* p = s_scr + (gg * cpr + cc2) * 8;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[j] += p[j];
+      }
+      push(cc2, acc);
+    }
+    __syncthreads();  // s_scr is rewritten by the next tensor
+    return;
+  }
+  for (int cc = tid; cc < cpr; cc += kPThr) {
+    float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    for (int i = 0; i < nd; i += 4) {  // four rows' loads in flight
+      uint4 raw[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        raw[u] = *reinterpret_cast<const uint4*>(buf + (s_drow[i + u < nd ? i + u : nd - 1] - r0) * rowb + cc * 16);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const bool use = i + u < nd;
+        const float w = use ? s_w[s_drow[i + u]] : 0.f;
+        const T* e = reinterpret_cast<const T*>(&raw[u]);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[j] = fmaf(w, use ? static_cast<float>(e[j]) : 0.f, acc[j]);
+      }
+    }
+    push(cc, acc);
   }
 }
 
@@ -285,6 +337,9 @@ __global__ void __launch_bounds__(kPThr) keep_evit_cluster_kernel(T* __restrict_
   float* s_red = dyn + D;  // [kPC][3H][8]
   uint8_t* bufA = reinterpret_cast<uint8_t*>(s_red + 3 * H * 8 * kPC);
   uint8_t* bufB = bufA + R * rowb;
+  float* s_scr = reinterpret_cast<float*>(bufB + R * rowb);  // row-group partials (fuse_partial)
+  __shared__ int16_t s_drow[(kMaxN + kPC - 1) / kPC];
+  __shared__ int s_nd;
   const int c = (int)cluster_rank(), b = blockIdx.x / kPC, tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
   const int r0 = min(N, c * R), r1 = min(N, r0 + R);
@@ -383,6 +438,13 @@ __global__ void __launch_bounds__(kPThr) keep_evit_cluster_kernel(T* __restrict_
   if (tid > 0 && tid < N && !s_keep[tid]) atomicMin(&s_f, tid);
   __syncthreads();
   const int f = s_f;
+  if (warp == 0) {  // own dropped rows, ascending (the fused token's terms): R <= 32, one ballot
+    const int n = r0 + lane;
+    const bool d = n < r1 && !s_keep[n];
+    const unsigned m = __ballot_sync(0xffffffffu, d);
+    if (d) s_drow[__popc(m & ((1u << lane) - 1u))] = (int16_t)n;
+    if (lane == 0) s_nd = __popc(m);
+  }
   const bool fuse = kk >= 2 && f < N;  // uniform
   // max logit over dropped tokens, then their softmax weights (fixed-order sums:
   // every CTA computes the same bits)
@@ -412,13 +474,18 @@ __global__ void __launch_bounds__(kPThr) keep_evit_cluster_kernel(T* __restrict_
   // 3. partial fused token over own dropped rows (K from bufA while Q lands in
   // bufB; then V into bufA), pushed to the chunk owners
   if (fuse) {
-    fuse_partial<T>(bufA, 1, cpr, H, r0, r1, rowb, s_keep, s_w, s_red, c);
+    const int nd = s_nd;
+    fuse_partial<T>(bufA, 1, cpr, H, r0, rowb, s_drow, nd, s_w, s_red, s_scr, c);
+    PTL(8);
     __syncthreads();  // bufA (K) fully read
     copy_rows(bufA, iv, ldb, r0, r1, rowb, barA, [&](int n) { return s_keep[n] == 0; });
     tc::mbar_wait(barB, 0);
-    fuse_partial<T>(bufB, 0, cpr, H, r0, r1, rowb, s_keep, s_w, s_red, c);
+    PTL(9);
+    fuse_partial<T>(bufB, 0, cpr, H, r0, rowb, s_drow, nd, s_w, s_red, s_scr, c);
+    PTL(10);
     tc::mbar_wait(barA, 1);
-    fuse_partial<T>(bufA, 2, cpr, H, r0, r1, rowb, s_keep, s_w, s_red, c);
+    PTL(11);
+    fuse_partial<T>(bufA, 2, cpr, H, r0, rowb, s_drow, nd, s_w, s_red, s_scr, c);
   }
   PTL(6);
   cluster_sync_all();  // partial sums delivered; every CTA has read row f

@@ -29,14 +29,14 @@ for name, fn in (("l2", lambda i: rb.keep_topk_l2(xs[i % 4], kk, keep=keep)),
             for i in range(8):
                 fn(i)
         torch.cuda.synchronize()
-        buf = np.zeros((B * 8, 8), np.uint64)
+        buf = np.zeros((B * 8, 16), np.uint64)
         lib.ragged_debug_prune_timeline(buf.ctypes.data, B * 8)
         t = buf.astype(np.int64)
         t0 = t[:, 0].min()
         rel = (t - t0) / 1e3
-        nslot = 7 if name == "l2" else 8
+        nslot = 7 if name == "l2" else 12
         if name == "l2":
-            sm = buf[:, 7].astype(np.int64)
+            sm = buf[:, 15].astype(np.int64)
             cnt = np.bincount(sm, minlength=148)
             res[f"{name}_{mode}_sm_use"] = {"distinct_sms": int((cnt > 0).sum()), "max_ctas_per_sm": int(cnt.max()),
                                             "cluster0_sms": sm[:8].tolist()}
