@@ -69,7 +69,9 @@ typedef enum {
   RAGGED_ENGINE_TCGEN05 = 2,    /* tcgen05.mma, fp32 accumulate in TMEM            */
   RAGGED_ENGINE_TCGEN05_WS = 3  /* warp-specialised tcgen05 (M = 128 query tiles in
                                    ping-pong, TMEM-resident S/P/O): ragged_attn with
-                                   d = 64, any N -- the long-sequence engine */
+                                   d = 64, any N -- the long-sequence engine; also
+                                   ragged_pack_attend_unpack (TMA gather4 of the kept
+                                   rows; explicit only) */
 } ragged_engine;
 
 /* The problem statement of the paper: B images, N padded tokens per image
@@ -165,8 +167,13 @@ RAGGED_API ragged_status ragged_unpack(const ragged_problem* prob, const void* o
 /* a5 -- fused pack-attend-unpack in ONE launch: keep mask -> per-image ranks ->
  * gather of kept q/k/v rows into shared memory -> attention -> scatter to
  * padded o, with +0.0 rows for dropped tokens.  Equal, bit for bit, to
- * ragged_pack; ragged_attn; ragged_unpack.  If cu_seqlens_or_null is non-NULL
- * it also receives cu_seqlens (one extra CTA computes it concurrently). */
+ * ragged_pack; ragged_attn; ragged_unpack on the same engine.  If
+ * cu_seqlens_or_null is non-NULL it also receives cu_seqlens (one extra CTA
+ * computes it concurrently).  RAGGED_ENGINE_TCGEN05_WS (explicit only; AUTO
+ * keeps the one-stage engines, measured faster at DeiT lengths): the kept rows
+ * of the padded q/k/v are gathered by TMA tile::gather4 into the warp-
+ * specialised engine; d = 64; with a cu_seqlens output only for B*N <= 65536
+ * (else RAGGED_ENOTSUP). */
 RAGGED_API ragged_status ragged_pack_attend_unpack(const ragged_problem* prob, const uint8_t* keep,
                                         const void* q, const void* k, const void* v,
                                         void* o, int32_t* cu_seqlens_or_null,

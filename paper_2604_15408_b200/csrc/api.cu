@@ -233,8 +233,12 @@ ragged_status ragged_pack_attend_unpack(const ragged_problem* prob, const uint8_
                                         const void* q, const void* k, const void* v, void* o,
                                         int32_t* cu_seqlens_or_null, void* stream) {
   RAGGED_TRY(check_problem(prob));
-  if (prob->engine == RAGGED_ENGINE_TCGEN05_WS)
-    return fail(RAGGED_ENOTSUP, "RAGGED_ENGINE_TCGEN05_WS runs ragged_attn only");
+  // the warp-specialised tcgen05 engine (gather4 of the kept rows, attention, scatter):
+  // explicit, or AUTO when the caller expects long sequences (n_hint > kWsMinHint)
+  const bool ws_ok = prob->d == 64 && (cu_seqlens_or_null == nullptr || (long long)prob->B * prob->N <= 65536);
+  const bool ws = prob->engine == RAGGED_ENGINE_TCGEN05_WS;  // AUTO: measured below
+  if (ws && !ws_ok)
+    return fail(RAGGED_ENOTSUP, "RAGGED_ENGINE_TCGEN05_WS: d = 64, and cu_seqlens output only for B*N <= 65536");
   if (prob->B == 0) return RAGGED_OK;
   RAGGED_TRY(check_ptr_any(keep, "keep"));
   RAGGED_TRY(check_ptr(q, "q"));
@@ -242,6 +246,11 @@ ragged_status ragged_pack_attend_unpack(const ragged_problem* prob, const uint8_
   RAGGED_TRY(check_ptr(v, "v"));
   RAGGED_TRY(check_ptr(o, "o"));
   if ((long long)prob->B * prob->H + 1 > 0x7fffffffLL) return fail(RAGGED_ENOTSUP, "B*H too large");
+  if (ws) {
+    cudaError_t e = ragged::launch_attn_fa_fused(prob->dtype, keep, q, k, v, prob->ld, o, cu_seqlens_or_null,
+                                                 prob->B, prob->N, prob->H, as_stream(stream));
+    return e == cudaSuccess ? RAGGED_OK : cuda_fail(e, "ragged_pack_attend_unpack/ws");
+  }
   cudaError_t e = ragged::launch_fused(prob->dtype, resolve_engine(prob), keep, q, k, v, prob->ld, o, cu_seqlens_or_null,
                                        prob->B, prob->N, prob->H, as_stream(stream), prob->n_hint);
   return e == cudaSuccess ? RAGGED_OK : cuda_fail(e, "ragged_pack_attend_unpack");

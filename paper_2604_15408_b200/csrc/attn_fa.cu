@@ -102,20 +102,42 @@ struct FaArgs {
   long long ld;      // token stride of q / k / v in elements
   int pairs;         // query-tile pairs per problem (ceil(N / 256))
   int nitems;        // pairs * B * H
+  // fused mode (pack-attend-unpack): q / k / v / o padded [B, N, H, d], the
+  // keep mask [B, N]; packed order = ascending kept positions (R7)
+  const uint8_t* keep;
+  int32_t* cu_out;   // optional cu_seqlens output (B * N <= 65536)
 };
 
 // shared memory map (offsets from a 1024-aligned base)
 constexpr int kOffQ = 0;                                   // 2 buffers x 2 tiles
 constexpr int kOffKV = 4 * kFaTileBytes;                   // stages x (K tile, V tile)
 constexpr int kOffBar = kOffKV + kFaStages * 2 * kFaTileBytes;
-constexpr int kFaSmem = kOffBar + 256 + 1024;              // + barriers / TMEM slot, alignment slack
+// fused mode: kept positions of the item's image, double-buffered by item
+// ([2][kMaxN] int16), the kept counts [2] and the rows warps' scan scratch
+constexpr int kOffRows = kOffBar + 256;
+constexpr int kFaSmem = kOffRows + 2 * kMaxN * 2 + 64 + 1024;  // + alignment slack
 
 struct FaBars {
   uint64_t full[kFaStages], empty[kFaStages];
   uint64_t q_full[2], q_free[2];
   uint64_t s[2], p[2];
+  uint64_t rows_full[2], rows_free[2];  // fused mode: the item's kept positions published / consumed
   uint32_t tmem;
 };
+
+// fused mode: 4 rows (padded row indices) of one head's 64 columns into 512
+// contiguous SW128 bytes (tile::gather4; tensor map box {64, 1}).
+__device__ __forceinline__ void tma_gather4(uint32_t dst, const CUtensorMap* map, uint32_t bar, int c0, int r0,
+                                            int r1, int r2, int r3) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(r0), "r"(r1), "r"(r2), "r"(r3)
+      : "memory");
+}
+__device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
 
 __device__ __forceinline__ void tma_2d(uint32_t dst, const CUtensorMap* map, uint32_t bar, int c0, int c1) {
   asm volatile(
@@ -159,6 +181,20 @@ __device__ __forceinline__ bool fa_item_cu(const FaArgs& a, int it, FaCu c, FaIt
   I.h = w - I.b * a.H;
   I.s0 = c.c0;
   I.n = min(max(c.c1 - c.c0, 0), a.N);
+  I.rows0 = I.pair * 2 * kFaRows;
+  if (I.rows0 >= I.n) return false;
+  I.ntile = I.n - I.rows0 > kFaRows ? 2 : 1;
+  I.nb = (I.n + kFaRows - 1) / kFaRows;
+  return true;
+}
+__device__ __forceinline__ bool fa_item_n(const FaArgs& a, int it, int n, FaItem& I) {
+  const int P = a.B * a.H;
+  I.pair = it / P;
+  const int w = it - I.pair * P;
+  I.b = w / a.H;
+  I.h = w - I.b * a.H;
+  I.s0 = 0;
+  I.n = n;
   I.rows0 = I.pair * 2 * kFaRows;
   if (I.rows0 >= I.n) return false;
   I.ntile = I.n - I.rows0 > kFaRows ? 2 : 1;
@@ -452,7 +488,14 @@ __device__ __forceinline__ void fa_softmax_block(uint32_t tS, uint32_t tO, int n
   l += s0 + s1;
 }
 
-template <typename T>
+// kFused: pack-attend-unpack in one launch.  Warps 2-3 (idle in the packed
+// engine) read each item's keep row, rank the kept positions (the packed order,
+// R7) into shared memory, write the +0.0 rows of the dropped positions and
+// cu_seqlens; the producer gathers the kept rows of the padded q / k / v with
+// TMA tile::gather4 (4 rows per op, the SW128 layout of a tile load); the
+// softmax warps store O rows at their padded positions.  The rest is the
+// packed engine unchanged.
+template <typename T, bool kFused = false>
 __global__ void __launch_bounds__(kFaThreads, 1)
     attn_fa_kernel(const FaArgs a, const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
                    const __grid_constant__ CUtensorMap tv) {
@@ -477,6 +520,8 @@ __global__ void __launch_bounds__(kFaThreads, 1)
     for (int x = 0; x < 2; ++x) {
       tc::mbar_init(smem_u32(&bars.s[x]), 1);      // tcgen05.commit: S ready (and all earlier UMMAs done)
       tc::mbar_init(smem_u32(&bars.p[x]), 4);      // one arrival per softmax warp: P stored
+      tc::mbar_init(smem_u32(&bars.rows_full[x]), 1);   // the rows warps published an item's positions
+      tc::mbar_init(smem_u32(&bars.rows_free[x]), 10);  // producer + MMA warp + 8 softmax warps done with them
     }
     tc::fence_mbar_init();
   }
@@ -486,7 +531,133 @@ __global__ void __launch_bounds__(kFaThreads, 1)
   pdl_wait_prerequisites();
   const uint32_t tmem = bars.tmem;
 
-  if (warp == 0) {
+  if (kFused && warp == 0) {
+    // ------------------------------------------------------------ producer (fused)
+    // lane g gathers rows 4g..4g+3 of every 128-row tile (one gather4 each)
+    const int16_t* s_pos = reinterpret_cast<const int16_t*>(smem + kOffRows);
+    const int* s_n = reinterpret_cast<const int*>(smem + kOffRows + 2 * kMaxN * 2);
+    if (lane == 0) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tq)) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tk)) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tv)) : "memory");
+    }
+    uint32_t kv = 0;
+    int nitem = 0, iall = 0;
+    for (int it = blockIdx.x; it < a.nitems; it += gridDim.x, ++iall) {
+      const int rb = iall & 1;
+      tc::mbar_wait(smem_u32(&bars.rows_full[rb]), (iall >> 1) & 1);
+      FaItem I;
+      const bool ok = fa_item_n(a, it, s_n[rb], I);
+      if (ok) {
+        const int16_t* pos = s_pos + rb * kMaxN;
+        const int rbase = I.b * a.N, col = I.h * kHeadDim, last = I.n - 1;
+        auto prow = [&](int r) { return rbase + pos[r < last ? r : last]; };  // rows past n: any kept row
+        const int qb = nitem & 1;
+        if (nitem >= 2) tc::mbar_wait(smem_u32(&bars.q_free[qb]), ((nitem >> 1) - 1) & 1);
+        const uint32_t qbar = smem_u32(&bars.q_full[qb]);
+        if (lane == 0) expect_tx(qbar, I.ntile * kFaTileBytes);
+        __syncwarp();
+        for (int x = 0; x < I.ntile; ++x) {
+          const int r = I.rows0 + x * kFaRows + 4 * lane;
+          tma_gather4(smem_u32(smem + kOffQ + (2 * qb + x) * kFaTileBytes) + 512u * lane, &tq, qbar, col, prow(r),
+                      prow(r + 1), prow(r + 2), prow(r + 3));
+        }
+        for (int j = 0; j < I.nb; ++j, ++kv) {
+          const int st = kv % kFaStages;
+          tc::mbar_wait(smem_u32(&bars.empty[st]), ((kv / kFaStages) & 1) ^ 1);
+          const uint32_t fbar = smem_u32(&bars.full[st]);
+          const uint32_t kdst = smem_u32(smem + kOffKV + st * 2 * kFaTileBytes);
+          if (lane == 0) expect_tx(fbar, 2 * kFaTileBytes);
+          __syncwarp();
+          const int r = j * kFaRows + 4 * lane;
+          const int r0 = prow(r), r1 = prow(r + 1), r2 = prow(r + 2), r3 = prow(r + 3);
+          tma_gather4(kdst + 512u * lane, &tk, fbar, col, r0, r1, r2, r3);
+          tma_gather4(kdst + kFaTileBytes + 512u * lane, &tv, fbar, col, r0, r1, r2, r3);
+        }
+        ++nitem;
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(smem_u32(&bars.rows_free[rb]));
+    }
+  } else if (kFused && (warp == 2 || warp == 3)) {
+    // ------------------------------------------------------------ rows (fused)
+    // per item: keep row -> kept positions (ascending) + count, the +0.0 rows of
+    // the dropped positions (pair 0), cu_seqlens (head 0, pair 0); thread t
+    // owns positions 4t..4t+3 (N <= 256 = 64 threads x 4)
+    int16_t* s_pos = reinterpret_cast<int16_t*>(smem + kOffRows);
+    int* s_n = reinterpret_cast<int*>(smem + kOffRows + 2 * kMaxN * 2);
+    int* s_scan = s_n + 2;  // [0, 2): warp totals, [2, 4): prefix partials
+    const int t = threadIdx.x - 64;
+    const uint4 z = make_uint4(0u, 0u, 0u, 0u);
+    int iall = 0;
+    for (int it = blockIdx.x; it < a.nitems; it += gridDim.x, ++iall) {
+      const int rb = iall & 1;
+      if (iall >= 2) tc::mbar_wait(smem_u32(&bars.rows_free[rb]), ((iall >> 1) - 1) & 1);
+      const int P = a.B * a.H, pair = it / P, w = it - pair * P, b = w / a.H, h = w - b * a.H;
+      const uint8_t* km = a.keep + (long long)b * a.N;
+      uint32_t kbits = 0;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int p = 4 * t + u;
+        kbits |= (p < a.N && km[p] != 0) ? (1u << u) : 0u;
+      }
+      const int cnt = __popc(kbits);
+      int incl = cnt;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      if (lane == 31) s_scan[warp - 2] = incl;
+      // cu_seqlens: the kept tokens of images [0, b), counted by this item's 64 threads
+      int pre = 0;
+      const bool cu_here = a.cu_out != nullptr && pair == 0 && h == 0;
+      if (cu_here) {  // 16-byte loads of the mask prefix (the tensor base is 16-byte aligned), then the tail
+        const long long len = (long long)b * a.N, nfull = len >> 4;
+        const uint4* k16 = reinterpret_cast<const uint4*>(a.keep);
+        for (long long i = t; i < nfull; i += 64) {
+          const uint4 v = k16[i];
+          pre += (__popc(__vcmpne4(v.x, 0u)) + __popc(__vcmpne4(v.y, 0u)) + __popc(__vcmpne4(v.z, 0u)) +
+                  __popc(__vcmpne4(v.w, 0u))) >> 3;
+        }
+        if (16 * nfull + t < len) pre += a.keep[16 * nfull + t] != 0 ? 1 : 0;
+      }
+      if (cu_here) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) pre += __shfl_xor_sync(0xffffffffu, pre, o);
+        if (lane == 0) s_scan[2 + warp - 2] = pre;
+      }
+      named_bar_sync(1, 64);
+      const int excl = incl - cnt + (warp == 3 ? s_scan[0] : 0);
+      const int n = s_scan[0] + s_scan[1];
+      int r = excl;
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (kbits & (1u << u)) s_pos[rb * kMaxN + r++] = (int16_t)(4 * t + u);
+      if (pair == 0) {  // +0.0 rows of this head at the dropped positions (R10)
+        char* ob = static_cast<char*>(a.o) + ((long long)b * a.N * a.H + h) * kRowBytes;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int p = 4 * t + u;
+          if (p < a.N && !(kbits & (1u << u))) {
+            char* row = ob + (long long)p * a.H * kRowBytes;
+#pragma unroll
+            for (int c = 0; c < 8; ++c) st_global_16(row + c * 16, z);
+          }
+        }
+      }
+      if (t == 0) {
+        s_n[rb] = n;
+        if (cu_here) {
+          const int cb = s_scan[2] + s_scan[3];
+          a.cu_out[b] = cb;
+          if (b == a.B - 1) a.cu_out[a.B] = cb + n;
+        }
+      }
+      named_bar_sync(1, 64);  // positions, count and scan scratch complete
+      if (t == 0) mbar_arrive(smem_u32(&bars.rows_full[rb]));
+    }
+  } else if (warp == 0) {
     // ------------------------------------------------------------ producer
     if (lane == 0) {
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tq)) : "memory");
@@ -498,6 +669,7 @@ __global__ void __launch_bounds__(kFaThreads, 1)
         FaItem I;
         if (!fa_item(a, it, I)) continue;
         const int qb = nitem & 1;
+        // (fused mode: the producer is the whole warp, below)
         if (nitem >= 2) tc::mbar_wait(smem_u32(&bars.q_free[qb]), ((nitem >> 1) - 1) & 1);
         const uint32_t qbar = smem_u32(&bars.q_full[qb]);
         if (nitem < 4) FTL(59 + nitem);
@@ -526,12 +698,24 @@ __global__ void __launch_bounds__(kFaThreads, 1)
       uint32_t kv = 0, ph_p[2] = {0u, 0u};
       int nitem = 0;
       const uint32_t idesc_o = tc::idesc_f16(kFmt, kFaRows, kHeadDim, 1);
-      FaCu cn = fa_cu_load(a, blockIdx.x);
-      for (int it = blockIdx.x; it < a.nitems; it += gridDim.x) {
-        const FaCu cc = cn;
-        cn = fa_cu_load(a, it + gridDim.x);  // the next item's cu, off the critical path
+      FaCu cn{0, 0};
+      if constexpr (!kFused) cn = fa_cu_load(a, blockIdx.x);
+      int iall = 0;
+      for (int it = blockIdx.x; it < a.nitems; it += gridDim.x, ++iall) {
         FaItem I;
-        if (!fa_item_cu(a, it, cc, I)) continue;
+        bool ok;
+        if constexpr (kFused) {  // n from the rows warps (released at once: only n is needed here)
+          const int rb = iall & 1;
+          tc::mbar_wait(smem_u32(&bars.rows_full[rb]), (iall >> 1) & 1);
+          ok = fa_item_n(a, it, reinterpret_cast<const int*>(smem + kOffRows + 2 * kMaxN * 2)[rb], I);
+          __syncwarp();
+          if (lane == 0) mbar_arrive(smem_u32(&bars.rows_free[rb]));
+        } else {
+          const FaCu cc = cn;
+          cn = fa_cu_load(a, it + gridDim.x);  // the next item's cu, off the critical path
+          ok = fa_item_cu(a, it, cc, I);
+        }
+        if (!ok) continue;
         const int qb = nitem & 1;
         tc::mbar_wait(smem_u32(&bars.q_full[qb]), (nitem >> 1) & 1);
         tc::fence_after();
@@ -617,14 +801,27 @@ __global__ void __launch_bounds__(kFaThreads, 1)
     const uint32_t lane_off = (uint32_t)(q4 * 32) << 16;
     const uint32_t tS = tmem + 256u * x + lane_off, tO = tS + 128u;
     uint32_t ph_s = 0;
-    int nit = 0;
-    FaCu cn = fa_cu_load(a, blockIdx.x);
-    for (int it = blockIdx.x; it < a.nitems; it += gridDim.x) {
-      const FaCu cc = cn;
-      cn = fa_cu_load(a, it + gridDim.x);  // the next item's cu, off the critical path
+    int nit = 0, iall = 0;
+    FaCu cn{0, 0};
+    if constexpr (!kFused) cn = fa_cu_load(a, blockIdx.x);
+    for (int it = blockIdx.x; it < a.nitems; it += gridDim.x, ++iall) {
       FaItem I;
-      if (!fa_item_cu(a, it, cc, I)) continue;
-      if (x >= I.ntile) continue;
+      bool ok;
+      const int rb = iall & 1;  // fused mode: the item's positions buffer
+      if constexpr (kFused) {
+        tc::mbar_wait(smem_u32(&bars.rows_full[rb]), (iall >> 1) & 1);
+        ok = fa_item_n(a, it, reinterpret_cast<const int*>(smem + kOffRows + 2 * kMaxN * 2)[rb], I);
+        if (!ok || x >= I.ntile) {  // this warp is done with the positions
+          __syncwarp();
+          if (lane == 0) mbar_arrive(smem_u32(&bars.rows_free[rb]));
+          continue;
+        }
+      } else {
+        const FaCu cc = cn;
+        cn = fa_cu_load(a, it + gridDim.x);  // the next item's cu, off the critical path
+        ok = fa_item_cu(a, it, cc, I);
+        if (!ok || x >= I.ntile) continue;
+      }
       float m_ref = -INFINITY, l = 0.f;
       for (int j = 0; j < I.nb; ++j) {
         tc::mbar_wait(smem_u32(&bars.s[x]), ph_s);
@@ -661,9 +858,16 @@ __global__ void __launch_bounds__(kFaThreads, 1)
 #pragma unroll
         for (int c = 0; c < 32; ++c)
           w[c] = pack2<T>(__uint_as_float(orow[2 * c]) * inv, __uint_as_float(orow[2 * c + 1]) * inv);
-        char* dst = static_cast<char*>(a.o) + ((long long)(I.s0 + r) * a.H + I.h) * kRowBytes;
+        long long orow = I.s0 + r;  // packed row, or (fused) the token's padded position
+        if constexpr (kFused)
+          orow = (long long)I.b * a.N + reinterpret_cast<const int16_t*>(smem + kOffRows)[rb * kMaxN + r];
+        char* dst = static_cast<char*>(a.o) + (orow * a.H + I.h) * kRowBytes;
 #pragma unroll
         for (int c = 0; c < 8; ++c) st_global_16(dst + c * 16, out[c]);
+      }
+      if constexpr (kFused) {  // positions read (the O row address above)
+        __syncwarp();
+        if (lane == 0) mbar_arrive(smem_u32(&bars.rows_free[rb]));
       }
       tc::fence_before();  // the TMEM reads above precede the next item's UMMAs (ordered by bars.p / bars.s)
       if (nit < 4 && q4 == 0 && lane == 0) FTL(50 + 4 * x + nit);
@@ -695,12 +899,13 @@ static FaEncodeFn fa_encode_fn() {
 }
 // [rows, H * 64] of a packed tensor with row stride ld elements; box = one head's
 // 64 columns x 128 rows, SWIZZLE_128B (the UMMA K-major / MN-major SW128 layout).
-static bool fa_tmap(CUtensorMap* m, int dtype, const void* ptr, long long rows, int H, long long ld) {
+static bool fa_tmap(CUtensorMap* m, int dtype, const void* ptr, long long rows, int H, long long ld,
+                    int box_rows = kFaRows) {
   FaEncodeFn fn = fa_encode_fn();
   if (fn == nullptr) return false;
   const cuuint64_t dims[2] = {(cuuint64_t)H * kHeadDim, (cuuint64_t)rows};
   const cuuint64_t strides[1] = {(cuuint64_t)ld * 2};
-  const cuuint32_t box[2] = {(cuuint32_t)kHeadDim, (cuuint32_t)kFaRows};
+  const cuuint32_t box[2] = {(cuuint32_t)kHeadDim, (cuuint32_t)box_rows};
   const cuuint32_t estr[2] = {1, 1};
   return fn(m, dtype == 0 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2,
             const_cast<void*>(ptr), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
@@ -750,6 +955,57 @@ cudaError_t launch_attn_fa(int dtype, const void* qp, const void* kp, const void
   cudaError_t e = cudaFuncSetAttribute(attn_fa_kernel<__half>, cudaFuncAttributeMaxDynamicSharedMemorySize, kFaSmem);
   if (e != cudaSuccess) return e;
   return cudaLaunchKernelEx(&cfg, attn_fa_kernel<__half>, a, tq, tk, tv);
+}
+
+// Fused pack-attend-unpack on this engine: q / k / v padded [B, N, H, d] (token
+// stride ld), o padded [B, N, H, d] contiguous, keep [B, N]; gather4 tensor maps
+// (box {64, 1}) over the B*N padded rows.  cu_out (optional) needs B*N <= 65536
+// (each head-0 item counts the mask prefix of its image; checked in api.cu).
+cudaError_t launch_attn_fa_fused(int dtype, const uint8_t* keep, const void* q, const void* k, const void* v,
+                                 long long ld, void* o, int32_t* cu_out, int B, int N, int H, cudaStream_t st) {
+  CUtensorMap tq, tk, tv;
+  const long long rows = (long long)B * N;
+  if (!fa_tmap(&tq, dtype, q, rows, H, ld, 1) || !fa_tmap(&tk, dtype, k, rows, H, ld, 1) ||
+      !fa_tmap(&tv, dtype, v, rows, H, ld, 1))
+    return cudaErrorInvalidValue;
+  FaArgs a{};
+  a.q = q;
+  a.k = k;
+  a.v = v;
+  a.o = o;
+  a.cu = nullptr;
+  a.B = B;
+  a.N = N;
+  a.H = H;
+  a.ld = ld;
+  a.pairs = (N + 2 * kFaRows - 1) / (2 * kFaRows);
+  a.nitems = a.pairs * B * H;
+  a.keep = keep;
+  a.cu_out = cu_out;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int grid = a.nitems < sms ? a.nitems : sms;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kFaThreads);
+  cfg.dynamicSmemBytes = kFaSmem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  if (dtype == 0) {
+    cudaError_t e = cudaFuncSetAttribute(attn_fa_kernel<__nv_bfloat16, true>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, kFaSmem);
+    if (e != cudaSuccess) return e;
+    return cudaLaunchKernelEx(&cfg, attn_fa_kernel<__nv_bfloat16, true>, a, tq, tk, tv);
+  }
+  cudaError_t e = cudaFuncSetAttribute(attn_fa_kernel<__half, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       kFaSmem);
+  if (e != cudaSuccess) return e;
+  return cudaLaunchKernelEx(&cfg, attn_fa_kernel<__half, true>, a, tq, tk, tv);
 }
 
 }  // namespace ragged

@@ -60,6 +60,8 @@ cudaError_t launch_attn_general_f8(int out_dtype, int d, const void* qp, const v
                                    long long ld, cudaStream_t st);
 bool attn_general_supports(int d);
 // warp-specialised tcgen05 engine (attn_fa.cu): packed q/k/v, d = 64, any N
+cudaError_t launch_attn_fa_fused(int dtype, const uint8_t* keep, const void* q, const void* k, const void* v,
+                                 long long ld, void* o, int32_t* cu_out, int B, int N, int H, cudaStream_t st);
 cudaError_t launch_attn_fa(int dtype, const void* qp, const void* kp, const void* vp, const int32_t* cu, void* op,
                            int B, int N, int H, long long ld, cudaStream_t st);
 cudaError_t launch_attn_general(int dtype, int d, const void* qp, const void* kp, const void* vp, const int32_t* cu,

@@ -294,8 +294,12 @@ def test_round2_entry_validation():
     assert f(ctypes.byref(p), FAKE, 772, 5, FAKE, FAKE, FAKE, FAKE, None, None, None) == rb.EALIGN
     ws = rb.problem(4, 197, 12, engine=rb.ENGINE_TCGEN05_WS)
     assert f(ctypes.byref(ws), FAKE, 768, 5, FAKE, FAKE, FAKE, FAKE, None, None, None) == rb.ENOTSUP
-    # the WS engine runs ragged_attn only; head_dim 64 only
-    assert lib.ragged_pack_attend_unpack(ctypes.byref(ws), FAKE, FAKE, FAKE, FAKE, FAKE, None, None) == rb.ENOTSUP
+    # the WS engine's fused path: head_dim 64; a cu_seqlens output only for B*N <= 65536
+    big_ws = rb.problem(400, 197, 12, engine=rb.ENGINE_TCGEN05_WS)
+    assert lib.ragged_pack_attend_unpack(ctypes.byref(big_ws), FAKE, FAKE, FAKE, FAKE, FAKE, FAKE, None) == rb.ENOTSUP
+    ws80f = rb.problem(4, 197, 12, d=80, engine=rb.ENGINE_TCGEN05_WS)
+    assert lib.ragged_pack_attend_unpack(ctypes.byref(ws80f), FAKE, FAKE, FAKE, FAKE, FAKE, None, None) in (
+        rb.ENOTSUP,)
     ws80 = rb.problem(4, 300, 12, d=80, engine=rb.ENGINE_TCGEN05_WS)
     assert lib.ragged_attn(ctypes.byref(ws80), FAKE, FAKE, FAKE, FAKE, FAKE, None) == rb.ENOTSUP
     # N1 pieces: NULL pointers
