@@ -555,6 +555,7 @@ __global__ void __launch_bounds__(kFaThreads, 1)
         const int qb = nitem & 1;
         if (nitem >= 2) tc::mbar_wait(smem_u32(&bars.q_free[qb]), ((nitem >> 1) - 1) & 1);
         const uint32_t qbar = smem_u32(&bars.q_full[qb]);
+        if (lane == 0 && nitem < 4) FTL(59 + nitem);
         if (lane == 0) expect_tx(qbar, I.ntile * kFaTileBytes);
         __syncwarp();
         for (int x = 0; x < I.ntile; ++x) {
@@ -574,6 +575,7 @@ __global__ void __launch_bounds__(kFaThreads, 1)
           tma_gather4(kdst + 512u * lane, &tk, fbar, col, r0, r1, r2, r3);
           tma_gather4(kdst + kFaTileBytes + 512u * lane, &tv, fbar, col, r0, r1, r2, r3);
         }
+        if (lane == 0 && nitem < 4) FTL(74 + nitem);  // last K/V gather of the item issued
         ++nitem;
       }
       __syncwarp();
@@ -656,6 +658,7 @@ __global__ void __launch_bounds__(kFaThreads, 1)
       }
       named_bar_sync(1, 64);  // positions, count and scan scratch complete
       if (t == 0) mbar_arrive(smem_u32(&bars.rows_full[rb]));
+      if (t == 0 && iall < 4) FTL(70 + iall);  // the item's positions published
     }
   } else if (warp == 0) {
     // ------------------------------------------------------------ producer

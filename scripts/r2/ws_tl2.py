@@ -10,7 +10,15 @@ import torch
 import paper_2604_15408_b200 as rb
 case = os.environ.get("CASE", "c3p0")
 sys.argv = [sys.argv[0], "--case", case, "--iters", "3"]
-exec(open(os.path.join(ROOT, "scripts", "r2", "ws_one.py")).read().replace('print("ok")', ''))
+if os.environ.get("FUSED"):
+    import synth
+    B, N, H, p = {"c3p0": (32, 197, 12, 0.0), "c3p05": (32, 197, 12, 0.5), "c3p08": (32, 197, 12, 0.8)}[case]
+    q, k, v, keep = (x.cuda() for x in synth.make_inputs(B, N, H, p, "random", "bf16", seed=0))
+    for _ in range(3):
+        rb.pack_attend_unpack(q, k, v, keep, engine=3)
+    torch.cuda.synchronize()
+else:
+    exec(open(os.path.join(ROOT, "scripts", "r2", "ws_one.py")).read().replace('print("ok")', ''))
 lib = rb.lib()
 lib.ragged_debug_fa_timeline.argtypes = [ctypes.c_void_p, ctypes.c_int32]
 buf = np.zeros((148, 128), np.uint64)
@@ -28,6 +36,6 @@ for c in (0, 1, 60, 147):
                           "PVA0_issued": us(33 + 4 * it),
                           "A": [(us(4 * it + 2 * j), us(4 * it + 2 * j + 1)) for j in range(2)],
                           "B": [(us(16 + 4 * it + 2 * j), us(16 + 4 * it + 2 * j + 1)) for j in range(2)],
-                          "epiA": us(50 + it), "epiB": us(54 + it)}
+                          "epiA": us(50 + it), "epiB": us(54 + it), "rows_pub": us(70 + it), "kv_last_issue": us(74 + it)}
     res[f"cta{c}"] = r
 print(json.dumps(res, indent=1))
