@@ -561,7 +561,7 @@ def measure_e2e_zero_copy(args, rb, torch, dev, q, k, v, keep, ws, B, N, H, dt, 
     input set (enough sets that their kept rows exceed 2x L2, so no step is
     served from cache); 3 streams pipeline the independent steps."""
     import math
-    nst = 3
+    nst = int(os.environ.get("RAGGED_E2E_STREAMS", "3"))  # (experiments only)
     T = int(keep.numpy().astype(bool).sum())
     kept = keep.numel() + 3 * T * H * 64 * q.element_size()
     set_bytes = sum(t.numel() * t.element_size() for t in (q, k, v, keep))
