@@ -70,8 +70,8 @@ typedef enum {
   RAGGED_ENGINE_TCGEN05_WS = 3  /* warp-specialised tcgen05 (M = 128 query tiles in
                                    ping-pong, TMEM-resident S/P/O): ragged_attn with
                                    d = 64, any N -- the long-sequence engine; also
-                                   ragged_pack_attend_unpack (TMA gather4 of the kept
-                                   rows; explicit only) */
+                                   ragged_pack_attend_unpack (cp.async gather of the
+                                   kept rows; AUTO at n_hint >= 188) */
 } ragged_engine;
 
 /* The problem statement of the paper: B images, N padded tokens per image
@@ -169,11 +169,11 @@ RAGGED_API ragged_status ragged_unpack(const ragged_problem* prob, const void* o
  * padded o, with +0.0 rows for dropped tokens.  Equal, bit for bit, to
  * ragged_pack; ragged_attn; ragged_unpack on the same engine.  If
  * cu_seqlens_or_null is non-NULL it also receives cu_seqlens (one extra CTA
- * computes it concurrently).  RAGGED_ENGINE_TCGEN05_WS (explicit only; AUTO
- * keeps the one-stage engines, measured faster at DeiT lengths): the kept rows
- * of the padded q/k/v are gathered by TMA tile::gather4 into the warp-
- * specialised engine; d = 64; with a cu_seqlens output only for B*N <= 65536
- * (else RAGGED_ENOTSUP). */
+ * computes it concurrently).  RAGGED_ENGINE_TCGEN05_WS (and AUTO when n_hint
+ * >= 188, nearly unpruned images -- measured faster there, slower from 10 %
+ * pruning on): the kept rows of the padded q/k/v are gathered (cp.async) into
+ * the warp-specialised engine; d = 64; with a cu_seqlens output only for
+ * B*N <= 65536 (else RAGGED_ENOTSUP; AUTO then keeps the one-stage engines). */
 RAGGED_API ragged_status ragged_pack_attend_unpack(const ragged_problem* prob, const uint8_t* keep,
                                         const void* q, const void* k, const void* v,
                                         void* o, int32_t* cu_seqlens_or_null,

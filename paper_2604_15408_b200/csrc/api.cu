@@ -236,7 +236,12 @@ ragged_status ragged_pack_attend_unpack(const ragged_problem* prob, const uint8_
   // the warp-specialised tcgen05 engine (gather4 of the kept rows, attention, scatter):
   // explicit, or AUTO when the caller expects long sequences (n_hint > kWsMinHint)
   const bool ws_ok = prob->d == 64 && (cu_seqlens_or_null == nullptr || (long long)prob->B * prob->N <= 65536);
-  const bool ws = prob->engine == RAGGED_ENGINE_TCGEN05_WS;  // AUTO: measured below
+  // AUTO: only for (nearly) unpruned images -- measured at DeiT-B B = 32: p = 0 28.0 vs 30.0 us
+  // (B = 64: 51.4 vs 57.7), but p = 0.1 27.0 vs 24.9: the row gathers cost more than the
+  // one-stage engines' HMMA work saves once a tenth of the tokens is dropped
+  constexpr int kWsFusedMinHint = 188;
+  const bool ws = prob->engine == RAGGED_ENGINE_TCGEN05_WS ||
+                  (prob->engine == RAGGED_ENGINE_AUTO && prob->n_hint >= kWsFusedMinHint && ws_ok);
   if (ws && !ws_ok)
     return fail(RAGGED_ENOTSUP, "RAGGED_ENGINE_TCGEN05_WS: d = 64, and cu_seqlens output only for B*N <= 65536");
   if (prob->B == 0) return RAGGED_OK;

@@ -125,16 +125,6 @@ struct FaBars {
   uint32_t tmem;
 };
 
-// fused mode: 4 rows (padded row indices) of one head's 64 columns into 512
-// contiguous SW128 bytes (tile::gather4; tensor map box {64, 1}).
-__device__ __forceinline__ void tma_gather4(uint32_t dst, const CUtensorMap* map, uint32_t bar, int c0, int r0,
-                                            int r1, int r2, int r3) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(dst),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(r0), "r"(r1), "r"(r2), "r"(r3)
-      : "memory");
-}
 __device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
@@ -509,19 +499,22 @@ __global__ void __launch_bounds__(kFaThreads, 1)
   pdl_launch_dependents();
   if (warp == 0) tc::alloc(smem_u32(&bars.tmem), 512);
   if (threadIdx.x == 32) {
+    // fused mode: the 64 rows threads fill the stages with cp.async and each
+    // arrives once its own copies have landed
+    constexpr uint32_t kFill = kFused ? 64u : 1u;
     for (int s = 0; s < kFaStages; ++s) {
-      tc::mbar_init(smem_u32(&bars.full[s]), 1);   // producer arrive + expect_tx (TMA bytes)
-      tc::mbar_init(smem_u32(&bars.empty[s]), 1);  // tcgen05.commit
+      tc::mbar_init(smem_u32(&bars.full[s]), kFill);  // producer arrive + expect_tx (TMA bytes) | rows threads
+      tc::mbar_init(smem_u32(&bars.empty[s]), 1);     // tcgen05.commit
     }
     for (int qb = 0; qb < 2; ++qb) {
-      tc::mbar_init(smem_u32(&bars.q_full[qb]), 1);
+      tc::mbar_init(smem_u32(&bars.q_full[qb]), kFill);
       tc::mbar_init(smem_u32(&bars.q_free[qb]), 1);
     }
     for (int x = 0; x < 2; ++x) {
       tc::mbar_init(smem_u32(&bars.s[x]), 1);      // tcgen05.commit: S ready (and all earlier UMMAs done)
       tc::mbar_init(smem_u32(&bars.p[x]), 4);      // one arrival per softmax warp: P stored
       tc::mbar_init(smem_u32(&bars.rows_full[x]), 1);   // the rows warps published an item's positions
-      tc::mbar_init(smem_u32(&bars.rows_free[x]), 10);  // producer + MMA warp + 8 softmax warps done with them
+      tc::mbar_init(smem_u32(&bars.rows_free[x]), 9);   // MMA warp + 8 softmax warps done with them
     }
     tc::fence_mbar_init();
   }
@@ -532,55 +525,7 @@ __global__ void __launch_bounds__(kFaThreads, 1)
   const uint32_t tmem = bars.tmem;
 
   if (kFused && warp == 0) {
-    // ------------------------------------------------------------ producer (fused)
-    // lane g gathers rows 4g..4g+3 of every 128-row tile (one gather4 each)
-    const int16_t* s_pos = reinterpret_cast<const int16_t*>(smem + kOffRows);
-    const int* s_n = reinterpret_cast<const int*>(smem + kOffRows + 2 * kMaxN * 2);
-    if (lane == 0) {
-      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tq)) : "memory");
-      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tk)) : "memory");
-      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tv)) : "memory");
-    }
-    uint32_t kv = 0;
-    int nitem = 0, iall = 0;
-    for (int it = blockIdx.x; it < a.nitems; it += gridDim.x, ++iall) {
-      const int rb = iall & 1;
-      tc::mbar_wait(smem_u32(&bars.rows_full[rb]), (iall >> 1) & 1);
-      FaItem I;
-      const bool ok = fa_item_n(a, it, s_n[rb], I);
-      if (ok) {
-        const int16_t* pos = s_pos + rb * kMaxN;
-        const int rbase = I.b * a.N, col = I.h * kHeadDim, last = I.n - 1;
-        auto prow = [&](int r) { return rbase + pos[r < last ? r : last]; };  // rows past n: any kept row
-        const int qb = nitem & 1;
-        if (nitem >= 2) tc::mbar_wait(smem_u32(&bars.q_free[qb]), ((nitem >> 1) - 1) & 1);
-        const uint32_t qbar = smem_u32(&bars.q_full[qb]);
-        if (lane == 0 && nitem < 4) FTL(59 + nitem);
-        if (lane == 0) expect_tx(qbar, I.ntile * kFaTileBytes);
-        __syncwarp();
-        for (int x = 0; x < I.ntile; ++x) {
-          const int r = I.rows0 + x * kFaRows + 4 * lane;
-          tma_gather4(smem_u32(smem + kOffQ + (2 * qb + x) * kFaTileBytes) + 512u * lane, &tq, qbar, col, prow(r),
-                      prow(r + 1), prow(r + 2), prow(r + 3));
-        }
-        for (int j = 0; j < I.nb; ++j, ++kv) {
-          const int st = kv % kFaStages;
-          tc::mbar_wait(smem_u32(&bars.empty[st]), ((kv / kFaStages) & 1) ^ 1);
-          const uint32_t fbar = smem_u32(&bars.full[st]);
-          const uint32_t kdst = smem_u32(smem + kOffKV + st * 2 * kFaTileBytes);
-          if (lane == 0) expect_tx(fbar, 2 * kFaTileBytes);
-          __syncwarp();
-          const int r = j * kFaRows + 4 * lane;
-          const int r0 = prow(r), r1 = prow(r + 1), r2 = prow(r + 2), r3 = prow(r + 3);
-          tma_gather4(kdst + 512u * lane, &tk, fbar, col, r0, r1, r2, r3);
-          tma_gather4(kdst + kFaTileBytes + 512u * lane, &tv, fbar, col, r0, r1, r2, r3);
-        }
-        if (lane == 0 && nitem < 4) FTL(74 + nitem);  // last K/V gather of the item issued
-        ++nitem;
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(smem_u32(&bars.rows_free[rb]));
-    }
+    // fused mode: the rows warps below gather the tiles (warp 0 idle)
   } else if (kFused && (warp == 2 || warp == 3)) {
     // ------------------------------------------------------------ rows (fused)
     // per item: keep row -> kept positions (ascending) + count, the +0.0 rows of
@@ -591,7 +536,8 @@ __global__ void __launch_bounds__(kFaThreads, 1)
     int* s_scan = s_n + 2;  // [0, 2): warp totals, [2, 4): prefix partials
     const int t = threadIdx.x - 64;
     const uint4 z = make_uint4(0u, 0u, 0u, 0u);
-    int iall = 0;
+    int iall = 0, fnitem = 0;  // all items / items with attention work
+    uint32_t fkv = 0;          // K/V blocks gathered (stage = fkv % kFaStages)
     for (int it = blockIdx.x; it < a.nitems; it += gridDim.x, ++iall) {
       const int rb = iall & 1;
       if (iall >= 2) tc::mbar_wait(smem_u32(&bars.rows_free[rb]), ((iall >> 1) - 1) & 1);
@@ -659,6 +605,60 @@ __global__ void __launch_bounds__(kFaThreads, 1)
       named_bar_sync(1, 64);  // positions, count and scan scratch complete
       if (t == 0) mbar_arrive(smem_u32(&bars.rows_full[rb]));
       if (t == 0 && iall < 4) FTL(70 + iall);  // the item's positions published
+      FaItem I;
+      if (!fa_item_n(a, it, n, I)) continue;
+      // gather the kept rows (ascending positions; rows past n repeat the last kept row,
+      // their results are discarded) of the padded q / k / v: 16-byte cp.async per
+      // thread-chunk into the SW128 layout (chunk c of tile row r at c ^ (r & 7)); one
+      // commit group per tile set, drained in order: wait, proxy fence (generic-proxy
+      // writes read by the async-proxy UMMAs), arrive
+      const int16_t* pos = s_pos + rb * kMaxN;
+      const long long ldb = a.ld * 2;
+      const long long ibase = (long long)I.b * a.N;
+      const int last = I.n - 1;
+      auto gather_tile = [&](const void* ten, uint32_t dst, int row0) {
+        const char* base = static_cast<const char*>(ten) + ibase * ldb + I.h * kRowBytes;
+#pragma unroll 4
+        for (int i = 0; i < 16; ++i) {
+          const int cidx = t + 64 * i, row = cidx >> 3, ch = cidx & 7;
+          const int r = row0 + row;
+          const int p = pos[r < last ? r : last];
+          cp_async_16(dst + row * kRowBytes + ((ch ^ (row & 7)) << 4), base + p * ldb + ch * 16, 16);
+        }
+      };
+      const int qb = fnitem & 1;
+      if (fnitem >= 2) tc::mbar_wait(smem_u32(&bars.q_free[qb]), ((fnitem >> 1) - 1) & 1);
+      for (int x = 0; x < I.ntile; ++x)
+        gather_tile(a.q, smem_u32(smem + kOffQ + (2 * qb + x) * kFaTileBytes), I.rows0 + x * kFaRows);
+      cp_async_commit();
+      int st[2] = {0, 0};
+      for (int j = 0; j < I.nb; ++j, ++fkv) {
+        st[j] = fkv % kFaStages;
+        tc::mbar_wait(smem_u32(&bars.empty[st[j]]), ((fkv / kFaStages) & 1) ^ 1);
+        const uint32_t kdst = smem_u32(smem + kOffKV + st[j] * 2 * kFaTileBytes);
+        gather_tile(a.k, kdst, j * kFaRows);
+        gather_tile(a.v, kdst + kFaTileBytes, j * kFaRows);
+        cp_async_commit();
+      }
+      auto publish = [&](uint32_t bar) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_arrive(bar);
+      };
+      if (I.nb == 2) {
+        cp_async_wait_group<2>();
+        publish(smem_u32(&bars.q_full[qb]));
+        cp_async_wait_group<1>();
+        publish(smem_u32(&bars.full[st[0]]));
+        cp_async_wait_group<0>();
+        publish(smem_u32(&bars.full[st[1]]));
+      } else {
+        cp_async_wait_group<1>();
+        publish(smem_u32(&bars.q_full[qb]));
+        cp_async_wait_group<0>();
+        publish(smem_u32(&bars.full[st[0]]));
+      }
+      if (t == 0 && fnitem < 4) FTL(74 + fnitem);  // the item's tiles landed (this thread's share)
+      ++fnitem;
     }
   } else if (warp == 0) {
     // ------------------------------------------------------------ producer

@@ -234,7 +234,7 @@ def test_gather_kernel_variant_follows_n_hint(n_hint):
     ragged_attn on the mma.sync engine with that n_hint."""
     B, N, H = 6, 197, 12
     q, k, v, keep = _inputs(B, N, H, 0.0 if n_hint == 197 else 0.8, seed=31)
-    ref = rb.pack_attend_unpack(q, k, v, keep, n_hint=n_hint)
+    ref = rb.pack_attend_unpack(q, k, v, keep, n_hint=n_hint, engine=rb.ENGINE_MMA_SYNC)
     o = _sentinel((B, N, H, 64), q.dtype)
     rb.pack_attend_unpack_gather(q, k, v, keep, rb.gather_desc(1, 0, out=[o]), n_hint=n_hint)
     qp, kp, vp, cu, _, _ = rb.pack(q, k, v, keep)

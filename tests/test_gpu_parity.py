@@ -439,8 +439,9 @@ def test_long_sequence_variant(dtype, B, N, H, p, method):
     keep_np[B // 2, :] = 0                      # an empty image
     keep = torch.from_numpy(keep_np)
     qd, kd, vd, keepd = _dev(q, k, v, keep)
-    o_long, cu_long = rb.pack_attend_unpack(qd, kd, vd, keepd, want_cu=True, n_hint=N)
-    again = rb.pack_attend_unpack(qd, kd, vd, keepd, n_hint=N)
+    MMA = rb.ENGINE_MMA_SYNC  # the long variant of the one-stage kernel (AUTO at n_hint >= 188: the WS engine)
+    o_long, cu_long = rb.pack_attend_unpack(qd, kd, vd, keepd, want_cu=True, n_hint=N, engine=MMA)
+    again = rb.pack_attend_unpack(qd, kd, vd, keepd, n_hint=N, engine=MMA)
     qp, kp, vp, cu, dst, src = rb.pack(qd, kd, vd, keepd)
     # composed path on the fused kernel's engine (AUTO takes the warp-specialised
     # engine at n_hint > 148: equal within tolerance, not bitwise -- tested below)
@@ -480,7 +481,7 @@ def test_long_variant_running_max_paths(dtype, ramp):
     keep = torch.from_numpy(keep_np)
     qd, kd, vd, keepd = _dev(q, k, v, keep)
     ref, _ = fused_oracle(q, k, v, keep)
-    o_long = rb.pack_attend_unpack(qd, kd, vd, keepd, n_hint=N)
+    o_long = rb.pack_attend_unpack(qd, kd, vd, keepd, n_hint=N, engine=rb.ENGINE_MMA_SYNC)
     o_short = rb.pack_attend_unpack(qd, kd, vd, keepd)
     qp, kp, vp, cu, dst, src = rb.pack(qd, kd, vd, keepd)
     # composed path on the fused kernel's engine (AUTO takes the warp-specialised
@@ -538,8 +539,9 @@ def test_query_split_small_batch_bitwise_equals_unsplit(n_hint):
     rep = lambda t: torch.cat([t] * (big // B)).contiguous()  # noqa: E731
     qd, kd, vd, kp = _dev(q, k, v, keep)
     Qd, Kd, Vd, Kp = _dev(rep(q), rep(k), rep(v), rep(keep))
-    o_small, cu_small = rb.pack_attend_unpack(qd, kd, vd, kp, want_cu=True, n_hint=n_hint)
-    o_big = rb.pack_attend_unpack(Qd, Kd, Vd, Kp, n_hint=n_hint)
+    MMA = rb.ENGINE_MMA_SYNC  # the query split is the mma.sync engine's
+    o_small, cu_small = rb.pack_attend_unpack(qd, kd, vd, kp, want_cu=True, n_hint=n_hint, engine=MMA)
+    o_big = rb.pack_attend_unpack(Qd, Kd, Vd, Kp, n_hint=n_hint, engine=MMA)
     torch.cuda.synchronize()
     assert np.array_equal(bits(o_small), bits(o_big[:B]))
     assert cu_small.cpu().tolist() == [0, 197, 347]
@@ -547,7 +549,7 @@ def test_query_split_small_batch_bitwise_equals_unsplit(n_hint):
     check_attention(to_np(o_small), ref, torch.bfloat16)
     qp, kpk, vp, cu, _, _ = rb.pack(qd, kd, vd, kp)
     Qp, Kpk, Vp, CU, _, _ = rb.pack(Qd, Kd, Vd, Kp)
-    a_small = rb.attn(qp, kpk, vp, cu, N, n_hint=n_hint)
-    a_big = rb.attn(Qp, Kpk, Vp, CU, N, n_hint=n_hint)
+    a_small = rb.attn(qp, kpk, vp, cu, N, n_hint=n_hint, engine=MMA)
+    a_big = rb.attn(Qp, Kpk, Vp, CU, N, n_hint=n_hint, engine=MMA)
     torch.cuda.synchronize()
     assert np.array_equal(bits(a_small[:347]), bits(a_big[:347]))

@@ -148,7 +148,8 @@ def test_prune_l2_fused_matches_oracle(dtype, B, N, H, p):
     assert cu.cpu().tolist() == [b * min(kk, N) for b in range(B + 1)]
     ref, _ = oracle.pack_attend_unpack(q, k, v, km)
     check_attention(to_np(o), ref, DT[dtype])
-    o2 = rb.pack_attend_unpack(qd, kd, vd, keep, n_hint=min(kk, N))
+    # the prune-fused kernel is the mma.sync engine (AUTO would take the WS engine at n_hint >= 188)
+    o2 = rb.pack_attend_unpack(qd, kd, vd, keep, n_hint=min(kk, N), engine=rb.ENGINE_MMA_SYNC)
     torch.cuda.synchronize()
     assert np.array_equal(bits(o), bits(o2))
 

@@ -152,3 +152,16 @@ def test_ws_fused_qkv_layout():
     torch.cuda.synchronize()
     ref, _ = oracle.pack_attend_unpack(q, k, v, keep.numpy())
     check_attention(to_np(o), ref, torch.bfloat16)
+
+
+@pytest.mark.parametrize("n_hint,engine", [(197, WS), (188, WS), (187, 1), (39, 1)])
+def test_fused_auto_engine_choice(n_hint, engine):
+    """AUTO for the fused call: the warp-specialised engine only for nearly
+    unpruned images (n_hint >= 188), else the one-stage kernels; bitwise the
+    chosen engine's result."""
+    B, N, H = 6, 197, 4
+    q, k, v, keep = (t.to(DEV) for t in synth.make_inputs(B, N, H, 0.0, "all", "bf16", seed=n_hint))
+    auto = rb.pack_attend_unpack(q, k, v, keep, n_hint=n_hint)
+    ref = rb.pack_attend_unpack(q, k, v, keep, n_hint=n_hint, engine=engine)
+    torch.cuda.synchronize()
+    assert torch.equal(auto.view(torch.int16), ref.view(torch.int16))
