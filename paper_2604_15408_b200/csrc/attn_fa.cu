@@ -481,10 +481,11 @@ __device__ __forceinline__ void fa_softmax_block(uint32_t tS, uint32_t tO, int n
 // kFused: pack-attend-unpack in one launch.  Warps 2-3 (idle in the packed
 // engine) read each item's keep row, rank the kept positions (the packed order,
 // R7) into shared memory, write the +0.0 rows of the dropped positions and
-// cu_seqlens; the producer gathers the kept rows of the padded q / k / v with
-// TMA tile::gather4 (4 rows per op, the SW128 layout of a tile load); the
-// softmax warps store O rows at their padded positions.  The rest is the
-// packed engine unchanged.
+// cu_seqlens, and gather the kept rows of the padded q / k / v into the Q
+// buffers and the K/V ring with cp.async (SW128 layout; warp 0, the TMA
+// producer of the packed engine, idles); the softmax warps store O rows at
+// their padded positions.  The rest is the packed engine unchanged.  (A TMA
+// tile::gather4 producer was measured first: ~30 ns per 4-row op per SM.)
 template <typename T, bool kFused = false>
 __global__ void __launch_bounds__(kFaThreads, 1)
     attn_fa_kernel(const FaArgs a, const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
@@ -961,9 +962,10 @@ cudaError_t launch_attn_fa(int dtype, const void* qp, const void* kp, const void
 }
 
 // Fused pack-attend-unpack on this engine: q / k / v padded [B, N, H, d] (token
-// stride ld), o padded [B, N, H, d] contiguous, keep [B, N]; gather4 tensor maps
-// (box {64, 1}) over the B*N padded rows.  cu_out (optional) needs B*N <= 65536
-// (each head-0 item counts the mask prefix of its image; checked in api.cu).
+// stride ld), o padded [B, N, H, d] contiguous, keep [B, N].  The kernel's tensor
+// map parameters are unused in this mode (the rows warps gather with cp.async);
+// valid maps are passed all the same.  cu_out (optional) needs B*N <= 65536 (each
+// head-0 item counts the mask prefix of its image; checked in api.cu).
 cudaError_t launch_attn_fa_fused(int dtype, const uint8_t* keep, const void* q, const void* k, const void* v,
                                  long long ld, void* o, int32_t* cu_out, int B, int N, int H, cudaStream_t st) {
   CUtensorMap tq, tk, tv;
