@@ -96,6 +96,13 @@ cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
 // RAGGED_ENGINE_AUTO -> the engine measured fastest; the
 // mma.sync engine's long-sequence variant when the caller expects > 64 kept
 // tokens per image (ragged_problem.n_hint).
+static int device_sms() {
+  int dev = 0, v = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+  return v;
+}
+
 // ragged_attn / ragged_vit_block AUTO: the warp-specialised tcgen05 engine at
 // d = 64 when the caller expects more than this many kept tokens per image
 // (measured crossover at DeiT-B, scripts/r2/ws_cross.py).
@@ -236,12 +243,15 @@ ragged_status ragged_pack_attend_unpack(const ragged_problem* prob, const uint8_
   // the warp-specialised tcgen05 engine (gather4 of the kept rows, attention, scatter):
   // explicit, or AUTO when the caller expects long sequences (n_hint > kWsMinHint)
   const bool ws_ok = prob->d == 64 && (cu_seqlens_or_null == nullptr || (long long)prob->B * prob->N <= 65536);
-  // AUTO: only for (nearly) unpruned images -- measured at DeiT-B B = 32: p = 0 28.0 vs 30.0 us
-  // (B = 64: 51.4 vs 57.7), but p = 0.1 27.0 vs 24.9: the row gathers cost more than the
-  // one-stage engines' HMMA work saves once a tenth of the tokens is dropped
+  // AUTO: only for (nearly) unpruned images and at least two problems per SM -- measured at
+  // DeiT-B B = 32: p = 0 28.0 vs 30.0 us (B = 64: 51.4 vs 57.7), but p = 0.1 27.0 vs 24.9 (the
+  // row gathers cost more than the one-stage engines' HMMA work saves once a tenth of the
+  // tokens is dropped), and with fewer problems (DeiT-S B = 32, 192; BS 4 / 16) 20.1 vs 19.1,
+  // 12.0 vs 11.6, 19.4 vs 18.9 (the one-stage engines split the queries of small batches)
   constexpr int kWsFusedMinHint = 188;
   const bool ws = prob->engine == RAGGED_ENGINE_TCGEN05_WS ||
-                  (prob->engine == RAGGED_ENGINE_AUTO && prob->n_hint >= kWsFusedMinHint && ws_ok);
+                  (prob->engine == RAGGED_ENGINE_AUTO && prob->n_hint >= kWsFusedMinHint && ws_ok &&
+                   (long long)prob->B * prob->H >= 2LL * device_sms());
   if (ws && !ws_ok)
     return fail(RAGGED_ENOTSUP, "RAGGED_ENGINE_TCGEN05_WS: d = 64, and cu_seqlens output only for B*N <= 65536");
   if (prob->B == 0) return RAGGED_OK;
@@ -510,13 +520,6 @@ ragged_status ragged_attn_gather(const ragged_problem* prob, const void* qp, con
 }
 
 // ---- ragged_block.h (NEXT row N1) -------------------------------------------
-static int device_sms() {
-  int dev = 0, v = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
-  return v;
-}
-
 static ragged_status check_stride(int64_t ld, int64_t min_ld, const char* name) {
   static thread_local char buf[96];
   if (ld < min_ld) {

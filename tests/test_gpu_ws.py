@@ -154,12 +154,12 @@ def test_ws_fused_qkv_layout():
     check_attention(to_np(o), ref, torch.bfloat16)
 
 
-@pytest.mark.parametrize("n_hint,engine", [(197, WS), (188, WS), (187, 1), (39, 1)])
-def test_fused_auto_engine_choice(n_hint, engine):
+@pytest.mark.parametrize("B,n_hint,engine", [(32, 197, WS), (32, 188, WS), (32, 187, 1), (32, 39, 1), (6, 197, 1)])
+def test_fused_auto_engine_choice(B, n_hint, engine):
     """AUTO for the fused call: the warp-specialised engine only for nearly
-    unpruned images (n_hint >= 188), else the one-stage kernels; bitwise the
-    chosen engine's result."""
-    B, N, H = 6, 197, 4
+    unpruned images (n_hint >= 188) and at least two (image, head) problems per
+    SM, else the one-stage kernels; bitwise the chosen engine's result."""
+    N, H = 197, 12
     q, k, v, keep = (t.to(DEV) for t in synth.make_inputs(B, N, H, 0.0, "all", "bf16", seed=n_hint))
     auto = rb.pack_attend_unpack(q, k, v, keep, n_hint=n_hint)
     ref = rb.pack_attend_unpack(q, k, v, keep, n_hint=n_hint, engine=engine)
