@@ -358,8 +358,6 @@ ragged_status ragged_graph_create(const ragged_problem* prob, const uint8_t* kee
   if (out == nullptr) return fail(RAGGED_EINVAL, "out is NULL");
   *out = nullptr;
   RAGGED_TRY(check_problem(prob));
-  if (prob->engine == RAGGED_ENGINE_TCGEN05_WS)
-    return fail(RAGGED_ENOTSUP, "RAGGED_ENGINE_TCGEN05_WS runs ragged_attn only");
   cudaStream_t st = nullptr;
   cudaError_t e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
   if (e != cudaSuccess) return cuda_fail(e, "ragged_graph_create/stream");

@@ -212,7 +212,7 @@ def test_fused_equals_composed_bitwise(engine, dtype, p):
     assert np.array_equal(bits(o1), bits(o2))
 
 
-@pytest.mark.parametrize("engine", ENGINES)
+@pytest.mark.parametrize("engine", ENGINES + [rb.ENGINE_TCGEN05_WS])
 def test_graph_replay_and_determinism_bitwise(engine):
     q, k, v, keep = synth.make_inputs(32, 197, 12, 0.8, "l2", "bf16", seed=9)
     qd, kd, vd, keepd = _dev(q, k, v, keep)
@@ -495,8 +495,8 @@ def test_long_variant_running_max_paths(dtype, ramp):
     check_attention(to_np(o_auto), ref, DT[dtype], dist="peaked")  # the warp-specialised engine's lazy rescale
 
 
-@pytest.mark.parametrize("n_hint", [0, 197])
-def test_mask_rewritten_by_previous_kernel(n_hint):
+@pytest.mark.parametrize("n_hint,engine", [(0, 0), (197, 0), (197, 3)])
+def test_mask_rewritten_by_previous_kernel(n_hint, engine):
     """The fused kernel reads the keep row (and prefetches kept rows) BEFORE its
     PDL grid-dependency wait; only the post-wait read may reach results.  Here
     the N2 mask kernel rewrites ONE keep buffer right before every fused call
@@ -512,14 +512,14 @@ def test_mask_rewritten_by_previous_kernel(n_hint):
     for x in xs:
         km = rb.keep_topk_l2(x, kk)
         torch.cuda.synchronize()
-        ref.append(rb.pack_attend_unpack(q, k, v, km, n_hint=n_hint))
+        ref.append(rb.pack_attend_unpack(q, k, v, km, n_hint=n_hint, engine=engine))
         torch.cuda.synchronize()
     assert not torch.equal(rb.keep_topk_l2(xs[0], kk), rb.keep_topk_l2(xs[1], kk))
     keep = torch.empty(B, N, dtype=torch.uint8, device=DEV)
     outs = [torch.empty_like(ref[0]) for _ in range(40)]
     for i, o in enumerate(outs):
         rb.keep_topk_l2(xs[i % 2], kk, keep=keep)
-        rb.pack_attend_unpack(q, k, v, keep, o=o, n_hint=n_hint)
+        rb.pack_attend_unpack(q, k, v, keep, o=o, n_hint=n_hint, engine=engine)
     torch.cuda.synchronize()
     for i, o in enumerate(outs):
         assert np.array_equal(bits(o), bits(ref[i % 2])), f"call {i}"
