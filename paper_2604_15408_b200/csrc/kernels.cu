@@ -174,10 +174,14 @@ __device__ void scan_cta(const uint8_t* __restrict__ keep, int B, int N, int32_t
 
 // a1 as ONE flat prefix sum.  In image-major order the definition
 // restates as: dst[i] = #kept positions in [0, i) for a kept i, and
-// cu[b] = #kept positions in [0, b*N).  One CTA; each round 1024 threads take 16
-// contiguous mask bytes each (16-byte vector load when aligned), a block-wide
-// exclusive scan of the per-thread counts gives every position's rank, and a
-// carry links the rounds.  Deterministic, no atomics.
+// cu[b] = #kept positions in [0, b*N).  CTA c takes the c-th 16 KB of the mask
+// (1024 threads x 16 contiguous bytes, 16-byte vector loads when aligned): its
+// carry is the count of kept bytes before it -- counted by the CTA itself with
+// 16-byte loads (redundant across CTAs: ~(#CTAs / 2) x the mask of L2 reads, 20
+// MB at B = 4096, N = 197) -- then a block-wide exclusive scan of the
+// per-thread counts gives every position's rank.  Round 1 ran the chunks as
+// rounds of ONE CTA linked by a carry: 265 us at B = 4096 (one DRAM round trip
+// and two barriers per 16 KB).  Deterministic, no atomics, one launch.
 constexpr int kScanThreads = 1024;
 constexpr int kScanRun = 16;  // mask bytes per thread per round
 
@@ -192,9 +196,33 @@ __global__ void __launch_bounds__(kScanThreads, 1)
   const long long total = (long long)B * N;
   const bool vec_in = (reinterpret_cast<uintptr_t>(keep) & 15) == 0;
   const bool vec_out = (reinterpret_cast<uintptr_t>(dst) & 15) == 0;
-  if (tid == 0) s_carry = 0;
-  __syncthreads();
-  for (long long base = 0; base < total; base += (long long)kScanThreads * kScanRun) {
+  const long long chunk = (long long)kScanThreads * kScanRun;
+  {  // carry: kept bytes in [0, blockIdx.x * chunk)
+    const long long pre = (long long)blockIdx.x * chunk;
+    int c = 0;
+    if (vec_in) {
+      const uint4* k16 = reinterpret_cast<const uint4*>(keep);
+      for (long long i = tid; i < pre / 16; i += kScanThreads) {
+        const uint4 v = k16[i];
+        c += (__popc(__vcmpne4(v.x, 0u)) + __popc(__vcmpne4(v.y, 0u)) + __popc(__vcmpne4(v.z, 0u)) +
+              __popc(__vcmpne4(v.w, 0u))) >> 3;
+      }
+    } else {
+      for (long long i = tid; i < pre; i += kScanThreads) c += keep[i] != 0 ? 1 : 0;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    if (lane == 0) s_warp[warp] = c;
+    __syncthreads();
+    if (tid == 0) {
+      int t = 0;
+      for (int w = 0; w < kScanThreads / 32; ++w) t += s_warp[w];
+      s_carry = t;
+    }
+    __syncthreads();
+  }
+  for (long long base = (long long)blockIdx.x * chunk; base < total && base < (long long)(blockIdx.x + 1) * chunk;
+       base += chunk) {
     const long long p0 = base + (long long)tid * kScanRun;
     uint32_t flags = 0;  // bit e: position p0 + e is kept
     if (vec_in && p0 + kScanRun <= total) {
@@ -272,7 +300,7 @@ __global__ void __launch_bounds__(kScanThreads, 1)
     if (tid == 0) s_carry = carry + s_warp[31];
     __syncthreads();
   }
-  if (tid == 0) cu[B] = s_carry;
+  if (tid == 0 && (long long)(blockIdx.x + 1) * chunk >= total) cu[B] = s_carry;  // the last chunk's CTA
 }
 
 // ---------------------------------------------------------------- pack ----
@@ -1507,7 +1535,8 @@ cudaError_t launch_scan(const uint8_t* keep, int B, int N, int32_t* cu, int32_t*
                       dst, src, (const uint8_t*)nullptr, (const uint8_t*)nullptr,
                       (const uint8_t*)nullptr, 0LL, (uint8_t*)nullptr, (uint8_t*)nullptr,
                       (uint8_t*)nullptr);
-  return launch_pdl(scan_kernel, dim3(1), dim3(kScanThreads), 0, st, keep, B, N, cu, dst, src);
+  const long long chunks = ((long long)B * N + (long long)kScanThreads * kScanRun - 1) / ((long long)kScanThreads * kScanRun);
+  return launch_pdl(scan_kernel, dim3((unsigned)chunks), dim3(kScanThreads), 0, st, keep, B, N, cu, dst, src);
 }
 
 // a1 + a2: one launch (one CTA per (image, head)) for small batches, else

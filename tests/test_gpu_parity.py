@@ -57,6 +57,28 @@ def test_scan_c5_scale_exact():
     _scan_case(keep)
 
 
+@pytest.mark.parametrize("offset", [0, 1, 3])
+def test_scan_large_batch_chunked_unaligned(offset):
+    """B*N > 65536 takes the chunked scan (one CTA per 16 KB of mask, each
+    counting the kept bytes before its chunk): bit-exact for a mask that does
+    not start on a 16-byte boundary (byte-load carry path) and for one that
+    does, with image boundaries falling inside chunks."""
+    B, N = 420, 197
+    rng = np.random.default_rng(offset + 7)
+    keep_np = (rng.random((B, N)) < 0.45).astype(np.uint8)
+    keep_np[rng.random(B) < 0.05] = 0
+    buf = torch.zeros(B * N + 16, dtype=torch.uint8)
+    buf[offset:offset + B * N] = torch.from_numpy(keep_np.reshape(-1))
+    keep = buf.to(DEV)[offset:offset + B * N].view(B, N)
+    cu, dst, src = rb.scan(keep)
+    torch.cuda.synchronize()
+    rcu, rdst, rsrc = oracle.scan(keep_np)
+    T = int(rcu[-1])
+    assert cu.cpu().numpy().tolist() == rcu.tolist()
+    assert dst.cpu().numpy().tolist() == rdst.tolist()
+    assert src[:T].cpu().numpy().tolist() == rsrc[:T].tolist()
+
+
 # ------------------------------------------------------------------ pack ----
 
 @pytest.mark.parametrize("dtype", ["bf16", "fp16"])
