@@ -315,6 +315,9 @@ constexpr int kCopyThreads = 256;              // 8 warps, one row each per step
 constexpr int kCopyWarps = kCopyThreads / 32;
 constexpr int kCopyU = 3;                      // chunks per lane per tensor per pass
 
+// kOne: a single tensor (q -> qp; the hidden state packed once at the prune
+// point, ragged_pack_rows), k / v unused.
+template <bool kOne = false>
 __global__ void __launch_bounds__(kCopyThreads)
     pack_kernel(const uint8_t* __restrict__ q, const uint8_t* __restrict__ k,
                 const uint8_t* __restrict__ v, const int32_t* __restrict__ cu,
@@ -336,8 +339,10 @@ __global__ void __launch_bounds__(kCopyThreads)
         const int c = c0 + lane + 32 * u;
         if (c < cpr) {
           vq[u] = ld_global_nc_16(q + so + c * 16);
-          vk[u] = ld_global_nc_16(k + so + c * 16);
-          vv[u] = ld_global_nc_16(v + so + c * 16);
+          if constexpr (!kOne) {
+            vk[u] = ld_global_nc_16(k + so + c * 16);
+            vv[u] = ld_global_nc_16(v + so + c * 16);
+          }
         }
       }
 #pragma unroll
@@ -345,8 +350,10 @@ __global__ void __launch_bounds__(kCopyThreads)
         const int c = c0 + lane + 32 * u;
         if (c < cpr) {
           st_global_16(qp + dof + c * 16, vq[u]);
-          st_global_16(kp + dof + c * 16, vk[u]);
-          st_global_16(vp + dof + c * 16, vv[u]);
+          if constexpr (!kOne) {
+            st_global_16(kp + dof + c * 16, vk[u]);
+            st_global_16(vp + dof + c * 16, vv[u]);
+          }
         }
       }
     }
@@ -1563,7 +1570,12 @@ cudaError_t launch_pack(const void* q, const void* k, const void* v, long long l
   const long long want = (cap_rows + kCopyWarps - 1) / kCopyWarps;   // live rows are known on the device only
   const long long most = (long long)sm_count(dev) * 8;              // 8 CTAs (64 warps) per SM
   const int grid = (int)(want < most ? want : most);
-  return launch_pdl(pack_kernel, dim3(grid), dim3(kCopyThreads), 0, st,
+  if (k == nullptr)  // one tensor (ragged_pack_rows)
+    return launch_pdl(pack_kernel<true>, dim3(grid), dim3(kCopyThreads), 0, st, static_cast<const uint8_t*>(q),
+                      (const uint8_t*)nullptr, (const uint8_t*)nullptr, cu, (const int32_t*)src,
+                      static_cast<uint8_t*>(qp), (uint8_t*)nullptr, (uint8_t*)nullptr, B, ld_elems * 2,
+                      H * kHeadDim * 2);
+  return launch_pdl(pack_kernel<false>, dim3(grid), dim3(kCopyThreads), 0, st,
                     static_cast<const uint8_t*>(q), static_cast<const uint8_t*>(k),
                     static_cast<const uint8_t*>(v), cu, (const int32_t*)src, static_cast<uint8_t*>(qp),
                     static_cast<uint8_t*>(kp), static_cast<uint8_t*>(vp), B, ld_elems * 2,
@@ -1801,8 +1813,10 @@ cudaError_t launch_pack_rows(const uint8_t* keep, const void* x, long long ld_el
     return launch_pdl(image_scan_kernel<true, true>, dim3(B * H), dim3(kImgThreads), 0, st, keep, B, N, H, cu, dst,
                       src, static_cast<const uint8_t*>(x), (const uint8_t*)nullptr, (const uint8_t*)nullptr,
                       ld_elems * 2, static_cast<uint8_t*>(xp), (uint8_t*)nullptr, (uint8_t*)nullptr);
-  // large batches: the three-tensor path with the same source / destination
-  return launch_scan_pack(keep, x, x, x, ld_elems, B, N, H, cu, dst, src, xp, xp, xp, st);
+  // large batches: the chunked scan, then the one-tensor gather
+  cudaError_t e = launch_scan(keep, B, N, cu, dst, src, st);
+  if (e != cudaSuccess) return e;
+  return launch_pack(x, nullptr, nullptr, ld_elems, B, N, H, cu, src, xp, nullptr, nullptr, st);
 }
 
 // CLS readout from packed rows: out[b] = xp[cu[b]] if image b kept any

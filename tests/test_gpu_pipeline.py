@@ -21,7 +21,7 @@ def _store(dtype):
     return lambda t: torch.from_numpy(np.asarray(t)).to(dtype).double().numpy()
 
 
-@pytest.mark.parametrize("B,N,D,p", [(5, 197, 768, 0.7), (3, 33, 192, 0.3), (400, 197, 64, 0.5)])
+@pytest.mark.parametrize("B,N,D,p", [(5, 197, 768, 0.7), (3, 33, 192, 0.3), (400, 197, 64, 0.5), (340, 197, 768, 0.7)])
 def test_pack_rows_bitwise(B, N, D, p):
     """x [B, N, D] -> xp rows [0, T) = x[src], cu / dst / src exact (oracle.scan,
     oracle.pack); includes an empty image and a dropped CLS; B*N > 65536 takes
