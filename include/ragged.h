@@ -228,9 +228,11 @@ RAGGED_API ragged_status ragged_keep_topk_l2(const ragged_problem* prob, const v
  * prob->dtype): keep = CLS + the k - 1 other tokens with the largest ||x||_2,
  * exactly as ragged_keep_topk_l2 defines it (fp32 scores; ties to the lower
  * position; NaN last), then O = ragged_pack_attend_unpack(q, k, v, keep).
- * The image's H CTAs form one thread-block cluster (H <= 16, else
- * RAGGED_ENOTSUP) that exchanges per-head partial squared norms through
- * distributed shared memory; no mask round trip through HBM, no second launch.
+ * Consecutive heads of an image form thread-block clusters of C CTAs (C = the
+ * largest divisor of H that is <= 8 and leaves <= 2 slices of x per CTA, e.g.
+ * H = 12 -> C = 6; else C = H; H <= 16, else RAGGED_ENOTSUP) that exchange
+ * partial squared norms through distributed shared memory; every cluster of an
+ * image derives the same mask; no mask round trip through HBM, no second launch.
  * keep_or_null receives the mask [B, N] if non-NULL; cu_seqlens_or_null
  * receives b * min(k, N) (every image keeps min(k, N) tokens).  k < 1 ->
  * RAGGED_EINVAL; RAGGED_ENGINE_TCGEN05 -> RAGGED_ENOTSUP (mma.sync engine;

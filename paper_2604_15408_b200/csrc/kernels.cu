@@ -423,6 +423,7 @@ struct AttnArgs {
   long long ldx;
   int kkeep;
   uint8_t* keep_out;       // optional [B, N] copy of the computed mask
+  int pc;                  // CTAs per cluster (divides H); each stages H / pc slices of x
 };
 
 // Zero (+0.0) the 128-byte head slices of dropped rows sDrop[first], [first +
@@ -976,6 +977,11 @@ __device__ __forceinline__ void cluster_arrive_relaxed() {
   asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
 }
 __device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.wait.aligned;" ::: "memory"); }
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
 __device__ __forceinline__ void cluster_sync_all() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
@@ -991,82 +997,93 @@ __device__ __forceinline__ void st_peer_f32(const void* p, uint32_t rank, float 
 }
 
 // N2 fused ahead of the scan (Threshold-l2; R20): the
-// keep row of image b computed inside the attention kernel.  The image's H
-// CTAs (one per head, head fastest) form one thread-block cluster.  CTA h
-// stages its head's 64-column slice of x for every token (the same 128-byte
-// slices the kernel already works with) with cp.async, squares and sums them in
-// fp32, and stores the N partial sums into every CTA of the cluster (DSMEM);
-// after one cluster barrier each CTA adds the H partials in head order
-// (identical bits in every CTA); CTA h ranks tokens h, h + H, ... (CLS = +inf,
-// NaN last, ties to the lower position) and pushes their keep flags to every
-// CTA; a second cluster barrier publishes them.  Layout: x
-// slices in the K area, partials / keys / keep row in the V + Q areas; the
-// gather overwrites them only after image_rows' barrier (every read done).
-// Returns the keep row in shared memory.
+// keep row of image b computed inside the attention kernel.  Consecutive heads
+// of one image (head fastest) form thread-block clusters of C = a.pc CTAs
+// (C divides H; H / C = S <= 2 slices per CTA, so clusters stay within the
+// portable size 8 up to H = 16 -- clusters of 12 CTAs of 70 KB were not all
+// co-resident at C3 and ran in a second wave).  CTA r of a cluster stages the
+// 64-column slices r S .. r S + S - 1 of x for every token (the same 128-byte
+// slices the kernel works with) with cp.async, squares and sums them in fp32
+// (slice order), and stores the N partial sums into every CTA of the cluster
+// (DSMEM); after one cluster barrier each CTA adds the C partials in rank order
+// (identical bits in every CTA, and in every cluster of the image: cluster j's
+// CTA r computes exactly cluster 0's CTA r's sums); CTA r ranks tokens r, r + C,
+// ... (CLS = +inf, NaN last, ties to the lower position) and pushes their keep
+// flags to every CTA; a second cluster barrier publishes them.  Layout: x
+// slices in the K (and V) area; partials / keys / keep row in the V area when
+// S = 1, else in the Q area; the gather overwrites them only after
+// image_rows' barrier (every read done).  Returns the keep row in shared memory.
 template <typename T>
 __device__ __forceinline__ const uint8_t* prune_l2_row(const AttnArgs& a, int b, int h, uint8_t* smem, int tid) {
   const int rows_cap = attn_rows_cap(a.N);
-  uint8_t* s_x = smem;                                                      // [N][128 B]
-  float* s_part = reinterpret_cast<float*>(smem + rows_cap * kRowBytes);   // [H][N]
-  uint32_t* s_key = reinterpret_cast<uint32_t*>(s_part + a.H * a.N);       // [N]
+  const int C = a.pc, S = a.H / C, r = (int)cluster_rank();
+  uint8_t* s_x = smem;                                                      // [S][N][128 B]
+  float* s_part = reinterpret_cast<float*>(smem + (S == 1 ? 1 : 2) * rows_cap * kRowBytes);  // [C][N]
+  uint32_t* s_key = reinterpret_cast<uint32_t*>(s_part + C * a.N);         // [N]
   uint8_t* s_keep = reinterpret_cast<uint8_t*>(s_key + kMaxN);              // [N]
-  const char* xb = static_cast<const char*>(a.x) + (long long)b * a.N * a.ldx * 2 + h * kRowBytes;
+  const char* xb = static_cast<const char*>(a.x) + (long long)b * a.N * a.ldx * 2 + r * S * kRowBytes;
   {  // 8 threads per 128-byte row slice; every copy in flight at once
     const int c = tid & 7;
-    for (int p = tid >> 3; p < a.N; p += kAttnThreads / 8)
-      cp_async_16(smem_u32(s_x + p * kRowBytes + c * 16), xb + p * a.ldx * 2 + c * 16, 16);
+    for (int j = tid >> 3; j < S * a.N; j += kAttnThreads / 8) {
+      const int sl = j >= a.N ? 1 : 0, p = j - sl * a.N;
+      cp_async_16(smem_u32(s_x + j * kRowBytes + c * 16), xb + p * a.ldx * 2 + sl * kRowBytes + c * 16, 16);
+    }
     cp_async_commit();
     cp_async_wait_all();
   }
   __syncthreads();
   TL(7);
   float sq[2] = {0.f, 0.f};
+  for (int sl = 0; sl < S; ++sl) {
 #pragma unroll
-  for (int i = 0; i < 2; ++i) {
-    const int p = min(tid + i * kAttnThreads, a.N - 1);
+    for (int i = 0; i < 2; ++i) {
+      const int p = sl * a.N + min(tid + i * kAttnThreads, a.N - 1);
 #pragma unroll
-    for (int c = 0; c < 8; ++c) {
-      const uint4 raw = *reinterpret_cast<const uint4*>(s_x + p * kRowBytes + ((c + tid) & 7) * 16);
-      const T* e = reinterpret_cast<const T*>(&raw);
+      for (int c = 0; c < 8; ++c) {
+        const uint4 raw = *reinterpret_cast<const uint4*>(s_x + p * kRowBytes + ((c + tid) & 7) * 16);
+        const T* e = reinterpret_cast<const T*>(&raw);
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const float f = static_cast<float>(e[j]);
-        sq[i] = fmaf(f, f, sq[i]);
+        for (int j = 0; j < 8; ++j) {
+          const float f = static_cast<float>(e[j]);
+          sq[i] = fmaf(f, f, sq[i]);
+        }
       }
     }
   }
   cluster_wait();  // every CTA of the cluster has started: DSMEM is live
   TL(8);
-  for (int r = 0; r < a.H; ++r) {
-    if (tid < a.N) st_peer_f32(s_part + h * a.N + tid, r, sq[0]);
-    if (tid + kAttnThreads < a.N) st_peer_f32(s_part + h * a.N + tid + kAttnThreads, r, sq[1]);
+  for (int d = 0; d < C; ++d) {
+    if (tid < a.N) st_peer_f32(s_part + r * a.N + tid, d, sq[0]);
+    if (tid + kAttnThreads < a.N) st_peer_f32(s_part + r * a.N + tid + kAttnThreads, d, sq[1]);
   }
   TL(9);
-  cluster_sync_all();  // all H partials of every token delivered
+  cluster_sync_all();  // all C partials of every token delivered
   TL(10);
   float* s_score = reinterpret_cast<float*>(s_key);
   for (int p = tid; p < a.N; p += kAttnThreads) {
     float t = 0.f;
-    for (int r = 0; r < a.H; ++r) t += s_part[r * a.N + p];
+    for (int d = 0; d < C; ++d) t += s_part[d * a.N + p];
     s_score[p] = p == 0 ? INFINITY : (t != t ? -INFINITY : t);
   }
   __syncthreads();
   TL(11);
-  // this CTA ranks tokens p = h, h + H, ... (g lanes per token) and stores the
-  // flags into every CTA of the cluster: the O(N^2) comparisons are split H ways
+  // this CTA ranks tokens p = r, r + C, ... (g lanes per token) and stores the
+  // flags into every CTA of the cluster: the O(N^2) comparisons are split C ways;
+  // the image's first cluster also writes keep_out
   {
-    const int cnt = (a.N - h + a.H - 1) / a.H;             // tokens of this CTA
+    const bool out = a.keep_out != nullptr && h < C;
+    const int cnt = (a.N - r + C - 1) / C;                  // tokens of this CTA
     int g = 32;
     while (g > 1 && g * cnt > kAttnThreads) g >>= 1;
     const int per = kAttnThreads / g;                       // tokens per round
     for (int base = 0; base < cnt; base += per) {          // uniform trip count
       const int slot = base + tid / g;
-      const int p = h + a.H * min(slot, cnt - 1);
-      const int r = group_rank(s_score, p, 0, a.N, g, tid & (g - 1));
+      const int p = r + C * min(slot, cnt - 1);
+      const int rk = group_rank(s_score, p, 0, a.N, g, tid & (g - 1));
       if ((tid & (g - 1)) == 0 && slot < cnt) {
-        const uint8_t kp = r < a.kkeep ? 1 : 0;
-        for (int d = 0; d < a.H; ++d) st_peer_u8(s_keep + p, d, kp);
-        if (a.keep_out != nullptr) a.keep_out[(long long)b * a.N + p] = kp;
+        const uint8_t kp = rk < a.kkeep ? 1 : 0;
+        for (int d = 0; d < C; ++d) st_peer_u8(s_keep + p, d, kp);
+        if (out) a.keep_out[(long long)b * a.N + p] = kp;
       }
     }
   }
@@ -1094,9 +1111,10 @@ __global__ void __launch_bounds__(kAttnThreads, 3) attn_kernel(const AttnArgs a,
 #ifndef RAGGED_NO_KEEP_PREFETCH
   if constexpr (kPrune) {
     // the image's hidden rows (this head's 128-byte slice) into L2 before the wait
-    const int pb = (int)blockIdx.x / a.H, ph = (int)blockIdx.x - pb * a.H;
-    const char* xb = static_cast<const char*>(a.x) + (long long)pb * a.N * a.ldx * 2 + ph * kRowBytes;
-    for (int p = tid; p < a.N; p += kAttnThreads) prefetch_l2(xb + p * a.ldx * 2);
+    const int pb = (int)blockIdx.x / a.H, S = a.H / a.pc, pr = ((int)blockIdx.x - pb * a.H) % a.pc;
+    const char* xb = static_cast<const char*>(a.x) + (long long)pb * a.N * a.ldx * 2 + pr * S * kRowBytes;
+    for (int j = tid; j < S * a.N; j += kAttnThreads)
+      prefetch_l2(xb + (j % a.N) * a.ldx * 2 + (j / a.N) * kRowBytes);
   } else if constexpr (kFused) {
     // Before the grid-dependency wait (PDL: this CTA may be resident while the
     // previous kernel in the stream still runs): read this image's keep row
@@ -1637,14 +1655,14 @@ static int attn_qsplit(int problems, int N, int n_hint) {
   return qs < 1 ? 1 : qs;
 }
 
-// N2 fused ahead of the scan: one cluster of H CTAs per image (H <= 16).
+// N2 fused ahead of the scan: clusters of a.pc consecutive heads of one image (H <= 16).
 template <typename T, bool kLargeN>
 static cudaError_t launch_attn_prune(const AttnArgs& a, cudaStream_t st) {
   static bool done[64] = {false};
   auto kern = attn_kernel<T, true, false, kLargeN, true>;
   cudaError_t e = smem_attr_once(kern, attn_smem_bytes(kMaxN), done);
   if (e != cudaSuccess) return e;
-  if (a.H > 8) {
+  if (a.pc > 8) {
     e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     if (e != cudaSuccess) return e;
   }
@@ -1657,7 +1675,7 @@ static cudaError_t launch_attn_prune(const AttnArgs& a, cudaStream_t st) {
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   attr[1].id = cudaLaunchAttributeClusterDimension;
-  attr[1].val.clusterDim.x = a.H;
+  attr[1].val.clusterDim.x = a.pc;
   attr[1].val.clusterDim.y = 1;
   attr[1].val.clusterDim.z = 1;
   cfg.attrs = attr;
@@ -1683,6 +1701,14 @@ cudaError_t launch_prune_l2_fused(int dtype, int engine, const void* x, long lon
   a.ldx = ldx;
   a.kkeep = kkeep;
   a.keep_out = keep_out;
+  // cluster size: the largest divisor of H <= 8 leaving <= 2 slices per CTA
+  // (H = 12 -> 6, 16 -> 8, 10 -> 5); else all H heads (9, 11, 13, 15)
+  a.pc = H;
+  for (int c = 8; c >= 1 && H > 8; --c)
+    if (H % c == 0 && H / c <= 2) {
+      a.pc = c;
+      break;
+    }
   const bool large = engine == kEngineMmaLong;
   if (dtype == 0)
     return large ? launch_attn_prune<__nv_bfloat16, true>(a, st) : launch_attn_prune<__nv_bfloat16, false>(a, st);

@@ -26,3 +26,25 @@ res["evit_k1_us"] = bench._graph_time(torch, [lambda: rb.keep_evit(q, k, v, 1, k
 res["evit_hot_us"] = bench._graph_time(torch, [lambda: rb.keep_evit(q, k, v, kk, keep=keep)], 500)
 res["empty_256x256_us"] = bench._graph_time(torch, [lambda: rb.empty_launch(256, 256)], 500)
 print(json.dumps(res, indent=1))
+# mask -> fused (two launches) vs the single-launch prune kernel, H = 12 and 6
+for Hh in (12, 6):
+    xs = [synth.hidden_states(B, N, Hh * 64, "bf16", seed=40 + i).to(dev) for i in range(17)]
+    qs = [tuple(t.to(dev) for t in synth.activations(B, N, Hh, 64, "bf16", seed=90 + i)) for i in range(16)]
+    o = torch.empty_like(qs[0][0])
+    keeps = [torch.empty(B, N, dtype=torch.uint8, device=dev) for _ in range(16)]
+    def two(j):
+        rb.keep_topk_l2(xs[j % 17], kk, keep=keeps[j % 16])
+        q_, k_, v_ = qs[j % 16]
+        rb.pack_attend_unpack(q_, k_, v_, keeps[j % 16], o=o, n_hint=kk)
+    def one(j):
+        q_, k_, v_ = qs[j % 16]
+        rb.prune_l2_pack_attend_unpack(xs[j % 17], q_, k_, v_, kk, o=o)
+    def fused_only(j):
+        q_, k_, v_ = qs[j % 16]
+        rb.pack_attend_unpack(q_, k_, v_, keeps[j % 16], o=o, n_hint=kk)
+    L = 16 * 17
+    res[f"H{Hh}_mask_then_fused_us"] = bench._graph_time(torch, [(lambda j=j: two(j)) for j in range(L)], 500)
+    res[f"H{Hh}_fused_only_us"] = bench._graph_time(torch, [(lambda j=j: fused_only(j)) for j in range(L)], 500)
+    res[f"H{Hh}_prune_in_fused_us"] = bench._graph_time(torch, [(lambda j=j: one(j)) for j in range(L)], 500)
+    del xs, qs
+print(json.dumps(res, indent=1))

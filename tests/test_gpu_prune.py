@@ -129,7 +129,8 @@ def _l2_mask_ok(x, k, got):
 
 @pytest.mark.parametrize("dtype", ["bf16", "fp16"])
 @pytest.mark.parametrize("B,N,H,p", [(32, 197, 12, 0.8), (4, 197, 3, 0.5), (7, 33, 6, 0.3), (3, 256, 16, 0.9),
-                                     (5, 197, 12, 0.0), (2, 1, 4, 0.0), (6, 100, 12, 0.5)])
+                                     (5, 197, 12, 0.0), (2, 1, 4, 0.0), (6, 100, 12, 0.5),
+                                     (3, 150, 10, 0.6), (2, 197, 14, 0.8), (2, 64, 9, 0.5), (2, 256, 16, 0.0)])
 def test_prune_l2_fused_matches_oracle(dtype, B, N, H, p):
     """Mask computed inside the fused launch == ragged_keep_topk_l2's definition
     (oracle), output == oracle pack-attend-unpack on that mask, cu = b*min(k,N);
