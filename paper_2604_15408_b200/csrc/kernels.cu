@@ -1010,16 +1010,43 @@ __device__ __forceinline__ void st_peer_f32(const void* p, uint32_t rank, float 
 // CTA r computes exactly cluster 0's CTA r's sums); CTA r ranks tokens r, r + C,
 // ... (CLS = +inf, NaN last, ties to the lower position) and pushes their keep
 // flags to every CTA; a second cluster barrier publishes them.  Layout: x
-// slices in the K (and V) area; partials / keys / keep row in the V area when
+// slices in the K (and V) area; partials / 64-bit keys / keep row in the V area when
 // S = 1, else in the Q area; the gather overwrites them only after
 // image_rows' barrier (every read done).  Returns the keep row in shared memory.
+// Total order of (score, position) as one 64-bit key: the score's bits made
+// monotone as an unsigned integer (negative values flipped) above the inverted
+// position, so a larger key = a higher score, or the lower position on a tie --
+// the order group_rank compares in (R20), two integer compares per element.
+__device__ __forceinline__ unsigned long long rank_key(float sc, int p) {
+  const uint32_t u = __float_as_uint(sc);
+  const uint32_t m = (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+  return ((unsigned long long)m << 32) | (uint32_t)(0xffff - p);
+}
+// rank of token n = #{m : key[m] > key[n]} with g lanes per token (power of
+// two <= 32, part = lane index in the group); every lane of the warp calls it.
+__device__ __forceinline__ int group_rank_key(const unsigned long long* key, int n, int N, int g, int part) {
+  const unsigned long long kn = key[n];
+  int c0 = 0, c1 = 0, c2 = 0, c3 = 0;
+  int m = part;
+  for (; m + 3 * g < N; m += 4 * g) {
+    c0 += key[m] > kn ? 1 : 0;
+    c1 += key[m + g] > kn ? 1 : 0;
+    c2 += key[m + 2 * g] > kn ? 1 : 0;
+    c3 += key[m + 3 * g] > kn ? 1 : 0;
+  }
+  for (; m < N; m += g) c0 += key[m] > kn ? 1 : 0;
+  int r = c0 + c1 + c2 + c3;
+  for (int o = 1; o < g; o <<= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
+  return r;
+}
+
 template <typename T>
 __device__ __forceinline__ const uint8_t* prune_l2_row(const AttnArgs& a, int b, int h, uint8_t* smem, int tid) {
   const int rows_cap = attn_rows_cap(a.N);
   const int C = a.pc, S = a.H / C, r = (int)cluster_rank();
   uint8_t* s_x = smem;                                                      // [S][N][128 B]
   float* s_part = reinterpret_cast<float*>(smem + (S == 1 ? 1 : 2) * rows_cap * kRowBytes);  // [C][N]
-  uint32_t* s_key = reinterpret_cast<uint32_t*>(s_part + C * a.N);         // [N]
+  unsigned long long* s_key = reinterpret_cast<unsigned long long*>(s_part + ((C * a.N + 1) & ~1));  // [N]
   uint8_t* s_keep = reinterpret_cast<uint8_t*>(s_key + kMaxN);              // [N]
   const char* xb = static_cast<const char*>(a.x) + (long long)b * a.N * a.ldx * 2 + r * S * kRowBytes;
   {  // 8 threads per 128-byte row slice; every copy in flight at once
@@ -1059,11 +1086,10 @@ __device__ __forceinline__ const uint8_t* prune_l2_row(const AttnArgs& a, int b,
   TL(9);
   cluster_sync_all();  // all C partials of every token delivered
   TL(10);
-  float* s_score = reinterpret_cast<float*>(s_key);
   for (int p = tid; p < a.N; p += kAttnThreads) {
     float t = 0.f;
     for (int d = 0; d < C; ++d) t += s_part[d * a.N + p];
-    s_score[p] = p == 0 ? INFINITY : (t != t ? -INFINITY : t);
+    s_key[p] = rank_key(p == 0 ? INFINITY : (t != t ? -INFINITY : t), p);
   }
   __syncthreads();
   TL(11);
@@ -1079,7 +1105,7 @@ __device__ __forceinline__ const uint8_t* prune_l2_row(const AttnArgs& a, int b,
     for (int base = 0; base < cnt; base += per) {          // uniform trip count
       const int slot = base + tid / g;
       const int p = r + C * min(slot, cnt - 1);
-      const int rk = group_rank(s_score, p, 0, a.N, g, tid & (g - 1));
+      const int rk = group_rank_key(s_key, p, a.N, g, tid & (g - 1));
       if ((tid & (g - 1)) == 0 && slot < cnt) {
         const uint8_t kp = rk < a.kkeep ? 1 : 0;
         for (int d = 0; d < C; ++d) st_peer_u8(s_keep + p, d, kp);
@@ -1087,6 +1113,7 @@ __device__ __forceinline__ const uint8_t* prune_l2_row(const AttnArgs& a, int b,
       }
     }
   }
+  TL(13);
   cluster_sync_all();  // all N flags in every CTA
   TL(12);
   return s_keep;

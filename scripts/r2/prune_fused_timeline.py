@@ -1,6 +1,6 @@
 """Per-CTA timeline of the fused prune kernel (TL build): TL slots 0 entry,
 7 x loaded + squared, 8 cluster wait, 9 pushed, 10 cluster barrier, 11 scores,
-12 ranked, 1 ranks/ballots, 2 gathers issued, 3 gathers landed, 4 end."""
+13 ranks stored, 12 ranked (flags barrier), 1 ranks/ballots, 2 gathers issued, 3 gathers landed, 4 end."""
 import ctypes, json, os, sys
 ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, ROOT)
@@ -38,7 +38,7 @@ for B, H in ((128, 3), (32, 12)):
         t0 = t[:, 0].min()
         rel = (t - t0) / 1e3
         d = {}
-        for sl in (0, 7, 8, 9, 10, 11, 12, 1, 2, 3, 4):
+        for sl in (0, 7, 8, 9, 10, 11, 13, 12, 1, 2, 3, 4):
             d[f"s{sl}"] = [round(float(np.median(rel[:, sl])), 2), round(float(rel[:, sl].max()), 2)]
         d["distinct_sms"] = int(len(set(buf[:, 15].tolist())))
         res[f"B{B}_H{H}_{mode}"] = d
