@@ -182,6 +182,33 @@ __device__ __forceinline__ int group_rank(const float* s, int n, int first, int 
   return r;
 }
 
+// Total order of (score, position) as one 64-bit key: the score's bits made
+// monotone as an unsigned integer (negative values flipped) above the inverted
+// position, so a larger key = a higher score, or the lower position on a tie --
+// the order group_rank compares in (R20), two integer compares per element.
+__device__ __forceinline__ unsigned long long rank_key(float sc, int p) {
+  const uint32_t u = __float_as_uint(sc);
+  const uint32_t m = (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+  return ((unsigned long long)m << 32) | (uint32_t)(0xffff - p);
+}
+// rank of token n = #{m : key[m] > key[n]} with g lanes per token (power of
+// two <= 32, part = lane index in the group); every lane of the warp calls it.
+__device__ __forceinline__ int group_rank_key(const unsigned long long* key, int n, int N, int g, int part) {
+  const unsigned long long kn = key[n];
+  int c0 = 0, c1 = 0, c2 = 0, c3 = 0;
+  int m = part;
+  for (; m + 3 * g < N; m += 4 * g) {
+    c0 += key[m] > kn ? 1 : 0;
+    c1 += key[m + g] > kn ? 1 : 0;
+    c2 += key[m + 2 * g] > kn ? 1 : 0;
+    c3 += key[m + 3 * g] > kn ? 1 : 0;
+  }
+  for (; m < N; m += g) c0 += key[m] > kn ? 1 : 0;
+  int r = c0 + c1 + c2 + c3;
+  for (int o = 1; o < g; o <<= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
+  return r;
+}
+
 // Byte offset of 16-byte chunk c of row r in a 128-byte-row tile with the
 // XOR-8 swizzle (chunk c of row r lives at chunk c ^ (r & 7)): conflict-free
 // ldmatrix over 8 consecutive rows, identical to the TMA 128B swizzle pattern.

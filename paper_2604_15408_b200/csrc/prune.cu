@@ -77,6 +77,9 @@ __device__ __forceinline__ uint32_t peer_addr(const void* p, uint32_t rank) {
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
   return r;
 }
+__device__ __forceinline__ void st_peer_u64(uint32_t a, unsigned long long v) {
+  asm volatile("st.shared::cluster.u64 [%0], %1;" ::"r"(a), "l"(v) : "memory");
+}
 __device__ __forceinline__ void st_peer_f32(uint32_t a, float v) {
   asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(a), "f"(v) : "memory");
 }
@@ -162,7 +165,7 @@ template <typename T>
 __global__ void __launch_bounds__(kPThr) keep_l2_cluster_kernel(const T* __restrict__ x, long long ld, int N,
                                                                  int D, int k, uint8_t* __restrict__ keep) {
   extern __shared__ __align__(128) uint8_t s_rows[];  // [R][D] of x
-  __shared__ float s_score[kMaxN];
+  __shared__ unsigned long long s_key[kMaxN];
   __shared__ __align__(8) uint64_t s_bar;
   const int c = (int)cluster_rank(), b = blockIdx.x / kPC, tid = threadIdx.x;
   const int R = (N + kPC - 1) / kPC, r0 = min(N, c * R), r1 = min(N, r0 + R);
@@ -215,7 +218,7 @@ __global__ void __launch_bounds__(kPThr) keep_l2_cluster_kernel(const T* __restr
     for (int i = 0; i < 4; ++i) {
       const int n = r0 + warp + 8 * i;
       // ||x||^2 ranks like ||x|| (R20); CLS is +inf so it always survives (R6)
-      if (n < r1 && lane < kPC) st_peer_f32(peer_addr(&s_score[n], lane), n == 0 ? INFINITY : nan_low(acc[i]));
+      if (n < r1 && lane < kPC) st_peer_u64(peer_addr(&s_key[n], lane), rank_key(n == 0 ? INFINITY : nan_low(acc[i]), n));
     }
   }
   PTL(4);
@@ -224,7 +227,7 @@ __global__ void __launch_bounds__(kPThr) keep_l2_cluster_kernel(const T* __restr
   // rank own rows: 8 lanes per row (R <= 32 rows on 256 threads)
   {
     const int rr = tid >> 3, n = min(r0 + rr, N - 1);
-    const int r = group_rank(s_score, n, 0, N, 8, tid & 7);
+    const int r = group_rank_key(s_key, n, N, 8, tid & 7);
     if ((tid & 7) == 0 && r0 + rr < r1) keep[(long long)b * N + r0 + rr] = r < k ? 1 : 0;
   }
   PTL(6);
