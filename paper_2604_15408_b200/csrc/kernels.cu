@@ -1066,20 +1066,38 @@ __device__ __forceinline__ const uint8_t* prune_l2_row(const AttnArgs& a, int b,
   }
   __syncthreads();
   TL(11);
-  // this CTA ranks tokens p = r, r + C, ... (g lanes per token) and stores the
-  // flags into every CTA of the cluster: the O(N^2) comparisons are split C ways;
-  // the image's first cluster also writes keep_out
+  // this CTA ranks tokens p = r, r + C, ... (g lanes per token, g = the most
+  // that lets one round cover them, not only powers of two: C3's 33 tokens take
+  // g = 3, 66 compares per lane instead of 98 with g = 2) and stores the flags
+  // into every CTA of the cluster: the O(N^2) comparisons are split C ways; the
+  // image's first cluster also writes keep_out
   {
     const bool out = a.keep_out != nullptr && h < C;
     const int cnt = (a.N - r + C - 1) / C;                  // tokens of this CTA
+    const int warp = tid >> 5, lane = tid & 31;
     int g = 32;
-    while (g > 1 && g * cnt > kAttnThreads) g >>= 1;
-    const int per = kAttnThreads / g;                       // tokens per round
+    while (g > 1 && (kAttnThreads / 32) * (32 / g) < cnt) --g;
+    const int gw = 32 / g;                                  // groups per warp
+    const int per = (kAttnThreads / 32) * gw;               // tokens per round
+    const int j = min(lane / g, gw - 1), part = lane - j * g;  // lanes >= gw g: duplicates, discarded
+    const bool lead = part == 0 && lane < gw * g;
     for (int base = 0; base < cnt; base += per) {          // uniform trip count
-      const int slot = base + tid / g;
+      const int slot = base + warp * gw + j;
       const int p = r + C * min(slot, cnt - 1);
-      const int rk = group_rank_key(s_key, p, a.N, g, tid & (g - 1));
-      if ((tid & (g - 1)) == 0 && slot < cnt) {
+      const unsigned long long kn = s_key[p];
+      int c0 = 0, c1 = 0;
+      int m = lane < gw * g ? part : a.N;
+      for (; m + g < a.N; m += 2 * g) {
+        c0 += s_key[m] > kn ? 1 : 0;
+        c1 += s_key[m + g] > kn ? 1 : 0;
+      }
+      if (m < a.N) c0 += s_key[m] > kn ? 1 : 0;
+      int rk = c0 + c1;
+      for (int o = 1; o < g; o <<= 1) {  // segmented sum: the group's first lane gets it
+        const int v = __shfl_down_sync(0xffffffffu, rk, o);
+        if (part + o < g) rk += v;
+      }
+      if (lead && slot < cnt) {
         const uint8_t kp = rk < a.kkeep ? 1 : 0;
         for (int d = 0; d < C; ++d) st_peer_u8(s_keep + p, d, kp);
         if (out) a.keep_out[(long long)b * a.N + p] = kp;
