@@ -990,6 +990,11 @@ __device__ __forceinline__ void st_peer_u8(const void* p, uint32_t rank, uint8_t
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(a) : "r"(smem_u32(p)), "r"(rank));
   asm volatile("st.shared::cluster.u8 [%0], %1;" ::"r"(a), "h"((unsigned short)v) : "memory");
 }
+__device__ __forceinline__ void st_peer_u64(const void* p, uint32_t rank, unsigned long long v) {
+  uint32_t a;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(a) : "r"(smem_u32(p)), "r"(rank));
+  asm volatile("st.shared::cluster.u64 [%0], %1;" ::"r"(a), "l"(v) : "memory");
+}
 __device__ __forceinline__ void st_peer_f32(const void* p, uint32_t rank, float v) {
   uint32_t a;
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(a) : "r"(smem_u32(p)), "r"(rank));
@@ -1008,8 +1013,9 @@ __device__ __forceinline__ void st_peer_f32(const void* p, uint32_t rank, float 
 // (DSMEM); after one cluster barrier each CTA adds the C partials in rank order
 // (identical bits in every CTA, and in every cluster of the image: cluster j's
 // CTA r computes exactly cluster 0's CTA r's sums); CTA r ranks tokens r, r + C,
-// ... (CLS = +inf, NaN last, ties to the lower position) and pushes their keep
-// flags to every CTA; a second cluster barrier publishes them.  Layout: x
+// ... (CLS = +inf, NaN last, ties to the lower position); the CTA holding the
+// token of rank k - 1 pushes its key to every CTA (a second cluster barrier) and
+// each CTA keeps the tokens whose key is >= it.  Layout: x
 // slices in the K (and V) area; partials / 64-bit keys / keep row in the V area when
 // S = 1, else in the Q area; the gather overwrites them only after
 // image_rows' barrier (every read done).  Returns the keep row in shared memory.
@@ -1020,7 +1026,9 @@ __device__ __forceinline__ const uint8_t* prune_l2_row(const AttnArgs& a, int b,
   uint8_t* s_x = smem;                                                      // [S][N][128 B]
   float* s_part = reinterpret_cast<float*>(smem + (S == 1 ? 1 : 2) * rows_cap * kRowBytes);  // [C][N]
   unsigned long long* s_key = reinterpret_cast<unsigned long long*>(s_part + ((C * a.N + 1) & ~1));  // [N]
-  uint8_t* s_keep = reinterpret_cast<uint8_t*>(s_key + kMaxN);              // [N]
+  unsigned long long* s_tau = s_key + kMaxN;                                // the k-th largest key
+  uint8_t* s_keep = reinterpret_cast<uint8_t*>(s_key + kMaxN + 2);          // [N]
+  if (tid == 0) *s_tau = 0ull;  // k >= N: every key passes (stays 0; peers write only after the first barrier)
   const char* xb = static_cast<const char*>(a.x) + (long long)b * a.N * a.ldx * 2 + r * S * kRowBytes;
   {  // 8 threads per 128-byte row slice; every copy in flight at once
     const int c = tid & 7;
@@ -1098,14 +1106,22 @@ __device__ __forceinline__ const uint8_t* prune_l2_row(const AttnArgs& a, int b,
         if (part + o < g) rk += v;
       }
       if (lead && slot < cnt) {
-        const uint8_t kp = rk < a.kkeep ? 1 : 0;
-        for (int d = 0; d < C; ++d) st_peer_u8(s_keep + p, d, kp);
-        if (out) a.keep_out[(long long)b * a.N + p] = kp;
+        // keys are distinct, so exactly one token of the cluster has rank k - 1:
+        // its key is the threshold every CTA compares against (one push per CTA
+        // instead of every token's flag)
+        if (rk == a.kkeep - 1)
+          for (int d = 0; d < C; ++d) st_peer_u64(s_tau, d, kn);
+        if (out) a.keep_out[(long long)b * a.N + p] = rk < a.kkeep ? 1 : 0;
       }
     }
   }
   TL(13);
-  cluster_sync_all();  // all N flags in every CTA
+  cluster_sync_all();  // the threshold key in every CTA
+  {
+    const unsigned long long tau = *s_tau;
+    for (int p = tid; p < a.N; p += kAttnThreads) s_keep[p] = s_key[p] >= tau ? 1 : 0;
+  }
+  __syncthreads();
   TL(12);
   return s_keep;
 }
