@@ -1046,14 +1046,34 @@ __device__ __forceinline__ const uint8_t* prune_l2_row(const AttnArgs& a, int b,
 #pragma unroll
     for (int i = 0; i < 2; ++i) {
       const int p = sl * a.N + min(tid + i * kAttnThreads, a.N - 1);
+      if constexpr (std::is_same<T, __nv_bfloat16>::value) {
+        // bf16 -> fp32 is a shift / mask of each half-word; two lanes of sums in
+        // one packed fp32 FMA (fma.rn.f32x2), added at the end
+        uint64_t acc = 0;
 #pragma unroll
-      for (int c = 0; c < 8; ++c) {
-        const uint4 raw = *reinterpret_cast<const uint4*>(s_x + p * kRowBytes + ((c + tid) & 7) * 16);
-        const T* e = reinterpret_cast<const T*>(&raw);
+        for (int c = 0; c < 8; ++c) {
+          const uint4 raw = *reinterpret_cast<const uint4*>(s_x + p * kRowBytes + ((c + tid) & 7) * 16);
+          const uint32_t w[4] = {raw.x, raw.y, raw.z, raw.w};
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const float f = static_cast<float>(e[j]);
-          sq[i] = fmaf(f, f, sq[i]);
+          for (int j = 0; j < 4; ++j) {
+            uint64_t f;
+            asm("mov.b64 %0, {%1, %2};" : "=l"(f) : "r"(w[j] << 16), "r"(w[j] & 0xffff0000u));
+            asm("fma.rn.f32x2 %0, %1, %1, %0;" : "+l"(acc) : "l"(f));
+          }
+        }
+        uint32_t lo, hi;
+        asm("mov.b64 {%0, %1}, %2;" : "=r"(lo), "=r"(hi) : "l"(acc));
+        sq[i] += __uint_as_float(lo) + __uint_as_float(hi);
+      } else {
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          const uint4 raw = *reinterpret_cast<const uint4*>(s_x + p * kRowBytes + ((c + tid) & 7) * 16);
+          const T* e = reinterpret_cast<const T*>(&raw);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const float f = static_cast<float>(e[j]);
+            sq[i] = fmaf(f, f, sq[i]);
+          }
         }
       }
     }
