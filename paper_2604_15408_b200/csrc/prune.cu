@@ -331,6 +331,8 @@ __global__ void __launch_bounds__(kPThr) keep_evit_cluster_kernel(T* __restrict_
   __shared__ __align__(16) float s_logit[kMaxN];
   __shared__ float s_w[kMaxN];
   __shared__ uint8_t s_keep[kMaxN];
+  __shared__ unsigned long long s_key[kMaxN];
+  __shared__ unsigned long long s_tau;
   __shared__ float s_red1[kPThr / 32];
   __shared__ int s_f;
   __shared__ __align__(8) uint64_t s_bar[3];
@@ -359,6 +361,7 @@ __global__ void __launch_bounds__(kPThr) keep_evit_cluster_kernel(T* __restrict_
     tc::mbar_init(barQ, 1);
     tc::fence_mbar_init();
     s_f = N;
+    s_tau = kk - 2 >= 1 ? 0ull : ~0ull;  // no pushed threshold: keep every other token / only CLS
   }
 #ifndef RAGGED_NO_KEEP_PREFETCH
   {  // own k rows (scores), own q/v rows (fused token) and the CLS query into L2
@@ -424,20 +427,22 @@ __global__ void __launch_bounds__(kPThr) keep_evit_cluster_kernel(T* __restrict_
   PTL(3);
   cluster_sync_all();  // all N logits in every CTA
   PTL(4);
-  // 2. ranking (every CTA, all tokens: identical in every CTA): CLS + top-(kk-2)
-  // rank own rows among the other tokens [1, N) (8 lanes per row): kept if
-  // CLS or rank < kk - 2; the flags go to every CTA of the cluster
+  // 2. ranking: CLS + top-(kk-2) of the other tokens [1, N).  Every CTA holds
+  // all N logits; as 64-bit (logit, position) keys (key[0] = 0: CLS never counts)
+  // each CTA ranks its own rows (8 lanes per row); keys are distinct, so one
+  // token has rank kk - 3: the CTA holding it pushes its key to every CTA as the
+  // threshold (one DSMEM push per cluster instead of every row's flag)
+  for (int n = tid; n < N; n += kPThr) s_key[n] = n == 0 ? 0ull : rank_key(s_logit[n], n);
+  __syncthreads();
   {
     const int rr = tid >> 3, n = min(max(r0 + rr, 1), N - 1);
-    const int r = group_rank(s_logit, n, 1, N, 8, tid & 7);
-    const int nn = r0 + rr;
-    if ((tid & 7) == 0 && nn < r1) {
-      const uint8_t kp = (nn == 0 || r < kk - 2) ? 1 : 0;
+    const int r = group_rank_key(s_key, n, N, 8, tid & 7);
+    if ((tid & 7) == 0 && r0 + rr < r1 && r0 + rr > 0 && r == kk - 3)
 #pragma unroll
-      for (int d = 0; d < kPC; ++d) st_peer_u8(peer_addr(&s_keep[nn], d), kp);
-    }
+      for (int d = 0; d < kPC; ++d) st_peer_u64(peer_addr(&s_tau, d), s_key[n]);
   }
-  cluster_sync_all();  // every CTA holds all N keep flags
+  cluster_sync_all();  // the threshold in every CTA
+  if (tid < N) s_keep[tid] = (tid == 0 || s_key[tid] >= s_tau) ? 1 : 0;
   if (tid > 0 && tid < N && !s_keep[tid]) atomicMin(&s_f, tid);
   __syncthreads();
   const int f = s_f;
