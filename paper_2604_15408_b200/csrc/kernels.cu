@@ -995,6 +995,12 @@ __device__ __forceinline__ void st_peer_u64(const void* p, uint32_t rank, unsign
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(a) : "r"(smem_u32(p)), "r"(rank));
   asm volatile("st.shared::cluster.u64 [%0], %1;" ::"r"(a), "l"(v) : "memory");
 }
+__device__ __forceinline__ void st_peer_v4(const void* p, uint32_t rank, float4 v) {
+  uint32_t a;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(a) : "r"(smem_u32(p)), "r"(rank));
+  asm volatile("st.shared::cluster.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(a), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
+               : "memory");
+}
 __device__ __forceinline__ void st_peer_f32(const void* p, uint32_t rank, float v) {
   uint32_t a;
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(a) : "r"(smem_u32(p)), "r"(rank));
@@ -1024,25 +1030,31 @@ __device__ __forceinline__ const uint8_t* prune_l2_row(const AttnArgs& a, int b,
   const int rows_cap = attn_rows_cap(a.N);
   const int C = a.pc, S = a.H / C, r = (int)cluster_rank();
   uint8_t* s_x = smem;                                                      // [S][N][128 B]
-  float* s_part = reinterpret_cast<float*>(smem + (S == 1 ? 1 : 2) * rows_cap * kRowBytes);  // [C][N]
-  unsigned long long* s_key = reinterpret_cast<unsigned long long*>(s_part + ((C * a.N + 1) & ~1));  // [N]
+  float* s_part = reinterpret_cast<float*>(smem + (S == 1 ? 1 : 2) * rows_cap * kRowBytes);  // [C][Np]
+  const int Np = (a.N + 3) & ~3;                                            // partial row stride
+  unsigned long long* s_key = reinterpret_cast<unsigned long long*>(s_part + C * Np);  // [N]
   unsigned long long* s_tau = s_key + kMaxN;                                // the k-th largest key
   uint8_t* s_keep = reinterpret_cast<uint8_t*>(s_key + kMaxN + 2);          // [N]
   if (tid == 0) *s_tau = 0ull;  // k >= N: every key passes (stays 0; peers write only after the first barrier)
   const char* xb = static_cast<const char*>(a.x) + (long long)b * a.N * a.ldx * 2 + r * S * kRowBytes;
-  {  // 8 threads per 128-byte row slice; every copy in flight at once
+  {  // 8 threads per 128-byte row slice; one commit group per slice (slice 1
+     // lands while slice 0 is squared)
     const int c = tid & 7;
-    for (int j = tid >> 3; j < S * a.N; j += kAttnThreads / 8) {
-      const int sl = j >= a.N ? 1 : 0, p = j - sl * a.N;
-      cp_async_16(smem_u32(s_x + j * kRowBytes + c * 16), xb + p * a.ldx * 2 + sl * kRowBytes + c * 16, 16);
+    for (int sl = 0; sl < S; ++sl) {
+      for (int p = tid >> 3; p < a.N; p += kAttnThreads / 8)
+        cp_async_16(smem_u32(s_x + (sl * a.N + p) * kRowBytes + c * 16), xb + p * a.ldx * 2 + sl * kRowBytes + c * 16,
+                    16);
+      cp_async_commit();
     }
-    cp_async_commit();
-    cp_async_wait_all();
   }
-  __syncthreads();
-  TL(7);
   float sq[2] = {0.f, 0.f};
   for (int sl = 0; sl < S; ++sl) {
+    if (sl + 1 < S)
+      cp_async_wait_group<1>();
+    else
+      cp_async_wait_all();
+    __syncthreads();
+    if (sl == 0) TL(7);
 #pragma unroll
     for (int i = 0; i < 2; ++i) {
       const int p = sl * a.N + min(tid + i * kAttnThreads, a.N - 1);
@@ -1080,16 +1092,27 @@ __device__ __forceinline__ const uint8_t* prune_l2_row(const AttnArgs& a, int b,
   }
   cluster_wait();  // every CTA of the cluster has started: DSMEM is live
   TL(8);
-  for (int d = 0; d < C; ++d) {
-    if (tid < a.N) st_peer_f32(s_part + r * a.N + tid, d, sq[0]);
-    if (tid + kAttnThreads < a.N) st_peer_f32(s_part + r * a.N + tid + kAttnThreads, d, sq[1]);
+  {  // four consecutive tokens' partials per 16-byte DSMEM store (lanes 4j..4j+3 -> lane 4j)
+    float4 v[2];
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      v[i].x = sq[i];
+      v[i].y = __shfl_down_sync(0xffffffffu, sq[i], 1);
+      v[i].z = __shfl_down_sync(0xffffffffu, sq[i], 2);
+      v[i].w = __shfl_down_sync(0xffffffffu, sq[i], 3);
+    }
+    if ((tid & 3) == 0)
+      for (int d = 0; d < C; ++d) {
+        if (tid < a.N) st_peer_v4(s_part + r * Np + tid, d, v[0]);
+        if (tid + kAttnThreads < a.N) st_peer_v4(s_part + r * Np + tid + kAttnThreads, d, v[1]);
+      }
   }
   TL(9);
   cluster_sync_all();  // all C partials of every token delivered
   TL(10);
   for (int p = tid; p < a.N; p += kAttnThreads) {
     float t = 0.f;
-    for (int d = 0; d < C; ++d) t += s_part[d * a.N + p];
+    for (int d = 0; d < C; ++d) t += s_part[d * Np + p];
     s_key[p] = rank_key(p == 0 ? INFINITY : (t != t ? -INFINITY : t), p);
   }
   __syncthreads();
