@@ -27,6 +27,8 @@
 // between the loads, so only 2-3 were in flight -- l2 mask 10.8 us at C3.)
 #include <utility>
 
+#include <type_traits>
+
 #include "device.cuh"
 #include "launch.h"
 #include "tcgen05.cuh"
@@ -204,14 +206,29 @@ __global__ void __launch_bounds__(kPThr) keep_l2_cluster_kernel(const T* __restr
   {  // unconditional (convergent shuffles); a CTA without rows reads slot 0 and discards it
     float acc[4];
     rows4_reduce(s_rows, max(r1 - r0, 1), rowb, cpr, [](uint4 raw, int) {
-      const T* e = reinterpret_cast<const T*>(&raw);
-      float a = 0.f;
+      if constexpr (std::is_same<T, __nv_bfloat16>::value) {
+        // bf16 -> fp32 is a shift / mask of each half-word: packed fp32 FMAs
+        const uint32_t w[4] = {raw.x, raw.y, raw.z, raw.w};
+        uint64_t acc2 = 0;
 #pragma unroll
-      for (int t = 0; t < 8; ++t) {
-        const float f = static_cast<float>(e[t]);
-        a = fmaf(f, f, a);
+        for (int j = 0; j < 4; ++j) {
+          uint64_t f;
+          asm("mov.b64 %0, {%1, %2};" : "=l"(f) : "r"(w[j] << 16), "r"(w[j] & 0xffff0000u));
+          asm("fma.rn.f32x2 %0, %1, %1, %0;" : "+l"(acc2) : "l"(f));
+        }
+        uint32_t lo, hi;
+        asm("mov.b64 {%0, %1}, %2;" : "=r"(lo), "=r"(hi) : "l"(acc2));
+        return __uint_as_float(lo) + __uint_as_float(hi);
+      } else {
+        const T* e = reinterpret_cast<const T*>(&raw);
+        float a = 0.f;
+#pragma unroll
+        for (int t = 0; t < 8; ++t) {
+          const float f = static_cast<float>(e[t]);
+          a = fmaf(f, f, a);
+        }
+        return a;
       }
-      return a;
     }, acc);
     PTL(3);
 #pragma unroll
