@@ -1025,17 +1025,68 @@ __device__ __forceinline__ void st_peer_f32(const void* p, uint32_t rank, float 
 // slices in the K (and V) area; partials / 64-bit keys / keep row in the V area when
 // S = 1, else in the Q area; the gather overwrites them only after
 // image_rows' barrier (every read done).  Returns the keep row in shared memory.
+// Shared-memory layout of prune_l2_row: partials [C][Np] floats, keys [kMaxN],
+// the threshold key, the keep row [kMaxN] bytes, the partials' mbarrier.
+struct PruneSmem {
+  float* part;
+  unsigned long long* key;
+  unsigned long long* tau;
+  uint8_t* keep;
+  unsigned long long* mb;
+  int Np;
+};
+__device__ __forceinline__ PruneSmem prune_smem(const AttnArgs& a, uint8_t* smem) {
+  PruneSmem p;
+  const int C = a.pc, S = a.H / C;
+  p.Np = (a.N + 3) & ~3;
+  p.part = reinterpret_cast<float*>(smem + (S == 1 ? 1 : 2) * attn_rows_cap(a.N) * kRowBytes);
+  p.key = reinterpret_cast<unsigned long long*>(p.part + C * p.Np);
+  p.tau = p.key + kMaxN;
+  p.keep = reinterpret_cast<uint8_t*>(p.key + kMaxN + 2);
+  p.mb = p.key + kMaxN + 2 + kMaxN / 8;
+  return p;
+}
+// Before the cluster arrive at kernel entry: the partials' mbarrier, armed for
+// the bytes the C - 1 peers will store into this CTA (st.async completes it):
+// (C - 1) x ceil(N/4) 16-byte stores.
+__device__ __forceinline__ void prune_mbar_init(const AttnArgs& a, uint8_t* smem) {
+  const PruneSmem ps = prune_smem(a, smem);
+  const uint32_t m0 = smem_u32(ps.mb), m1 = smem_u32(ps.mb + 1);
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(m0) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  const uint32_t b0 = (uint32_t)(a.pc - 1) * (uint32_t)((a.N + 3) / 4) * 16u;
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(m0), "r"(b0) : "memory");
+  (void)m1;
+}
+__device__ __forceinline__ uint32_t peer_u32(const void* p, uint32_t rank) {
+  uint32_t a;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(a) : "r"(smem_u32(p)), "r"(rank));
+  return a;
+}
+__device__ __forceinline__ void st_async_v4(const void* p, const void* mb, uint32_t rank, float4 v) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.f32 [%0], {%1, %2, %3, %4}, [%5];" ::"r"(
+                   peer_u32(p, rank)),
+               "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w), "r"(peer_u32(mb, rank))
+               : "memory");
+}
+__device__ __forceinline__ void st_async_b64(const void* p, const void* mb, uint32_t rank, unsigned long long v) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];" ::"r"(peer_u32(p, rank)),
+               "l"(v), "r"(peer_u32(mb, rank))
+               : "memory");
+}
+
 template <typename T>
 __device__ __forceinline__ const uint8_t* prune_l2_row(const AttnArgs& a, int b, int h, uint8_t* smem, int tid) {
   const int rows_cap = attn_rows_cap(a.N);
   const int C = a.pc, S = a.H / C, r = (int)cluster_rank();
   uint8_t* s_x = smem;                                                      // [S][N][128 B]
-  float* s_part = reinterpret_cast<float*>(smem + (S == 1 ? 1 : 2) * rows_cap * kRowBytes);  // [C][Np]
-  const int Np = (a.N + 3) & ~3;                                            // partial row stride
-  unsigned long long* s_key = reinterpret_cast<unsigned long long*>(s_part + C * Np);  // [N]
-  unsigned long long* s_tau = s_key + kMaxN;                                // the k-th largest key
-  uint8_t* s_keep = reinterpret_cast<uint8_t*>(s_key + kMaxN + 2);          // [N]
-  if (tid == 0) *s_tau = 0ull;  // k >= N: every key passes (stays 0; peers write only after the first barrier)
+  const PruneSmem ps = prune_smem(a, smem);
+  float* s_part = ps.part;                      // [C][Np]
+  const int Np = ps.Np;                         // partial row stride
+  unsigned long long* s_key = ps.key;           // [N]
+  unsigned long long* s_tau = ps.tau;           // the k-th largest key
+  uint8_t* s_keep = ps.keep;                    // [N]
+  (void)rows_cap;
   const char* xb = static_cast<const char*>(a.x) + (long long)b * a.N * a.ldx * 2 + r * S * kRowBytes;
   {  // 8 threads per 128-byte row slice; one commit group per slice (slice 1
      // lands while slice 0 is squared)
@@ -1101,14 +1152,21 @@ __device__ __forceinline__ const uint8_t* prune_l2_row(const AttnArgs& a, int b,
       v[i].z = __shfl_down_sync(0xffffffffu, sq[i], 2);
       v[i].w = __shfl_down_sync(0xffffffffu, sq[i], 3);
     }
-    if ((tid & 3) == 0)
+    if ((tid & 3) == 0) {
+      if (tid < a.N) *reinterpret_cast<float4*>(s_part + r * Np + tid) = v[0];
+      if (tid + kAttnThreads < a.N) *reinterpret_cast<float4*>(s_part + r * Np + tid + kAttnThreads) = v[1];
       for (int d = 0; d < C; ++d) {
-        if (tid < a.N) st_peer_v4(s_part + r * Np + tid, d, v[0]);
-        if (tid + kAttnThreads < a.N) st_peer_v4(s_part + r * Np + tid + kAttnThreads, d, v[1]);
+        if (d == r) continue;
+        if (tid < a.N) st_async_v4(s_part + r * Np + tid, ps.mb, d, v[0]);
+        if (tid + kAttnThreads < a.N) st_async_v4(s_part + r * Np + tid + kAttnThreads, ps.mb, d, v[1]);
       }
+    }
   }
   TL(9);
-  cluster_sync_all();  // all C partials of every token delivered
+  // the peers' partials delivered (complete_tx on this CTA's mbarrier, no
+  // cluster-wide barrier); own partials by the barrier
+  tc::mbar_wait(smem_u32(ps.mb), 0);
+  __syncthreads();
   TL(10);
   for (int p = tid; p < a.N; p += kAttnThreads) {
     float t = 0.f;
@@ -1161,9 +1219,10 @@ __device__ __forceinline__ const uint8_t* prune_l2_row(const AttnArgs& a, int b,
   TL(13);
   cluster_sync_all();  // the threshold key in every CTA
   {
-    const unsigned long long tau = *s_tau;
+    const unsigned long long tau = a.kkeep < a.N ? *s_tau : 0ull;  // k >= N: every key passes
     for (int p = tid; p < a.N; p += kAttnThreads) s_keep[p] = s_key[p] >= tau ? 1 : 0;
   }
+  if (tid == 0) asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(smem_u32(ps.mb)) : "memory");  // memory reused by the gather
   __syncthreads();
   TL(12);
   return s_keep;
@@ -1183,7 +1242,10 @@ __global__ void __launch_bounds__(kAttnThreads, 3) attn_kernel(const AttnArgs a,
   uint32_t* sWords = reinterpret_cast<uint32_t*>(sDrop + kMaxN);
 
   TL(0);
-  if constexpr (kPrune) cluster_arrive_relaxed();  // paired with the wait before the first DSMEM store
+  if constexpr (kPrune) {
+    if (tid == 0) prune_mbar_init(a, smem);
+    cluster_arrive_relaxed();  // paired with the wait before the first DSMEM store (release: the mbarrier fence)
+  }
   pdl_launch_dependents();
 #ifndef RAGGED_NO_KEEP_PREFETCH
   if constexpr (kPrune) {
